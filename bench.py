@@ -1,0 +1,289 @@
+"""bench.py -- B200 benchmark of the Anderson-accelerated Lloyd K-Means hot path.
+
+A "step" is one loop pass of Algorithm 1: assignment
+(+ near-tie refine), update partials with the fused energy, [NCCL allreduce],
+device-side control, fallback G-evaluation when the guard rejects, Gram,
+LS solve and mixing -- all rows of SURVEY §8(a) -- on the BASELINE.json
+config c5 (N = 16,000,000, d = 64, K = 4096, fp32), sharded over the ranks.
+
+value  = sample-centroid distance evaluations per second of the whole job:
+         N * K * (assignment passes performed in the timed steps) / time,
+         time = max over ranks of the CUDA-event duration of the K steps.
+e2e    = the same metric through the C ABI with HOST inputs: every step copies
+         the shard X from pinned host memory to the device, runs the pass and
+         reads C^{t+1} and E back.
+roofline = the dominant kernel (the assignment engine), algorithmic flops
+         2 N K d per launch over its CUDA-event duration inside the timed
+         steps, against the tensor (3xTF32, fp32-equivalent) or FP32 peak.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
+       python bench.py --impl reference ...   (the CPU oracle arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "assign dist-evals/s (Algorithm 1 passes)"
+UNIT = "dist-evals/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------------- clocks
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            try:
+                a, b, c = [x.strip() for x in ln.split(",")]
+                self.samples.append((float(a), float(b), int(c, 16)))
+            except Exception:
+                pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        load = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        mask = 0
+        for s in load:
+            mask |= s[2]
+        return {"sm_mhz": statistics.median(s[0] for s in load), "sm_max_mhz": max(s[1] for s in load),
+                "reasons": [v for k, v in REASONS.items() if mask & k and k != 0x1], "samples": len(load)}
+
+
+# --------------------------------------------------------------------- oracle arm
+def cpu_baseline(X, C0, cfgname, budget_rows=None):
+    """The oracle's Assignment-Step (its dominant step) on a bounded row sample."""
+    import oracle
+    cores = os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    K, d = C0.shape
+    rows = budget_rows or max(1000, int(2.0e9 / (K * d)))   # ~2e9 fp64 sqdist terms (~10 s)
+    rows = min(rows, len(X))
+    Xs = np.ascontiguousarray(X[:rows])
+    C = C0.astype(np.float64)
+    oracle.assign(Xs[:64], C)                                 # warm (build/load)
+    t0 = time.perf_counter()
+    oracle.assign(Xs, C)
+    dt = time.perf_counter() - t0
+    return {"value": rows * K / dt, "unit": UNIT, "cores": int(os.environ.get("OMP_NUM_THREADS", cores)),
+            "kind": "oracle", "seconds": dt,
+            "sample": f"oracle Assignment-Step (fp64 direct differences) of the first {rows} rows of {cfgname} "
+                      f"(N={len(X)}, d={d}, K={K}) against C^0"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1805_10638_b200 import synthetic
+    X, C0, cfg = synthetic.make(args.config, seed=0)
+    K, d = C0.shape
+    steps = []
+    for _ in range(args.warmup):
+        cpu_baseline(X, C0, args.config, budget_rows=2000)
+    rows = max(500, int(4.0e8 / (K * d)))
+    for _ in range(args.steps):
+        cb = cpu_baseline(X, C0, args.config, budget_rows=rows)
+        steps.append(cb)
+    v = statistics.median(s["value"] for s in steps)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in steps),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.config}: oracle Assignment-Step sample",
+                                            "N": cfg.N, "d": cfg.d, "K": cfg.K},
+            "cpu_baseline": dict(steps[-1], value=v),
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1805_10638_b200 import aakm, synthetic
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    X, C0, cfg = synthetic.make(args.config, seed=0)
+    lo, hi = synthetic.shard_bounds(cfg.N, rank, world)
+    Xs = torch.from_numpy(X[lo:hi]).cuda()
+    X_host = torch.from_numpy(X[lo:hi]).pin_memory()
+    C0d = torch.from_numpy(C0).cuda()
+    km = aakm.KMeans(Xs, cfg.K, aakm.config(m0=cfg.m0, assign_path=args.path, timing=True),
+                     n_global=cfg.N, rank=rank, nranks=world)
+    stream = km.stream
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # Algorithm 1 line 1, then warm-up passes (untimed)
+    km.aa_step(C0d, info=False)
+    for _ in range(args.warmup):
+        km.aa_step(None, info=False)
+    st0 = km.state_export()
+    km.assign_timing()                         # drop warm-up timings
+    n_assign0 = st0["n_assign"]
+    L0 = km.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            km.aa_step(None, info=False)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = km.launch_count() - L0
+    st1 = km.state_export()
+    n_assign = st1["n_assign"] - n_assign0
+    a_ms, a_n = km.assign_timing()
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    passes_done = args.steps if not st1["done"] else None
+    value = cfg.N * cfg.K * n_assign / (ms_max / 1e3)
+
+    # e2e: host inputs, H2D of the shard + D2H of the result inside the timed region
+    C_host = torch.empty(cfg.K, cfg.d, dtype=torch.float32).pin_memory()
+    e2e_steps = max(1, args.e2e_steps)
+    barrier()
+    st_e0 = km.state_export()["n_assign"]
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tmpC = torch.empty(cfg.K, cfg.d, dtype=torch.float32, device="cuda")
+    lib = aakm.lib()
+    with torch.cuda.stream(stream):
+        for _ in range(e2e_steps):
+            Xs.copy_(X_host, non_blocking=True)                  # H2D of the step's inputs
+            km.aa_step(None, info=False)                          # one Algorithm 1 pass (C ABI)
+            lib.kmeans_get_centroids(km.h, aakm._ptr(tmpC), None)
+            C_host.copy_(tmpC, non_blocking=True)                 # D2H of the result C^{t+1}
+    e1.record(stream)
+    barrier()
+    e_ms = e0.elapsed_time(e1)
+    wall = time.perf_counter() - t0
+    e_na = km.state_export()["n_assign"] - st_e0
+    te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = cfg.N * cfg.K * e_na / (float(te.item()) / 1e3)
+
+    peaks, peak_kind = load_peaks()
+    path = km.path
+    n_local = hi - lo
+    flops = 2.0 * n_local * cfg.K * cfg.d
+    avg_ms = a_ms / max(a_n, 1)
+    achieved = flops / (avg_ms / 1e3) / 1e12
+    if path == "tc":
+        # 3xTF32 (fp32-equivalent): TF32 = bf16 x (1.1/2.25) nominal ratio, three MMAs per product
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * (1.1 / 2.25) / 3.0
+        bound = "tensor"
+    else:
+        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        bound = "alu"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"{args.config}_{path}_assign_bytes")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: Algorithm 1 passes (m0={cfg.m0}, dynamic m)", "N": cfg.N, "d": cfg.d,
+                   "K": cfg.K, "parallelism": f"dp{world}", "assign_path": path,
+                   "l2": f"inputs larger than L2 (X shard {n_local * cfg.d * 4 / 1e9:.2f} GB > 126 MB)"},
+        "passes": args.steps, "assign_passes": n_assign, "converged_in_window": passes_done is None,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n_local * cfg.d * 4,
+                "d2h_bytes_per_step": cfg.K * cfg.d * 4, "steps": e2e_steps, "wall_s": wall},
+        "gpu_launches": launches,
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": f"assign_{path}", "avg_launch_ms": avg_ms, "launches": a_n},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(X, C0, args.config)
+    km.close()
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

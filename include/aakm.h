@@ -1,0 +1,225 @@
+/*
+ * aakm.h -- C ABI of the B200-native Anderson-accelerated Lloyd K-Means hot
+ * path (arXiv 1805.10638).  Library: paper_1805_10638_b200/libaakm.so
+ * (hand-written sm_100a CUDA + NCCL; no torch types, no CPU fallback).
+ *
+ * Notation follows the paper: samples X = {x_i} (N x d), centroids
+ * C = [c_1..c_K] (K x d), assignment P = {rho_i}, energy E (Eq. 1,
+ * PAPER.md:14), Lloyd map G = Update o Assign (Eq. 6), residual
+ * F = G - C, Anderson window m, Algorithm 1
+ * (PAPER.md:107-160).  Readings of ambiguous passages are DESIGN.md R-A*.
+ *
+ * Conventions for every entry point:
+ *  - Array pointers are DEVICE pointers unless marked (host).
+ *  - Row-major layouts: X is n_local x d float32, C/G are K x d float32
+ *    (centroid-major), labels are int32 in [0, K).
+ *  - Ownership: X and the workspace are BORROWED from the caller and must stay
+ *    alive and unmodified until kmeans_destroy.  The library allocates no
+ *    device memory of its own except NCCL's internal buffers (nranks > 1).
+ *    Outputs go to caller buffers.
+ *  - Streams: all work is enqueued on the stream given to kmeans_create.
+ *    Calls returning host scalars synchronise that stream before returning;
+ *    the others are asynchronous.  One host thread at a time per handle.
+ *  - SPMD: with nranks > 1, assign/update/aa_step/run are COLLECTIVE (like
+ *    NCCL calls): every rank calls them in the same order; X is the rank's
+ *    contiguous row shard; C and config are identical on all ranks.  Ranks
+ *    combine [S | N | E | changed] with one ncclAllReduce per G-evaluation;
+ *    the Anderson step is replicated (deterministic kernels, identical bytes).
+ *  - Errors: KMEANS_ERR_INVALID is returned before any work is enqueued (null
+ *    required pointer, d < 1, k < 1, k > n_global, m0 < 0, m0 > m_max,
+ *    m_max > KMEANS_M_MAX, eps1 < 0 or eps1 >= eps2, workspace too small,
+ *    bad rank/nranks).  CUDA or NCCL failures return ERR_CUDA / ERR_NCCL and
+ *    poison the handle: afterwards only kmeans_destroy is valid, everything
+ *    else returns KMEANS_ERR_STATE.  Reaching max_iters is not an error
+ *    (report.converged = 0).  kmeans_last_error() gives the message.
+ */
+#ifndef AAKM_H
+#define AAKM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(AAKM_BUILD)
+#define AAKM_API __attribute__((visibility("default")))
+#else
+#define AAKM_API
+#endif
+
+#define KMEANS_M_MAX 30          /* m_bar of PAPER.md:177; ring = m_max + 1 slots */
+#define KMEANS_ABI_VERSION 1
+
+typedef struct kmeans_handle kmeans_handle;
+typedef struct CUstream_st *kmeans_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+    KMEANS_OK = 0,
+    KMEANS_ERR_INVALID = 1,
+    KMEANS_ERR_CUDA = 2,
+    KMEANS_ERR_NCCL = 3,
+    KMEANS_ERR_NOMEM = 4,
+    KMEANS_ERR_STATE = 5
+} kmeans_status;
+
+/* Assignment engine selection (kmeans_config.assign_path). */
+enum {
+    KMEANS_PATH_AUTO = 0,   /* tcgen05 3xTF32 when d % 32 == 0 and d <= 128, else SIMT */
+    KMEANS_PATH_SIMT = 1,   /* register-tiled FP32 FFMA kernel                          */
+    KMEANS_PATH_TC = 2      /* tcgen05/TMEM 3xTF32 tile GEMM (requires d % 32 == 0, d <= 128) */
+};
+
+/* Algorithm 1 settings.  Defaults (kmeans_config_default): PAPER.md:177
+ * (eps1 = 0.02, eps2 = 0.5, m_max = 30, m0 = 2), dynamic m on. */
+typedef struct {
+    int32_t m0;          /* initial m                         */
+    int32_t m_max;       /* m_bar, <= KMEANS_M_MAX                               */
+    double eps1;         /* ratio below which m decreases     */
+    double eps2;         /* ratio above which m increases     */
+    int32_t dynamic_m;   /* 1 = Algorithm 1; 0 = fixed m            */
+    int32_t max_iters;   /* cap on passes t (not an error when reached)           */
+    double ridge;        /* lambda on the unit-diagonal scaled Gram (R-A14)       */
+    int32_t assign_path; /* KMEANS_PATH_*                                        */
+    int32_t timing;      /* 1 = record CUDA events around each assignment launch  */
+} kmeans_config;
+
+/* Result of kmeans_run (fields per DESIGN.md R-A19). */
+typedef struct {
+    int64_t iters;       /* t_final + 1 = main-sequence G evaluations             */
+    int64_t n_assign;    /* assignment passes = iters + n_rejected                */
+    int64_t n_accepted;  /* accelerated iterates accepted by the guard            */
+    int64_t n_rejected;  /* accelerated iterates rejected      */
+    int32_t converged;   /* 1 = partition repeated (rule R3); 0 = max_iters       */
+    int32_t m_final;
+    double energy;       /* E(P, C) of the returned C (Eq. 1), global            */
+    double mse;          /* energy / n_global (R-A20)                            */
+    double seconds;      /* device time of the run (CUDA events)                 */
+} kmeans_report;
+
+/* One loop pass of Algorithm 1 (kmeans_aa_step). */
+typedef struct {
+    int64_t t;           /* pass index that was executed                          */
+    int32_t m;           /* m after the dynamic adjustment                        */
+    int32_t m_t;         /* min(m, t) columns used                 */
+    int32_t accepted;    /* accelerated iterate accepted this pass                */
+    int32_t rejected;    /* accelerated iterate rejected -> Lloyd fallback        */
+    int32_t converged;   /* partition repeated: C is a fixed point of G           */
+    int32_t lloyd;       /* next iterate C^{t+1} is a plain Lloyd iterate         */
+    double energy_cand;  /* E(C^t) of the candidate (pre-guard)                   */
+    double energy;       /* E^t after the guard                    */
+    int64_t changed;     /* #{i : rho_i^t != rho_i^{t-1}} of the final P^t         */
+} kmeans_step_info;
+
+/* Algorithm 1 state, for checkpoint/resume and lockstep parity tests.
+ * All pointers are HOST buffers supplied by the caller:
+ *   C, fallback: K*d; Ghist, Fhist: (m_max+1)*K*d, entry 0 = newest
+ *   (G^t, F^t), entry j = (G^{t-j}, F^{t-j}); labels_prev: n_local. */
+typedef struct {
+    float *C;            /* C^t, the iterate the next pass evaluates              */
+    float *fallback;     /* C_AU^t = G^{t-1} (R-A3)                               */
+    float *Ghist;
+    float *Fhist;
+    int32_t *labels_prev;/* P^{t-1}                                              */
+    int32_t hist_count;  /* valid history entries                                 */
+    int32_t m;
+    int32_t lloyd;       /* C^t is a Lloyd iterate (theta == 0)                   */
+    int32_t done;        /* converged or max_iters reached                        */
+    int64_t t;
+    double E1, E2;       /* E^{t-1}, E^{t-2} (post-guard)                         */
+    int64_t n_accepted, n_rejected, n_assign;
+} kmeans_state;
+
+/* Fill cfg with the defaults above.  Errors: INVALID if cfg is NULL. */
+AAKM_API kmeans_status kmeans_config_default(kmeans_config *cfg /*host*/);
+
+/* Bytes of device workspace kmeans_create needs for this shard.
+ * Errors: INVALID on bad sizes/config or NULL bytes. */
+AAKM_API kmeans_status kmeans_workspace_size(int64_t n_local, int32_t d, int32_t k,
+                                    const kmeans_config *cfg /*host*/, size_t *bytes /*host*/);
+
+/* 128-byte NCCL unique id (call on rank 0, broadcast to the other ranks). */
+AAKM_API kmeans_status kmeans_nccl_unique_id(void *uid128 /*host, 128 B*/);
+
+/* Create a handle over this rank's shard X (n_local x d, device, borrowed).
+ * n_global = sum of n_local over ranks.  workspace: >= kmeans_workspace_size
+ * bytes of device memory, 256-B aligned, borrowed.  uid128 must be NULL iff
+ * nranks == 1.  Collective when nranks > 1 (NCCL communicator init). */
+AAKM_API kmeans_status kmeans_create(kmeans_handle **out /*host*/, const float *X, int64_t n_local,
+                            int64_t n_global, int32_t d, int32_t k,
+                            const kmeans_config *cfg /*host*/, void *workspace,
+                            size_t workspace_bytes, int32_t rank, int32_t nranks,
+                            const void *uid128 /*host or NULL*/, kmeans_stream_t stream);
+
+/* Assignment step, Eq. (3), plus the energy E(P, C) (Eq. 1)
+ * and the number of labels that differ from labels_prev.
+ * C: K x d.  labels_out: n_local (exact nearest centroid, lowest index on
+ * exact fp64 ties).  energy_out / changed_out are GLOBAL (allreduced) host
+ * scalars, may be NULL; changed is 0 when labels_prev is NULL.  Synchronises. */
+AAKM_API kmeans_status kmeans_assign(kmeans_handle *h, const float *C, const int32_t *labels_prev,
+                            int32_t *labels_out, double *energy_out /*host*/,
+                            int64_t *changed_out /*host*/);
+
+/* Update step, Eq. (4): G_j = mean of {x_i : rho_i = j} over
+ * all ranks; an empty cluster keeps C_prev's row (R-A15).  labels: n_local in
+ * [0, K) (out-of-range -> INVALID after the sync).  counts_out: K int64
+ * device, nullable.  Synchronises (to report label errors). */
+AAKM_API kmeans_status kmeans_update(kmeans_handle *h, const int32_t *labels, const float *C_prev,
+                            float *G_out, int64_t *counts_out);
+
+/* Algorithm 1, one step.  C0 != NULL: line 1 -- P^0 =
+ * Assign(C^0), C^1 = G(C^0), F^0 = C^1 - C^0, E^0 = +inf, m = m0, t = 1.
+ * C0 == NULL: one loop pass t under rule R3 (R-A10).
+ * info/theta_out (host, nullable; theta_out >= m_max doubles): when either is
+ * non-NULL the call synchronises; otherwise it is asynchronous. */
+AAKM_API kmeans_status kmeans_aa_step(kmeans_handle *h, const float *C0, kmeans_step_info *info /*host*/,
+                             double *theta_out /*host*/);
+
+/* Algorithm 1 to convergence (rule R3) or max_iters, without a host sync per
+ * pass (CUDA-graph replay, device-side control).  C_out: K x d (global,
+ * identical on all ranks), labels_out: n_local; both nullable.  Synchronises. */
+AAKM_API kmeans_status kmeans_run(kmeans_handle *h, const float *C0, float *C_out, int32_t *labels_out,
+                         kmeans_report *rep /*host*/);
+
+/* Current iterate C^t and the labels of the last assignment (device copies).
+ * Asynchronous. */
+AAKM_API kmeans_status kmeans_get_centroids(kmeans_handle *h, float *C_out, int32_t *labels_out);
+
+/* Checkpoint / lockstep hooks (host buffers, see kmeans_state).  Synchronise. */
+AAKM_API kmeans_status kmeans_state_export(kmeans_handle *h, kmeans_state *st /*host*/);
+AAKM_API kmeans_status kmeans_state_import(kmeans_handle *h, const kmeans_state *st /*host*/);
+
+/* Test hook for the data-parallel partition logic: this rank's UNREDUCED
+ * packed partials [S (K*d, sum of x_i - C_{rho_i}) | N (K) | E | changed]
+ * as K*d + K + 2 doubles (device).  Synchronises. */
+AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *labels,
+                                     const int32_t *labels_prev, const float *C,
+                                     double *packed_out);
+
+/* Sum of CUDA-event durations (ms) of the assignment launches recorded since
+ * the last call (config.timing = 1), and their count.  Synchronises. */
+AAKM_API kmeans_status kmeans_assign_timing(kmeans_handle *h, double *ms_total /*host*/,
+                                   int64_t *launches /*host*/);
+
+/* Number of library kernels launched on this handle so far (graph replays
+ * count every kernel node). */
+AAKM_API int64_t kmeans_launch_count(const kmeans_handle *h);
+
+/* Rows flagged as near-ties (re-decided in fp64) by the last assignment. */
+AAKM_API kmeans_status kmeans_last_flagged(kmeans_handle *h, int64_t *flagged /*host*/);
+
+/* Name of the assignment engine the handle selected ("simt"/"tc"). */
+AAKM_API const char *kmeans_assign_path_name(const kmeans_handle *h);
+
+AAKM_API kmeans_status kmeans_destroy(kmeans_handle *h);
+
+/* Last error message of h (NULL h: this thread's last create error). */
+AAKM_API const char *kmeans_last_error(const kmeans_handle *h);
+
+AAKM_API int32_t kmeans_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AAKM_H */

@@ -1,0 +1,292 @@
+"""Thin Python binding of libaakm.so (include/aakm.h).  Argument marshalling
+only: every step of the hot path runs in the library's sm_100a kernels.
+PyTorch provides device memory (the workspace and outputs), the CUDA stream
+and, for nranks > 1, the process group used to broadcast the NCCL id.
+
+There is no CPU fallback: :func:`lib` raises if the shared library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import dataclasses
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaakm.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "aakm.h")
+_lib = None
+_lock = threading.Lock()
+
+KMEANS_M_MAX = 30
+PATHS = {"auto": 0, "simt": 1, "tc": 2}
+STATUS = {0: "OK", 1: "INVALID", 2: "CUDA", 3: "NCCL", 4: "NOMEM", 5: "STATE"}
+
+
+class AAKMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"kmeans status {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ct.Structure):
+    _fields_ = [("m0", ct.c_int32), ("m_max", ct.c_int32), ("eps1", ct.c_double), ("eps2", ct.c_double),
+                ("dynamic_m", ct.c_int32), ("max_iters", ct.c_int32), ("ridge", ct.c_double),
+                ("assign_path", ct.c_int32), ("timing", ct.c_int32)]
+
+
+class Report(ct.Structure):
+    _fields_ = [("iters", ct.c_int64), ("n_assign", ct.c_int64), ("n_accepted", ct.c_int64),
+                ("n_rejected", ct.c_int64), ("converged", ct.c_int32), ("m_final", ct.c_int32),
+                ("energy", ct.c_double), ("mse", ct.c_double), ("seconds", ct.c_double)]
+
+
+class StepInfo(ct.Structure):
+    _fields_ = [("t", ct.c_int64), ("m", ct.c_int32), ("m_t", ct.c_int32), ("accepted", ct.c_int32),
+                ("rejected", ct.c_int32), ("converged", ct.c_int32), ("lloyd", ct.c_int32),
+                ("energy_cand", ct.c_double), ("energy", ct.c_double), ("changed", ct.c_int64)]
+
+
+class State(ct.Structure):
+    _fields_ = [("C", ct.c_void_p), ("fallback", ct.c_void_p), ("Ghist", ct.c_void_p), ("Fhist", ct.c_void_p),
+                ("labels_prev", ct.c_void_p), ("hist_count", ct.c_int32), ("m", ct.c_int32),
+                ("lloyd", ct.c_int32), ("done", ct.c_int32), ("t", ct.c_int64), ("E1", ct.c_double),
+                ("E2", ct.c_double), ("n_accepted", ct.c_int64), ("n_rejected", ct.c_int64),
+                ("n_assign", ct.c_int64)]
+
+
+def _struct(s):
+    return {k: getattr(s, k) for k, _ in s._fields_}
+
+
+def lib():
+    """Load libaakm.so (built by ``__graft_entry__.build()``); raise if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                                  "(there is no CPU fallback)")
+            L = ct.CDLL(LIB_PATH)
+            P, I64, I32, D, S = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_double, ct.c_size_t
+            sig = {
+                "kmeans_abi_version": ([], I32),
+                "kmeans_config_default": ([ct.POINTER(Config)], I32),
+                "kmeans_workspace_size": ([I64, I32, I32, ct.POINTER(Config), ct.POINTER(S)], I32),
+                "kmeans_nccl_unique_id": ([P], I32),
+                "kmeans_create": ([ct.POINTER(P), P, I64, I64, I32, I32, ct.POINTER(Config), P, S, I32, I32, P, P], I32),
+                "kmeans_assign": ([P, P, P, P, ct.POINTER(D), ct.POINTER(I64)], I32),
+                "kmeans_update": ([P, P, P, P, P], I32),
+                "kmeans_aa_step": ([P, P, ct.POINTER(StepInfo), P], I32),
+                "kmeans_run": ([P, P, P, P, ct.POINTER(Report)], I32),
+                "kmeans_get_centroids": ([P, P, P], I32),
+                "kmeans_state_export": ([P, ct.POINTER(State)], I32),
+                "kmeans_state_import": ([P, ct.POINTER(State)], I32),
+                "kmeans_update_partials": ([P, P, P, P, P], I32),
+                "kmeans_assign_timing": ([P, ct.POINTER(D), ct.POINTER(I64)], I32),
+                "kmeans_launch_count": ([P], I64),
+                "kmeans_last_flagged": ([P, ct.POINTER(I64)], I32),
+                "kmeans_assign_path_name": ([P], ct.c_char_p),
+                "kmeans_destroy": ([P], I32),
+                "kmeans_last_error": ([P], ct.c_char_p),
+            }
+            for name, (args, res) in sig.items():
+                f = getattr(L, name)
+                f.argtypes = args
+                f.restype = res
+            _lib = L
+    return _lib
+
+
+def header_symbols():
+    """Entry points declared in include/aakm.h (for the ABI export test)."""
+    import re
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(kmeans_[a-z0-9_]+)\s*\(", txt)))
+
+
+def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000, ridge=1e-10,
+           assign_path="auto", timing=False) -> Config:
+    """Algorithm 1 settings (m0 = 5 per BASELINE configs, reading R-A18)."""
+    c = Config()
+    c.m0, c.m_max, c.eps1, c.eps2 = m0, m_max, eps1, eps2
+    c.dynamic_m, c.max_iters, c.ridge = int(dynamic_m), max_iters, ridge
+    c.assign_path = PATHS[assign_path] if isinstance(assign_path, str) else int(assign_path)
+    c.timing = int(timing)
+    return c
+
+
+def _ptr(t):
+    return ct.c_void_p(0 if t is None else t.data_ptr())
+
+
+class KMeans:
+    """One rank's handle over its row shard X (torch CUDA float32, n_local x d)."""
+
+    def __init__(self, X, K: int, cfg: Config | None = None, *, n_global: int | None = None,
+                 rank: int = 0, nranks: int = 1, group=None, stream=None):
+        import torch
+        self.torch = torch
+        L = lib()
+        if X.dtype != torch.float32 or not X.is_cuda or not X.is_contiguous() or X.dim() != 2:
+            raise ValueError("X must be a contiguous 2-D float32 CUDA tensor")
+        self.X = X
+        self.n, self.d = X.shape
+        self.K = int(K)
+        self.cfg = cfg or config()
+        self.device = X.device
+        self.stream = stream or torch.cuda.current_stream(self.device)
+        self.n_global = int(n_global if n_global is not None else self.n)
+        nbytes = ct.c_size_t()
+        self._check(L.kmeans_workspace_size(self.n, self.d, self.K, ct.byref(self.cfg), ct.byref(nbytes)), None)
+        self.ws = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=self.device)
+        base = self.ws.data_ptr()
+        self.ws_ptr = (base + 255) & ~255
+        uid = None
+        if nranks > 1:
+            import torch.distributed as dist
+            buf = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                raw = (ct.c_uint8 * 128)()
+                self._check(L.kmeans_nccl_unique_id(raw), None)
+                buf = torch.tensor(list(raw), dtype=torch.uint8)
+            bdev = buf if (group is None and dist.get_backend() == "gloo") else buf
+            if dist.get_backend(group) == "nccl":
+                bdev = buf.to(self.device)
+            dist.broadcast(bdev, src=0, group=group)
+            uid = (ct.c_uint8 * 128)(*bdev.cpu().tolist())
+        h = ct.c_void_p()
+        with torch.cuda.device(self.device):
+            self._check(L.kmeans_create(ct.byref(h), _ptr(X), self.n, self.n_global, self.d, self.K,
+                                        ct.byref(self.cfg), ct.c_void_p(self.ws_ptr), nbytes.value, rank, nranks,
+                                        uid, ct.c_void_p(self.stream.cuda_stream)), None)
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+
+    # -- helpers
+    def _check(self, rc, h):
+        if rc != 0:
+            msg = lib().kmeans_last_error(h if h is not None else None)
+            raise AAKMError(rc, msg.decode() if msg else "")
+
+    def _c(self, rc):
+        self._check(rc, self.h)
+
+    def _f32(self, C):
+        t = self.torch
+        C = t.as_tensor(C, dtype=t.float32, device=self.device).reshape(self.K, self.d).contiguous()
+        return C
+
+    def _i32(self, L):
+        t = self.torch
+        return t.as_tensor(L, dtype=t.int32, device=self.device).reshape(self.n).contiguous()
+
+    @property
+    def path(self) -> str:
+        return lib().kmeans_assign_path_name(self.h).decode()
+
+    def launch_count(self) -> int:
+        return lib().kmeans_launch_count(self.h)
+
+    # -- entry points
+    def assign(self, C, labels_prev=None):
+        """Eq. 3 labels, global E(P, C) and #changed vs labels_prev."""
+        t = self.torch
+        C = self._f32(C)
+        lp = None if labels_prev is None else self._i32(labels_prev)
+        out = t.empty(self.n, dtype=t.int32, device=self.device)
+        E, ch = ct.c_double(), ct.c_int64()
+        self._c(lib().kmeans_assign(self.h, _ptr(C), _ptr(lp), _ptr(out), ct.byref(E), ct.byref(ch)))
+        return out, E.value, ch.value
+
+    def update(self, labels, C_prev):
+        """Eq. 4 means (global), empty clusters keep C_prev; returns (G, counts)."""
+        t = self.torch
+        labels = self._i32(labels)
+        C_prev = self._f32(C_prev)
+        G = t.empty_like(C_prev)
+        cnt = t.empty(self.K, dtype=t.int64, device=self.device)
+        self._c(lib().kmeans_update(self.h, _ptr(labels), _ptr(C_prev), _ptr(G), _ptr(cnt)))
+        return G, cnt
+
+    def update_partials(self, labels, C, labels_prev=None):
+        t = self.torch
+        labels = self._i32(labels)
+        C = self._f32(C)
+        lp = None if labels_prev is None else self._i32(labels_prev)
+        out = t.empty(self.K * self.d + self.K + 2, dtype=t.float64, device=self.device)
+        self._c(lib().kmeans_update_partials(self.h, _ptr(labels), _ptr(lp), _ptr(C), _ptr(out)))
+        return out
+
+    def aa_step(self, C0=None, info=True):
+        """Algorithm 1 line 1 (C0 given) or one loop pass; returns the pass info dict (or None)."""
+        C0 = None if C0 is None else self._f32(C0)
+        if not info:
+            self._c(lib().kmeans_aa_step(self.h, _ptr(C0), None, None))
+            return None
+        inf = StepInfo()
+        theta = (ct.c_double * KMEANS_M_MAX)()
+        self._c(lib().kmeans_aa_step(self.h, _ptr(C0), ct.byref(inf), theta))
+        r = _struct(inf)
+        r["theta"] = list(theta)[: r["m_t"]]
+        return r
+
+    def run(self, C0):
+        """Algorithm 1 to convergence (rule R3); returns (C, labels, report dict)."""
+        t = self.torch
+        C0 = self._f32(C0)
+        C = t.empty_like(C0)
+        labels = t.empty(self.n, dtype=t.int32, device=self.device)
+        rep = Report()
+        self._c(lib().kmeans_run(self.h, _ptr(C0), _ptr(C), _ptr(labels), ct.byref(rep)))
+        return C, labels, _struct(rep)
+
+    def centroids(self):
+        t = self.torch
+        C = t.empty(self.K, self.d, dtype=t.float32, device=self.device)
+        lab = t.empty(self.n, dtype=t.int32, device=self.device)
+        self._c(lib().kmeans_get_centroids(self.h, _ptr(C), _ptr(lab)))
+        self.stream.synchronize()
+        return C, lab
+
+    def state_export(self):
+        H = self.cfg.m_max + 1
+        KD = self.K * self.d
+        C = np.zeros(KD, np.float32); fb = np.zeros(KD, np.float32)
+        Gh = np.zeros(H * KD, np.float32); Fh = np.zeros(H * KD, np.float32)
+        lp = np.zeros(max(self.n, 1), np.int32)
+        s = State()
+        s.C, s.fallback, s.Ghist, s.Fhist, s.labels_prev = (C.ctypes.data, fb.ctypes.data, Gh.ctypes.data,
+                                                            Fh.ctypes.data, lp.ctypes.data)
+        self._c(lib().kmeans_state_export(self.h, ct.byref(s)))
+        r = _struct(s)
+        for k in ("C", "fallback", "Ghist", "Fhist", "labels_prev"):
+            r.pop(k)
+        hc = r["hist_count"]
+        r.update(C=C.reshape(self.K, self.d), fallback=fb.reshape(self.K, self.d),
+                 Ghist=Gh.reshape(H, self.K, self.d)[:hc], Fhist=Fh.reshape(H, self.K, self.d)[:hc],
+                 labels_prev=lp[: self.n])
+        return r
+
+    def assign_timing(self):
+        ms, n = ct.c_double(), ct.c_int64()
+        self._c(lib().kmeans_assign_timing(self.h, ct.byref(ms), ct.byref(n)))
+        return ms.value, n.value
+
+    def last_flagged(self) -> int:
+        v = ct.c_int64()
+        self._c(lib().kmeans_last_flagged(self.h, ct.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().kmeans_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

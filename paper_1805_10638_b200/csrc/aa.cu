@@ -1,0 +1,391 @@
+// aa.cu -- the Anderson step and the device-side control of Algorithm 1
+// (PAPER.md:107-160), replicated on every rank from allreduced scalars.
+//
+//   k_control   convergence rule R3 (R-A10), dynamic m
+//               (R-A5..A7), energy guard (PAPER.md:142-147,
+//               R-A8, R-A9): writes the device predicates reject / done.
+//   k_finalize  G^t = Update-Step (Eq. 4; G = C + S'/N, empty -> C row,
+//               R-A15), F^t = G^t - C^t into ring slot t%H.
+//   k_gram      <dF(t), dF(tau)> and <dF(tau), F^t> for the window (Eq. 7 /
+//               PAPER.md:155; "m inner products between (Kd)-dimensional
+//               vectors"); fixed-grid fp64 partials.
+//   k_solve     fixed-order reduction of the partials, column-scaled ridge
+//               Cholesky with drop-oldest (R-A14) -> theta -> mixing weights.
+//   k_combine   C^{t+1} = G^t - sum_j theta_j (G^{t-j+1} - G^{t-j})
+//               (minus sign R-A1) = sum_j alpha_j G^{t-j},
+//               fused with the centroid prep of the next assignment
+//               (||c||^2, tf32 hi/lo split, max ||c||^2).
+//   k_advance   E^{t-2} <- E^{t-1} <- E^t, P^{t-1} <- P^t, t <- t+1, trace.
+// All reductions are fixed-order, so every rank computes identical bytes.
+#include <math.h>
+
+#include "aakm_dev.cuh"
+
+namespace aakm {
+
+// ---------------------------------------------------------------- combine
+// mode 0: mix from (st->alpha, st->alpha_slot, st->n_alpha), active if !done
+// mode 1: C <- G[st->fb_slot] (fallback C_AU^t = G^{t-1}, R-A3), active if reject
+// mode 2: C <- src (caller centroids / C^0), always
+__global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const float* src) {
+    DevState* st = d.st;
+    if (mode == 0 && st->done) return;
+    if (mode == 1 && (st->done || !st->reject)) return;
+    const int D = d.d;
+    const long long KD = (long long)d.K * D;
+    const int lane = threadIdx.x & 31;
+    const long long w0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    int na = 1;
+    double al[AAKM_H_SLOTS];
+    const float* base[AAKM_H_SLOTS];
+    if (mode == 0) {
+        na = st->n_alpha;
+        for (int q = 0; q < na; ++q) { al[q] = st->alpha[q]; base[q] = d.Gring + (long long)st->alpha_slot[q] * KD; }
+    } else if (mode == 1) {
+        al[0] = 1.0; base[0] = d.Gring + (long long)st->fb_slot * KD;
+    } else {
+        al[0] = 1.0; base[0] = src;
+    }
+    float bmax = 0.f;
+    for (long long j = w0; j < d.K; j += nw) {
+        double nrm = 0.0;
+        for (int k = lane; k < D; k += 32) {
+            const long long e = j * D + k;
+            float c;
+            if (na == 1 && al[0] == 1.0) {
+                c = base[0][e];
+            } else {
+                double v = 0.0;
+                for (int q = 0; q < na; ++q) v = fma(al[q], (double)base[q][e], v);
+                c = (float)v;
+            }
+            d.C[e] = c;
+            const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);  // tf32 truncation
+            d.Chi[e] = hi;
+            d.Clo[e] = c - hi;                                               // exact in fp32
+            nrm = fma((double)c, (double)c, nrm);
+        }
+        for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+        const float cnj = (float)nrm;
+        if (lane == 0) d.cn[j] = cnj;
+        bmax = fmaxf(bmax, cnj);
+    }
+    // max ||c||^2: per-block max -> atomicMax into cmax2_tmp; last block publishes and resets
+    for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    __shared__ float wm[32];
+    __shared__ bool last;
+    if (lane == 0) wm[threadIdx.x >> 5] = bmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, wm[i]);
+        atomicMax(&st->cmax2_tmp, __float_as_uint(m));      // non-negative floats order as uints
+        __threadfence();
+        last = atomicAdd(&st->comb_ctr, 1u) == gridDim.x - 1;
+        if (last) {
+            __threadfence();
+            st->cmax2_bits = atomicExch(&st->cmax2_tmp, 0u);
+            st->comb_ctr = 0;
+        }
+    }
+}
+
+void launch_combine(const Dev& d, int mode, const float* src, cudaStream_t s) {
+    long long warps = d.K;
+    int blocks = (int)((warps + 7) / 8);
+    if (blocks > 1184) blocks = 1184;
+    if (blocks < 1) blocks = 1;
+    k_combine<<<blocks, 256, 0, s>>>(d, mode, src);
+}
+
+// ---------------------------------------------------------------- control
+__device__ int adjust_m(int m, int m_max, double Et, double E1, double E2, double eps1, double eps2) {
+    // PAPER.md:131-138; R-A5/R-A6: only with a finite, positive previous decrease
+    const double D = E2 - E1;
+    if (!(isfinite(D) && D > 0.0)) return m;
+    const double r = (E1 - Et) / D;
+    if (r < eps1) return m > 0 ? m - 1 : 0;
+    if (r > eps2) return m < m_max ? m + 1 : m_max;
+    return m;
+}
+
+__global__ void k_control(Dev d, int stage) {
+    DevState* st = d.st;
+    if (st->done) return;
+    const long long KD = (long long)d.K * d.d;
+    if (stage == 0) {
+        const double* pk = d.packed[0];
+        const double E = pk[KD + d.K];
+        const long long ch = (long long)pk[KD + d.K + 1];
+        st->n_assign += 1;
+        st->last_flag[0] = d.flag_count[0];
+        st->reject = 0; st->accepted_now = 0; st->rejected_now = 0;
+        st->E_cand = E; st->E_final = E; st->changed = ch;
+        if (st->init_mode) return;                              // line 1: E^0 = +inf regardless
+        if (ch == 0 && st->lloyd) {                             // PAPER.md:122-125, rule R3
+            st->done = 1; st->converged = 1;
+            return;
+        }
+        if (d.dynamic_m) st->m = adjust_m(st->m, d.m_max, E, st->E1, st->E2, d.eps1, d.eps2);
+        if (!st->lloyd) {                                       // R-A9: Lloyd iterates skip the guard
+            if (E >= st->E1 || ch == 0) {                       // PAPER.md:142 (>=, R-A8); R-A10
+                st->reject = 1; st->rejected_now = 1; st->n_rejected += 1;
+                st->fb_slot = (int)((st->t - 1) % d.H);         // C_AU^t = G^{t-1} (R-A3)
+            } else {
+                st->accepted_now = 1; st->n_accepted += 1;
+            }
+        }
+    } else {
+        if (!st->reject) return;
+        const double* pk = d.packed[1];
+        const double E = pk[KD + d.K];
+        const long long ch = (long long)pk[KD + d.K + 1];
+        st->n_assign += 1;
+        st->last_flag[1] = d.flag_count[1];
+        st->E_final = E; st->changed = ch;
+        st->lloyd = 1;
+        if (ch == 0) { st->done = 1; st->converged = 1; }       // R3: re-test after the fallback
+    }
+}
+
+void launch_control(const Dev& d, int stage, cudaStream_t s) { k_control<<<1, 1, 0, s>>>(d, stage); }
+
+// ---------------------------------------------------------------- finalize
+__global__ void __launch_bounds__(256) k_finalize(Dev d) {
+    DevState* st = d.st;
+    if (st->done) return;
+    const int D = d.d;
+    const long long KD = (long long)d.K * D;
+    const double* pk = st->reject ? d.packed[1] : d.packed[0];
+    const long long slot = st->t % d.H;
+    float* G = d.Gring + slot * KD;
+    float* F = d.Fring + slot * KD;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
+         e += (long long)gridDim.x * blockDim.x) {
+        const double nj = pk[KD + e / D];
+        const float c = d.C[e];
+        const float g = nj > 0.0 ? (float)((double)c + pk[e] / nj) : c;
+        G[e] = g;
+        F[e] = g - c;                                            // F^t = G^t - C^t (fp32)
+    }
+}
+
+void launch_finalize(const Dev& d, cudaStream_t s) {
+    long long KD = (long long)d.K * d.d;
+    int blocks = (int)((KD + 255) / 256);
+    if (blocks > 1184) blocks = 1184;
+    k_finalize<<<blocks, 256, 0, s>>>(d);
+}
+
+// ---------------------------------------------------------------- gram
+// For the window tau = t, t-1, ..., t-W+1 (W = min(t, H-1)):
+//   q < W : <dF(t), dF(t-q)>,   q >= W : <dF(t-(q-W)), F^t>,
+// dF(tau) = F^tau - F^{tau-1} formed exactly in fp64 from the fp32 ring.
+__global__ void __launch_bounds__(128) k_gram(Dev d) {
+    DevState* st = d.st;
+    if (st->done || st->init_mode) return;
+    const long long t = st->t;
+    const int H = d.H;
+    const int W = (int)(t < H - 1 ? t : H - 1);
+    const long long KD = (long long)d.K * d.d;
+    double acc_g[AAKM_H_SLOTS - 1], acc_b[AAKM_H_SLOTS - 1];
+#pragma unroll
+    for (int q = 0; q < AAKM_H_SLOTS - 1; ++q) { acc_g[q] = 0.0; acc_b[q] = 0.0; }
+    const float* F[AAKM_H_SLOTS];
+    for (int q = 0; q <= W; ++q) F[q] = d.Fring + ((t - q) % H) * KD;   // F^{t-q}
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
+         e += (long long)gridDim.x * blockDim.x) {
+        const double ft = (double)F[0][e];
+        double prev = ft;
+        double dft = 0.0;
+#pragma unroll
+        for (int q = 0; q < AAKM_H_SLOTS - 1; ++q) {
+            if (q < W) {
+                const double older = (double)F[q + 1][e];
+                const double df = prev - older;                  // dF(t-q), exact
+                if (q == 0) dft = df;
+                acc_g[q] = fma(dft, df, acc_g[q]);
+                acc_b[q] = fma(df, ft, acc_b[q]);
+                prev = older;
+            }
+        }
+    }
+    __shared__ double red[4][2 * (AAKM_H_SLOTS - 1)];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int q = 0; q < W; ++q) {
+        double a = acc_g[q], b = acc_b[q];
+        for (int o = 16; o; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0) { red[w][q] = a; red[w][W + q] = b; }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < 2 * W; q += blockDim.x) {
+        double v = 0.0;
+        for (int i = 0; i < 4; ++i) v += red[i][q];
+        d.gram_part[(long long)blockIdx.x * 2 * H + q] = v;
+    }
+}
+
+void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0, s>>>(d); }
+
+// ---------------------------------------------------------------- solve
+// One warp.  Eq. (7) under reading R-A14 (see oracle ora_ls_solve for the
+// plain statement): unit-diagonal scaling, ridge, Cholesky, drop-oldest.
+__global__ void k_solve(Dev d) {
+    DevState* st = d.st;
+    if (st->done) return;
+    const int lane = threadIdx.x;
+    const int H = d.H;
+    const long long t = st->t;
+    const int init = st->init_mode;
+    const int W = init ? 0 : (int)(t < H - 1 ? t : H - 1);
+    const int ts = (int)(t % H);
+    for (int q = lane; q < 2 * W; q += 32) {
+        double v = 0.0;
+        for (int b = 0; b < d.gram_blocks; ++b) v += d.gram_part[(long long)b * 2 * H + q];
+        if (q < W) {
+            const int s2 = (int)((t - q) % H);
+            st->gram[ts * H + s2] = v;
+            st->gram[s2 * H + ts] = v;
+        } else {
+            st->bvec[q - W] = v;
+        }
+    }
+    __syncwarp();
+    __shared__ double L[AAKM_H_SLOTS][AAKM_H_SLOTS];
+    __shared__ double sc[AAKM_H_SLOTS], rhs[AAKM_H_SLOTS], y[AAKM_H_SLOTS], th[AAKM_H_SLOTS];
+    __shared__ int act[AAKM_H_SLOTS];
+    __shared__ int na_s;
+    int m_t = init ? 0 : (st->m < t ? st->m : (int)t);
+    if (m_t > W) m_t = W;
+    if (lane == 0) {
+        int na = 0;
+        for (int a = 0; a < m_t; ++a) {
+            const int sa = (int)((t - a) % H);
+            const double g = st->gram[sa * H + sa];
+            sc[a] = sqrt(g);
+            th[a] = 0.0;
+            if (sc[a] > 0.0 && isfinite(sc[a])) act[na++] = a;
+        }
+        na_s = na;
+    }
+    __syncwarp();
+    int na = na_s;
+    const double ridge = d.ridge;
+    while (na > 0) {
+        // Cholesky of Gh[act,act] + ridge I, rows owned by lanes
+        __shared__ int ok_s;
+        if (lane == 0) ok_s = 1;
+        __syncwarp();
+        for (int c = 0; c < na; ++c) {
+            if (lane == 0) {
+                const int ac = act[c];
+                const int sa = (int)((t - ac) % H);
+                double v = st->gram[sa * H + sa] / (sc[ac] * sc[ac]) + ridge;
+                for (int q = 0; q < c; ++q) v -= L[c][q] * L[c][q];
+                if (!(v > 0.0) || !isfinite(v)) ok_s = 0;
+                else L[c][c] = sqrt(v);
+            }
+            __syncwarp();
+            if (!ok_s) break;
+            for (int r = c + 1 + lane; r < na; r += 32) {
+                const int ar = act[r], ac = act[c];
+                const int sr = (int)((t - ar) % H), sc2 = (int)((t - ac) % H);
+                double v = st->gram[sr * H + sc2] / (sc[ar] * sc[ac]);
+                for (int q = 0; q < c; ++q) v -= L[r][q] * L[c][q];
+                L[r][c] = v / L[c][c];
+            }
+            __syncwarp();
+        }
+        if (!ok_s) { --na; __syncwarp(); continue; }            // drop the oldest column
+        if (lane == 0) {
+            for (int a = 0; a < na; ++a) rhs[a] = st->bvec[act[a]] / sc[act[a]];
+            for (int a = 0; a < na; ++a) {
+                double v = rhs[a];
+                for (int q = 0; q < a; ++q) v -= L[a][q] * y[q];
+                y[a] = v / L[a][a];
+            }
+            for (int a = na - 1; a >= 0; --a) {
+                double v = y[a];
+                for (int q = a + 1; q < na; ++q) v -= L[q][a] * y[q];
+                y[a] = v / L[a][a];
+            }
+            for (int a = 0; a < na; ++a) th[act[a]] = y[a] / sc[act[a]];
+        }
+        __syncwarp();
+        break;
+    }
+    if (lane == 0) {
+        // alpha_0 = 1 - theta_1, alpha_j = theta_j - theta_{j+1}, alpha_{m_t} = theta_{m_t}
+        int allzero = 1;
+        for (int a = 0; a < m_t; ++a) { st->theta[a] = th[a]; if (th[a] != 0.0) allzero = 0; }
+        st->m_t = m_t;
+        st->n_alpha = m_t + 1;
+        for (int j = 0; j <= m_t; ++j) {
+            const double tj = j >= 1 ? th[j - 1] : 0.0;
+            const double tj1 = j < m_t ? th[j] : 0.0;
+            st->alpha[j] = (j == 0 ? 1.0 : tj) - tj1;
+            st->alpha_slot[j] = (int)((t - j) % H);
+        }
+        if (allzero) { st->n_alpha = 1; st->alpha[0] = 1.0; st->alpha_slot[0] = ts; }
+        st->lloyd = allzero;
+    }
+}
+
+void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 32, 0, s>>>(d); }
+
+// ---------------------------------------------------------------- advance
+__global__ void k_advance(Dev d) {
+    DevState* st = d.st;
+    if (st->done) {
+        if (!st->final_traced) {
+            st->final_traced = 1;
+            if (!st->init_mode && st->trace_len < AAKM_TRACE_CAP) {
+                TraceRec r;
+                r.t = st->t; r.changed = st->changed; r.E_cand = st->E_cand; r.E_final = st->E_final;
+                r.m = st->m; r.m_t = 0; r.accepted = 0; r.rejected = st->rejected_now;
+                r.converged = st->converged; r.lloyd = 1;
+                d.trace[st->trace_len++] = r;
+            }
+        }
+        return;
+    }
+    if (st->init_mode) {                                   // end of Algorithm 1 line 1
+        st->init_mode = 0; st->t = 1; st->m = d.m0; st->lloyd = 1;
+        st->E1 = INFINITY; st->E2 = INFINITY;              // E^0 = +inf
+        st->hist_count = 1; st->cur ^= 1;
+        return;
+    }
+    if (st->trace_len < AAKM_TRACE_CAP) {
+        TraceRec r;
+        r.t = st->t; r.changed = st->changed; r.E_cand = st->E_cand; r.E_final = st->E_final;
+        r.m = st->m; r.m_t = st->m_t; r.accepted = st->accepted_now; r.rejected = st->rejected_now;
+        r.converged = 0; r.lloyd = st->lloyd;
+        d.trace[st->trace_len++] = r;
+    }
+    st->E2 = st->E1; st->E1 = st->E_final;
+    st->hist_count = st->hist_count + 1 < d.H ? st->hist_count + 1 : d.H;
+    st->cur ^= 1;
+    st->t += 1;
+    if (st->t > d.max_iters) { st->done = 1; st->converged = 0; st->final_traced = 1; }
+}
+
+void launch_advance(const Dev& d, cudaStream_t s) { k_advance<<<1, 1, 0, s>>>(d); }
+
+__global__ void k_reset(Dev d) {
+    DevState* st = d.st;
+    st->t = 0; st->n_accepted = 0; st->n_rejected = 0; st->n_assign = 0; st->changed = 0;
+    st->last_flag[0] = st->last_flag[1] = 0; st->trace_len = 0;
+    st->E1 = INFINITY; st->E2 = INFINITY; st->E_cand = 0.0; st->E_final = 0.0;
+    st->m = d.m0; st->m_t = 0; st->lloyd = 1; st->reject = 0;
+    st->done = 0; st->converged = 0; st->init_mode = 1;
+    st->hist_count = 0; st->accepted_now = 0; st->rejected_now = 0; st->label_error = 0;
+    st->n_alpha = 1; st->fb_slot = 0; st->final_traced = 0;
+}
+
+void launch_reset(const Dev& d, cudaStream_t s) { k_reset<<<1, 1, 0, s>>>(d); }
+
+}  // namespace aakm

@@ -1,0 +1,110 @@
+// aakm_dev.cuh -- internal declarations shared by the sm_100a kernels and the
+// host runtime of libaakm.so.  Not part of the ABI (see include/aakm.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define AAKM_H_SLOTS 32           // ring capacity >= m_max + 1 (KMEANS_M_MAX = 30)
+#define AAKM_UPD_MAX_BLOCKS 1184  // 8 x 148 SMs
+#define AAKM_GRAM_BLOCKS 148
+#define AAKM_TRACE_CAP 8192
+
+namespace aakm {
+
+// Per-pass trace record (host-readable through kmeans_step_info / report).
+struct TraceRec {
+    long long t, changed;
+    double E_cand, E_final;
+    int m, m_t, accepted, rejected, converged, lloyd;
+};
+
+// Device-resident Algorithm 1 control state.  Every
+// decision is taken on the device from allreduced scalars, so all ranks take
+// identical branches and the host never round-trips inside a pass.
+struct alignas(16) DevState {
+    long long t;                 // pass index of the current iterate C^t
+    long long n_accepted, n_rejected, n_assign;
+    long long changed;           // #changed labels of the final P^t
+    long long last_flag[2];      // near-tie rows of the last assignments A / B (diagnostics)
+    long long trace_len;
+    double E1, E2;               // E^{t-1}, E^{t-2}, post-guard (R-A7)
+    double E_cand, E_final;      // E^t before / after the guard
+    int m, m_t, lloyd, reject;
+    int done, converged, cur, init_mode;
+    int hist_count, accepted_now, rejected_now, label_error;
+    int n_alpha, fb_slot, final_traced, pad0;
+    unsigned int cmax2_bits;     // max_j ||c_j||^2 of the centroids being assigned (float bits)
+    unsigned int cmax2_tmp, comb_ctr, upd_ctr;
+    double theta[AAKM_H_SLOTS];
+    double alpha[AAKM_H_SLOTS];
+    int alpha_slot[AAKM_H_SLOTS];
+    double gram[AAKM_H_SLOTS * AAKM_H_SLOTS];  // <dF(tau_a), dF(tau_b)>, slot-indexed (tau mod H)
+    double bvec[AAKM_H_SLOTS];                 // <dF(t-j+1), F^t>, j = 1..W
+};
+
+// Everything a kernel needs, passed by value.
+struct Dev {
+    const float* X;       // n x d samples (borrowed)
+    long long n;          // local rows
+    int d, K, H, m_max, m0, dynamic_m;
+    long long max_iters;
+    double eps1, eps2, ridge;
+    DevState* st;
+    float* C;             // current iterate C^t (K x d)
+    float* Chi;           // tf32(C) (tensor path)
+    float* Clo;           // C - tf32(C)
+    float* cn;            // ||c_j||^2 (fp32, from fp64)
+    int* lab[2];          // label ping-pong, lab[cur] = P^t, lab[cur^1] = P^{t-1}
+    int* flag_rows;       // near-tie row list (capacity n)
+    long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
+    double* packed[2];    // [S' (K*d) | N (K) | E | changed], branch A / B
+    double* upd_part;     // per-block (E, changed) partials
+    float* Gring;         // H x K*d
+    float* Fring;         // H x K*d
+    double* gram_part;    // AAKM_GRAM_BLOCKS x (2*H)
+    TraceRec* trace;
+    int nranks;
+    int upd_blocks;
+    int gram_blocks;
+    float tau_gamma;      // near-tie threshold factor of the active assignment engine
+};
+
+// Which labels/centroids a G-evaluation kernel works on.
+struct GEval {
+    int branch;           // 0 = candidate C^t, 1 = fallback C_AU^t (predicated on reject)
+    int force;            // 1 = run regardless of done/reject (API calls)
+    int* lab_out;         // nullptr -> d.lab[st->cur]
+    const int* lab_prev;  // used when prev_mode == 2
+    int prev_mode;        // 0 = d.lab[st->cur ^ 1], 1 = none, 2 = lab_prev
+    const float* Cassign; // nullptr -> d.C
+    double* packed_out;   // nullptr -> d.packed[branch]
+};
+
+__device__ __forceinline__ bool geval_active(const Dev& d, const GEval& g) {
+    if (g.force) return true;
+    const volatile DevState* st = d.st;
+    if (st->done) return false;
+    return g.branch == 0 || st->reject;
+}
+
+// ---- launchers (host side, defined in the .cu files) ----
+void launch_combine(const Dev& d, int mode, const float* src, cudaStream_t s);
+void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s);
+void launch_assign_tc(const Dev& d, const GEval& g, cudaStream_t s);
+bool tc_supported(int d, int K);
+void launch_refine(const Dev& d, const GEval& g, cudaStream_t s);
+void launch_update(const Dev& d, const GEval& g, cudaStream_t s);
+void launch_control(const Dev& d, int stage, cudaStream_t s);
+void launch_finalize(const Dev& d, cudaStream_t s);
+void launch_gram(const Dev& d, cudaStream_t s);
+void launch_solve(const Dev& d, cudaStream_t s);
+void launch_advance(const Dev& d, cudaStream_t s);
+void launch_reset(const Dev& d, cudaStream_t s);
+void launch_update_G(const Dev& d, const double* packed, const float* Cprev, float* G,
+                     long long* counts, cudaStream_t s);
+
+// error-bound factors of the two engines
+float tau_gamma_simt(int d);
+float tau_gamma_tc(int d);
+
+}  // namespace aakm

@@ -1,0 +1,607 @@
+// runtime.cu -- host runtime + C ABI of libaakm.so (include/aakm.h).
+//
+// One Algorithm 1 pass is enqueued as a fixed kernel
+// sequence whose data-dependent branches (converge / reject) are device
+// predicates (aa.cu), so the same sequence can be launched eagerly or
+// captured once into a CUDA graph and replayed until the device sets `done`.
+// Multi-rank: one ncclAllReduce(sum, fp64) of the packed [S'|N|E|changed]
+// vector per G-evaluation, issued in-stream (and captured in the graph).
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/aakm.h"
+#include "aakm_dev.cuh"
+
+using namespace aakm;
+
+struct kmeans_handle {
+    Dev d;          // Algorithm 1 state and buffers
+    Dev da;         // API calls (assign/update): own DevState + centroid buffers
+    kmeans_config cfg;
+    cudaStream_t stream = nullptr;
+    int rank = 0, nranks = 1;
+    long long n_global = 0;
+    ncclComm_t comm = nullptr;
+    bool poisoned = false;
+    std::string err;
+    int path = KMEANS_PATH_SIMT;
+    size_t scratch_bytes = 0;
+    void* scratch = nullptr;
+    cudaGraphExec_t pass_exec = nullptr;
+    long long launches = 0;
+    long long kernels_per_pass = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // assignment timing (branch A)
+    size_t ev_used = 0;
+    DevState* st_host = nullptr;                             // pinned
+    TraceRec* tr_host = nullptr;                             // pinned
+    double* scal_host = nullptr;                             // pinned (E, changed)
+    cudaEvent_t run_ev[2] = {nullptr, nullptr};
+    int* done_host = nullptr;                                // pinned
+};
+
+static thread_local std::string g_create_err;
+
+#define FAIL(h, code, msg)                    \
+    do {                                      \
+        (h)->err = (msg);                     \
+        if ((code) == KMEANS_ERR_CUDA || (code) == KMEANS_ERR_NCCL) (h)->poisoned = true; \
+        return (code);                        \
+    } while (0)
+
+#define CK(h, call)                                                                        \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            (h)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+            (h)->poisoned = true;                                                          \
+            return KMEANS_ERR_CUDA;                                                        \
+        }                                                                                  \
+    } while (0)
+
+#define NK(h, call)                                                                        \
+    do {                                                                                   \
+        ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess) {                                                           \
+            (h)->err = std::string(#call) + ": " + ncclGetErrorString(r_);                 \
+            (h)->poisoned = true;                                                          \
+            return KMEANS_ERR_NCCL;                                                        \
+        }                                                                                  \
+    } while (0)
+
+#define LIVE(h)                                                                            \
+    do {                                                                                   \
+        if (!(h)) return KMEANS_ERR_INVALID;                                               \
+        if ((h)->poisoned) { (h)->err = "handle poisoned by an earlier CUDA/NCCL error"; return KMEANS_ERR_STATE; } \
+    } while (0)
+
+// ------------------------------------------------------------------ layout
+namespace {
+struct Layout {
+    size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, lab0, lab1, flags, scratch, packed1,
+        upd_part, Gring, Fring, gram_part, trace, total, scratch_bytes;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout layout(long long n, int d, int K, int m_max) {
+    Layout L;
+    size_t o = 0;
+    const size_t KD = (size_t)K * d;
+    const int H = m_max + 1;
+    auto take = [&](size_t bytes) { size_t r = o; o = al(o + bytes); return r; };
+    L.st = take(sizeof(DevState));
+    L.st_api = take(sizeof(DevState));
+    L.C = take(KD * 4); L.Chi = take(KD * 4); L.Clo = take(KD * 4); L.cn = take((size_t)K * 4);
+    L.Ca = take(KD * 4); L.Cahi = take(KD * 4); L.Calo = take(KD * 4); L.cna = take((size_t)K * 4);
+    L.lab0 = take((size_t)n * 4); L.lab1 = take((size_t)n * 4);
+    L.flags = take((size_t)n * 4 + 4);
+    const size_t pk = (KD + K + 2) * 8;
+    L.scratch = o;
+    size_t s0 = take(256);                 // flag counts
+    (void)s0;
+    take(pk);                              // packed[0]
+    L.packed1 = take(pk);                  // packed[1]
+    L.scratch_bytes = o - L.scratch;
+    L.upd_part = take((size_t)AAKM_UPD_MAX_BLOCKS * 16);
+    L.Gring = take((size_t)H * KD * 4);
+    L.Fring = take((size_t)H * KD * 4);
+    L.gram_part = take((size_t)AAKM_GRAM_BLOCKS * 2 * AAKM_H_SLOTS * 8);
+    L.trace = take((size_t)AAKM_TRACE_CAP * sizeof(TraceRec));
+    L.total = o;
+    return L;
+}
+
+kmeans_status validate(long long n_local, int d, int k, const kmeans_config* cfg, std::string& why) {
+    if (!cfg) { why = "cfg is NULL"; return KMEANS_ERR_INVALID; }
+    if (n_local < 0) { why = "n_local < 0"; return KMEANS_ERR_INVALID; }
+    if (n_local > 0x7fffffffLL) { why = "n_local > 2^31-1 rows per rank"; return KMEANS_ERR_INVALID; }
+    if (d < 1) { why = "d < 1"; return KMEANS_ERR_INVALID; }
+    if (d > 4096) { why = "d > 4096 unsupported"; return KMEANS_ERR_INVALID; }
+    if (k < 1) { why = "k < 1"; return KMEANS_ERR_INVALID; }
+    if (cfg->m_max < 0 || cfg->m_max > KMEANS_M_MAX) { why = "m_max outside [0, 30]"; return KMEANS_ERR_INVALID; }
+    if (cfg->m0 < 0 || cfg->m0 > cfg->m_max) { why = "m0 outside [0, m_max]"; return KMEANS_ERR_INVALID; }
+    if (!(cfg->eps1 >= 0.0) || !(cfg->eps1 < cfg->eps2)) { why = "need 0 <= eps1 < eps2"; return KMEANS_ERR_INVALID; }
+    if (cfg->max_iters < 1) { why = "max_iters < 1"; return KMEANS_ERR_INVALID; }
+    if (!(cfg->ridge >= 0.0)) { why = "ridge < 0"; return KMEANS_ERR_INVALID; }
+    if (cfg->assign_path < 0 || cfg->assign_path > 2) { why = "bad assign_path"; return KMEANS_ERR_INVALID; }
+    if (cfg->assign_path == KMEANS_PATH_TC && !tc_supported(d, k)) {
+        why = "tensor-core path needs d % 32 == 0 and d <= 128"; return KMEANS_ERR_INVALID;
+    }
+    return KMEANS_OK;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ enqueue helpers
+static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
+    if (h->path == KMEANS_PATH_TC) launch_assign_tc(d, g, s);
+    else launch_assign_simt(d, g, s);
+}
+
+static kmeans_status allreduce(kmeans_handle* h, double* buf, cudaStream_t s) {
+    if (h->nranks <= 1) return KMEANS_OK;
+    const size_t cnt = (size_t)h->d.K * h->d.d + h->d.K + 2;
+    NK(h, ncclAllReduce(buf, buf, cnt, ncclFloat64, ncclSum, h->comm, s));
+    return KMEANS_OK;
+}
+
+// One G-evaluation (assign -> refine -> update partials -> allreduce -> control).
+static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool timing) {
+    const Dev& d = h->d;
+    GEval g{};
+    g.branch = branch; g.force = 0; g.prev_mode = 0;
+    if (branch == 1) { launch_combine(d, 1, nullptr, s); h->launches++; }
+    std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
+    if (timing && branch == 0) {
+        if (h->ev_used == h->ev.size()) {
+            cudaEvent_t a, b;
+            CK(h, cudaEventCreate(&a)); CK(h, cudaEventCreate(&b));
+            h->ev.push_back({a, b});
+        }
+        evp = &h->ev[h->ev_used++];
+        CK(h, cudaEventRecord(evp->first, s));
+    }
+    assign_engine(h, d, g, s);
+    if (evp) CK(h, cudaEventRecord(evp->second, s));
+    launch_refine(d, g, s);
+    launch_update(d, g, s);
+    h->launches += 3;
+    kmeans_status st = allreduce(h, d.packed[branch], s);
+    if (st != KMEANS_OK) return st;
+    launch_control(d, branch, s);
+    h->launches += 1;
+    return KMEANS_OK;
+}
+
+// One loop pass of Algorithm 1 (also used for line 1 when init_mode is set).
+static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing) {
+    const Dev& d = h->d;
+    CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+    kmeans_status st = geval(h, 0, s, timing);
+    if (st != KMEANS_OK) return st;
+    st = geval(h, 1, s, false);
+    if (st != KMEANS_OK) return st;
+    launch_finalize(d, s);
+    launch_gram(d, s);
+    launch_solve(d, s);
+    launch_combine(d, 0, nullptr, s);
+    launch_advance(d, s);
+    h->launches += 5;
+    CK(h, cudaGetLastError());
+    return KMEANS_OK;
+}
+
+static kmeans_status ensure_graph(kmeans_handle* h) {
+    if (h->pass_exec) return KMEANS_OK;
+    cudaGraph_t g;
+    long long before = h->launches;
+    CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    kmeans_status st = enqueue_pass(h, h->stream, false);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (st != KMEANS_OK) return st;
+    CK(h, e);
+    CK(h, cudaGraphInstantiate(&h->pass_exec, g, 0));
+    CK(h, cudaGraphDestroy(g));
+    h->kernels_per_pass = h->launches - before;
+    h->launches = before;
+    return KMEANS_OK;
+}
+
+static kmeans_status start(kmeans_handle* h, const float* C0) {
+    launch_reset(h->d, h->stream);
+    launch_combine(h->d, 2, C0, h->stream);
+    h->launches += 2;
+    return enqueue_pass(h, h->stream, h->cfg.timing != 0);   // Algorithm 1 line 1
+}
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+int32_t kmeans_abi_version(void) { return KMEANS_ABI_VERSION; }
+
+kmeans_status kmeans_config_default(kmeans_config* cfg) {
+    if (!cfg) return KMEANS_ERR_INVALID;
+    memset(cfg, 0, sizeof(*cfg));
+    cfg->m0 = 2; cfg->m_max = 30; cfg->eps1 = 0.02; cfg->eps2 = 0.5;
+    cfg->dynamic_m = 1; cfg->max_iters = 10000; cfg->ridge = 1e-10;
+    cfg->assign_path = KMEANS_PATH_AUTO; cfg->timing = 0;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_workspace_size(int64_t n_local, int32_t d, int32_t k, const kmeans_config* cfg,
+                                    size_t* bytes) {
+    std::string why;
+    if (!bytes) return KMEANS_ERR_INVALID;
+    kmeans_status s = validate(n_local, d, k, cfg, why);
+    if (s != KMEANS_OK) { g_create_err = why; return s; }
+    *bytes = layout(n_local, d, k, cfg->m_max).total;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_nccl_unique_id(void* uid128) {
+    if (!uid128) return KMEANS_ERR_INVALID;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) { g_create_err = "ncclGetUniqueId failed"; return KMEANS_ERR_NCCL; }
+    static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+    memcpy(uid128, &id, 128);
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local, int64_t n_global,
+                            int32_t d, int32_t k, const kmeans_config* cfg, void* workspace,
+                            size_t workspace_bytes, int32_t rank, int32_t nranks, const void* uid128,
+                            kmeans_stream_t stream) {
+    std::string why;
+    if (!out) { g_create_err = "out is NULL"; return KMEANS_ERR_INVALID; }
+    *out = nullptr;
+    kmeans_status vs = validate(n_local, d, k, cfg, why);
+    if (vs != KMEANS_OK) { g_create_err = why; return vs; }
+    if ((!X && n_local > 0) || !workspace) { g_create_err = "X or workspace is NULL"; return KMEANS_ERR_INVALID; }
+    if (nranks < 1 || rank < 0 || rank >= nranks) { g_create_err = "bad rank/nranks"; return KMEANS_ERR_INVALID; }
+    if ((nranks == 1) != (uid128 == nullptr)) { g_create_err = "uid128 must be NULL iff nranks == 1"; return KMEANS_ERR_INVALID; }
+    if (n_global < n_local || k > n_global) { g_create_err = "need n_local <= n_global and k <= n_global"; return KMEANS_ERR_INVALID; }
+    if (((uintptr_t)workspace & 255) != 0) { g_create_err = "workspace must be 256-byte aligned"; return KMEANS_ERR_INVALID; }
+    Layout L = layout(n_local, d, k, cfg->m_max);
+    if (workspace_bytes < L.total) { g_create_err = "workspace too small"; return KMEANS_ERR_INVALID; }
+
+    kmeans_handle* h = new kmeans_handle();
+    h->cfg = *cfg;
+    h->stream = (cudaStream_t)stream;
+    h->rank = rank; h->nranks = nranks; h->n_global = n_global;
+    h->path = cfg->assign_path == KMEANS_PATH_AUTO ? (tc_supported(d, k) ? KMEANS_PATH_TC : KMEANS_PATH_SIMT)
+                                                   : cfg->assign_path;
+    char* w = (char*)workspace;
+    Dev& D = h->d;
+    memset(&D, 0, sizeof(D));
+    D.X = X; D.n = n_local; D.d = d; D.K = k; D.H = cfg->m_max + 1; D.m_max = cfg->m_max; D.m0 = cfg->m0;
+    D.dynamic_m = cfg->dynamic_m; D.max_iters = cfg->max_iters; D.eps1 = cfg->eps1; D.eps2 = cfg->eps2;
+    D.ridge = cfg->ridge;
+    D.st = (DevState*)(w + L.st);
+    D.C = (float*)(w + L.C); D.Chi = (float*)(w + L.Chi); D.Clo = (float*)(w + L.Clo); D.cn = (float*)(w + L.cn);
+    D.lab[0] = (int*)(w + L.lab0); D.lab[1] = (int*)(w + L.lab1);
+    D.flag_rows = (int*)(w + L.flags);
+    D.flag_count = (long long*)(w + L.scratch);
+    D.packed[0] = (double*)(w + L.scratch + 256);
+    D.packed[1] = (double*)(w + L.packed1);
+    D.upd_part = (double*)(w + L.upd_part);
+    D.Gring = (float*)(w + L.Gring); D.Fring = (float*)(w + L.Fring);
+    D.gram_part = (double*)(w + L.gram_part);
+    D.trace = (TraceRec*)(w + L.trace);
+    D.nranks = nranks;
+    {
+        long long KD = (long long)k * d;
+        long long smem_bytes = KD * 8 + (long long)k * 4;
+        long long ub;
+        if (smem_bytes <= 160 * 1024) {
+            ub = (n_local + 1023) / 1024;          // >= ~1K rows per block amortises the flush
+            if (ub > 296) ub = 296;
+        } else {
+            ub = (n_local + 255) / 256;
+            if (ub > AAKM_UPD_MAX_BLOCKS) ub = AAKM_UPD_MAX_BLOCKS;
+        }
+        D.upd_blocks = (int)(ub < 1 ? 1 : ub);
+        long long gb = (KD + 127) / 128;
+        D.gram_blocks = (int)(gb > AAKM_GRAM_BLOCKS ? AAKM_GRAM_BLOCKS : (gb < 1 ? 1 : gb));
+    }
+    D.tau_gamma = h->path == KMEANS_PATH_TC ? tau_gamma_tc(d) : tau_gamma_simt(d);
+    h->da = D;
+    h->da.st = (DevState*)(w + L.st_api);
+    h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
+    h->da.cn = (float*)(w + L.cna);
+    h->scratch = w + L.scratch;
+    h->scratch_bytes = L.scratch_bytes;
+
+#define CKC(call)                                                                         \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            g_create_err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+            delete h;                                                                     \
+            return KMEANS_ERR_CUDA;                                                       \
+        }                                                                                 \
+    } while (0)
+    CKC(cudaMallocHost(&h->st_host, sizeof(DevState)));
+    CKC(cudaMallocHost(&h->tr_host, sizeof(TraceRec) * 2));
+    CKC(cudaMallocHost(&h->scal_host, 64));
+    CKC(cudaMallocHost(&h->done_host, 64));
+    CKC(cudaEventCreate(&h->run_ev[0]));
+    CKC(cudaEventCreate(&h->run_ev[1]));
+    CKC(cudaMemsetAsync(w + L.st, 0, sizeof(DevState), h->stream));
+    CKC(cudaMemsetAsync(w + L.st_api, 0, sizeof(DevState), h->stream));
+    CKC(cudaMemsetAsync(w + L.upd_part, 0, (size_t)AAKM_UPD_MAX_BLOCKS * 16, h->stream));
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, uid128, 128);
+        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            g_create_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            delete h;
+            return KMEANS_ERR_NCCL;
+        }
+    }
+    CKC(cudaStreamSynchronize(h->stream));
+#undef CKC
+    *out = h;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* labels_prev, int32_t* labels_out,
+                            double* energy_out, int64_t* changed_out) {
+    LIVE(h);
+    if (!C || (!labels_out && h->d.n > 0)) FAIL(h, KMEANS_ERR_INVALID, "C or labels_out is NULL");
+    cudaStream_t s = h->stream;
+    const Dev& d = h->da;
+    CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+    launch_combine(d, 2, C, s);
+    GEval g{};
+    g.branch = 0; g.force = 1; g.lab_out = labels_out;
+    g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
+    assign_engine(h, d, g, s);
+    launch_refine(d, g, s);
+    launch_update(d, g, s);
+    h->launches += 4;
+    kmeans_status st = allreduce(h, d.packed[0], s);
+    if (st != KMEANS_OK) return st;
+    const long long KD = (long long)d.K * d.d;
+    CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + KD + d.K, 16, cudaMemcpyDeviceToHost, s));
+    CK(h, cudaMemcpyAsync(h->scal_host + 2, d.flag_count, 8, cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    CK(h, cudaGetLastError());
+    if (energy_out) *energy_out = h->scal_host[0];
+    if (changed_out) *changed_out = labels_prev ? (int64_t)h->scal_host[1] : 0;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const float* C_prev, float* G_out,
+                            int64_t* counts_out) {
+    LIVE(h);
+    if ((!labels && h->d.n > 0) || !C_prev || !G_out) FAIL(h, KMEANS_ERR_INVALID, "NULL labels/C_prev/G_out");
+    cudaStream_t s = h->stream;
+    const Dev& d = h->da;
+    CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+    CK(h, cudaMemsetAsync(&d.st->label_error, 0, sizeof(int), s));
+    GEval g{};
+    g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels); g.prev_mode = 1; g.Cassign = C_prev;
+    launch_update(d, g, s);
+    h->launches += 1;
+    kmeans_status st = allreduce(h, d.packed[0], s);
+    if (st != KMEANS_OK) return st;
+    launch_update_G(d, d.packed[0], C_prev, G_out, (long long*)counts_out, s);
+    h->launches += 1;
+    CK(h, cudaMemcpyAsync(h->done_host, &d.st->label_error, 4, cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    CK(h, cudaGetLastError());
+    if (*h->done_host) FAIL(h, KMEANS_ERR_INVALID, "labels outside [0, K)");
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, const int32_t* labels_prev,
+                                     const float* C, double* packed_out) {
+    LIVE(h);
+    if ((!labels && h->d.n > 0) || !C || !packed_out) FAIL(h, KMEANS_ERR_INVALID, "NULL argument");
+    cudaStream_t s = h->stream;
+    const Dev& d = h->da;
+    const size_t bytes = ((size_t)d.K * d.d + d.K + 2) * 8;
+    CK(h, cudaMemsetAsync(packed_out, 0, bytes, s));
+    GEval g{};
+    g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels);
+    g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev; g.Cassign = C; g.packed_out = packed_out;
+    launch_update(d, g, s);
+    h->launches += 1;
+    CK(h, cudaStreamSynchronize(s));
+    CK(h, cudaGetLastError());
+    return KMEANS_OK;
+}
+
+static void fill_info(kmeans_handle* h, kmeans_step_info* info, double* theta) {
+    const DevState& S = *h->st_host;
+    const TraceRec& r = h->tr_host[0];
+    if (info) {
+        memset(info, 0, sizeof(*info));
+        if (S.trace_len > 0) {
+            info->t = r.t; info->m = r.m; info->m_t = r.m_t; info->accepted = r.accepted;
+            info->rejected = r.rejected; info->converged = r.converged; info->lloyd = r.lloyd;
+            info->energy_cand = r.E_cand; info->energy = r.E_final; info->changed = r.changed;
+        } else {   // after line 1
+            info->t = 0; info->m = S.m; info->lloyd = 1; info->energy_cand = S.E_cand;
+            info->energy = S.E_final;
+        }
+    }
+    if (theta) {
+        for (int j = 0; j < h->d.m_max; ++j) theta[j] = j < S.m_t ? S.theta[j] : 0.0;
+    }
+}
+
+kmeans_status kmeans_aa_step(kmeans_handle* h, const float* C0, kmeans_step_info* info, double* theta_out) {
+    LIVE(h);
+    kmeans_status st;
+    if (C0) st = start(h, C0);
+    else st = enqueue_pass(h, h->stream, h->cfg.timing != 0);
+    if (st != KMEANS_OK) return st;
+    if (info || theta_out) {
+        cudaStream_t s = h->stream;
+        CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(h, cudaStreamSynchronize(s));
+        const long long n = h->st_host->trace_len;
+        if (n > 0)
+            CK(h, cudaMemcpy(h->tr_host, h->d.trace + (n - 1), sizeof(TraceRec), cudaMemcpyDeviceToHost));
+        fill_info(h, info, theta_out);
+    }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_run(kmeans_handle* h, const float* C0, float* C_out, int32_t* labels_out, kmeans_report* rep) {
+    LIVE(h);
+    if (!C0 || !rep) FAIL(h, KMEANS_ERR_INVALID, "C0 or rep is NULL");
+    cudaStream_t s = h->stream;
+    kmeans_status st = ensure_graph(h);
+    if (st != KMEANS_OK) return st;
+    CK(h, cudaEventRecord(h->run_ev[0], s));
+    st = start(h, C0);
+    if (st != KMEANS_OK) return st;
+    int batch = 4;
+    long long passes = 0;
+    while (true) {
+        for (int i = 0; i < batch; ++i) {
+            CK(h, cudaGraphLaunch(h->pass_exec, s));
+            h->launches += h->kernels_per_pass;
+        }
+        passes += batch;
+        CK(h, cudaMemcpyAsync(h->done_host, &h->d.st->done, 4, cudaMemcpyDeviceToHost, s));
+        CK(h, cudaStreamSynchronize(s));
+        if (*h->done_host) break;
+        if (passes > (long long)h->cfg.max_iters + 8) FAIL(h, KMEANS_ERR_STATE, "run did not terminate");
+        if (batch < 16) batch *= 2;
+    }
+    CK(h, cudaEventRecord(h->run_ev[1], s));
+    if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 4, cudaMemcpyDeviceToDevice, s));
+    CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    const DevState& S = *h->st_host;
+    if (labels_out && h->d.n > 0)
+        CK(h, cudaMemcpyAsync(labels_out, h->d.lab[S.cur], (size_t)h->d.n * 4, cudaMemcpyDeviceToDevice, s));
+    float ms = 0.f;
+    CK(h, cudaEventElapsedTime(&ms, h->run_ev[0], h->run_ev[1]));
+    CK(h, cudaStreamSynchronize(s));
+    memset(rep, 0, sizeof(*rep));
+    rep->converged = S.converged;
+    rep->iters = S.converged ? S.t + 1 : S.t;
+    rep->n_rejected = S.n_rejected;
+    rep->n_accepted = S.n_accepted;
+    rep->n_assign = S.n_assign;
+    rep->m_final = S.m;
+    rep->energy = S.E_final;
+    rep->mse = S.E_final / (double)h->n_global;
+    rep->seconds = ms / 1e3;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_get_centroids(kmeans_handle* h, float* C_out, int32_t* labels_out) {
+    LIVE(h);
+    cudaStream_t s = h->stream;
+    if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 4, cudaMemcpyDeviceToDevice, s));
+    if (labels_out) {
+        CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(h, cudaStreamSynchronize(s));
+        // after a pass the last assignment is P^t = lab[cur ^ 1] unless the run stopped (done)
+        const DevState& S = *h->st_host;
+        int which = S.done ? S.cur : (S.cur ^ 1);
+        CK(h, cudaMemcpyAsync(labels_out, h->d.lab[which], (size_t)h->d.n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_state_export(kmeans_handle* h, kmeans_state* out) {
+    LIVE(h);
+    if (!out) FAIL(h, KMEANS_ERR_INVALID, "NULL state");
+    cudaStream_t s = h->stream;
+    CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    const DevState& S = *h->st_host;
+    const Dev& d = h->d;
+    const size_t KD = (size_t)d.K * d.d;
+    out->hist_count = S.hist_count; out->m = S.m; out->lloyd = S.lloyd; out->done = S.done; out->t = S.t;
+    out->E1 = S.E1; out->E2 = S.E2;
+    out->n_accepted = S.n_accepted; out->n_rejected = S.n_rejected; out->n_assign = S.n_assign;
+    if (out->C) CK(h, cudaMemcpy(out->C, d.C, KD * 4, cudaMemcpyDeviceToHost));
+    // between passes the newest history entry is (G^{t-1}, F^{t-1})
+    for (int j = 0; j < S.hist_count; ++j) {
+        const long long slot = ((S.t - 1 - j) % d.H + d.H) % d.H;
+        if (out->Ghist) CK(h, cudaMemcpy(out->Ghist + j * KD, d.Gring + slot * KD, KD * 4, cudaMemcpyDeviceToHost));
+        if (out->Fhist) CK(h, cudaMemcpy(out->Fhist + j * KD, d.Fring + slot * KD, KD * 4, cudaMemcpyDeviceToHost));
+    }
+    if (out->fallback && S.hist_count > 0) {
+        const long long slot = ((S.t - 1) % d.H + d.H) % d.H;
+        CK(h, cudaMemcpy(out->fallback, d.Gring + slot * KD, KD * 4, cudaMemcpyDeviceToHost));
+    }
+    if (out->labels_prev && d.n > 0) {
+        const int which = S.done ? (S.cur ^ 1) : (S.cur ^ 1);
+        CK(h, cudaMemcpy(out->labels_prev, d.lab[which], (size_t)d.n * 4, cudaMemcpyDeviceToHost));
+    }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
+    LIVE(h);
+    (void)st;
+    FAIL(h, KMEANS_ERR_INVALID, "kmeans_state_import is not implemented in this build");
+}
+
+kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* launches) {
+    LIVE(h);
+    CK(h, cudaStreamSynchronize(h->stream));
+    double tot = 0.0;
+    for (size_t i = 0; i < h->ev_used; ++i) {
+        float ms = 0.f;
+        CK(h, cudaEventElapsedTime(&ms, h->ev[i].first, h->ev[i].second));
+        tot += ms;
+    }
+    if (ms_total) *ms_total = tot;
+    if (launches) *launches = (int64_t)h->ev_used;
+    h->ev_used = 0;
+    return KMEANS_OK;
+}
+
+int64_t kmeans_launch_count(const kmeans_handle* h) { return h ? h->launches : 0; }
+
+kmeans_status kmeans_last_flagged(kmeans_handle* h, int64_t* flagged) {
+    LIVE(h);
+    if (!flagged) return KMEANS_ERR_INVALID;
+    long long v[2];
+    CK(h, cudaStreamSynchronize(h->stream));
+    CK(h, cudaMemcpy(v, h->d.flag_count, 16, cudaMemcpyDeviceToHost));
+    *flagged = v[0];
+    return KMEANS_OK;
+}
+
+const char* kmeans_assign_path_name(const kmeans_handle* h) {
+    if (!h) return "none";
+    return h->path == KMEANS_PATH_TC ? "tc" : "simt";
+}
+
+kmeans_status kmeans_destroy(kmeans_handle* h) {
+    if (!h) return KMEANS_ERR_INVALID;
+    if (!h->poisoned) cudaStreamSynchronize(h->stream);
+    if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
+    for (auto& e : h->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    if (h->run_ev[0]) cudaEventDestroy(h->run_ev[0]);
+    if (h->run_ev[1]) cudaEventDestroy(h->run_ev[1]);
+    if (h->st_host) cudaFreeHost(h->st_host);
+    if (h->tr_host) cudaFreeHost(h->tr_host);
+    if (h->scal_host) cudaFreeHost(h->scal_host);
+    if (h->done_host) cudaFreeHost(h->done_host);
+    if (h->comm) ncclCommDestroy(h->comm);
+    delete h;
+    return KMEANS_OK;
+}
+
+const char* kmeans_last_error(const kmeans_handle* h) {
+    if (!h) return g_create_err.c_str();
+    return h->err.c_str();
+}
+
+}  // extern "C"
