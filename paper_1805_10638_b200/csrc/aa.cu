@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(128) k_gram(Dev d) {
             }
         }
     }
-    __shared__ double red[4][2 * (AAKM_H_SLOTS - 1)];
+    __shared__ __align__(16) double red[4][2 * (AAKM_H_SLOTS - 1)];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int q = 0; q < W; ++q) {
         double a = acc_g[q], b = acc_b[q];
@@ -234,7 +234,10 @@ void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0,
 // ---------------------------------------------------------------- solve
 // One warp.  Eq. (7) under reading R-A14 (see oracle ora_ls_solve for the
 // plain statement): unit-diagonal scaling, ridge, Cholesky, drop-oldest.
-__global__ void k_solve(Dev d) {
+// Lane r owns row r of the Cholesky factor in registers (compile-time
+// indexed, fully unrolled); columns move between lanes with shuffles.
+#define FULL 0xffffffffu
+__global__ void __launch_bounds__(32) k_solve(Dev d) {
     DevState* st = d.st;
     if (st->done) return;
     const int lane = threadIdx.x;
@@ -243,6 +246,7 @@ __global__ void k_solve(Dev d) {
     const int init = st->init_mode;
     const int W = init ? 0 : (int)(t < H - 1 ? t : H - 1);
     const int ts = (int)(t % H);
+    // fixed-order reduction of the Gram partials of this pass
     for (int q = lane; q < 2 * W; q += 32) {
         double v = 0.0;
         for (int b = 0; b < d.gram_blocks; ++b) v += d.gram_part[(long long)b * 2 * H + q];
@@ -254,86 +258,130 @@ __global__ void k_solve(Dev d) {
             st->bvec[q - W] = v;
         }
     }
+    __threadfence_block();
     __syncwarp();
-    __shared__ double L[AAKM_H_SLOTS][AAKM_H_SLOTS];
-    __shared__ double sc[AAKM_H_SLOTS], rhs[AAKM_H_SLOTS], y[AAKM_H_SLOTS], th[AAKM_H_SLOTS];
-    __shared__ int act[AAKM_H_SLOTS];
-    __shared__ int na_s;
     int m_t = init ? 0 : (st->m < t ? st->m : (int)t);
     if (m_t > W) m_t = W;
-    if (lane == 0) {
-        int na = 0;
-        for (int a = 0; a < m_t; ++a) {
-            const int sa = (int)((t - a) % H);
-            const double g = st->gram[sa * H + sa];
-            sc[a] = sqrt(g);
-            th[a] = 0.0;
-            if (sc[a] > 0.0 && isfinite(sc[a])) act[na++] = a;
-        }
-        na_s = na;
+    // column a <-> dF(t - a); lane a holds column a's scale and rhs
+    const int sa = (int)((((t - lane) % H) + H) % H);
+    double s_a = 0.0, b_a = 0.0;
+    bool act = false;
+    if (lane < m_t) {
+        s_a = sqrt(st->gram[sa * H + sa]);
+        act = s_a > 0.0 && isfinite(s_a);
+        b_a = act ? st->bvec[lane] / s_a : 0.0;
     }
-    __syncwarp();
-    int na = na_s;
+    // compact the active columns (newest first): lane i <- column idx[i]
+    const unsigned am = __ballot_sync(FULL, act);
+    int na = __popc(am);
+    int col = -1;                                   // column held by this lane after compaction
+    {
+        // the i-th set bit of am
+        unsigned m = am;
+        for (int i = 0; i < lane && m; ++i) m &= m - 1;
+        col = (lane < na) ? __ffs(m) - 1 : -1;
+    }
+    const int my_slot = col >= 0 ? (int)((((t - col) % H) + H) % H) : 0;
+    const double my_s = __shfl_sync(FULL, s_a, col >= 0 ? col : 0);
+    const double my_b = __shfl_sync(FULL, b_a, col >= 0 ? col : 0);
+    double phi_mine = 0.0;
     const double ridge = d.ridge;
     while (na > 0) {
-        // Cholesky of Gh[act,act] + ridge I, rows owned by lanes
-        __shared__ int ok_s;
-        if (lane == 0) ok_s = 1;
-        __syncwarp();
-        for (int c = 0; c < na; ++c) {
-            if (lane == 0) {
-                const int ac = act[c];
-                const int sa = (int)((t - ac) % H);
-                double v = st->gram[sa * H + sa] / (sc[ac] * sc[ac]) + ridge;
-                for (int q = 0; q < c; ++q) v -= L[c][q] * L[c][q];
-                if (!(v > 0.0) || !isfinite(v)) ok_s = 0;
-                else L[c][c] = sqrt(v);
+        double Lr[AAKM_H_SLOTS];                    // row `lane` of L
+#pragma unroll
+        for (int q = 0; q < AAKM_H_SLOTS; ++q) Lr[q] = 0.0;
+        bool ok = true;
+#pragma unroll
+        for (int c = 0; c < AAKM_H_SLOTS; ++c) {
+            if (c < na) {
+                const int slot_c = __shfl_sync(FULL, my_slot, c);
+                const double s_c = __shfl_sync(FULL, my_s, c);
+                // A[lane][c] of the scaled, ridged normal matrix
+                double v = 0.0;
+                if (lane >= c && lane < na) {
+                    v = st->gram[my_slot * H + slot_c] / (my_s * s_c);
+                    if (lane == c) v += ridge;
+                }
+#pragma unroll
+                for (int q = 0; q < AAKM_H_SLOTS; ++q) {
+                    if (q < c) {
+                        const double Lcq = __shfl_sync(FULL, Lr[q], c);
+                        v -= Lr[q] * Lcq;
+                    }
+                }
+                const double diag = __shfl_sync(FULL, v, c);
+                if (!(diag > 0.0) || !isfinite(diag)) { ok = false; break; }
+                const double Lcc = sqrt(diag);
+                if (lane == c) Lr[c] = Lcc;
+                else if (lane > c && lane < na) Lr[c] = v / Lcc;
             }
-            __syncwarp();
-            if (!ok_s) break;
-            for (int r = c + 1 + lane; r < na; r += 32) {
-                const int ar = act[r], ac = act[c];
-                const int sr = (int)((t - ar) % H), sc2 = (int)((t - ac) % H);
-                double v = st->gram[sr * H + sc2] / (sc[ar] * sc[ac]);
-                for (int q = 0; q < c; ++q) v -= L[r][q] * L[c][q];
-                L[r][c] = v / L[c][c];
-            }
-            __syncwarp();
         }
-        if (!ok_s) { --na; __syncwarp(); continue; }            // drop the oldest column
-        if (lane == 0) {
-            for (int a = 0; a < na; ++a) rhs[a] = st->bvec[act[a]] / sc[act[a]];
-            for (int a = 0; a < na; ++a) {
-                double v = rhs[a];
-                for (int q = 0; q < a; ++q) v -= L[a][q] * y[q];
-                y[a] = v / L[a][a];
+        if (!ok) { --na; continue; }                 // drop the oldest active column
+        // forward: L y = bh   (y replicated in every lane via broadcast)
+        double y_mine = 0.0;
+#pragma unroll
+        for (int a = 0; a < AAKM_H_SLOTS; ++a) {
+            if (a < na) {
+                double v = my_b;
+#pragma unroll
+                for (int q = 0; q < AAKM_H_SLOTS; ++q) {
+                    if (q < a) v -= Lr[q] * __shfl_sync(FULL, y_mine, q);
+                }
+                v = v / Lr[a < AAKM_H_SLOTS ? a : 0];
+                const double ya = __shfl_sync(FULL, v, a);
+                if (lane == a) y_mine = ya;
             }
-            for (int a = na - 1; a >= 0; --a) {
-                double v = y[a];
-                for (int q = a + 1; q < na; ++q) v -= L[q][a] * y[q];
-                y[a] = v / L[a][a];
-            }
-            for (int a = 0; a < na; ++a) th[act[a]] = y[a] / sc[act[a]];
         }
-        __syncwarp();
+        // backward: L^T phi = y
+        phi_mine = 0.0;
+        for (int a = na - 1; a >= 0; --a) {
+            double contrib = 0.0;
+#pragma unroll
+            for (int q = 0; q < AAKM_H_SLOTS; ++q) {
+                if (q == a && lane > a && lane < na) contrib = Lr[q] * phi_mine;
+            }
+            for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(FULL, contrib, o);
+            double Laa = 0.0;
+#pragma unroll
+            for (int q = 0; q < AAKM_H_SLOTS; ++q) if (q == a) Laa = Lr[q];
+            Laa = __shfl_sync(FULL, Laa, a);
+            const double ya = __shfl_sync(FULL, y_mine, a);
+            const double pa = (ya - contrib) / Laa;
+            if (lane == a) phi_mine = pa;
+        }
         break;
     }
-    if (lane == 0) {
-        // alpha_0 = 1 - theta_1, alpha_j = theta_j - theta_{j+1}, alpha_{m_t} = theta_{m_t}
-        int allzero = 1;
-        for (int a = 0; a < m_t; ++a) { st->theta[a] = th[a]; if (th[a] != 0.0) allzero = 0; }
-        st->m_t = m_t;
-        st->n_alpha = m_t + 1;
-        for (int j = 0; j <= m_t; ++j) {
-            const double tj = j >= 1 ? th[j - 1] : 0.0;
-            const double tj1 = j < m_t ? th[j] : 0.0;
-            st->alpha[j] = (j == 0 ? 1.0 : tj) - tj1;
-            st->alpha_slot[j] = (int)((t - j) % H);
+    // theta per original column: theta_col = phi / s
+    double th_lane = 0.0;                            // theta of column `lane`
+    {
+        const double th_c = (col >= 0 && col < m_t && lane < na) ? phi_mine / my_s : 0.0;
+        // scatter back: column j takes th_c from the lane holding it
+        for (int i = 0; i < AAKM_H_SLOTS; ++i) {
+            const int ci = __shfl_sync(FULL, (lane < na) ? col : -1, i);
+            const double v = __shfl_sync(FULL, th_c, i);
+            if (ci == lane) th_lane = v;
         }
-        if (allzero) { st->n_alpha = 1; st->alpha[0] = 1.0; st->alpha_slot[0] = ts; }
+    }
+    const unsigned nz = __ballot_sync(FULL, lane < m_t && th_lane != 0.0);
+    // alpha_0 = 1 - theta_1, alpha_j = theta_j - theta_{j+1}, alpha_{m_t} = theta_{m_t}
+    const double th_prev = __shfl_up_sync(FULL, th_lane, 1);     // theta of column lane-1
+    if (lane < m_t) st->theta[lane] = th_lane;
+    if (lane <= m_t) {
+        const double tj = lane >= 1 ? th_prev : 1.0;              // "theta_0" := 1
+        const double tj1 = lane < m_t ? th_lane : 0.0;
+        st->alpha[lane] = tj - tj1;
+        st->alpha_slot[lane] = (int)((((t - lane) % H) + H) % H);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const int allzero = nz == 0;
+        st->m_t = m_t;
+        st->n_alpha = allzero ? 1 : m_t + 1;
+        if (allzero) { st->alpha[0] = 1.0; st->alpha_slot[0] = ts; }
         st->lloyd = allzero;
     }
 }
+#undef FULL
 
 void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 32, 0, s>>>(d); }
 

@@ -103,6 +103,12 @@ void launch_reset(const Dev& d, cudaStream_t s);
 void launch_update_G(const Dev& d, const double* packed, const float* Cprev, float* G,
                      long long* counts, cudaStream_t s);
 
+// one-time kernel attribute setup (max dynamic smem); never during stream capture
+void setup_simt();
+void setup_refine();
+void setup_update();
+void setup_tc();
+
 // error-bound factors of the two engines
 float tau_gamma_simt(int d);
 float tau_gamma_tc(int d);

@@ -164,14 +164,20 @@ static void launch_t(const Dev& d, const GEval& g, cudaStream_t s) {
     const int max_smem = 96 * 1024;
     if ((size_t)KT * (D + 1) * 4 > (size_t)max_smem) KT = max_smem / ((D + 1) * 4);
     size_t smem = (size_t)KT * (D + 1) * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_assign_simt<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-        attr_set = true;
-    }
     long long blocks = (d.n + 256LL * R - 1) / (256LL * R);
     if (blocks < 1) blocks = 1;
     k_assign_simt<D><<<(unsigned)blocks, 256, smem, s>>>(d, g, KT);
+}
+
+void setup_simt() {
+    cudaFuncSetAttribute(k_assign_simt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_assign_simt_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s) {
@@ -192,11 +198,6 @@ void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s) {
     if (KT > d.K) KT = d.K;
     if (KT < 1) KT = 1;
     size_t smem = xs + (size_t)KT * (d.d + 1) * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_assign_simt_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-        attr_set = true;
-    }
     long long blocks = (d.n + RB - 1) / RB;
     if (blocks < 1) blocks = 1;
     k_assign_simt_generic<<<(unsigned)blocks, RB, smem, s>>>(d, g, (int)KT);

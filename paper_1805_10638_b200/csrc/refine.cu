@@ -94,13 +94,12 @@ __global__ void __launch_bounds__(256) k_refine(Dev d, GEval g) {
     }
 }
 
+void setup_refine() {
+    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (4096 + CAND) * 4);
+}
+
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s) {
     size_t smem = (size_t)8 * (d.d + CAND) * 4;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
     k_refine<<<296, 256, smem, s>>>(d, g);
 }
 

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -45,6 +46,15 @@ struct kmeans_handle {
 };
 
 static thread_local std::string g_create_err;
+static bool g_dbg = getenv("AAKM_DEBUG_SYNC") != nullptr;
+
+// AAKM_DEBUG_SYNC=1: synchronise after every launch and name the failing kernel.
+static void dbg(const char* what, cudaStream_t s) {
+    if (!g_dbg) return;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    fprintf(stderr, "[aakm dbg] %-16s %s\n", what, cudaGetErrorString(e));
+}
 
 #define FAIL(h, code, msg)                    \
     do {                                      \
@@ -154,7 +164,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     const Dev& d = h->d;
     GEval g{};
     g.branch = branch; g.force = 0; g.prev_mode = 0;
-    if (branch == 1) { launch_combine(d, 1, nullptr, s); h->launches++; }
+    if (branch == 1) { launch_combine(d, 1, nullptr, s); h->launches++; dbg("combine_fb", s); }
     std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
     if (timing && branch == 0) {
         if (h->ev_used == h->ev.size()) {
@@ -166,13 +176,17 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         CK(h, cudaEventRecord(evp->first, s));
     }
     assign_engine(h, d, g, s);
+    dbg("assign", s);
     if (evp) CK(h, cudaEventRecord(evp->second, s));
     launch_refine(d, g, s);
+    dbg("refine", s);
     launch_update(d, g, s);
+    dbg("update", s);
     h->launches += 3;
     kmeans_status st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
     launch_control(d, branch, s);
+    dbg("control", s);
     h->launches += 1;
     return KMEANS_OK;
 }
@@ -186,10 +200,15 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
     st = geval(h, 1, s, false);
     if (st != KMEANS_OK) return st;
     launch_finalize(d, s);
+    dbg("finalize", s);
     launch_gram(d, s);
+    dbg("gram", s);
     launch_solve(d, s);
+    dbg("solve", s);
     launch_combine(d, 0, nullptr, s);
+    dbg("combine_mix", s);
     launch_advance(d, s);
+    dbg("advance", s);
     h->launches += 5;
     CK(h, cudaGetLastError());
     return KMEANS_OK;
@@ -213,7 +232,9 @@ static kmeans_status ensure_graph(kmeans_handle* h) {
 
 static kmeans_status start(kmeans_handle* h, const float* C0) {
     launch_reset(h->d, h->stream);
+    dbg("reset", h->stream);
     launch_combine(h->d, 2, C0, h->stream);
+    dbg("combine_c0", h->stream);
     h->launches += 2;
     return enqueue_pass(h, h->stream, h->cfg.timing != 0);   // Algorithm 1 line 1
 }
@@ -324,6 +345,11 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             return KMEANS_ERR_CUDA;                                                       \
         }                                                                                 \
     } while (0)
+    {
+        static bool once = false;
+        if (!once) { setup_simt(); setup_refine(); setup_update(); setup_tc(); once = true; }
+        CKC(cudaGetLastError());
+    }
     CKC(cudaMallocHost(&h->st_host, sizeof(DevState)));
     CKC(cudaMallocHost(&h->tr_host, sizeof(TraceRec) * 2));
     CKC(cudaMallocHost(&h->scal_host, 64));

@@ -148,14 +148,13 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 
 static size_t smem_bytes(const Dev& d) { return (size_t)d.K * d.d * 8 + (size_t)d.K * 4; }
 
+void setup_update() {
+    cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+}
+
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     const size_t sm = smem_bytes(d);
     if (sm <= 160 * 1024) {
-        static bool set = false;
-        if (!set) {
-            cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            set = true;
-        }
         k_update<true><<<d.upd_blocks, 256, sm, s>>>(d, g);
     } else {
         k_update<false><<<d.upd_blocks, 256, 0, s>>>(d, g);

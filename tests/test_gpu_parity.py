@@ -93,7 +93,7 @@ def test_assign_edge_cases():
 def test_assign_duplicate_centroids_and_self(cfg):
     # duplicated centroid rows are exact ties (lowest index wins); rows that ARE
     # centroids have d_best = 0; K = 1 degenerates to all-zero labels.
-    X, C0, c = make(cfg, N=3001)
+    X, C0, c = make(cfg, N=5001)
     C = C0.copy()
     C[7] = C[3]
     km = handle(X, c.K)
