@@ -90,7 +90,9 @@ __device__ __forceinline__ bool geval_active(const Dev& d, const GEval& g) {
 // ---- launchers (host side, defined in the .cu files) ----
 void launch_combine(const Dev& d, int mode, const float* src, cudaStream_t s);
 void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s);
-void launch_assign_tc(const Dev& d, const GEval& g, cudaStream_t s);
+void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
+void* tc_make_maps(const Dev& d);   // TMA tensor maps of (X, C_hi, C_lo); nullptr if unsupported
+void tc_free_maps(void* m);
 bool tc_supported(int d, int K);
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s);
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s);
@@ -104,10 +106,10 @@ void launch_update_G(const Dev& d, const double* packed, const float* Cprev, flo
                      long long* counts, cudaStream_t s);
 
 // one-time kernel attribute setup (max dynamic smem); never during stream capture
-void setup_simt();
-void setup_refine();
-void setup_update();
-void setup_tc();
+cudaError_t setup_simt();
+cudaError_t setup_refine();
+cudaError_t setup_update();
+cudaError_t setup_tc();
 
 // error-bound factors of the two engines
 float tau_gamma_simt(int d);

@@ -169,15 +169,21 @@ static void launch_t(const Dev& d, const GEval& g, cudaStream_t s) {
     k_assign_simt<D><<<(unsigned)blocks, 256, smem, s>>>(d, g, KT);
 }
 
-void setup_simt() {
-    cudaFuncSetAttribute(k_assign_simt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_assign_simt_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+cudaError_t setup_simt() {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](const void* f, int bytes) {
+        cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (r != cudaSuccess) e = r;
+    };
+    set((const void*)k_assign_simt<1>, 96 * 1024);
+    set((const void*)k_assign_simt<2>, 96 * 1024);
+    set((const void*)k_assign_simt<3>, 96 * 1024);
+    set((const void*)k_assign_simt<4>, 96 * 1024);
+    set((const void*)k_assign_simt<8>, 96 * 1024);
+    set((const void*)k_assign_simt<16>, 96 * 1024);
+    set((const void*)k_assign_simt<32>, 96 * 1024);
+    set((const void*)k_assign_simt_generic, 200 * 1024);
+    return e;
 }
 
 void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s) {

@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(256) k_refine(Dev d, GEval g) {
     }
 }
 
-void setup_refine() {
-    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (4096 + CAND) * 4);
+cudaError_t setup_refine() {
+    return cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (4096 + CAND) * 4);
 }
 
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s) {

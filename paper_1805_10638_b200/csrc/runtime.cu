@@ -34,6 +34,9 @@ struct kmeans_handle {
     size_t scratch_bytes = 0;
     void* scratch = nullptr;
     cudaGraphExec_t pass_exec = nullptr;
+    cudaStream_t cap_stream = nullptr;   // private non-blocking stream used only for graph capture
+    void* tcm = nullptr;                 // TMA maps for d (tensor-core engine)
+    void* tcm_api = nullptr;             // TMA maps for da
     long long launches = 0;
     long long kernels_per_pass = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // assignment timing (branch A)
@@ -148,7 +151,7 @@ kmeans_status validate(long long n_local, int d, int k, const kmeans_config* cfg
 
 // ------------------------------------------------------------------ enqueue helpers
 static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
-    if (h->path == KMEANS_PATH_TC) launch_assign_tc(d, g, s);
+    if (h->path == KMEANS_PATH_TC) launch_assign_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
     else launch_assign_simt(d, g, s);
 }
 
@@ -216,11 +219,13 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
 
 static kmeans_status ensure_graph(kmeans_handle* h) {
     if (h->pass_exec) return KMEANS_OK;
+    // The caller's stream may be the legacy NULL stream (torch's default), which
+    // cannot be captured: capture on a private stream, replay on the caller's.
     cudaGraph_t g;
     long long before = h->launches;
-    CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    kmeans_status st = enqueue_pass(h, h->stream, false);
-    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    kmeans_status st = enqueue_pass(h, h->cap_stream, false);
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (st != KMEANS_OK) return st;
     CK(h, e);
     CK(h, cudaGraphInstantiate(&h->pass_exec, g, 0));
@@ -347,8 +352,20 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     } while (0)
     {
         static bool once = false;
-        if (!once) { setup_simt(); setup_refine(); setup_update(); setup_tc(); once = true; }
-        CKC(cudaGetLastError());
+        if (!once) {
+            CKC(setup_simt()); CKC(setup_refine()); CKC(setup_update()); CKC(setup_tc());
+            once = true;
+        }
+    }
+    CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    if (h->path == KMEANS_PATH_TC) {
+        h->tcm = tc_make_maps(h->d);
+        h->tcm_api = tc_make_maps(h->da);
+        if (!h->tcm || !h->tcm_api) {
+            g_create_err = "cuTensorMapEncodeTiled failed for the tensor-core engine";
+            delete h;
+            return KMEANS_ERR_CUDA;
+        }
     }
     CKC(cudaMallocHost(&h->st_host, sizeof(DevState)));
     CKC(cudaMallocHost(&h->tr_host, sizeof(TraceRec) * 2));
@@ -613,6 +630,9 @@ kmeans_status kmeans_destroy(kmeans_handle* h) {
     if (!h) return KMEANS_ERR_INVALID;
     if (!h->poisoned) cudaStreamSynchronize(h->stream);
     if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    if (h->tcm) tc_free_maps(h->tcm);
+    if (h->tcm_api) tc_free_maps(h->tcm_api);
     for (auto& e : h->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (h->run_ev[0]) cudaEventDestroy(h->run_ev[0]);
     if (h->run_ev[1]) cudaEventDestroy(h->run_ev[1]);

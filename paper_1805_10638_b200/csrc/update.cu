@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 
 static size_t smem_bytes(const Dev& d) { return (size_t)d.K * d.d * 8 + (size_t)d.K * 4; }
 
-void setup_update() {
-    cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+cudaError_t setup_update() {
+    return cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 }
 
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
