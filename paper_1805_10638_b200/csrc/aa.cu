@@ -4,7 +4,7 @@
 //   k_control   convergence rule R3 (R-A10), dynamic m
 //               (R-A5..A7), energy guard (PAPER.md:142-147,
 //               R-A8, R-A9): writes the device predicates reject / done.
-//   k_finalize  G^t = Update-Step (Eq. 4; G = C + S'/N, empty -> C row,
+//   k_finalize  G^t = Update-Step (Eq. 4; G = S/N, empty -> C row,
 //               R-A15), F^t = G^t - C^t into ring slot t%H.
 //   k_gram      <dF(t), dF(tau)> and <dF(tau), F^t> for the window (Eq. 7 /
 //               PAPER.md:155; "m inner products between (Kd)-dimensional
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
          e += (long long)gridDim.x * blockDim.x) {
         const double nj = pk[KD + e / D];
         const float c = d.C[e];
-        const float g = nj > 0.0 ? (float)((double)c + pk[e] / nj) : c;
+        const float g = nj > 0.0 ? (float)(pk[e] / nj) : c;        // G = S / N (Eq. 4)
         G[e] = g;
         F[e] = g - c;                                            // F^t = G^t - C^t (fp32)
     }

@@ -8,6 +8,7 @@
 #define AAKM_UPD_MAX_BLOCKS 1184  // 8 x 148 SMs
 #define AAKM_GRAM_BLOCKS 148
 #define AAKM_TRACE_CAP 8192
+#define AAKM_MAXC 32               // candidates kept per flagged row
 
 namespace aakm {
 
@@ -56,8 +57,14 @@ struct Dev {
     float* cn;            // ||c_j||^2 (fp32, from fp64)
     int* lab[2];          // label ping-pong, lab[cur] = P^t, lab[cur^1] = P^{t-1}
     int* flag_rows;       // near-tie row list (capacity n)
+    float* flag_b1;       // best fp32/3xTF32 score of each flagged row (capacity fcap)
+    float* flag_tau;      // its gap threshold tau_i
+    float* Xf;            // gathered flagged rows (fcap x d) for the candidate pass
+    int* cand;            // candidate centroids per flagged row (fcap x AAKM_MAXC)
+    int* cand_cnt;        // candidate count per flagged row (> AAKM_MAXC = overflow)
+    long long fcap;       // capacity of the candidate path (rows beyond -> SIMT refine)
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
-    double* packed[2];    // [S' (K*d) | N (K) | E | changed], branch A / B
+    double* packed[2];    // [S (K*d) | N (K) | E | changed], branch A / B
     double* upd_part;     // per-block (E, changed) partials
     float* Gring;         // H x K*d
     float* Fring;         // H x K*d
@@ -94,7 +101,8 @@ void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream
 void* tc_make_maps(const Dev& d);   // TMA tensor maps of (X, C_hi, C_lo); nullptr if unsupported
 void tc_free_maps(void* m);
 bool tc_supported(int d, int K);
-void launch_refine(const Dev& d, const GEval& g, cudaStream_t s);
+void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
+void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s);
 void launch_control(const Dev& d, int stage, cudaStream_t s);
 void launch_finalize(const Dev& d, cudaStream_t s);

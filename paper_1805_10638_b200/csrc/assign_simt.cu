@@ -26,7 +26,7 @@ float tau_gamma_simt(int d) { return 8.0f * (float)(d + 2) * 5.9604645e-8f; }
 template <int D>
 struct RowsPerThread { static constexpr int value = D <= 4 ? 8 : (D <= 16 ? 4 : 2); };
 
-__device__ __forceinline__ void push_flag(const Dev& d, int branch, bool flag, long long row) {
+__device__ __forceinline__ void push_flag(const Dev& d, int branch, bool flag, long long row, float b1, float tau) {
     unsigned mask = __ballot_sync(0xffffffffu, flag);
     if (mask == 0) return;
     int lane = threadIdx.x & 31;
@@ -36,7 +36,11 @@ __device__ __forceinline__ void push_flag(const Dev& d, int branch, bool flag, l
         base = (long long)atomicAdd((unsigned long long*)&d.flag_count[branch],
                                     (unsigned long long)__popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (flag) d.flag_rows[base + __popc(mask & ((1u << lane) - 1))] = (int)row;
+    if (flag) {
+        const long long f = base + __popc(mask & ((1u << lane) - 1));
+        d.flag_rows[f] = (int)row;
+        if (f < d.fcap) { d.flag_b1[f] = b1; d.flag_tau[f] = tau; }
+    }
 }
 
 template <int D>
@@ -105,9 +109,10 @@ __global__ void __launch_bounds__(256) k_assign_simt(Dev d, GEval g, int KT) {
     for (int r = 0; r < R; ++r) {
         long long row = row0 + (long long)r * 256;
         bool ok = row < d.n;
-        bool flag = ok && (b2[r] - b1[r] <= gam * (xn[r] + cmax2));
+        const float tau = gam * (xn[r] + cmax2);
+        bool flag = ok && (b2[r] - b1[r] <= tau);
         if (ok) lab_out[row] = i1[r];
-        push_flag(d, g.branch, flag, row);
+        push_flag(d, g.branch, flag, row, b1[r], tau);
     }
 }
 
@@ -152,9 +157,10 @@ __global__ void __launch_bounds__(128) k_assign_simt_generic(Dev d, GEval g, int
     }
     long long row = rbase + threadIdx.x;
     bool ok = row < d.n;
-    bool flag = ok && (b2 - b1 <= d.tau_gamma * (xn + cmax2));
+    const float tau = d.tau_gamma * (xn + cmax2);
+    bool flag = ok && (b2 - b1 <= tau);
     if (ok) lab_out[row] = i1;
-    push_flag(d, g.branch, flag, row);
+    push_flag(d, g.branch, flag, row, b1, tau);
 }
 
 template <int D>

@@ -43,7 +43,7 @@ constexpr int SMEM_LIMIT = 232448;                 // 227 KB opt-in
 float tau_gamma_tc(int d) { return 4.0f * (3.0f * 9.5367432e-7f + (3.0f * d / 8.0f + 8.0f) * 2.3841858e-7f); }
 
 struct TcMaps {
-    CUtensorMap x, chi, clo;
+    CUtensorMap x, chi, clo, xf;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -118,7 +118,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag, long long row) {
+__device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag, long long row, float b1, float tau) {
     unsigned mask = __ballot_sync(0xffffffffu, flag);
     if (mask == 0) return;
     int lane = threadIdx.x & 31;
@@ -127,15 +127,30 @@ __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag
     if (lane == leader)
         base = (long long)atomicAdd((unsigned long long*)&d.flag_count[branch], (unsigned long long)__popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (flag) d.flag_rows[base + __popc(mask & ((1u << lane) - 1))] = (int)row;
+    if (flag) {
+        const long long f = base + __popc(mask & ((1u << lane) - 1));
+        d.flag_rows[f] = (int)row;
+        if (f < d.fcap) { d.flag_b1[f] = b1; d.flag_tau[f] = tau; }
+    }
 }
 
 // ------------------------------------------------------------------ kernel
-template <int A>   // d = 32 * A
+// MODE 0: assignment of the shard (labels + near-tie flags).
+// MODE 1: candidate pass over the gathered flagged rows Xf: re-computes the
+//         same scores (bitwise: same operands, same MMA sequence) and emits
+//         every centroid j with s_j <= b1 + tau_i -- the only centroids that
+//         can be the exact argmin (refine.cu decides them in fp64).
+template <int A, int MODE>   // d = 32 * A
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
             const __grid_constant__ CUtensorMap tm_clo, Dev d, GEval g, int S, int NT) {
     if (!geval_active(d, g)) return;
+    long long n_rows = d.n;
+    if (MODE == 1) {
+        n_rows = d.flag_count[g.branch];
+        if (n_rows > d.fcap) n_rows = d.fcap;
+        if (n_rows == 0) return;
+    }
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* xhi = smem;
@@ -170,7 +185,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const long long n_tiles = (d.n + TC_BM - 1) / TC_BM;
+    const long long n_tiles = (n_rows + TC_BM - 1) / TC_BM;
 
     if (warp == 0) {
         if (lane == 0) {                                           // ---- TMA producer
@@ -261,6 +276,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             if (lane == 0) mbar_arrive(xready);
             float b1 = INFINITY, b2 = INFINITY;
             int i1 = 0;
+            const long long frow = tile * TC_BM + r;
+            float lim = -INFINITY;
+            int cnt = 0;
+            if (MODE == 1 && frow < n_rows) lim = d.flag_b1[frow] + d.flag_tau[frow];
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(accf + acc, aph);
                 tc_fence_after();
@@ -278,10 +297,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const float sc = fmaf(-2.0f, __uint_as_float(v[j + u]), cj[u]);
-                            const bool p = sc < b1;
-                            b2 = fminf(b2, fmaxf(sc, b1));
-                            i1 = p ? j0 + j + u : i1;
-                            b1 = fminf(b1, sc);
+                            if (MODE == 0) {
+                                const bool p = sc < b1;
+                                b2 = fminf(b2, fmaxf(sc, b1));
+                                i1 = p ? j0 + j + u : i1;
+                                b1 = fminf(b1, sc);
+                            } else if (sc <= lim) {
+                                if (cnt < AAKM_MAXC) d.cand[frow * AAKM_MAXC + cnt] = j0 + j + u;
+                                ++cnt;
+                            }
                         }
                     }
                 }
@@ -290,10 +314,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (lane == 0) mbar_arrive(acce + acc);
                 if (++acc == 2) { acc = 0; aph ^= 1; }
             }
-            const long long row = tile * TC_BM + r;
-            const bool ok = row < d.n;
-            if (ok) lab_out[row] = i1;
-            push_flag_tc(d, g.branch, ok && (b2 - b1 <= gam * (xn + cmax2)), row);
+            if (MODE == 0) {
+                const long long row = frow;
+                const bool ok = row < d.n;
+                const float tau = gam * (xn + cmax2);
+                if (ok) lab_out[row] = i1;
+                push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
+            } else if (frow < n_rows) {
+                d.cand_cnt[frow] = cnt;
+            }
         }
     }
     tc_fence_before();
@@ -329,8 +358,10 @@ cudaError_t setup_tc() {
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    const void* fns[4] = {(const void*)k_assign_tc<1>, (const void*)k_assign_tc<2>, (const void*)k_assign_tc<3>,
-                          (const void*)k_assign_tc<4>};
+    const void* fns[8] = {(const void*)k_assign_tc<1, 0>, (const void*)k_assign_tc<2, 0>,
+                          (const void*)k_assign_tc<3, 0>, (const void*)k_assign_tc<4, 0>,
+                          (const void*)k_assign_tc<1, 1>, (const void*)k_assign_tc<2, 1>,
+                          (const void*)k_assign_tc<3, 1>, (const void*)k_assign_tc<4, 1>};
     for (auto f : fns) {
         e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
         if (e != cudaSuccess) return e;
@@ -373,28 +404,100 @@ void* tc_make_maps(const Dev& d) {
     TcMaps* m = nullptr;
     if (posix_memalign((void**)&m, 64, sizeof(TcMaps)) != 0) return nullptr;
     bool ok = encode_rows(&m->x, d.X, d.n, d.d, TC_BM) && encode_rows(&m->chi, d.Chi, d.K, d.d, TC_BN) &&
-              encode_rows(&m->clo, d.Clo, d.K, d.d, TC_BN);
+              encode_rows(&m->clo, d.Clo, d.K, d.d, TC_BN) && encode_rows(&m->xf, d.Xf, d.fcap, d.d, TC_BM);
     if (!ok) { free(m); return nullptr; }
     return m;
 }
 
 void tc_free_maps(void* m) { free(m); }
 
-void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
-    const TcMaps* m = static_cast<const TcMaps*>(maps);
+template <int MODE>
+static void launch_tc_mode(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
     const int A = d.d / 32;
     const int NT = (d.K + TC_BN - 1) / TC_BN;
     const int S = pick_stages(A, NT);
     const size_t smem = smem_need(A, S, NT);
-    const long long n_tiles = (d.n + TC_BM - 1) / TC_BM;
-    int grid = (int)(n_tiles < g_num_sms ? n_tiles : g_num_sms);
+    int grid = g_num_sms;
+    const CUtensorMap& xm = MODE == 0 ? m->x : m->xf;
+    if (MODE == 0) {
+        const long long n_tiles = (d.n + TC_BM - 1) / TC_BM;
+        if (n_tiles < grid) grid = (int)n_tiles;
+    }
     if (grid < 1) grid = 1;
     switch (A) {
-        case 1: k_assign_tc<1><<<grid, TC_THREADS, smem, s>>>(m->x, m->chi, m->clo, d, g, S, NT); break;
-        case 2: k_assign_tc<2><<<grid, TC_THREADS, smem, s>>>(m->x, m->chi, m->clo, d, g, S, NT); break;
-        case 3: k_assign_tc<3><<<grid, TC_THREADS, smem, s>>>(m->x, m->chi, m->clo, d, g, S, NT); break;
-        default: k_assign_tc<4><<<grid, TC_THREADS, smem, s>>>(m->x, m->chi, m->clo, d, g, S, NT); break;
+        case 1: k_assign_tc<1, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+        case 2: k_assign_tc<2, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+        case 3: k_assign_tc<3, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+        default: k_assign_tc<4, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
     }
+}
+
+void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
+    launch_tc_mode<0>(d, g, static_cast<const TcMaps*>(maps), s);
+}
+
+// ---- refine for the tensor-core engine: gather -> candidate pass -> exact fp64
+__global__ void __launch_bounds__(256) k_gather_flagged(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    long long nf = d.flag_count[g.branch];
+    if (nf > d.fcap) nf = d.fcap;
+    const int D = d.d;
+    const long long total = nf * D;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long f = e / D;
+        d.Xf[e] = d.X[(long long)d.flag_rows[f] * D + (e - f * D)];
+    }
+}
+
+__device__ __forceinline__ double exact_sqdist_tc(const float* __restrict__ x, const float* __restrict__ c, int D) {
+    double acc = 0.0;
+    for (int k = 0; k < D; ++k) {
+        const double diff = __dsub_rn((double)x[k], (double)c[k]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
+// Exact fp64 argmin over the candidates of each flagged row (Eq. 3 by its
+// definition, direct differences, k ascending, lowest index on ties).
+__global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    extern __shared__ float xs_all[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int D = d.d;
+    float* xw = xs_all + warp * D;
+    int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
+    long long nf = d.flag_count[g.branch];
+    if (nf > d.fcap) nf = d.fcap;
+    for (long long f = (long long)blockIdx.x * 8 + warp; f < nf; f += (long long)gridDim.x * 8) {
+        const long long row = d.flag_rows[f];
+        for (int k = lane; k < D; k += 32) xw[k] = d.X[row * D + k];
+        __syncwarp();
+        const int cnt = d.cand_cnt[f];
+        const bool all = cnt > AAKM_MAXC || cnt == 0;
+        const int nc = all ? d.K : cnt;
+        double bd = INFINITY;
+        int bj = 0x7fffffff;
+        for (int q = lane; q < nc; q += 32) {
+            const int j = all ? q : d.cand[f * AAKM_MAXC + q];
+            const double v = exact_sqdist_tc(xw, d.C + (long long)j * D, D);
+            if (v < bd || (v == bd && j < bj)) { bd = v; bj = j; }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bd, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ov < bd || (ov == bd && oj < bj)) { bd = ov; bj = oj; }
+        }
+        if (lane == 0) lab_out[row] = bj;
+        __syncwarp();
+    }
+}
+
+void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
+    k_gather_flagged<<<2 * g_num_sms, 256, 0, s>>>(d, g);
+    launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
+    k_refine_exact<<<2 * g_num_sms, 256, (size_t)8 * d.d * 4, s>>>(d, g);
 }
 
 }  // namespace aakm

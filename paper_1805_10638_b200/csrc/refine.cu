@@ -28,7 +28,7 @@ __device__ __forceinline__ double exact_sqdist(const float* __restrict__ x, cons
 // dynamic smem: per warp, x (fp32, d floats) + candidate list (CAND ints)
 constexpr int CAND = 64;
 
-__global__ void __launch_bounds__(256) k_refine(Dev d, GEval g) {
+__global__ void __launch_bounds__(256) k_refine(Dev d, GEval g, long long first) {
     if (!geval_active(d, g)) return;
     extern __shared__ float4 smem4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) k_refine(Dev d, GEval g) {
     int* cand = reinterpret_cast<int*>(xw + D);
     int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
     const long long nflag = d.flag_count[g.branch];
-    const long long gw = (long long)blockIdx.x * 8 + warp;
+    const long long gw = first + (long long)blockIdx.x * 8 + warp;
     const long long nw = (long long)gridDim.x * 8;
     for (long long f = gw; f < nflag; f += nw) {
         const long long row = d.flag_rows[f];
@@ -98,9 +98,9 @@ cudaError_t setup_refine() {
     return cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (4096 + CAND) * 4);
 }
 
-void launch_refine(const Dev& d, const GEval& g, cudaStream_t s) {
+void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first) {
     size_t smem = (size_t)8 * (d.d + CAND) * 4;
-    k_refine<<<296, 256, smem, s>>>(d, g);
+    k_refine<<<296, 256, smem, s>>>(d, g, first);
 }
 
 }  // namespace aakm

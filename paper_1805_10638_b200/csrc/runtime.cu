@@ -50,9 +50,44 @@ struct kmeans_handle {
 
 static thread_local std::string g_create_err;
 static bool g_dbg = getenv("AAKM_DEBUG_SYNC") != nullptr;
+static bool g_prof = getenv("AAKM_PROFILE") != nullptr;
+
+// AAKM_PROFILE=1 (eager launches only): per-kernel CUDA-event durations,
+// printed to stderr by kmeans_destroy.
+struct ProfRec { const char* name; cudaEvent_t a, b; };
+static std::vector<ProfRec> g_prof_recs;
+static cudaEvent_t g_prof_last = nullptr;
+static void prof_mark(const char* what, cudaStream_t s) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    if (g_prof_last) g_prof_recs.push_back({what, g_prof_last, e});
+    g_prof_last = e;
+}
+static void prof_dump() {
+    if (g_prof_recs.empty()) return;
+    cudaDeviceSynchronize();
+    std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+    for (auto& r : g_prof_recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        bool f = false;
+        for (auto& a : agg) if (a.first == r.name) { a.second.first += ms; a.second.second++; f = true; }
+        if (!f) agg.push_back({r.name, {ms, 1}});
+    }
+    fprintf(stderr, "[aakm prof] kernel            total_ms    calls   avg_ms\n");
+    for (auto& a : agg)
+        fprintf(stderr, "[aakm prof] %-16s %10.3f %8d %9.4f\n", a.first.c_str(), a.second.first, a.second.second,
+                a.second.first / a.second.second);
+    g_prof_recs.clear();
+    g_prof_last = nullptr;
+}
 
 // AAKM_DEBUG_SYNC=1: synchronise after every launch and name the failing kernel.
 static void dbg(const char* what, cudaStream_t s) {
+    if (g_prof) prof_mark(what, s);
     if (!g_dbg) return;
     cudaError_t e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -95,11 +130,15 @@ static void dbg(const char* what, cudaStream_t s) {
 // ------------------------------------------------------------------ layout
 namespace {
 struct Layout {
-    size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, lab0, lab1, flags, scratch, packed1,
+    size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
+        scratch, packed1,
         upd_part, Gring, Fring, gram_part, trace, total, scratch_bytes;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// rows the tensor-core candidate refine can hold (more -> SIMT refine for the rest)
+long long fcap_of(long long n) { return n / 4 + 4096; }
 
 Layout layout(long long n, int d, int K, int m_max) {
     Layout L;
@@ -113,6 +152,12 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.Ca = take(KD * 4); L.Cahi = take(KD * 4); L.Calo = take(KD * 4); L.cna = take((size_t)K * 4);
     L.lab0 = take((size_t)n * 4); L.lab1 = take((size_t)n * 4);
     L.flags = take((size_t)n * 4 + 4);
+    const long long fc = fcap_of(n);
+    L.fb1 = take((size_t)fc * 4 + 4);
+    L.ftau = take((size_t)fc * 4 + 4);
+    L.Xf = take((size_t)fc * d * 4 + 16);
+    L.cand = take((size_t)fc * AAKM_MAXC * 4 + 4);
+    L.cand_cnt = take((size_t)fc * 4 + 4);
     const size_t pk = (KD + K + 2) * 8;
     L.scratch = o;
     size_t s0 = take(256);                 // flag counts
@@ -155,6 +200,19 @@ static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
     else launch_assign_simt(d, g, s);
 }
 
+// Exact re-decision of the near-tie rows: the tensor-core engine re-runs the
+// flagged rows in candidate mode (gather -> MMA pass -> fp64 on candidates);
+// rows beyond the candidate capacity (and the SIMT engine) use the SIMT refine.
+static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
+    if (h->path == KMEANS_PATH_TC) {
+        launch_refine_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
+        launch_refine(d, g, s, d.fcap);
+        h->launches += 3;
+    } else {
+        launch_refine(d, g, s, 0);
+    }
+}
+
 static kmeans_status allreduce(kmeans_handle* h, double* buf, cudaStream_t s) {
     if (h->nranks <= 1) return KMEANS_OK;
     const size_t cnt = (size_t)h->d.K * h->d.d + h->d.K + 2;
@@ -181,13 +239,14 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     assign_engine(h, d, g, s);
     dbg("assign", s);
     if (evp) CK(h, cudaEventRecord(evp->second, s));
-    launch_refine(d, g, s);
+    refine_engine(h, d, g, s);
     dbg("refine", s);
     launch_update(d, g, s);
     dbg("update", s);
     h->launches += 3;
     kmeans_status st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
+    if (h->nranks > 1) dbg("allreduce", s);
     launch_control(d, branch, s);
     dbg("control", s);
     h->launches += 1;
@@ -198,6 +257,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
 static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing) {
     const Dev& d = h->d;
     CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+    dbg("memset", s);
     kmeans_status st = geval(h, 0, s, timing);
     if (st != KMEANS_OK) return st;
     st = geval(h, 1, s, false);
@@ -310,6 +370,12 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.C = (float*)(w + L.C); D.Chi = (float*)(w + L.Chi); D.Clo = (float*)(w + L.Clo); D.cn = (float*)(w + L.cn);
     D.lab[0] = (int*)(w + L.lab0); D.lab[1] = (int*)(w + L.lab1);
     D.flag_rows = (int*)(w + L.flags);
+    D.flag_b1 = (float*)(w + L.fb1);
+    D.flag_tau = (float*)(w + L.ftau);
+    D.Xf = (float*)(w + L.Xf);
+    D.cand = (int*)(w + L.cand);
+    D.cand_cnt = (int*)(w + L.cand_cnt);
+    D.fcap = fcap_of(n_local);
     D.flag_count = (long long*)(w + L.scratch);
     D.packed[0] = (double*)(w + L.scratch + 256);
     D.packed[1] = (double*)(w + L.packed1);
@@ -320,15 +386,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.nranks = nranks;
     {
         long long KD = (long long)k * d;
-        long long smem_bytes = KD * 8 + (long long)k * 4;
-        long long ub;
-        if (smem_bytes <= 160 * 1024) {
-            ub = (n_local + 1023) / 1024;          // >= ~1K rows per block amortises the flush
-            if (ub > 296) ub = 296;
-        } else {
-            ub = (n_local + 255) / 256;
-            if (ub > AAKM_UPD_MAX_BLOCKS) ub = AAKM_UPD_MAX_BLOCKS;
-        }
+        long long ub = (n_local + 255) / 256;
+        if (ub > AAKM_UPD_MAX_BLOCKS) ub = AAKM_UPD_MAX_BLOCKS;
         D.upd_blocks = (int)(ub < 1 ? 1 : ub);
         long long gb = (KD + 127) / 128;
         D.gram_blocks = (int)(gb > AAKM_GRAM_BLOCKS ? AAKM_GRAM_BLOCKS : (gb < 1 ? 1 : gb));
@@ -404,7 +463,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     g.branch = 0; g.force = 1; g.lab_out = labels_out;
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
     assign_engine(h, d, g, s);
-    launch_refine(d, g, s);
+    refine_engine(h, d, g, s);
     launch_update(d, g, s);
     h->launches += 4;
     kmeans_status st = allreduce(h, d.packed[0], s);
@@ -628,6 +687,7 @@ const char* kmeans_assign_path_name(const kmeans_handle* h) {
 
 kmeans_status kmeans_destroy(kmeans_handle* h) {
     if (!h) return KMEANS_ERR_INVALID;
+    if (g_prof) prof_dump();
     if (!h->poisoned) cudaStreamSynchronize(h->stream);
     if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);

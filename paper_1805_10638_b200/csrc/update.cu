@@ -3,22 +3,12 @@
 // Update step, Eq. (4): c_j = (1/N_j) sum_{rho_i = j} x_i.
 // One pass over the local shard produces the packed vector that the ranks
 // allreduce:
-//   S'_j = sum_{rho_i = j} (x_i - c_j)   (centred on the centroids C the
-//                                         assignment was made against; the
-//                                         mean is G_j = c_j + S'_j / N_j)
+//   S_j  = sum_{rho_i = j} x_i           (fp64; the mean is G_j = S_j / N_j)
 //   N_j  = #{i : rho_i = j}
 //   E    = sum_i ||x_i - c_{rho_i}||^2  (Eq. 1 with the given P, PAPER.md:113;
 //                                         fp64 direct differences)
 //   changed = #{i : rho_i != rho_i^{prev}}
-// Centring keeps the fp32 shared-memory partial sums small (accuracy), the
-// energy reuses the same loads of x_i and c_{rho_i}, so X is read once.
-//
-// Two engines:
-//  * smem (K*d small): lanes grouped per row (group = next pow2 >= d, <= 32),
-//    shared-memory privatised fp32 S' and int N, flushed once per block with
-//    global fp64 atomics (red.global.add.f64);
-//  * global (large K*d): same mapping, fp64 atomics straight to the packed
-//    vector (coalesced: a row's d doubles are contiguous).
+// The energy reuses the same loads of x_i and c_{rho_i}, so X is read once.
 // E/changed: fixed-order per-block partials, reduced by the last block in a
 // fixed tree -> bitwise reproducible for a fixed launch geometry.
 #include "aakm_dev.cuh"
@@ -92,21 +82,15 @@ __device__ void finish_scalars(const Dev& d, double* out, double e, long long ch
     }
 }
 
-template <bool SMEM>
+// Lanes are grouped per row (group = next pow2 >= d, <= 32) so a row's d
+// coordinates are read and reduced as one coalesced segment; S_j and N_j go
+// to global memory with fp64 red.global.add (native on sm_100a; the fp32
+// shared-memory atomics compile to CAS loops and measured slower).
 __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     const int D = d.d, K = d.K;
     const long long KD = (long long)K * D;
-    extern __shared__ float4 smem4[];
-    float* Ss = reinterpret_cast<float*>(smem4);       // K*D (SMEM only)
-    float* Cs = Ss + KD;                               // K*D
-    int* Ns = reinterpret_cast<int*>(Cs + KD);         // K
-    if (SMEM) {
-        for (long long e = threadIdx.x; e < KD; e += blockDim.x) { Ss[e] = 0.f; Cs[e] = p.C[e]; }
-        for (int e = threadIdx.x; e < K; e += blockDim.x) Ns[e] = 0;
-        __syncthreads();
-    }
     int GS = 1;
     while (GS < D && GS < 32) GS <<= 1;
     const int lane = threadIdx.x & 31;
@@ -122,53 +106,35 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
         if (j < 0 || j >= K) { bad = 1; continue; }
         if (gl == 0) {
             if (p.prev) ch += (p.prev[row] != j);
-            if (SMEM) atomicAdd(&Ns[j], 1);
-            else red_add_f64(p.out + KD + j, 1.0);
+            red_add_f64(p.out + KD + j, 1.0);
         }
         const float* x = d.X + row * D;
+        const float* c = p.C + (long long)j * D;
         for (int k = gl; k < D; k += GS) {
             const float xv = __ldcs(x + k);
-            const float cv = SMEM ? Cs[(long long)j * D + k] : __ldg(p.C + (long long)j * D + k);
-            const double diff = (double)xv - (double)cv;   // exact in fp64
+            const double diff = (double)xv - (double)__ldg(c + k);   // exact in fp64
             e_acc = fma(diff, diff, e_acc);
-            if (SMEM) atomicAdd(&Ss[(long long)j * D + k], xv - cv);
-            else red_add_f64(p.out + (long long)j * D + k, diff);
+            red_add_f64(p.out + (long long)j * D + k, (double)xv);
         }
     }
     if (bad) d.st->label_error = 1;
-    if (SMEM) {
-        __syncthreads();
-        for (long long e = threadIdx.x; e < KD; e += blockDim.x)
-            if (Ss[e] != 0.f) red_add_f64(p.out + e, (double)Ss[e]);
-        for (int e = threadIdx.x; e < K; e += blockDim.x)
-            if (Ns[e]) red_add_f64(p.out + KD + e, (double)Ns[e]);
-    }
     finish_scalars(d, p.out, e_acc, ch);
 }
 
-static size_t smem_bytes(const Dev& d) { return (size_t)d.K * d.d * 8 + (size_t)d.K * 4; }
-
-cudaError_t setup_update() {
-    return cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-}
+cudaError_t setup_update() { return cudaSuccess; }
 
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
-    const size_t sm = smem_bytes(d);
-    if (sm <= 160 * 1024) {
-        k_update<true><<<d.upd_blocks, 256, sm, s>>>(d, g);
-    } else {
-        k_update<false><<<d.upd_blocks, 256, 0, s>>>(d, g);
-    }
+    k_update<<<d.upd_blocks, 256, 0, s>>>(d, g);
 }
 
-// kmeans_update API: G = C_prev + S'/N (empty -> C_prev row), counts.
+// kmeans_update API: G = S / N (empty -> C_prev row, R-A15), counts.
 __global__ void k_update_G(long long KD, int D, int K, const double* packed, const float* Cprev,
                            float* G, long long* counts) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
          e += (long long)gridDim.x * blockDim.x) {
         const int j = (int)(e / D);
         const double nj = packed[KD + j];
-        G[e] = nj > 0.0 ? (float)((double)Cprev[e] + packed[e] / nj) : Cprev[e];
+        G[e] = nj > 0.0 ? (float)(packed[e] / nj) : Cprev[e];
         if (counts && e % D == 0) counts[j] = (long long)nj;
     }
 }
