@@ -118,6 +118,25 @@ def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000,
     return c
 
 
+def broadcast_uid(rank: int, group=None, device=None):
+    """Rank 0 draws the 128-byte NCCL unique id (kmeans_nccl_unique_id); every
+    rank receives it over the torch process group (gloo: CPU tensor, nccl:
+    device tensor).  Returns a ctypes uint8[128]."""
+    import torch
+    import torch.distributed as dist
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        raw = (ct.c_uint8 * 128)()
+        rc = lib().kmeans_nccl_unique_id(raw)
+        if rc != 0:
+            raise AAKMError(rc, lib().kmeans_last_error(None).decode())
+        buf = torch.tensor(list(raw), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        buf = buf.to(device if device is not None else "cuda")
+    dist.broadcast(buf, src=0, group=group)
+    return (ct.c_uint8 * 128)(*buf.cpu().tolist())
+
+
 def _ptr(t):
     return ct.c_void_p(0 if t is None else t.data_ptr())
 
@@ -146,17 +165,7 @@ class KMeans:
         self.ws_ptr = (base + 255) & ~255
         uid = None
         if nranks > 1:
-            import torch.distributed as dist
-            buf = torch.zeros(128, dtype=torch.uint8)
-            if rank == 0:
-                raw = (ct.c_uint8 * 128)()
-                self._check(L.kmeans_nccl_unique_id(raw), None)
-                buf = torch.tensor(list(raw), dtype=torch.uint8)
-            bdev = buf if (group is None and dist.get_backend() == "gloo") else buf
-            if dist.get_backend(group) == "nccl":
-                bdev = buf.to(self.device)
-            dist.broadcast(bdev, src=0, group=group)
-            uid = (ct.c_uint8 * 128)(*bdev.cpu().tolist())
+            uid = broadcast_uid(rank, group, self.device)
         h = ct.c_void_p()
         with torch.cuda.device(self.device):
             self._check(L.kmeans_create(ct.byref(h), _ptr(X), self.n, self.n_global, self.d, self.K,
