@@ -9,6 +9,7 @@
 #define AAKM_GRAM_BLOCKS 148
 #define AAKM_TRACE_CAP 8192
 #define AAKM_MAXC 32               // candidates kept per flagged row
+#define AAKM_SORTED_MIN_ROWS 65536  // label-sorted update engine from this many rows
 
 namespace aakm {
 
@@ -35,7 +36,7 @@ struct alignas(16) DevState {
     int hist_count, accepted_now, rejected_now, label_error;
     int n_alpha, fb_slot, final_traced, pad0;
     unsigned int cmax2_bits;     // max_j ||c_j||^2 of the centroids being assigned (float bits)
-    unsigned int cmax2_tmp, comb_ctr, upd_ctr;
+    unsigned int cmax2_tmp, comb_ctr, upd_ctr, hist_ctr, pad2[3];
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -66,6 +67,11 @@ struct Dev {
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
     double* packed[2];    // [S (K*d) | N (K) | E | changed], branch A / B
     double* upd_part;     // per-block (E, changed) partials
+    int* seg_count;       // sorted update engine: N_j (K)
+    int* seg_off;         // row offsets of cluster j in perm (K+1)
+    int* seg_cursor;      // scatter cursors (K)
+    int* seg_chunk;       // chunk offsets (K+1)
+    int* perm;            // rows bucketed by label (n)
     float* Gring;         // H x K*d
     float* Fring;         // H x K*d
     double* gram_part;    // AAKM_GRAM_BLOCKS x (2*H)
@@ -104,6 +110,7 @@ bool tc_supported(int d, int K);
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
 void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s);
+bool update_sorted(const Dev& d);
 void launch_control(const Dev& d, int stage, cudaStream_t s);
 void launch_finalize(const Dev& d, cudaStream_t s);
 void launch_gram(const Dev& d, cudaStream_t s);
