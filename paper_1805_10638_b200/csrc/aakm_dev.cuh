@@ -10,6 +10,8 @@
 #define AAKM_TRACE_CAP 8192
 #define AAKM_MAXC 32               // candidates kept per flagged row
 #define AAKM_SORTED_MIN_ROWS 65536  // label-sorted update engine from this many rows
+#define AAKM_SORTED_MAX_K 16384     // ... and up to this many clusters (smem histograms)
+#define AAKM_SEG_BLOCKS 148         // row blocks of the histogram / scatter
 
 namespace aakm {
 
@@ -67,10 +69,10 @@ struct Dev {
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
     double* packed[2];    // [S (K*d) | N (K) | E | changed], branch A / B
     double* upd_part;     // per-block (E, changed) partials
-    int* seg_count;       // sorted update engine: N_j (K)
+    int* seg_bh;          // sorted update engine: per-block histograms -> scatter bases (SEG_BLOCKS x K)
     int* seg_off;         // row offsets of cluster j in perm (K+1)
-    int* seg_cursor;      // scatter cursors (K)
     int* seg_chunk;       // chunk offsets (K+1)
+    int* seg_cmap;        // chunk -> cluster (n/SEG_ROWS + K)
     int* perm;            // rows bucketed by label (n)
     float* Gring;         // H x K*d
     float* Fring;         // H x K*d

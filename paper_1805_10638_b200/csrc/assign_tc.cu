@@ -437,67 +437,66 @@ void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream
 }
 
 // ---- refine for the tensor-core engine: gather -> candidate pass -> exact fp64
+// one warp per flagged row, float4 lanes (d % 32 == 0 on this engine)
 __global__ void __launch_bounds__(256) k_gather_flagged(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     long long nf = d.flag_count[g.branch];
     if (nf > d.fcap) nf = d.fcap;
-    const int D = d.d;
-    const long long total = nf * D;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const long long f = e / D;
-        d.Xf[e] = d.X[(long long)d.flag_rows[f] * D + (e - f * D)];
+    const int D4 = d.d >> 2;
+    const int lane = threadIdx.x & 31;
+    for (long long f = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); f < nf; f += (long long)gridDim.x * 8) {
+        const float4* src = reinterpret_cast<const float4*>(d.X + (long long)d.flag_rows[f] * d.d);
+        float4* dst = reinterpret_cast<float4*>(d.Xf + f * d.d);
+        for (int k = lane; k < D4; k += 32) dst[k] = __ldg(src + k);
     }
 }
 
-__device__ __forceinline__ double exact_sqdist_tc(const float* __restrict__ x, const float* __restrict__ c, int D) {
-    double acc = 0.0;
-    for (int k = 0; k < D; ++k) {
-        const double diff = __dsub_rn((double)x[k], (double)c[k]);
-        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-    }
-    return acc;
-}
-
-// Exact fp64 argmin over the candidates of each flagged row (Eq. 3 by its
-// definition, direct differences, k ascending, lowest index on ties).
+// Exact fp64 argmin over the candidates of each flagged row: Eq. 3 by its
+// definition (direct differences); each lane owns d/32 coordinates, the warp
+// reduces in a fixed xor-tree order; lowest index wins exact ties.
 __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
-    extern __shared__ float xs_all[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = d.d;
-    float* xw = xs_all + warp * D;
     int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
     long long nf = d.flag_count[g.branch];
     if (nf > d.fcap) nf = d.fcap;
     for (long long f = (long long)blockIdx.x * 8 + warp; f < nf; f += (long long)gridDim.x * 8) {
         const long long row = d.flag_rows[f];
-        for (int k = lane; k < D; k += 32) xw[k] = d.X[row * D + k];
-        __syncwarp();
+        double xv[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int k = lane + 32 * v;
+            xv[v] = k < D ? (double)__ldg(d.X + row * D + k) : 0.0;
+        }
         const int cnt = d.cand_cnt[f];
         const bool all = cnt > AAKM_MAXC || cnt == 0;
         const int nc = all ? d.K : cnt;
         double bd = INFINITY;
         int bj = 0x7fffffff;
-        for (int q = lane; q < nc; q += 32) {
+        for (int q = 0; q < nc; ++q) {
             const int j = all ? q : d.cand[f * AAKM_MAXC + q];
-            const double v = exact_sqdist_tc(xw, d.C + (long long)j * D, D);
-            if (v < bd || (v == bd && j < bj)) { bd = v; bj = j; }
-        }
-        for (int o = 16; o; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bd, o);
-            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-            if (ov < bd || (ov == bd && oj < bj)) { bd = ov; bj = oj; }
+            double acc = 0.0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int k = lane + 32 * v;
+                if (k < D) {
+                    const double df = xv[v] - (double)__ldg(d.C + (long long)j * D + k);
+                    acc = fma(df, df, acc);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (acc < bd || (acc == bd && j < bj)) { bd = acc; bj = j; }
         }
         if (lane == 0) lab_out[row] = bj;
-        __syncwarp();
     }
 }
 
 void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
-    k_gather_flagged<<<2 * g_num_sms, 256, 0, s>>>(d, g);
+    k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
-    k_refine_exact<<<2 * g_num_sms, 256, (size_t)8 * d.d * 4, s>>>(d, g);
+    k_refine_exact<<<4 * g_num_sms, 256, 0, s>>>(d, g);
 }
 
 }  // namespace aakm

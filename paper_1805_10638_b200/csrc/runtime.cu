@@ -132,7 +132,7 @@ namespace {
 struct Layout {
     size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
         scratch, packed1,
-        upd_part, seg_count, seg_off, seg_cursor, seg_chunk, perm, Gring, Fring, gram_part, trace, total,
+        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, perm, Gring, Fring, gram_part, trace, total,
         scratch_bytes;
 };
 
@@ -167,10 +167,10 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.packed1 = take(pk);                  // packed[1]
     L.scratch_bytes = o - L.scratch;
     L.upd_part = take((size_t)AAKM_UPD_MAX_BLOCKS * 16);
-    L.seg_count = take((size_t)K * 4);
+    L.seg_bh = take((size_t)AAKM_SEG_BLOCKS * K * 4);
     L.seg_off = take((size_t)K * 4 + 4);
-    L.seg_cursor = take((size_t)K * 4);
     L.seg_chunk = take((size_t)K * 4 + 4);
+    L.seg_cmap = take(((size_t)n / 256 + K + 1) * 4);
     L.perm = take((size_t)n * 4 + 4);
     L.Gring = take((size_t)H * KD * 4);
     L.Fring = take((size_t)H * KD * 4);
@@ -386,10 +386,10 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.packed[0] = (double*)(w + L.scratch + 256);
     D.packed[1] = (double*)(w + L.packed1);
     D.upd_part = (double*)(w + L.upd_part);
-    D.seg_count = (int*)(w + L.seg_count);
+    D.seg_bh = (int*)(w + L.seg_bh);
     D.seg_off = (int*)(w + L.seg_off);
-    D.seg_cursor = (int*)(w + L.seg_cursor);
     D.seg_chunk = (int*)(w + L.seg_chunk);
+    D.seg_cmap = (int*)(w + L.seg_cmap);
     D.perm = (int*)(w + L.perm);
     D.Gring = (float*)(w + L.Gring); D.Fring = (float*)(w + L.Fring);
     D.gram_part = (double*)(w + L.gram_part);

@@ -166,37 +166,44 @@ __device__ __forceinline__ void finish_changed(const Dev& d, double* out, long l
     }
 }
 
-__global__ void __launch_bounds__(256) k_hist(Dev d, GEval g) {
+// Block b histograms its contiguous row range [b*R, (b+1)*R) into smem and
+// stores it to seg_bh[b][K]; k_scan turns counts into per-(block, cluster)
+// base offsets, and k_scatter re-walks the same rows placing each at
+// base + local rank (shared-memory counters): no global atomics on the
+// contended per-cluster cursors.
+__device__ __forceinline__ void block_rows(const Dev& d, long long& r0, long long& r1) {
+    const long long per = (d.n + gridDim.x - 1) / gridDim.x;
+    r0 = (long long)blockIdx.x * per;
+    r1 = min(d.n, r0 + per);
+}
+
+__global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     extern __shared__ int hs[];
     const int K = d.K;
-    const bool use_smem = K <= 16384;
-    if (use_smem) {
-        for (int j = threadIdx.x; j < K; j += blockDim.x) hs[j] = 0;
-        __syncthreads();
-    }
+    for (int j = threadIdx.x; j < K; j += blockDim.x) hs[j] = 0;
+    __syncthreads();
+    long long r0, r1;
+    block_rows(d, r0, r1);
     long long ch = 0;
     int bad = 0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d.n;
-         i += (long long)gridDim.x * blockDim.x) {
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
         const int j = p.lab[i];
         if (j < 0 || j >= K) { bad = 1; continue; }
         if (p.prev) ch += (p.prev[i] != j);
-        if (use_smem) atomicAdd(&hs[j], 1);
-        else atomicAdd(&d.seg_count[j], 1);
+        atomicAdd(&hs[j], 1);
     }
     if (bad) d.st->label_error = 1;
-    if (use_smem) {
-        __syncthreads();
-        for (int j = threadIdx.x; j < K; j += blockDim.x)
-            if (hs[j]) atomicAdd(&d.seg_count[j], hs[j]);
-    }
+    __syncthreads();
+    int* bh = d.seg_bh + (long long)blockIdx.x * K;
+    for (int j = threadIdx.x; j < K; j += blockDim.x) bh[j] = hs[j];
     finish_changed(d, p.out, ch);
 }
 
-// one block: exclusive scans over K (counts -> offsets, chunks -> chunk offsets)
-__global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g) {
+// one block: per-cluster totals over blocks, exclusive scans over clusters,
+// per-(block, cluster) scatter bases, chunk offsets and chunk -> cluster map.
+__global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g, int nblk) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     const int K = d.K;
@@ -208,14 +215,25 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int base = 0; base < K; base += blockDim.x) {
         const int j = base + threadIdx.x;
-        const long long c = j < K ? d.seg_count[j] : 0;
-        const long long nc = (c + SEG_ROWS - 1) / SEG_ROWS;
-        long long a = c, b = nc;
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long ta = __shfl_up_sync(0xffffffffu, a, o), tb = __shfl_up_sync(0xffffffffu, b, o);
-            if (lane >= o) { a += ta; b += tb; }
+        long long c = 0;
+        if (j < K) {
+            int b = 0;
+            for (; b + 8 <= nblk; b += 8) {
+                int t[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t[u] = d.seg_bh[(long long)(b + u) * K + j];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) c += t[u];
+            }
+            for (; b < nblk; ++b) c += d.seg_bh[(long long)b * K + j];
         }
-        if (lane == 31) { wsum[0][w] = a; wsum[1][w] = b; }
+        const long long nc = (c + SEG_ROWS - 1) / SEG_ROWS;
+        long long a = c, bb = nc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long ta = __shfl_up_sync(0xffffffffu, a, o), tb = __shfl_up_sync(0xffffffffu, bb, o);
+            if (lane >= o) { a += ta; bb += tb; }
+        }
+        if (lane == 31) { wsum[0][w] = a; wsum[1][w] = bb; }
         __syncthreads();
         if (w == 0) {
             long long x = lane < (int)(blockDim.x >> 5) ? wsum[0][lane] : 0;
@@ -228,12 +246,18 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g) {
         }
         __syncthreads();
         const long long pa = (w ? wsum[0][w - 1] : 0) + a - c + carry[0];
-        const long long pb = (w ? wsum[1][w - 1] : 0) + b - nc + carry[1];
+        const long long pb = (w ? wsum[1][w - 1] : 0) + bb - nc + carry[1];
         if (j < K) {
             d.seg_off[j] = (int)pa;
-            d.seg_cursor[j] = (int)pa;
             d.seg_chunk[j] = (int)pb;
             p.out[KD + j] = (double)c;                  // N_j
+            long long o = pa;                            // scatter base of (block b, cluster j)
+            for (int b = 0; b < nblk; ++b) {
+                const int v = d.seg_bh[(long long)b * K + j];
+                d.seg_bh[(long long)b * K + j] = (int)o;
+                o += v;
+            }
+            for (long long q = 0; q < nc; ++q) d.seg_cmap[pb + q] = j;
         }
         __syncthreads();
         if (threadIdx.x == blockDim.x - 1) { carry[0] = pa + c; carry[1] = pb + nc; }
@@ -242,21 +266,20 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g) {
     if (threadIdx.x == 0) { d.seg_off[K] = (int)carry[0]; d.seg_chunk[K] = (int)carry[1]; }
 }
 
-__global__ void __launch_bounds__(256) k_scatter(Dev d, GEval g) {
+__global__ void __launch_bounds__(1024) k_scatter(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
+    extern __shared__ int cur[];
     const int K = d.K;
-    const int lane = threadIdx.x & 31;
-    for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < d.n; i0 += (long long)gridDim.x * blockDim.x) {
-        const long long i = i0 + threadIdx.x;
-        int j = i < d.n ? p.lab[i] : -1;
-        if (j >= K) j = -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, j);
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane == leader && j >= 0) base = atomicAdd(&d.seg_cursor[j], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        if (j >= 0) d.perm[base + __popc(peers & ((1u << lane) - 1))] = (int)i;
+    const int* bh = d.seg_bh + (long long)blockIdx.x * K;
+    for (int j = threadIdx.x; j < K; j += blockDim.x) cur[j] = bh[j];
+    __syncthreads();
+    long long r0, r1;
+    block_rows(d, r0, r1);
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const int j = p.lab[i];
+        if (j < 0 || j >= K) continue;
+        d.perm[atomicAdd(&cur[j], 1)] = (int)i;
     }
 }
 
@@ -270,15 +293,16 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     double e_acc = 0.0;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
-        // cluster of chunk w: last j with seg_chunk[j] <= w
-        int lo = 0, hi = K - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (d.seg_chunk[mid] <= w) lo = mid; else hi = mid - 1;
-        }
-        const int j = lo;
+        const int j = d.seg_cmap[w];
         const long long r0 = d.seg_off[j] + (w - d.seg_chunk[j]) * SEG_ROWS;
-        const long long r1 = min((long long)d.seg_off[j + 1], r0 + SEG_ROWS);
+        const int cnt = (int)min((long long)SEG_ROWS, (long long)d.seg_off[j + 1] - r0);
+        // the chunk's row ids, 8 per lane, fetched up front (one round trip)
+        int rid[SEG_ROWS / 32];
+#pragma unroll
+        for (int u = 0; u < SEG_ROWS / 32; ++u) {
+            const int q = u * 32 + lane;
+            rid[u] = q < cnt ? d.perm[r0 + q] : -1;
+        }
         float c[V];
         double s[V];
 #pragma unroll
@@ -287,37 +311,36 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             c[v] = k < D ? __ldg(p.C + (long long)j * D + k) : 0.f;
             s[v] = 0.0;
         }
-        long long q = r0;
-        for (; q + 4 <= r1; q += 4) {
-            int rows[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) rows[u] = d.perm[q + u];
-            float xv[4][V];
+        for (int u = 0; u < SEG_ROWS / 32; ++u) {
+            if (u * 32 < cnt) {                   // predicate, not break: keeps rid[] in registers
+            float xv[8][V];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int b8 = 0; b8 < 32; b8 += 8) {
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    const int k = lane + 32 * v;
-                    xv[u][v] = k < D ? __ldcs(d.X + (long long)rows[u] * D + k) : 0.f;
+                for (int t = 0; t < 8; ++t) {
+                    const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const int k = lane + 32 * v;
+                        xv[t][v] = (row >= 0 && k < D) ? __ldcs(d.X + (long long)row * D + k) : 0.f;
+                    }
                 }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+                for (int t = 0; t < 8; ++t) {
+                    const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
+                    if (row < 0) continue;
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    s[v] += (double)xv[u][v];
-                    const double df = (double)xv[u][v] - (double)c[v];
-                    e_acc = fma(df, df, e_acc);
+                    for (int v = 0; v < V; ++v) {
+                        const int k = lane + 32 * v;
+                        if (k < D) {
+                            s[v] += (double)xv[t][v];
+                            const double df = (double)xv[t][v] - (double)c[v];
+                            e_acc = fma(df, df, e_acc);
+                        }
+                    }
                 }
-        }
-        for (; q < r1; ++q) {
-            const int row = d.perm[q];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const int k = lane + 32 * v;
-                const float x = k < D ? __ldcs(d.X + (long long)row * D + k) : 0.f;
-                s[v] += (double)x;
-                const double df = (double)x - (double)c[v];
-                e_acc = fma(df, df, e_acc);
+            }
             }
         }
 #pragma unroll
@@ -329,20 +352,102 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     finish_scalars(d, p.out, e_acc, 0);
 }
 
-cudaError_t setup_update() { return cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536); }
+// float4 variant (d = 4 * LPR, LPR in {1,2,4,8,16,32}): LPR lanes cover one
+// row, RPW = 32 / LPR rows per warp instruction, 16 rows in flight per warp.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    constexpr int RPW = 32 / LPR;
+    constexpr int U = (16 / RPW) > 0 ? 16 / RPW : 1;     // instructions per round
+    constexpr int ROUND = U * RPW;                       // rows per round (16, or 32 when RPW = 32)
+    const Pick p = pick(d, g);
+    const int D = d.d, K = d.K;
+    const int lane = threadIdx.x & 31;
+    const int h = lane / LPR, c4i = lane % LPR;          // row slot within the instruction, float4 index
+    const long long nchunks = d.seg_chunk[K];
+    const float4* X4 = reinterpret_cast<const float4*>(d.X);
+    double e_acc = 0.0;
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
+         w += (long long)gridDim.x * (blockDim.x >> 5)) {
+        const int j = d.seg_cmap[w];
+        const long long r0 = d.seg_off[j] + (w - d.seg_chunk[j]) * SEG_ROWS;
+        const int cnt = (int)min((long long)SEG_ROWS, (long long)d.seg_off[j + 1] - r0);
+        int rid[SEG_ROWS / 32];
+#pragma unroll
+        for (int t = 0; t < SEG_ROWS / 32; ++t) {
+            const int q = t * 32 + lane;
+            rid[t] = q < cnt ? d.perm[r0 + q] : -1;
+        }
+        const float4 c = __ldg(reinterpret_cast<const float4*>(p.C + (long long)j * D) + c4i);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int t = 0; t < SEG_ROWS / 32; ++t) {
+            if (t * 32 < cnt) {
+#pragma unroll
+                for (int r = 0; r < 32; r += ROUND) {
+                    float4 xv[U];
+                    int rw[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        rw[u] = __shfl_sync(0xffffffffu, rid[t], (r + u * RPW + h) & 31);
+                        xv[u] = rw[u] >= 0 ? __ldcs(X4 + (long long)rw[u] * LPR + c4i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (rw[u] >= 0) {
+                            s0 += (double)xv[u].x; s1 += (double)xv[u].y; s2 += (double)xv[u].z; s3 += (double)xv[u].w;
+                            double df = (double)xv[u].x - (double)c.x; e_acc = fma(df, df, e_acc);
+                            df = (double)xv[u].y - (double)c.y; e_acc = fma(df, df, e_acc);
+                            df = (double)xv[u].z - (double)c.z; e_acc = fma(df, df, e_acc);
+                            df = (double)xv[u].w - (double)c.w; e_acc = fma(df, df, e_acc);
+                        }
+                    }
+                }
+            }
+        }
+        // combine the RPW row slots (lanes with equal c4i), fixed xor order
+#pragma unroll
+        for (int o = LPR; o < 32; o <<= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+        }
+        if (h == 0) {
+            double* out = p.out + (long long)j * D + 4 * c4i;
+            red_add_f64(out, s0); red_add_f64(out + 1, s1); red_add_f64(out + 2, s2); red_add_f64(out + 3, s3);
+        }
+    }
+    finish_scalars(d, p.out, e_acc, 0);
+}
 
-bool update_sorted(const Dev& d) { return d.n >= AAKM_SORTED_MIN_ROWS && d.d <= 128; }
+cudaError_t setup_update() {
+    cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
+}
+
+bool update_sorted(const Dev& d) { return d.n >= AAKM_SORTED_MIN_ROWS && d.d <= 128 && d.K <= AAKM_SORTED_MAX_K; }
 
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     if (!update_sorted(d)) {
         k_update<<<d.upd_blocks, 256, 0, s>>>(d, g);
         return;
     }
-    cudaMemsetAsync(d.seg_count, 0, (size_t)d.K * 4, s);
-    const size_t hs = d.K <= 16384 ? (size_t)d.K * 4 : 0;
-    k_hist<<<d.upd_blocks, 256, hs, s>>>(d, g);
-    k_scan<<<1, 1024, 0, s>>>(d, g);
-    k_scatter<<<d.upd_blocks, 256, 0, s>>>(d, g);
+    const size_t hs = (size_t)d.K * 4;
+    k_hist<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
+    k_scan<<<1, 1024, 0, s>>>(d, g, AAKM_SEG_BLOCKS);
+    k_scatter<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
+    if (d.d % 4 == 0 && (d.d / 4) <= 32 && ((d.d / 4) & (d.d / 4 - 1)) == 0) {
+        switch (d.d / 4) {
+            case 1: k_segsum4<1><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+            case 2: k_segsum4<2><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+            case 4: k_segsum4<4><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+            case 8: k_segsum4<8><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+            case 16: k_segsum4<16><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+            default: k_segsum4<32><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+        }
+    }
     const int V = (d.d + 31) / 32;
     switch (V) {
         case 1: k_segsum<1><<<d.upd_blocks, 256, 0, s>>>(d, g); break;
