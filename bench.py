@@ -154,7 +154,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "tc16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -248,6 +248,10 @@ def main():
     if path == "tc":
         # 3xTF32 (fp32-equivalent): TF32 = bf16 x (1.1/2.25) nominal ratio, three MMAs per product
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * (1.1 / 2.25) / 3.0
+        bound = "tensor"
+    elif path == "tc16":
+        # 2xFP16 (fp32-equivalent): fp16 dense = bf16 dense, three MMAs per product
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 3.0
         bound = "tensor"
     else:
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12

@@ -21,7 +21,7 @@ _lib = None
 _lock = threading.Lock()
 
 KMEANS_M_MAX = 30
-PATHS = {"auto": 0, "simt": 1, "tc": 2}
+PATHS = {"auto": 0, "simt": 1, "tc": 2, "tc16": 3}
 STATUS = {0: "OK", 1: "INVALID", 2: "CUDA", 3: "NCCL", 4: "NOMEM", 5: "STATE"}
 
 

@@ -38,7 +38,10 @@ struct alignas(16) DevState {
     int hist_count, accepted_now, rejected_now, label_error;
     int n_alpha, fb_slot, final_traced, pad0;
     unsigned int cmax2_bits;     // max_j ||c_j||^2 of the centroids being assigned (float bits)
-    unsigned int cmax2_tmp, comb_ctr, upd_ctr, hist_ctr, pad2[3];
+    unsigned int cmax2_tmp, comb_ctr, upd_ctr, hist_ctr;
+    float c_scale;               // 2xFP16 engine: power-of-two scale of C
+    float tau_abs;               // 2xFP16 engine: absolute term of the near-tie bound
+    unsigned int pad2;
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -58,6 +61,12 @@ struct Dev {
     float* Chi;           // tf32(C) (tensor path)
     float* Clo;           // C - tf32(C)
     float* cn;            // ||c_j||^2 (fp32, from fp64)
+    void* Chi16;          // 2xFP16 engine: fp16 hi of C / s_c
+    void* Clo16;          // 2xFP16 engine: fp16 lo
+    int tc_kind;          // 0 = 3xTF32, 1 = 2xFP16
+    float x_scale;        // 2xFP16: power-of-two scale of X (|x|/s_x <= 2^13)
+    float x_inv_scale;
+    float x_absmax;
     int* lab[2];          // label ping-pong, lab[cur] = P^t, lab[cur^1] = P^{t-1}
     int* flag_rows;       // near-tie row list (capacity n)
     float* flag_b1;       // best fp32/3xTF32 score of each flagged row (capacity fcap)
@@ -109,6 +118,10 @@ void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream
 void* tc_make_maps(const Dev& d);   // TMA tensor maps of (X, C_hi, C_lo); nullptr if unsupported
 void tc_free_maps(void* m);
 bool tc_supported(int d, int K);
+bool tc16_supported(int d, int K);
+float tau_gamma_tc16(int d);
+void launch_csplit16(const Dev& d, int mode, cudaStream_t s);
+void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s);
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
 void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s);

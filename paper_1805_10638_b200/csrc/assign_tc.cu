@@ -22,6 +22,7 @@
 //              then per tile tcgen05.ld 32 columns at a time, score, argmin
 // X is read from HBM once; C tiles stream from L2.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <stdio.h>
 
 #include "aakm_dev.cuh"
@@ -43,7 +44,7 @@ constexpr int SMEM_LIMIT = 232448;                 // 227 KB opt-in
 float tau_gamma_tc(int d) { return 4.0f * (3.0f * 9.5367432e-7f + (3.0f * d / 8.0f + 8.0f) * 2.3841858e-7f); }
 
 struct TcMaps {
-    CUtensorMap x, chi, clo, xf;
+    CUtensorMap x, chi, clo, xf;     // chi/clo: tf32-split fp32 (kind 0) or fp16 (kind 1) operand maps
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -90,8 +91,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
     d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
     return d;
 }
-// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = TC_BN.
+// Instruction descriptors: D f32, both K-major, M = 128, N = TC_BN;
+// A/B tf32 (kind::tf32) or f16 (kind::f16).
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+constexpr uint32_t IDESC16 = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
     asm volatile(
@@ -100,6 +103,19 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(IDESC), "r"(accum)
         : "memory");
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(IDESC16), "r"(accum)
+        : "memory");
+}
+template <int KIND>
+__device__ __forceinline__ void mma_k(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+    if (KIND == 0) mma_tf32(tmem_d, a, b, accum);
+    else mma_f16(tmem_d, a, b, accum);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
@@ -140,7 +156,11 @@ __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag
 //         same scores (bitwise: same operands, same MMA sequence) and emits
 //         every centroid j with s_j <= b1 + tau_i -- the only centroids that
 //         can be the exact argmin (refine.cu decides them in fp64).
-template <int A, int MODE>   // d = 32 * A
+// KIND 0: 3xTF32 split (x_lo.c_hi + x_hi.c_lo + x_hi.c_hi, kind::tf32).
+// KIND 1: 2xFP16 split with power-of-two scales s_x, s_c: v/s = h + l, h and l
+//         fp16 (11-bit significands each, 22 bits together); the same three
+//         products at the f16 tensor rate (twice tf32), K = 16 per MMA.
+template <int A, int MODE, int KIND>   // d = 32 * A (KIND 1: A even)
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
             const __grid_constant__ CUtensorMap tm_clo, Dev d, GEval g, int S, int NT) {
@@ -153,9 +173,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     }
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* xhi = smem;
-    uint8_t* xlo = xhi + A * ATOM_BYTES_X;
-    uint8_t* stg = xlo + A * ATOM_BYTES_X;
+    constexpr int NATOM = KIND ? A / 2 : A;        // 128-B operand K-atoms per row
+    constexpr int AELEM = KIND ? 64 : 32;          // elements per operand atom
+    uint8_t* xst = smem;                            // fp32 X tile (TMA target)
+    uint8_t* xhi = KIND ? xst + A * ATOM_BYTES_X : xst;
+    uint8_t* xlo = xhi + NATOM * ATOM_BYTES_X;
+    uint8_t* stg = xlo + NATOM * ATOM_BYTES_X;
     float* cns = reinterpret_cast<float*>(stg + (size_t)S * STAGE_BYTES);
     uint64_t* bars = reinterpret_cast<uint64_t*>(cns + NT * TC_BN);
     uint64_t* full = bars;
@@ -194,14 +217,14 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 mbar_wait(xempty, xph ^ 1);
                 xph ^= 1;
                 mbar_expect_tx(xfull, A * ATOM_BYTES_X);
-                for (int a = 0; a < A; ++a) tma_load_2d(xhi + a * ATOM_BYTES_X, &tm_x, xfull, a * 32, (int)(tile * TC_BM));
+                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, &tm_x, xfull, a * 32, (int)(tile * TC_BM));
                 for (int nt = 0; nt < NT; ++nt) {
-                    for (int a = 0; a < A; ++a) {
+                    for (int a = 0; a < NATOM; ++a) {
                         mbar_wait(empty + s, ph ^ 1);
                         mbar_expect_tx(full + s, STAGE_BYTES);
                         uint8_t* st = stg + (size_t)s * STAGE_BYTES;
-                        tma_load_2d(st, &tm_chi, full + s, a * 32, nt * TC_BN);
-                        tma_load_2d(st + TC_BN * 128, &tm_clo, full + s, a * 32, nt * TC_BN);
+                        tma_load_2d(st, &tm_chi, full + s, a * AELEM, nt * TC_BN);
+                        tma_load_2d(st + TC_BN * 128, &tm_clo, full + s, a * AELEM, nt * TC_BN);
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                 }
@@ -219,7 +242,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     mbar_wait(acce + acc, aph ^ 1);
                     tc_fence_after();
                     const uint32_t dt = tmem + (uint32_t)(acc * TC_BN);
-                    for (int a = 0; a < A; ++a) {
+                    for (int a = 0; a < NATOM; ++a) {
                         mbar_wait(full + s, ph);
                         tc_fence_after();
                         const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
@@ -230,9 +253,9 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             const uint64_t al = sdesc(xlo_a + a * ATOM_BYTES_X + ko);
                             const uint64_t bh = sdesc(sb + ko);
                             const uint64_t bl = sdesc(sb + TC_BN * 128 + ko);
-                            mma_tf32(dt, al, bh, (a | kk) ? 1u : 0u);   // small terms first
-                            mma_tf32(dt, ah, bl, 1u);
-                            mma_tf32(dt, ah, bh, 1u);
+                            mma_k<KIND>(dt, al, bh, (a | kk) ? 1u : 0u);   // small terms first
+                            mma_k<KIND>(dt, ah, bl, 1u);
+                            mma_k<KIND>(dt, ah, bh, 1u);
                         }
                         mma_commit(empty + s);                     // frees the C stage when done
                         if (++s == S) { s = 0; ph ^= 1; }
@@ -249,26 +272,58 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
         const float gam = d.tau_gamma;
+        const float neg2s = KIND ? -2.0f * d.x_scale * d.st->c_scale : -2.0f;   // score = cn + neg2s * acc
+        const float tau_abs = KIND ? d.st->tau_abs : 0.0f;
         int acc = 0; uint32_t xph = 0, aph = 0;
         for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-            // split the X tile in place: hi = tf32(x) into xhi, lo = x - hi into xlo
+            // split the X tile: KIND 0 in place, hi = tf32(x) into xhi, lo = x - hi into xlo;
+            // KIND 1 from the fp32 staging tile into fp16 hi/lo operand tiles (scaled by 1/s_x)
             mbar_wait(xfull, xph);
             xph ^= 1;
             float xn = 0.f;
+            if (KIND == 0) {
 #pragma unroll
-            for (int a = 0; a < A; ++a) {
+                for (int a = 0; a < A; ++a) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
-                    float4 v = *reinterpret_cast<float4*>(xhi + off);
-                    float4 h, l;
-                    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
-                    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
-                    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
-                    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
-                    xn = fmaf(v.x, v.x, xn); xn = fmaf(v.y, v.y, xn); xn = fmaf(v.z, v.z, xn); xn = fmaf(v.w, v.w, xn);
-                    *reinterpret_cast<float4*>(xhi + off) = h;
-                    *reinterpret_cast<float4*>(xlo + off) = l;
+                    for (int c = 0; c < 8; ++c) {
+                        const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
+                        float4 v = *reinterpret_cast<float4*>(xhi + off);
+                        float4 h, l;
+                        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
+                        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
+                        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
+                        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
+                        xn = fmaf(v.x, v.x, xn); xn = fmaf(v.y, v.y, xn); xn = fmaf(v.z, v.z, xn); xn = fmaf(v.w, v.w, xn);
+                        *reinterpret_cast<float4*>(xhi + off) = h;
+                        *reinterpret_cast<float4*>(xlo + off) = l;
+                    }
+                }
+            } else {
+                const float inv_sx = d.x_inv_scale;
+#pragma unroll
+                for (int a16 = 0; a16 < NATOM; ++a16) {
+#pragma unroll
+                    for (int c16 = 0; c16 < 8; ++c16) {
+                        const int a32 = 2 * a16 + (c16 >> 2);
+                        const int c32 = (c16 & 3) * 2;
+                        const float4 v0 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + ((c32 ^ (r & 7)) << 4));
+                        const float4 v1 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + (((c32 + 1) ^ (r & 7)) << 4));
+                        const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                        uint32_t hp[4], lp[4];
+#pragma unroll
+                        for (int e = 0; e < 8; e += 2) {
+                            xn = fmaf(vv[e], vv[e], xn); xn = fmaf(vv[e + 1], vv[e + 1], xn);
+                            const float s0 = vv[e] * inv_sx, s1 = vv[e + 1] * inv_sx;       // exact (power of 2)
+                            const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
+                            const __half l0 = __float2half_rn(s0 - __half2float(h0));
+                            const __half l1 = __float2half_rn(s1 - __half2float(h1));
+                            hp[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                            lp[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+                        }
+                        const int off = a16 * ATOM_BYTES_X + r * 128 + ((c16 ^ (r & 7)) << 4);
+                        *reinterpret_cast<uint4*>(xhi + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+                        *reinterpret_cast<uint4*>(xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+                    }
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -296,7 +351,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         const float cj[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const float sc = fmaf(-2.0f, __uint_as_float(v[j + u]), cj[u]);
+                            const float sc = fmaf(neg2s, __uint_as_float(v[j + u]), cj[u]);
                             if (MODE == 0) {
                                 const bool p = sc < b1;
                                 b2 = fminf(b2, fmaxf(sc, b1));
@@ -317,7 +372,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             if (MODE == 0) {
                 const long long row = frow;
                 const bool ok = row < d.n;
-                const float tau = gam * (xn + cmax2);
+                const float tau = gam * (xn + cmax2) + tau_abs;
                 if (ok) lab_out[row] = i1;
                 push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
             } else if (frow < n_rows) {
@@ -336,21 +391,34 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 // ------------------------------------------------------------------ host side
 static int g_num_sms = 0;
 
-static size_t smem_need(int A, int S, int NT) {
-    return 1024 + (size_t)2 * A * ATOM_BYTES_X + (size_t)S * STAGE_BYTES + (size_t)NT * TC_BN * 4 + 256;
+static size_t smem_need(int kind, int A, int S, int NT) {
+    const int natom = kind ? A / 2 : A;
+    return 1024 + (size_t)(kind ? A : 0) * ATOM_BYTES_X + (size_t)2 * natom * ATOM_BYTES_X + (size_t)S * STAGE_BYTES +
+           (size_t)NT * TC_BN * 4 + 256;
 }
 
-static int pick_stages(int A, int NT) {
+static int pick_stages(int kind, int A, int NT) {
     for (int S = 6; S >= 2; --S)
-        if (smem_need(A, S, NT) <= (size_t)SMEM_LIMIT) return S;
+        if (smem_need(kind, A, S, NT) <= (size_t)SMEM_LIMIT) return S;
     return 0;
 }
 
 bool tc_supported(int d, int K) {
     if (d % 32 != 0 || d < 32 || d > 128) return false;
     const int NT = (K + TC_BN - 1) / TC_BN;
-    return pick_stages(d / 32, NT) >= 2;
+    return pick_stages(0, d / 32, NT) >= 2;
 }
+
+bool tc16_supported(int d, int K) {
+    if (d % 64 != 0 || d < 64 || d > 128) return false;
+    const int NT = (K + TC_BN - 1) / TC_BN;
+    return pick_stages(1, d / 32, NT) >= 2;
+}
+
+// 2xFP16 error bound: split error <= 3 * 2^-22 |x_k c_k|
+// (+ absolute subnormal term, tau_abs), accumulation over 3d/16 f16 MMA
+// k-steps (+16 for the internal 16-term dot) at <= 2^-22 each.
+float tau_gamma_tc16(int d) { return 4.0f * (3.0f * 2.3841858e-7f + (3.0f * d / 16.0f + 16.0f) * 2.3841858e-7f); }
 
 cudaError_t setup_tc() {
     int dev = 0;
@@ -358,10 +426,12 @@ cudaError_t setup_tc() {
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    const void* fns[8] = {(const void*)k_assign_tc<1, 0>, (const void*)k_assign_tc<2, 0>,
-                          (const void*)k_assign_tc<3, 0>, (const void*)k_assign_tc<4, 0>,
-                          (const void*)k_assign_tc<1, 1>, (const void*)k_assign_tc<2, 1>,
-                          (const void*)k_assign_tc<3, 1>, (const void*)k_assign_tc<4, 1>};
+    const void* fns[] = {(const void*)k_assign_tc<1, 0, 0>, (const void*)k_assign_tc<2, 0, 0>,
+                         (const void*)k_assign_tc<3, 0, 0>, (const void*)k_assign_tc<4, 0, 0>,
+                         (const void*)k_assign_tc<1, 1, 0>, (const void*)k_assign_tc<2, 1, 0>,
+                         (const void*)k_assign_tc<3, 1, 0>, (const void*)k_assign_tc<4, 1, 0>,
+                         (const void*)k_assign_tc<2, 0, 1>, (const void*)k_assign_tc<4, 0, 1>,
+                         (const void*)k_assign_tc<2, 1, 1>, (const void*)k_assign_tc<4, 1, 1>};
     for (auto f : fns) {
         e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
         if (e != cudaSuccess) return e;
@@ -385,38 +455,43 @@ static PFN_encodeTiled encoder() {
     return fn;
 }
 
-static bool encode_rows(CUtensorMap* m, const void* base, long long rows, int d, int box_rows) {
+// 2-D row-major map with a 128-byte inner box (32 fp32 or 64 fp16) and box_rows rows, SWIZZLE_128B
+static bool encode_rows(CUtensorMap* m, const void* base, long long rows, int d, int box_rows, bool f16) {
     PFN_encodeTiled enc = encoder();
     if (!enc) return false;
+    const int esz = f16 ? 2 : 4;
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)(rows > 0 ? rows : 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * esz};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-// Tensor maps for one Dev (X shard + its C_hi / C_lo buffers); opaque to the runtime.
+// Tensor maps for one Dev (X shard, C operand buffers, gathered rows); opaque to the runtime.
 void* tc_make_maps(const Dev& d) {
-    if (!tc_supported(d.d, d.K)) return nullptr;
+    const bool f16 = d.tc_kind == 1;
+    if (f16 ? !tc16_supported(d.d, d.K) : !tc_supported(d.d, d.K)) return nullptr;
     TcMaps* m = nullptr;
     if (posix_memalign((void**)&m, 64, sizeof(TcMaps)) != 0) return nullptr;
-    bool ok = encode_rows(&m->x, d.X, d.n, d.d, TC_BM) && encode_rows(&m->chi, d.Chi, d.K, d.d, TC_BN) &&
-              encode_rows(&m->clo, d.Clo, d.K, d.d, TC_BN) && encode_rows(&m->xf, d.Xf, d.fcap, d.d, TC_BM);
+    const void* chi = f16 ? (const void*)d.Chi16 : (const void*)d.Chi;
+    const void* clo = f16 ? (const void*)d.Clo16 : (const void*)d.Clo;
+    bool ok = encode_rows(&m->x, d.X, d.n, d.d, TC_BM, false) && encode_rows(&m->chi, chi, d.K, d.d, TC_BN, f16) &&
+              encode_rows(&m->clo, clo, d.K, d.d, TC_BN, f16) && encode_rows(&m->xf, d.Xf, d.fcap, d.d, TC_BM, false);
     if (!ok) { free(m); return nullptr; }
     return m;
 }
 
 void tc_free_maps(void* m) { free(m); }
 
-template <int MODE>
-static void launch_tc_mode(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
+template <int MODE, int KIND>
+static void launch_tc_kind(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
     const int A = d.d / 32;
     const int NT = (d.K + TC_BN - 1) / TC_BN;
-    const int S = pick_stages(A, NT);
-    const size_t smem = smem_need(A, S, NT);
+    const int S = pick_stages(KIND, A, NT);
+    const size_t smem = smem_need(KIND, A, S, NT);
     int grid = g_num_sms;
     const CUtensorMap& xm = MODE == 0 ? m->x : m->xf;
     if (MODE == 0) {
@@ -424,16 +499,74 @@ static void launch_tc_mode(const Dev& d, const GEval& g, const TcMaps* m, cudaSt
         if (n_tiles < grid) grid = (int)n_tiles;
     }
     if (grid < 1) grid = 1;
-    switch (A) {
-        case 1: k_assign_tc<1, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
-        case 2: k_assign_tc<2, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
-        case 3: k_assign_tc<3, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
-        default: k_assign_tc<4, MODE><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+    if (KIND == 0) {
+        switch (A) {
+            case 1: k_assign_tc<1, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+            case 2: k_assign_tc<2, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+            case 3: k_assign_tc<3, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+            default: k_assign_tc<4, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+        }
+    } else {
+        if (A == 2) k_assign_tc<2, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT);
+        else k_assign_tc<4, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT);
     }
+}
+
+template <int MODE>
+static void launch_tc_mode(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
+    if (d.tc_kind == 1) launch_tc_kind<MODE, 1>(d, g, m, s);
+    else launch_tc_kind<MODE, 0>(d, g, m, s);
 }
 
 void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
     launch_tc_mode<0>(d, g, static_cast<const TcMaps*>(maps), s);
+}
+
+// ---- 2xFP16 operand prep of the centroids (after every k_combine): power-of-two
+// scale s_c from max ||c||^2 (>= max |c_k|^2), C/s_c = h + l in fp16, and the
+// absolute (subnormal) part of the error bound.
+__global__ void __launch_bounds__(256) k_csplit16(Dev d, int mode) {
+    DevState* st = d.st;
+    if (mode == 0 && st->done) return;
+    if (mode == 1 && (st->done || !st->reject)) return;
+    const float cmax2 = __uint_as_float(st->cmax2_bits);
+    const float cmax = sqrtf(cmax2);
+    const float sc = cmax > 0.f ? exp2f(ceilf(log2f(cmax)) - 13.0f) : 1.0f;   // |c|/s_c <= 2^13 (< 65504)
+    const float inv = 1.0f / sc;                                                // exact (power of 2)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->c_scale = sc;
+        const float D = (float)d.d;
+        st->tau_abs = 8.0f * 2.9802322e-8f * (D * sc * d.x_absmax + sqrtf(D) * d.x_scale * cmax);
+    }
+    const long long KD = (long long)d.K * d.d;
+    __half* hi = reinterpret_cast<__half*>(d.Chi16);
+    __half* lo = reinterpret_cast<__half*>(d.Clo16);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
+        const float v = d.C[e] * inv;
+        const __half h = __float2half_rn(v);
+        hi[e] = h;
+        lo[e] = __float2half_rn(v - __half2float(h));
+    }
+}
+
+void launch_csplit16(const Dev& d, int mode, cudaStream_t s) {
+    long long KD = (long long)d.K * d.d;
+    int blocks = (int)((KD + 255) / 256);
+    if (blocks > 1184) blocks = 1184;
+    k_csplit16<<<blocks, 256, 0, s>>>(d, mode);
+}
+
+// max |x| over the shard (float bits of non-negative values order as uints)
+__global__ void k_absmax(const float* X, long long n, unsigned int* out) {
+    float m = 0.f;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(X[e]));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s) {
+    k_absmax<<<2 * (g_num_sms > 0 ? g_num_sms : 148), 256, 0, s>>>(X, n, out);
 }
 
 // ---- refine for the tensor-core engine: gather -> candidate pass -> exact fp64

@@ -8,6 +8,7 @@
 // vector per G-evaluation, issued in-stream (and captured in the graph).
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -130,7 +131,7 @@ static void dbg(const char* what, cudaStream_t s) {
 // ------------------------------------------------------------------ layout
 namespace {
 struct Layout {
-    size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
+    size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, perm, Gring, Fring, gram_part, trace, total,
         scratch_bytes;
@@ -151,6 +152,7 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.st_api = take(sizeof(DevState));
     L.C = take(KD * 4); L.Chi = take(KD * 4); L.Clo = take(KD * 4); L.cn = take((size_t)K * 4);
     L.Ca = take(KD * 4); L.Cahi = take(KD * 4); L.Calo = take(KD * 4); L.cna = take((size_t)K * 4);
+    L.C16h = take(KD * 2); L.C16l = take(KD * 2); L.Ca16h = take(KD * 2); L.Ca16l = take(KD * 2);
     L.lab0 = take((size_t)n * 4); L.lab1 = take((size_t)n * 4);
     L.flags = take((size_t)n * 4 + 4);
     const long long fc = fcap_of(n);
@@ -192,9 +194,12 @@ kmeans_status validate(long long n_local, int d, int k, const kmeans_config* cfg
     if (!(cfg->eps1 >= 0.0) || !(cfg->eps1 < cfg->eps2)) { why = "need 0 <= eps1 < eps2"; return KMEANS_ERR_INVALID; }
     if (cfg->max_iters < 1) { why = "max_iters < 1"; return KMEANS_ERR_INVALID; }
     if (!(cfg->ridge >= 0.0)) { why = "ridge < 0"; return KMEANS_ERR_INVALID; }
-    if (cfg->assign_path < 0 || cfg->assign_path > 2) { why = "bad assign_path"; return KMEANS_ERR_INVALID; }
+    if (cfg->assign_path < 0 || cfg->assign_path > 3) { why = "bad assign_path"; return KMEANS_ERR_INVALID; }
     if (cfg->assign_path == KMEANS_PATH_TC && !tc_supported(d, k)) {
-        why = "tensor-core path needs d % 32 == 0 and d <= 128"; return KMEANS_ERR_INVALID;
+        why = "tensor-core path needs d % 32 == 0, d <= 128, K <= ~8192"; return KMEANS_ERR_INVALID;
+    }
+    if (cfg->assign_path == KMEANS_PATH_TC16 && !tc16_supported(d, k)) {
+        why = "2xFP16 tensor-core path needs d in {64, 128}, K <= ~8192"; return KMEANS_ERR_INVALID;
     }
     return KMEANS_OK;
 }
@@ -202,15 +207,24 @@ kmeans_status validate(long long n_local, int d, int k, const kmeans_config* cfg
 
 // ------------------------------------------------------------------ enqueue helpers
 static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
-    if (h->path == KMEANS_PATH_TC) launch_assign_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
+    if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16)
+        launch_assign_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
     else launch_assign_simt(d, g, s);
+}
+
+// Centroid prep after every change of C (a1 / a13): ||c||^2, tf32 split, and
+// for the 2xFP16 engine the scaled fp16 hi/lo operands.
+static void combine(kmeans_handle* h, const Dev& d, int mode, const float* src, cudaStream_t s) {
+    launch_combine(d, mode, src, s);
+    h->launches++;
+    if (d.tc_kind == 1) { launch_csplit16(d, mode, s); h->launches++; }
 }
 
 // Exact re-decision of the near-tie rows: the tensor-core engine re-runs the
 // flagged rows in candidate mode (gather -> MMA pass -> fp64 on candidates);
 // rows beyond the candidate capacity (and the SIMT engine) use the SIMT refine.
 static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
-    if (h->path == KMEANS_PATH_TC) {
+    if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16) {
         launch_refine_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
         launch_refine(d, g, s, d.fcap);
         h->launches += 3;
@@ -231,7 +245,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     const Dev& d = h->d;
     GEval g{};
     g.branch = branch; g.force = 0; g.prev_mode = 0;
-    if (branch == 1) { launch_combine(d, 1, nullptr, s); h->launches++; dbg("combine_fb", s); }
+    if (branch == 1) { combine(h, d, 1, nullptr, s); dbg("combine_fb", s); }
     std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
     if (timing && branch == 0) {
         if (h->ev_used == h->ev.size()) {
@@ -274,7 +288,7 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
     dbg("gram", s);
     launch_solve(d, s);
     dbg("solve", s);
-    launch_combine(d, 0, nullptr, s);
+    combine(h, d, 0, nullptr, s);
     dbg("combine_mix", s);
     launch_advance(d, s);
     dbg("advance", s);
@@ -304,7 +318,7 @@ static kmeans_status ensure_graph(kmeans_handle* h) {
 static kmeans_status start(kmeans_handle* h, const float* C0) {
     launch_reset(h->d, h->stream);
     dbg("reset", h->stream);
-    launch_combine(h->d, 2, C0, h->stream);
+    combine(h, h->d, 2, C0, h->stream);
     dbg("combine_c0", h->stream);
     h->launches += 2;
     return enqueue_pass(h, h->stream, h->cfg.timing != 0);   // Algorithm 1 line 1
@@ -403,11 +417,16 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         long long gb = (KD + 127) / 128;
         D.gram_blocks = (int)(gb > AAKM_GRAM_BLOCKS ? AAKM_GRAM_BLOCKS : (gb < 1 ? 1 : gb));
     }
-    D.tau_gamma = h->path == KMEANS_PATH_TC ? tau_gamma_tc(d) : tau_gamma_simt(d);
+    D.tc_kind = h->path == KMEANS_PATH_TC16 ? 1 : 0;
+    D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
+    D.x_scale = 1.f; D.x_inv_scale = 1.f; D.x_absmax = 0.f;
+    D.tau_gamma = h->path == KMEANS_PATH_TC ? tau_gamma_tc(d)
+                : h->path == KMEANS_PATH_TC16 ? tau_gamma_tc16(d) : tau_gamma_simt(d);
     h->da = D;
     h->da.st = (DevState*)(w + L.st_api);
     h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
     h->da.cn = (float*)(w + L.cna);
+    h->da.Chi16 = w + L.Ca16h; h->da.Clo16 = w + L.Ca16l;
     h->scratch = w + L.scratch;
     h->scratch_bytes = L.scratch_bytes;
 
@@ -428,7 +447,20 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         }
     }
     CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
-    if (h->path == KMEANS_PATH_TC) {
+    if (h->path == KMEANS_PATH_TC16) {
+        // power-of-two scale of X for the fp16 split: |x| / s_x <= 2^13
+        unsigned int* amax = &((DevState*)(w + L.st))->pad2;
+        CKC(cudaMemsetAsync(amax, 0, 4, h->stream));
+        if (n_local > 0) launch_absmax(X, n_local * (long long)d, amax, h->stream);
+        unsigned int bits = 0;
+        CKC(cudaMemcpyAsync(&bits, amax, 4, cudaMemcpyDeviceToHost, h->stream));
+        CKC(cudaStreamSynchronize(h->stream));
+        float m;
+        memcpy(&m, &bits, 4);
+        const float sx = m > 0.f ? exp2f(ceilf(log2f(m)) - 13.0f) : 1.0f;
+        for (Dev* dv : {&h->d, &h->da}) { dv->x_absmax = m; dv->x_scale = sx; dv->x_inv_scale = 1.0f / sx; }
+    }
+    if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16) {
         h->tcm = tc_make_maps(h->d);
         h->tcm_api = tc_make_maps(h->da);
         if (!h->tcm || !h->tcm_api) {
@@ -469,7 +501,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     cudaStream_t s = h->stream;
     const Dev& d = h->da;
     CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
-    launch_combine(d, 2, C, s);
+    combine(h, d, 2, C, s);
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = labels_out;
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
@@ -693,7 +725,7 @@ kmeans_status kmeans_last_flagged(kmeans_handle* h, int64_t* flagged) {
 
 const char* kmeans_assign_path_name(const kmeans_handle* h) {
     if (!h) return "none";
-    return h->path == KMEANS_PATH_TC ? "tc" : "simt";
+    return h->path == KMEANS_PATH_TC ? "tc" : h->path == KMEANS_PATH_TC16 ? "tc16" : "simt";
 }
 
 kmeans_status kmeans_destroy(kmeans_handle* h) {

@@ -27,10 +27,18 @@ def handle(X, K, path="auto", **kw):
     return aakm.KMeans(dev(X), K, aakm.config(assign_path=path, **kw))
 
 
+def tc16_ok(d):
+    return d in (64, 128)
+
+
 @pytest.mark.parametrize("cfg,N,K", CASES)
-@pytest.mark.parametrize("path", ["auto", "simt"])
+@pytest.mark.parametrize("path", ["auto", "simt", "tc", "tc16"])
 def test_assign_parity(cfg, N, K, path):
     X, C0, c = make(cfg, N=N, K=K)
+    if path == "tc" and c.d % 32:
+        pytest.skip("3xTF32 engine needs d % 32 == 0")
+    if path == "tc16" and c.d not in (64, 128):
+        pytest.skip("2xFP16 engine needs d in {64, 128}")
     km = handle(X, c.K, path)
     rng = np.random.default_rng(1)
     prev = rng.integers(0, c.K, size=c.N).astype(np.int32)
@@ -121,9 +129,9 @@ def test_ragged_small_n(n):
     km.close()
 
 
-def _lockstep(cfg, N=None, K=None, seed=0, m0=5, max_passes=400):
+def _lockstep(cfg, N=None, K=None, seed=0, m0=5, max_passes=400, path="auto"):
     X, C0, c = make(cfg, seed=seed, N=N, K=K)
-    km = handle(X, c.K, m0=m0)
+    km = handle(X, c.K, path, m0=m0)
     info0 = km.aa_step(dev(C0))
     ora = oracle.AAState(X, oracle.OracleConfig(m0=m0, parity=True))
     ora.init(C0.astype(np.float64))
@@ -165,11 +173,17 @@ def test_aa_step_lockstep(cfg, N, K, seed):
     assert n >= 2
 
 
-@pytest.mark.parametrize("cfg,N,K,seed", [("c1", None, None, s) for s in range(5)] +
-                         [("c2", None, None, 0), ("c2", None, None, 1), ("c4", 8_000, 256, 0)])
-def test_end_to_end_parity(cfg, N, K, seed):
+@pytest.mark.parametrize("cfg,N,K", [("c4", 6_000, 128), ("c5", 4_000, 256)])
+def test_aa_step_lockstep_tc16(cfg, N, K):
+    assert _lockstep(cfg, N, K, 0, path="tc16") >= 2
+
+
+@pytest.mark.parametrize("cfg,N,K,seed,path", [("c1", None, None, s, "auto") for s in range(5)] +
+                         [("c2", None, None, 0, "auto"), ("c2", None, None, 1, "auto"), ("c4", 8_000, 256, 0, "tc"),
+                          ("c4", 8_000, 256, 0, "tc16"), ("c4", 20_000, 1024, 1, "tc16")])
+def test_end_to_end_parity(cfg, N, K, seed, path):
     X, C0, c = make(cfg, seed=seed, N=N, K=K)
-    km = handle(X, c.K, m0=5)
+    km = handle(X, c.K, path, m0=5)
     C, lab, rep = km.run(dev(C0))
     ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=5, parity=True))
     assert rep["converged"] and ref["converged"]

@@ -8,7 +8,7 @@ for cfg, N in [("c3", 30011), ("c4", 8003), ("c5", 8009), ("c5", 200000)]:
     X, C0, c = synthetic.make(cfg, N=N)
     Xd = torch.from_numpy(X).cuda()
     out = {}
-    for path in ("tc", "simt"):
+    for path in (("tc", "tc16", "simt") if c.d in (64, 128) else ("tc", "simt")):
         km = aakm.KMeans(Xd, c.K, aakm.config(assign_path=path))
         lab, E, _ = km.assign(torch.from_numpy(C0).cuda())
         torch.cuda.synchronize()
