@@ -105,7 +105,7 @@ def cpu_baseline(X, C0, cfgname, budget_rows=None):
     cores = os.cpu_count()
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     K, d = C0.shape
-    rows = budget_rows or max(1000, int(1.5e11 / (K * d)))  # ~1.5e11 fp64 sqdist terms (~10 s on 16 cores)
+    rows = budget_rows or max(1000, int(4.0e11 / (K * d)))  # ~4e11 fp64 sqdist terms (~10 s on 16 cores)
     rows = min(rows, len(X))
     Xs = np.ascontiguousarray(X[:rows])
     C = C0.astype(np.float64)

@@ -66,7 +66,7 @@ typedef enum {
 
 /* Assignment engine selection (kmeans_config.assign_path). */
 enum {
-    KMEANS_PATH_AUTO = 0,   /* tcgen05 3xTF32 when d % 32 == 0 and d <= 128, else SIMT */
+    KMEANS_PATH_AUTO = 0,   /* tcgen05 2xFP16 for d in {64,128}, 3xTF32 for other d % 32 == 0 <= 128, else SIMT */
     KMEANS_PATH_SIMT = 1,   /* register-tiled FP32 FFMA kernel                          */
     KMEANS_PATH_TC = 2,     /* tcgen05/TMEM 3xTF32 tile GEMM (requires d % 32 == 0, d <= 128) */
     KMEANS_PATH_TC16 = 3    /* tcgen05/TMEM 2xFP16 split (power-of-two scaled), d in {64, 128} */

@@ -73,7 +73,7 @@ struct Dev {
     float* flag_tau;      // its gap threshold tau_i
     float* Xf;            // gathered flagged rows (fcap x d) for the candidate pass
     int* cand;            // candidate centroids per flagged row (fcap x AAKM_MAXC)
-    int* cand_cnt;        // candidate count per flagged row (> AAKM_MAXC = overflow)
+    int* cand_cnt;        // candidate counts per flagged row and epilogue half (> AAKM_MAXC/2 = overflow)
     long long fcap;       // capacity of the candidate path (rows beyond -> SIMT refine)
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
     double* packed[2];    // [S (K*d) | N (K) | E | changed], branch A / B
@@ -91,6 +91,7 @@ struct Dev {
     int upd_blocks;
     int gram_blocks;
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
+    int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
 };
 
 // Which labels/centroids a G-evaluation kernel works on.

