@@ -61,14 +61,25 @@ __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const float* s
                 c = (float)v;
             }
             d.C[e] = c;
-            const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);  // tf32 truncation
+            // tensor operands hold -c (the engine accumulates ||c||^2/2 - x.c directly)
+            const float hi = __uint_as_float(__float_as_uint(-c) & 0xFFFFE000u);  // tf32 truncation
             d.Chi[e] = hi;
-            d.Clo[e] = c - hi;                                               // exact in fp32
+            d.Clo[e] = -c - hi;                                              // exact in fp32
             nrm = fma((double)c, (double)c, nrm);
         }
         for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
         const float cnj = (float)nrm;
         if (lane == 0) d.cn[j] = cnj;
+        if (d.cnimg && d.tc_kind == 0 && lane < 8) {
+            // 3xTF32 engine: ||c||^2/2 = h + m + l exactly (3 x 11 significand bits >= 24),
+            // row j of the folded K block; the A side holds (1, 1, 1, 0, ...)
+            const float v = 0.5f * cnj;
+            const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            const float m = __uint_as_float(__float_as_uint(v - h) & 0xFFFFE000u);
+            const float l = v - h - m;
+            const float val = lane == 0 ? h : lane == 1 ? m : lane == 2 ? l : 0.f;
+            *reinterpret_cast<float*>(d.cnimg + (size_t)(j >> 7) * AAKM_CNIMG_BYTES + cnimg_off((int)(j & 127), lane * 4)) = val;
+        }
         bmax = fmaxf(bmax, cnj);
     }
     // max ||c||^2: per-block max -> atomicMax into cmax2_tmp; last block publishes and resets

@@ -12,6 +12,7 @@
 #define AAKM_SORTED_MIN_ROWS 65536  // label-sorted update engine from this many rows
 #define AAKM_SORTED_MAX_K 16384     // ... and up to this many clusters (smem histograms)
 #define AAKM_SEG_BLOCKS 148         // row blocks of the histogram / scatter
+#define AAKM_CNIMG_BYTES 4096       // folded ||c||^2 block of one 128-centroid tile (128 rows x 32 B)
 
 namespace aakm {
 
@@ -41,7 +42,8 @@ struct alignas(16) DevState {
     unsigned int cmax2_tmp, comb_ctr, upd_ctr, hist_ctr;
     float c_scale;               // 2xFP16 engine: power-of-two scale of C
     float tau_abs;               // 2xFP16 engine: absolute term of the near-tie bound
-    unsigned int pad2;
+    float cn_amul;               // 2xFP16 engine: power-of-two A-side factor of the folded ||c||^2 column
+    unsigned int x_amax_bits;    // create-time scratch: max |x| over the shard (2xFP16 X scale)
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -61,6 +63,9 @@ struct Dev {
     float* Chi;           // tf32(C) (tensor path)
     float* Clo;           // C - tf32(C)
     float* cn;            // ||c_j||^2 (fp32, from fp64)
+    uint8_t* cnimg;       // tensor engines: ||c||^2/2 column block per 128-centroid tile, UMMA
+                          // no-swizzle K-major image (AAKM_CNIMG_BYTES per tile); nullptr on SIMT
+    unsigned int key_mul; // 32, from the host (keeps the key pack on the FMA pipe, see assign_tc.cu)
     void* Chi16;          // 2xFP16 engine: fp16 hi of C / s_c
     void* Clo16;          // 2xFP16 engine: fp16 lo
     int tc_kind;          // 0 = 3xTF32, 1 = 2xFP16
@@ -122,6 +127,9 @@ bool tc_supported(int d, int K);
 bool tc16_supported(int d, int K);
 float tau_gamma_tc16(int d);
 void launch_csplit16(const Dev& d, int mode, cudaStream_t s);
+__host__ __device__ inline unsigned int cnimg_off(int r, int byte) {   // (row, byte in its 32-B K row)
+    return (unsigned)((r >> 3) * 256 + (byte >> 4) * 128 + (r & 7) * 16 + (byte & 15));
+}
 void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s);
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
 void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);

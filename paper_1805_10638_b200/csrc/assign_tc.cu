@@ -6,25 +6,31 @@
 // tensor cores with a 3xTF32 split so the dot products keep ~fp32 accuracy:
 //     x.c ~= x_lo.c_hi + x_hi.c_lo + x_hi.c_hi,
 //     hi = tf32(v) (low 13 mantissa bits cleared), lo = v - hi (exact in fp32).
+// ||c||^2 is folded into the contraction: the C operands hold -c and one
+// extra K = 32-byte block pairs a constant A column (1's, or 2^p) with the
+// ||c||^2/2 column of each centroid tile (split into tf32 / fp16 parts, no
+// swizzle), so the accumulator IS the score ||c||^2/2 - x.c (no per-score FADD).
 // The argmin over centroids is fused into the epilogue (TMEM -> registers):
 // per row the best score b1 (index i1, lowest index on fp32 ties) and the
 // runner-up b2; rows with b2 - b1 within the engine's error bound are
 // flagged for the exact fp64 re-decision in refine.cu.
 //
 // Persistent, warp-specialised CTA (one per SM), BM = 128 rows, BN = 128
-// centroids per tile, UMMA 128 x 128 x 8 (kind::tf32, cta_group::1):
-//   warp 0     TMA producer: X tile (once per row tile, SWIZZLE_128B) and a
-//              ring of S stages, each one 32-element K-atom of C_hi and C_lo
-//   warp 1     MMA issuer (one elected thread), accumulators in TMEM,
-//              double-buffered (2 x 128 fp32 columns)
-//   warps 2-3  TMEM allocator (warp 2), then the X splitter: own a fp32
+// centroids per tile, UMMA 128 x 128 x 8 (kind::tf32) / x 16 (kind::f16),
+// cta_group::1.  Control warps have the highest warp ids (the SMSP arbiter
+// serves the highest eligible id first, so they are never starved):
+//   warp 16    TMA producer: ring of S stages, each one 128-B K-atom of C_hi
+//              and C_lo for 128 centroids (+ the folded ||c||^2 block)
+//   warp 17    MMA issuer (one elected thread), accumulators in TMEM,
+//              4 buffers x 128 fp32 columns
+//   warps 18-19 TMEM allocator (warp 18), then the X splitter: own a fp32
 //              staging tile, TMA-prefetch the next row tile, convert into
 //              (double-buffered) hi/lo operand tiles + ||x||^2
-//   warps 4-11 epilogue, two per SMSP (TMEM lane quarter = warp % 4): both
-//              halves split part of the X tile into hi/lo operands, then each
-//              half scores 64 of the 128 columns of every tile (tcgen05.ld 32
-//              at a time) with 4 independent running-min trackers per thread
-//              (no serial FMNMX chain), merged per row through shared memory
+//   warps 0-15 epilogue, four per SMSP (TMEM lane quarter = warp % 4): each
+//              column quarter scores 32 of the 128 columns of every tile (one
+//              tcgen05.ld.x32, accumulator released right after the load) with
+//              4 independent top-2 trackers per thread (no serial FMNMX chain);
+//              the quarters merge per row through shared memory
 // X is read from HBM once; C tiles stream from L2.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -36,12 +42,18 @@ namespace aakm {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BN = 128;
-constexpr int NTRK = 8;                            // independent top-2 trackers per thread (ILP)
+constexpr int NTRK = 4;                            // independent top-2 trackers per thread (ILP)
 constexpr int NACC = 4;                            // TMEM accumulator buffers (4 x 128 fp32 columns = 512)
-constexpr int TC_THREADS = 384;                    // 4 control warps + 8 epilogue warps
-constexpr int MAXCH = AAKM_MAXC / 2;              // candidate slots per row per epilogue half
+constexpr int NQ = 4;                              // epilogue column quarters (warps per SMSP)
+constexpr int TC_THREADS = 128 + NQ * 128;         // 4 control warps + 16 epilogue warps
+constexpr int MAXCH = AAKM_MAXC / NQ;              // candidate slots per row per column quarter
+constexpr int W_PROD = NQ * 4;                     // warp roles: epilogue warps 0..15 first, so the
+constexpr int W_MMA = W_PROD + 1;                  // SMSP arbiter (highest warp id first) never starves
+constexpr int W_SPLIT = W_PROD + 2;                // the producer / MMA issuer behind busy epilogue warps
+constexpr int XR = 8;                              // ||x||^2 ring depth (> max splitter lead of 2 + NACC tiles)
 constexpr int ATOM_BYTES_X = TC_BM * 128;          // one 32-element K-atom of the X tile
-constexpr int STAGE_BYTES = 2 * TC_BN * 128;       // C_hi atom + C_lo atom
+constexpr int STAGE_MAIN = 2 * TC_BN * 128;        // C_hi atom + C_lo atom
+constexpr int STAGE_BYTES = STAGE_MAIN + AAKM_CNIMG_BYTES;   // + the folded ||c||^2 block (first atom only)
 constexpr int SMEM_LIMIT = 232448;                 // 227 KB opt-in
 
 // Error bound of the 3xTF32 scores: per-product split
@@ -67,18 +79,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
-// Bounded wait: a lost arrival traps (error to the host) instead of hanging the GPU.
+// Bounded wait: a lost arrival traps (error to the host) after ~2^32 cycles
+// (2 s) instead of hanging the GPU.  No suspend-time hint: a sleeping warp
+// would wake late on the pipeline's critical path.
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    uint32_t ok = 0;
-    for (uint32_t spin = 0;; ++spin) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok) : "r"(su32(b)), "r"(parity), "r"(20000u) : "memory");   // suspend up to 20 us
-        if (ok) return;
-        if (spin > (1u << 22)) __trap();
-    }
+    if (mbar_try(b, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try(b, parity))
+        if (clock64() - t0 > (1ll << 32)) __trap();
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
@@ -99,6 +116,21 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
     d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
     return d;
 }
+// Same, SWIZZLE_NONE: 8-row x 16-B core matrices, LBO = 128 B between the two
+// K-adjacent core matrices of a 32-B K row, SBO = 256 B between 8-row groups.
+__device__ __forceinline__ uint64_t sdesc_ns(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(128 >> 4) << 16;                 // LBO: K direction
+    d |= (uint64_t)(256 >> 4) << 32;                 // SBO: M/N direction
+    d |= (uint64_t)1 << 46;
+    return d;                                        // layout type 0 = SWIZZLE_NONE
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+
 // Instruction descriptors: D f32, both K-major, M = 128, N = TC_BN;
 // A/B tf32 (kind::tf32) or f16 (kind::f16).
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
@@ -161,12 +193,14 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
     return r;
 }
 // key = score with its 5 low mantissa bits replaced by the column's position in
-// its 32-column batch; computed on the FMA pipe (IMAD.HI = >> 5, IMAD = *32 + j)
-__device__ __forceinline__ float pack_key(float sc, uint32_t j) {
+// its 32-column batch; computed on the FMA pipe (IMAD.HI = >> 5, IMAD = *k32 + j).
+// k32 == 32 comes from a kernel parameter: with a literal 32 ptxas emits an ALU-pipe
+// LEA, and the ALU pipe (FMNMX) is the epilogue's bottleneck.
+__device__ __forceinline__ float pack_key(uint32_t sc_bits, uint32_t j, uint32_t k32) {
     uint32_t hi, k;
-    asm("mul.hi.u32 %0, %1, 134217728;" : "=r"(hi) : "r"(__float_as_uint(sc)));
-    asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(k) : "r"(hi), "r"(j));
-    return __uint_as_float(k);
+    asm("mul.hi.u32 %0, %1, 134217728;" : "=r"(hi) : "r"(sc_bits));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(hi), "r"(k32), "n"(0));
+    return __uint_as_float(k + j);
 }
 
 __device__ __forceinline__ float4 lds128(uint32_t saddr) {
@@ -224,10 +258,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint8_t* xst = smem;                                           // fp32 X tile (TMA target, splitter-owned)
     uint8_t* opb = inplace ? smem : xst + A * ATOM_BYTES_X;        // operand buffers [hi | lo]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms
-    float* cns = reinterpret_cast<float*>(stg + (size_t)S * STAGE_BYTES);
-    float* xnorm = cns + NT * TC_BN;                               // [2][128] ||x||^2 per operand buffer
-    float* mrg = xnorm + 2 * TC_BM;                                // [128][4] half-1 partial results
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + 4 * TC_BM);
+    uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // constant A side of the folded ||c||^2 block
+    float* xnorm = reinterpret_cast<float*>(ablk + AAKM_CNIMG_BYTES); // [XR][128] ||x||^2 ring, slot = tile iteration % XR
+    float4* mrg = reinterpret_cast<float4*>(xnorm + XR * TC_BM);      // [NQ-1][128] partial results of quarters 1..3
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + (NQ - 1) * TC_BM);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* accf = bars + 2 * S;
@@ -235,22 +269,36 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint64_t* stfull = acce + NACC;                                // X staging landed
     uint64_t* opready = stfull + 1;                                // [2] operand buffer split
     uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(opempty + 2);
+    uint64_t* xready = opempty + 2;                                // [XR] ||x||^2 slot written (epilogue side)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XR);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = d.K;
-    // scores in units of U = 1 / (2 s_x s_c) (KIND 1) or 1/2 (KIND 0): s' = U cn - acc, so the
-    // epilogue needs one FADD per score (power-of-two scaling: exact)
-    const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;
-    for (int i = threadIdx.x; i < NT * TC_BN; i += TC_THREADS) cns[i] = i < K ? d.cn[i] * Usc : INFINITY;
+    // scores in units of U = 1 / (2 s_x s_c) (KIND 1) or 1/2 (KIND 0): the accumulator is
+    // s' = U cn - x.c/(s_x s_c) (power-of-two scaling: exact).  A side of the folded block:
+    // every row (1, 1, 1, 0, ...) in tf32 (KIND 0) or (2^p, 2^p, 0, ...) in fp16 (KIND 1).
+    {
+        uint32_t aw0 = 0x3F800000u;
+        if (KIND) {
+            const uint32_t hb = __half_as_ushort(__float2half_rn(d.st->cn_amul));
+            aw0 = hb | (hb << 16);
+        }
+        for (int i = threadIdx.x; i < TC_BM * 8; i += TC_THREADS) {
+            const int r = i >> 3, w = i & 7;
+            const uint32_t val = KIND ? (w == 0 ? aw0 : 0u) : (w < 3 ? aw0 : 0u);
+            *reinterpret_cast<uint32_t*>(ablk + cnimg_off(r, w * 4)) = val;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-        for (int b = 0; b < NACC; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, 8); }
+        for (int b = 0; b < NACC; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4); }
         for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2); mbar_init(opempty + b, 1); }
         mbar_init(stfull, 1);
+        for (int b = 0; b < XR; ++b) mbar_init(xready + b, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 2) {
+    if (warp == W_SPLIT) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                      "r"(NACC * TC_BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -262,28 +310,30 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     const long long n_tiles = (n_rows + TC_BM - 1) / TC_BM;
     const CUtensorMap* tmx = &tm_x;
 
-    if (warp == 0) {
+    if (warp == W_PROD) {
         if (lane == 0) {                                           // ---- TMA producer (C operands)
             int s = 0; uint32_t ph = 0;
             for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 for (int nt = 0; nt < NT; ++nt) {
                     for (int a = 0; a < NATOM; ++a) {
                         mbar_wait(empty + s, ph ^ 1);
-                        mbar_expect_tx(full + s, STAGE_BYTES);
+                        mbar_expect_tx(full + s, a == 0 ? STAGE_BYTES : STAGE_MAIN);
                         uint8_t* st = stg + (size_t)s * STAGE_BYTES;
                         const int ntl = (d.dbg & 1) ? 0 : nt;     // debug: re-load one C tile (L2-feed probe)
                         tma_load_2d(st, &tm_chi, full + s, a * AELEM, ntl * TC_BN);
                         tma_load_2d(st + TC_BN * 128, &tm_clo, full + s, a * AELEM, ntl * TC_BN);
+                        if (a == 0)
+                            bulk_load(st + STAGE_MAIN, d.cnimg + (size_t)ntl * AAKM_CNIMG_BYTES, AAKM_CNIMG_BYTES, full + s);
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         if (lane == 0) {                                           // ---- MMA issuer
             int s = 0, acc = 0; uint32_t ph = 0, aph = 0;
             uint32_t oph = 0;                                      // phase bit per operand buffer
-            const uint32_t opb_a = su32(opb), stg_a = su32(stg);
+            const uint32_t opb_a = su32(opb), stg_a = su32(stg), ablk_a = su32(ablk);
             int xb = 0;
             for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 mbar_wait(opready + xb, (oph >> xb) & 1u);
@@ -299,6 +349,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         mbar_wait(full + s, ph);
                         tc_fence_after();
                         const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
+                        if (a == 0 && !(d.dbg & 4))                // folded ||c||^2 block starts the sum
+                            mma_k<KIND>(dt, sdesc_ns(ablk_a), sdesc_ns(sb + STAGE_MAIN), 0u);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if (d.dbg & 4) break;                   // debug: no MMAs (feed/epilogue probe)
@@ -307,7 +359,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             const uint64_t al = sdesc(xlo_a + a * ATOM_BYTES_X + ko);
                             const uint64_t bh = sdesc(sb + ko);
                             const uint64_t bl = sdesc(sb + TC_BN * 128 + ko);
-                            mma_k<KIND>(dt, al, bh, (a | kk) ? 1u : 0u);   // small terms first
+                            mma_k<KIND>(dt, al, bh, 1u);               // small terms first
                             mma_k<KIND>(dt, ah, bl, 1u);
                             mma_k<KIND>(dt, ah, bh, 1u);
                         }
@@ -321,10 +373,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (++xb == nxb) xb = 0;
             }
         }
-    } else if (warp < 4) {                                         // ---- X splitter (warps 2, 3)
+    } else if (warp >= W_SPLIT) {                                  // ---- X splitter (warps 18, 19)
         // Owns the fp32 staging tile: TMA-prefetches the next row tile as soon as
         // the current one is converted, so the MMA never waits on X.
-        const int t = threadIdx.x - 64;                            // 0..63: rows t and t + 64
+        const int t = threadIdx.x - W_SPLIT * 32;                  // 0..63: rows t and t + 64
         uint32_t sph = 0;
         uint32_t eph = 0;                                          // phase bit per operand buffer
         int xb = 0;
@@ -334,7 +386,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile * TC_BM));
         }
         const float inv_sx = KIND ? d.x_inv_scale : 1.0f;
-        for (; tile < n_tiles; tile += gridDim.x) {
+        for (int it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
             mbar_wait(stfull, sph);
             sph ^= 1;
             if (!inplace) {
@@ -391,11 +443,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         }
                     }
                 }
-                xnorm[xb * TC_BM + r] = xn;
+                xnorm[(it % XR) * TC_BM + r] = xn;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(opready + xb);
+            if (lane == 0) { mbar_arrive(opready + xb); mbar_arrive(xready + it % XR); }
             // both splitter warps are done with the staging tile: prefetch the next one
             // (in place: only once the MMAs have consumed the tile)
             asm volatile("bar.sync 5, 64;" ::: "memory");
@@ -410,27 +462,27 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             }
             if (++xb == nxb) xb = 0;
         }
-    } else {                                                       // ---- epilogue (warps 4..11)
+    } else {                                                       // ---- epilogue (warps 0..15)
         const int q = warp & 3;                                    // TMEM lane quarter
-        const int half = (warp - 4) >> 2;                          // column half of every tile
+        const int cq = warp >> 2;                                  // column quarter of every tile
         const int r = q * 32 + lane;                               // row in tile == TMEM lane
         int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
         const float gam = d.tau_gamma;
-        const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;    // score units (see cns)
+        const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;    // score units
+        const uint32_t k32 = d.key_mul;
         const float tau_abs = KIND ? d.st->tau_abs : 0.0f;
-        int acc = 0, xb = 0; uint32_t aph = 0;
-        uint32_t oph = 0;
-        for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-            // ||x||^2 of this row: split already published (its MMAs cannot finish before this epilogue)
-            mbar_wait(opready + xb, (oph >> xb) & 1u);
-            oph ^= 1u << xb;
-            const float xn = half == 0 ? xnorm[xb * TC_BM + r] : 0.f;
-            if (++xb == nxb) xb = 0;
-            // 4 independent top-2 trackers (columns u = 0..3 mod 4).  MODE 0 keys pack the
-            // column's position inside its 32-column batch into the 5 low mantissa bits of
-            // the score (a <= 2^-18 |s| perturbation, added to tau), so one FMNMX carries
-            // value and index; BB remembers the batch base where each tracker's best moved.
+        int acc = 0; uint32_t aph = 0;
+        for (long long tile = blockIdx.x, it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+            // ||x||^2 of this row from its ring slot.  The splitter runs at most
+            // 2 + NACC tiles ahead of the epilogue (operand buffers + accumulators),
+            // so a ring of XR = 8 slots neither aliases a phase nor overwrites an unread slot.
+            mbar_wait(xready + it % XR, (uint32_t)(it / XR) & 1u);
+            const float xn = cq == 0 ? xnorm[(it % XR) * TC_BM + r] : 0.f;
+            // NTRK independent top-2 trackers.  MODE 0 keys pack the column's position
+            // inside its 32-column batch into the 5 low mantissa bits of the score (a
+            // <= 2^-18 |s| perturbation, added to tau), so one FMNMX carries value and
+            // index; BB remembers the batch base where each tracker's best moved.
             float B1[NTRK], B2[NTRK];
             int BB[NTRK];
 #pragma unroll
@@ -439,66 +491,55 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             float lim = -INFINITY;
             int cnt = 0;
             if (MODE == 1 && frow < n_rows) lim = d.flag_b1[frow] + d.flag_tau[frow];
-            const uint32_t cns_a = su32(cns);
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(accf + acc, aph);
                 tc_fence_after();
-                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_BN);
-                // both 32-column loads of this warp's half tile in flight, one wait
-                uint32_t vv[TC_BN / 64][32];
-#pragma unroll
-                for (int cbh = 0; cbh < TC_BN / 64; ++cbh)
-                    tmem_ld32_nowait(tbase + (half * (TC_BN / 64) + cbh) * 32, vv[cbh]);
-                tmem_wait_ld();
-#pragma unroll
-                for (int cbh = 0; cbh < TC_BN / 64; ++cbh) {
-                    const int cb = half * (TC_BN / 64) + cbh;
-                    const uint32_t* v = vv[cbh];
-                    if (d.dbg & 2) continue;                        // debug: no epilogue math
-                    const uint32_t cnp = cns_a + (uint32_t)((nt * TC_BN + cb * 32) * 4);
-                    const int j0 = nt * TC_BN + cb * 32;
-                    float O1[NTRK];
-#pragma unroll
-                    for (int u = 0; u < NTRK; ++u) O1[u] = B1[u];
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const float4 c4 = lds128(cnp + j * 4);
-                        const float sc0 = c4.x - __uint_as_float(v[j]), sc1 = c4.y - __uint_as_float(v[j + 1]);
-                        const float sc2 = c4.z - __uint_as_float(v[j + 2]), sc3 = c4.w - __uint_as_float(v[j + 3]);
-                        if (MODE == 0) {
-                            // two pairs -> trackers u = (j/2 + pp) mod NTRK
-#pragma unroll
-                            for (int pp = 0; pp < 2; ++pp) {
-                                const int u = ((j >> 1) + pp) & (NTRK - 1);
-                                const float ka = pack_key(pp ? sc2 : sc0, (uint32_t)(j + 2 * pp));
-                                const float kb = pack_key(pp ? sc3 : sc1, (uint32_t)(j + 2 * pp + 1));
-                                const float m = fminf(ka, kb), M = fmaxf(ka, kb);
-                                B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
-                                B1[u] = fminf(B1[u], m);
-                            }
-                        } else {
-                            const float sc[4] = {sc0, sc1, sc2, sc3};
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                if (sc[u] <= lim) {
-                                    if (cnt < MAXCH) d.cand[(frow * 2 + half) * MAXCH + cnt] = j0 + j + u;
-                                    ++cnt;
-                                }
-                            }
-                        }
-                    }
-                    if (MODE == 0) {
-#pragma unroll
-                        for (int u = 0; u < NTRK; ++u) BB[u] = B1[u] != O1[u] ? j0 : BB[u];
-                    }
-                }
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_BN + cq * 32), v);
+                // the scores are in registers: hand the accumulator back to the MMA warp
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acce + acc);
                 if (++acc == NACC) { acc = 0; aph ^= 1; }
+                if (d.dbg & 2) continue;                            // debug: no epilogue math
+                const int j0 = nt * TC_BN + cq * 32;
+                if (j0 + 32 > K) {                                  // ragged last tile: padded columns lose
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : 0x7F7FFFFFu;
+                }
+                float O1[NTRK];
+#pragma unroll
+                for (int u = 0; u < NTRK; ++u) O1[u] = B1[u];
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    if (MODE == 0) {
+                        // two pairs -> trackers u = (j/2 + pp) mod NTRK
+#pragma unroll
+                        for (int pp = 0; pp < 2; ++pp) {
+                            const int u = ((j >> 1) + pp) & (NTRK - 1);
+                            const float ka = pack_key(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
+                            const float kb = pack_key(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
+                            const float m = fminf(ka, kb), M = fmaxf(ka, kb);
+                            B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
+                            B1[u] = fminf(B1[u], m);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (__uint_as_float(v[j + u]) <= lim) {
+                                if (cnt < MAXCH) d.cand[(frow * NQ + cq) * MAXCH + cnt] = j0 + j + u;
+                                ++cnt;
+                            }
+                        }
+                    }
+                }
+                if (MODE == 0) {
+#pragma unroll
+                    for (int u = 0; u < NTRK; ++u) BB[u] = B1[u] != O1[u] ? j0 : BB[u];
+                }
             }
             if (MODE == 0) {
-                // merge the 4 trackers, then the two halves (ties -> lower column index)
+                // merge the trackers, then the column quarters (ties -> lower column index)
                 float b1 = B1[0], b2 = B2[0];
                 int i1 = BB[0] + (int)(__float_as_uint(B1[0]) & 31u);
 #pragma unroll
@@ -509,32 +550,36 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     i1 = tk ? iu : i1;
                     b1 = fminf(b1, B1[u]);
                 }
-                float* m = mrg + 4 * r;
-                if (half == 1) { m[0] = b1; m[1] = b2; m[2] = __int_as_float(i1); }
-                asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-                if (half == 0) {
-                    const float ob1 = m[0], ob2 = m[1];
-                    const int oi1 = __float_as_int(m[2]);
-                    b2 = fminf(fminf(b2, ob2), fmaxf(b1, ob1));
-                    const bool tk = ob1 < b1 || (ob1 == b1 && oi1 < i1);
-                    i1 = tk ? oi1 : i1;
-                    b1 = fminf(b1, ob1);
+                if (cq > 0) mrg[(cq - 1) * TC_BM + r] = make_float4(b1, b2, __int_as_float(i1), 0.f);
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");
+                if (cq == 0) {
+#pragma unroll
+                    for (int o = 0; o < NQ - 1; ++o) {
+                        const float4 m = mrg[o * TC_BM + r];
+                        const int oi1 = __float_as_int(m.z);
+                        b2 = fminf(fminf(b2, m.y), fmaxf(b1, m.x));
+                        const bool tk = m.x < b1 || (m.x == b1 && oi1 < i1);
+                        i1 = tk ? oi1 : i1;
+                        b1 = fminf(b1, m.x);
+                    }
                     const long long row = frow;
                     const bool ok = row < d.n;
-                    // tau in score units, + 2 key quanta (32 ulps each) of the larger-magnitude key
-                    const float tau = Usc * (gam * (xn + cmax2) + tau_abs) + 7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
+                    // tau in score units (the folded ||c||^2 term adds cmax2 to the accumulated
+                    // magnitude), + 2 key quanta (32 ulps each) of the larger-magnitude key
+                    const float tau = Usc * (gam * (xn + 2.0f * cmax2) + tau_abs) +
+                                      7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
                     if (ok) lab_out[row] = i1;
                     push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
                 }
-                asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // mrg reusable
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
             } else if (frow < n_rows) {
-                d.cand_cnt[frow * 2 + half] = cnt;
+                d.cand_cnt[frow * NQ + cq] = cnt;
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == W_SPLIT) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * TC_BN));
     }
@@ -548,7 +593,7 @@ static size_t smem_need(int kind, int A, int S, int NT, int NXB) {
     const int staging = NXB == 0 ? 0 : A;                  // NXB == 0: in place, one operand buffer
     const int nb = NXB == 0 ? 1 : NXB;
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * 2 * natom * ATOM_BYTES_X + (size_t)S * STAGE_BYTES +
-           (size_t)NT * TC_BN * 4 + 2 * TC_BM * 4 + 4 * TC_BM * 4 + 512;
+           AAKM_CNIMG_BYTES + XR * TC_BM * 4 + (NQ - 1) * TC_BM * 16 + 512;
 }
 
 // stages S and operand buffers NXB: prefer double-buffered X operands while
@@ -697,19 +742,41 @@ __global__ void __launch_bounds__(256) k_csplit16(Dev d, int mode) {
     const float cmax = sqrtf(cmax2);
     const float sc = cmax > 0.f ? exp2f(ceilf(log2f(cmax)) - 13.0f) : 1.0f;   // |c|/s_c <= 2^13 (< 65504)
     const float inv = 1.0f / sc;                                                // exact (power of 2)
+    // folded ||c||^2 column: score units U = 1 / (2 s_x s_c), cn U = amul (h + l) with h, l fp16
+    // and amul = 2^p (exact in fp16, p <= 15) keeping cn U / amul <= 2^14
+    const float U = 0.5f / (d.x_scale * sc);
+    const float cnu_max = cmax2 * U;
+    const float p = cnu_max > 16384.f ? fminf(ceilf(log2f(cnu_max)) - 14.0f, 15.0f) : 0.0f;
+    const float amul = exp2f(p), ainv = 1.0f / amul;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->c_scale = sc;
+        st->cn_amul = amul;
         const float D = (float)d.d;
-        st->tau_abs = 8.0f * 2.9802322e-8f * (D * sc * d.x_absmax + sqrtf(D) * d.x_scale * cmax);
+        // split subnormals of x and c, plus the fp16 subnormal floor of the folded column (amul 2^-24 in
+        // score units, i.e. amul 2^-24 / U in distance units)
+        st->tau_abs = 8.0f * 2.9802322e-8f * (D * sc * d.x_absmax + sqrtf(D) * d.x_scale * cmax) +
+                      amul * 5.9604645e-8f / U;
     }
     const long long KD = (long long)d.K * d.d;
     __half* hi = reinterpret_cast<__half*>(d.Chi16);
     __half* lo = reinterpret_cast<__half*>(d.Clo16);
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
-        const float v = d.C[e] * inv;
+        const float v = -d.C[e] * inv;                   // operands hold -c (scores accumulate directly)
         const __half h = __float2half_rn(v);
         hi[e] = h;
         lo[e] = __float2half_rn(v - __half2float(h));
+    }
+    if (d.cnimg) {
+        for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x) {
+            const float v = d.cn[j] * U * ainv;
+            const __half h = __float2half_rn(v);
+            const __half l = __float2half_rn(v - __half2float(h));
+            uint8_t* row = d.cnimg + (size_t)(j >> 7) * AAKM_CNIMG_BYTES;
+            const int r = (int)(j & 127);
+            *reinterpret_cast<uint32_t*>(row + cnimg_off(r, 0)) =
+                (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(l) << 16);
+            for (int b = 4; b < 32; b += 4) *reinterpret_cast<uint32_t*>(row + cnimg_off(r, b)) = 0u;
+        }
     }
 }
 
@@ -766,13 +833,21 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
             const int k = lane + 32 * v;
             xv[v] = k < D ? (double)__ldg(d.X + row * D + k) : 0.0;
         }
-        const int c0 = d.cand_cnt[2 * f], c1 = d.cand_cnt[2 * f + 1];
-        const bool all = c0 > MAXCH || c1 > MAXCH || c0 + c1 == 0;
-        const int nc = all ? d.K : c0 + c1;
+        int cc[NQ], tot = 0;
+        bool all = false;
+#pragma unroll
+        for (int o = 0; o < NQ; ++o) { cc[o] = d.cand_cnt[NQ * f + o]; all |= cc[o] > MAXCH; tot += cc[o]; }
+        all |= tot == 0;
+        const int nc = all ? d.K : tot;
         double bd = INFINITY;
         int bj = 0x7fffffff;
+        int qo = 0, qb = 0;                                   // quarter of candidate q, its first index
         for (int q = 0; q < nc; ++q) {
-            const int j = all ? q : (q < c0 ? d.cand[(2 * f) * MAXCH + q] : d.cand[(2 * f + 1) * MAXCH + q - c0]);
+            int j = q;
+            if (!all) {
+                while (q - qb >= cc[qo]) { qb += cc[qo]; ++qo; }
+                j = d.cand[(NQ * f + qo) * MAXCH + (q - qb)];
+            }
             double acc = 0.0;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {

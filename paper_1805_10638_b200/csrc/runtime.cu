@@ -131,7 +131,7 @@ static void dbg(const char* what, cudaStream_t s) {
 // ------------------------------------------------------------------ layout
 namespace {
 struct Layout {
-    size_t st, st_api, C, Chi, Clo, cn, Ca, Cahi, Calo, cna, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
+    size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, perm, Gring, Fring, gram_part, trace, total,
         scratch_bytes;
@@ -151,7 +151,10 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.st = take(sizeof(DevState));
     L.st_api = take(sizeof(DevState));
     L.C = take(KD * 4); L.Chi = take(KD * 4); L.Clo = take(KD * 4); L.cn = take((size_t)K * 4);
+    const size_t cnimg = (size_t)((K + 127) / 128) * AAKM_CNIMG_BYTES;
+    L.cnimg = take(cnimg);
     L.Ca = take(KD * 4); L.Cahi = take(KD * 4); L.Calo = take(KD * 4); L.cna = take((size_t)K * 4);
+    L.cnimga = take(cnimg);
     L.C16h = take(KD * 2); L.C16l = take(KD * 2); L.Ca16h = take(KD * 2); L.Ca16l = take(KD * 2);
     L.lab0 = take((size_t)n * 4); L.lab1 = take((size_t)n * 4);
     L.flags = take((size_t)n * 4 + 4);
@@ -160,7 +163,7 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.ftau = take((size_t)fc * 4 + 4);
     L.Xf = take((size_t)fc * d * 4 + 16);
     L.cand = take((size_t)fc * AAKM_MAXC * 4 + 4);
-    L.cand_cnt = take((size_t)fc * 8 + 8);
+    L.cand_cnt = take((size_t)fc * 16 + 16);
     const size_t pk = (KD + K + 2) * 8;
     L.scratch = o;
     size_t s0 = take(256);                 // flag counts
@@ -240,14 +243,11 @@ static kmeans_status allreduce(kmeans_handle* h, double* buf, cudaStream_t s) {
     return KMEANS_OK;
 }
 
-// One G-evaluation (assign -> refine -> update partials -> allreduce -> control).
-static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool timing) {
-    const Dev& d = h->d;
-    GEval g{};
-    g.branch = branch; g.force = 0; g.prev_mode = 0;
-    if (branch == 1) { combine(h, d, 1, nullptr, s); dbg("combine_fb", s); }
+// The assignment launch, bracketed by CUDA events on its own stream when timing
+// (kmeans_assign_timing reads them back).
+static kmeans_status timed_assign(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s, bool timing) {
     std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
-    if (timing && branch == 0) {
+    if (timing) {
         if (h->ev_used == h->ev.size()) {
             cudaEvent_t a, b;
             CK(h, cudaEventCreate(&a)); CK(h, cudaEventCreate(&b));
@@ -257,14 +257,25 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         CK(h, cudaEventRecord(evp->first, s));
     }
     assign_engine(h, d, g, s);
-    dbg("assign", s);
     if (evp) CK(h, cudaEventRecord(evp->second, s));
+    return KMEANS_OK;
+}
+
+// One G-evaluation (assign -> refine -> update partials -> allreduce -> control).
+static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool timing) {
+    const Dev& d = h->d;
+    GEval g{};
+    g.branch = branch; g.force = 0; g.prev_mode = 0;
+    if (branch == 1) { combine(h, d, 1, nullptr, s); dbg("combine_fb", s); }
+    kmeans_status st = timed_assign(h, d, g, s, timing && branch == 0);
+    if (st != KMEANS_OK) return st;
+    dbg("assign", s);
     refine_engine(h, d, g, s);
     dbg("refine", s);
     launch_update(d, g, s);
     dbg("update", s);
     h->launches += 3;
-    kmeans_status st = allreduce(h, d.packed[branch], s);
+    st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
     if (h->nranks > 1) dbg("allreduce", s);
     launch_control(d, branch, s);
@@ -421,6 +432,9 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         D.gram_blocks = (int)(gb > AAKM_GRAM_BLOCKS ? AAKM_GRAM_BLOCKS : (gb < 1 ? 1 : gb));
     }
     D.tc_kind = h->path == KMEANS_PATH_TC16 ? 1 : 0;
+    const bool tcpath = h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16;
+    D.cnimg = tcpath ? (uint8_t*)(w + L.cnimg) : nullptr;
+    D.key_mul = 32u;
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
     D.x_scale = 1.f; D.x_inv_scale = 1.f; D.x_absmax = 0.f;
@@ -430,6 +444,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     h->da.st = (DevState*)(w + L.st_api);
     h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
     h->da.cn = (float*)(w + L.cna);
+    h->da.cnimg = tcpath ? (uint8_t*)(w + L.cnimga) : nullptr;
     h->da.Chi16 = w + L.Ca16h; h->da.Clo16 = w + L.Ca16l;
     h->scratch = w + L.scratch;
     h->scratch_bytes = L.scratch_bytes;
@@ -453,7 +468,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     if (h->path == KMEANS_PATH_TC16) {
         // power-of-two scale of X for the fp16 split: |x| / s_x <= 2^13
-        unsigned int* amax = &((DevState*)(w + L.st))->pad2;
+        unsigned int* amax = &((DevState*)(w + L.st))->x_amax_bits;
         CKC(cudaMemsetAsync(amax, 0, 4, h->stream));
         if (n_local > 0) launch_absmax(X, n_local * (long long)d, amax, h->stream);
         unsigned int bits = 0;
@@ -509,11 +524,12 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = labels_out;
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
-    assign_engine(h, d, g, s);
+    kmeans_status st = timed_assign(h, d, g, s, h->cfg.timing != 0);
+    if (st != KMEANS_OK) return st;
     refine_engine(h, d, g, s);
     launch_update(d, g, s);
     h->launches += 4;
-    kmeans_status st = allreduce(h, d.packed[0], s);
+    st = allreduce(h, d.packed[0], s);
     if (st != KMEANS_OK) return st;
     const long long KD = (long long)d.K * d.d;
     CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + KD + d.K, 16, cudaMemcpyDeviceToHost, s));
