@@ -65,6 +65,7 @@ float tau_gamma_tc(int d) { return 4.0f * (3.0f * 9.5367432e-7f + (3.0f * d / 8.
 
 struct TcMaps {
     CUtensorMap x, chi, clo, xf;     // chi/clo: tf32-split fp32 (kind 0) or fp16 (kind 1) operand maps
+    CUtensorMap cn;                  // folded ||c||^2 image: rows of 1 KB, 4 rows (4 KB) per 128 centroids
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -225,6 +226,75 @@ __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag
     }
 }
 
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same object in CTA rank 0 of the cluster (the pair's leader)
+__device__ __forceinline__ uint32_t mapa0(uint32_t saddr) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t caddr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// Relaxed remote arrive: a pure "done reading TMEM" signal (the reads are ordered by
+// tcgen05.wait::ld + fence::before_thread_sync); release.cluster would add MEMBAR.GPU.
+__device__ __forceinline__ void mbar_arrive_cl_relaxed(uint32_t caddr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA 2-D load into this CTA's shared memory, completion signalled on the barrier at
+// cluster address bar (for CG == 2: the leader's, which counts both halves of a stage)
+template <int CG>
+__device__ __forceinline__ void tma_load_2d_cg(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+    if (CG == 2)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+            ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1) : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+            ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+template <int KIND, int CG>
+__device__ __forceinline__ void mma_cg(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum, uint32_t idesc) {
+    if (CG == 2) {
+        if (KIND == 0)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accum) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accum) : "memory");
+    } else {
+        if (KIND == 0)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accum) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accum) : "memory");
+    }
+}
+// completion of all prior MMAs arrives on bar in every CTA of the pair (same smem offset)
+template <int CG>
+__device__ __forceinline__ void commit_cg(uint64_t* bar) {
+    if (CG == 2)
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(su32(bar)), "h"((unsigned short)3) : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                     : "memory");
+}
+
 // ------------------------------------------------------------------ kernel
 // MODE 0: assignment of the shard (labels + near-tie flags).
 // MODE 1: candidate pass over the gathered flagged rows Xf: re-computes the
@@ -235,10 +305,13 @@ __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag
 // KIND 1: 2xFP16 split with power-of-two scales s_x, s_c: v/s = h + l, h and l
 //         fp16 (11-bit significands each, 22 bits together); the same three
 //         products at the f16 tensor rate (twice tf32), K = 16 per MMA.
-template <int A, int MODE, int KIND>   // d = 32 * A (KIND 1: A even)
+template <int A, int MODE, int KIND, int CG>   // d = 32 * A (KIND 1: A even); CG = CTAs per MMA (1 or 2)
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
-            const __grid_constant__ CUtensorMap tm_clo, Dev d, GEval g, int S, int NT, int NXB) {
+            const __grid_constant__ CUtensorMap tm_clo, const __grid_constant__ CUtensorMap tm_cn, Dev d, GEval g,
+            int S, int NT, int NXB) {
+    // Every CTA of a pair must run the same pipeline (barriers are shared), so the
+    // early exits depend only on grid-uniform device state.
     if (!geval_active(d, g)) return;
     long long n_rows = d.n;
     if (MODE == 1) {
@@ -249,6 +322,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     constexpr int NATOM = KIND ? A / 2 : A;        // 128-B operand K-atoms per row
     constexpr int AELEM = KIND ? 64 : 32;          // elements per operand atom
     constexpr int OPB = 2 * NATOM * ATOM_BYTES_X;  // one operand buffer: hi + lo
+    constexpr int AW = TC_BN * CG;                 // accumulator columns = centroids per pair tile
+    constexpr int NACC_ = 4 / CG;                  // accumulator buffers (512 TMEM columns)
+    constexpr uint32_t IDESC_ = (KIND ? IDESC16 : IDESC) & ~((0x3Fu << 17) | (0x1Fu << 24));
+    constexpr uint32_t IDESC_CG = IDESC_ | ((uint32_t)(AW >> 3) << 17) | ((uint32_t)((TC_BM * CG) >> 4) << 24);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     // NXB == 0: in-place mode (KIND 0, no room for a staging tile): the TMA
@@ -257,23 +334,25 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     const int nxb = inplace ? 1 : NXB;
     uint8_t* xst = smem;                                           // fp32 X tile (TMA target, splitter-owned)
     uint8_t* opb = inplace ? smem : xst + A * ATOM_BYTES_X;        // operand buffers [hi | lo]
-    uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms
+    uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
     uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // constant A side of the folded ||c||^2 block
     float* xnorm = reinterpret_cast<float*>(ablk + AAKM_CNIMG_BYTES); // [XR][128] ||x||^2 ring, slot = tile iteration % XR
     float4* mrg = reinterpret_cast<float4*>(xnorm + XR * TC_BM);      // [NQ-1][128] partial results of quarters 1..3
     uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + (NQ - 1) * TC_BM);
-    uint64_t* full = bars;
-    uint64_t* empty = bars + S;
-    uint64_t* accf = bars + 2 * S;
-    uint64_t* acce = accf + NACC;
-    uint64_t* stfull = acce + NACC;                                // X staging landed
-    uint64_t* opready = stfull + 1;                                // [2] operand buffer split
+    uint64_t* full = bars;                                         // [S]  stage landed (leader: both halves)
+    uint64_t* empty = bars + S;                                    // [S]  stage consumed (multicast commit)
+    uint64_t* accf = bars + 2 * S;                                 // [4]  accumulator ready (multicast commit)
+    uint64_t* acce = accf + 4;                                     // [4]  accumulator drained (leader: all epilogues)
+    uint64_t* stfull = acce + 4;                                   // X staging landed
+    uint64_t* opready = stfull + 1;                                // [2] operand buffer split (leader: both CTAs)
     uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
     uint64_t* xready = opempty + 2;                                // [XR] ||x||^2 slot written (epilogue side)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XR);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = d.K;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;          // position in the CTA pair
+    const bool leader = rank == 0;
     // scores in units of U = 1 / (2 s_x s_c) (KIND 1) or 1/2 (KIND 0): the accumulator is
     // s' = U cn - x.c/(s_x s_c) (power-of-two scaling: exact).  A side of the folded block:
     // every row (1, 1, 1, 0, ...) in tf32 (KIND 0) or (2^p, 2^p, 0, ...) in fp16 (KIND 1).
@@ -292,50 +371,66 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-        for (int b = 0; b < NACC; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4); }
-        for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2); mbar_init(opempty + b, 1); }
+        for (int b = 0; b < 4; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4 * CG); }
+        for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2 * CG); mbar_init(opempty + b, 1); }
         mbar_init(stfull, 1);
         for (int b = 0; b < XR; ++b) mbar_init(xready + b, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_SPLIT) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "r"(NACC * TC_BN));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)), "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)), "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync(); else __syncthreads();              // barrier inits visible to the peer
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const long long n_tiles = (n_rows + TC_BM - 1) / TC_BM;
+    // pair p processes row tiles (p + it * P) * CG + rank; both CTAs run the same
+    // iteration count (a partner past the end works on an all-OOB tile: zeros, no output)
+    const long long pair0 = blockIdx.x / CG, npairs = gridDim.x / CG;
+    auto tile_of = [&](long long it) { return (pair0 + it * npairs) * CG + rank; };
+    auto live = [&](long long it) { return (pair0 + it * npairs) * CG < n_tiles; };
+    // the leader's copy of a barrier (cluster address) -- where remote arrivals go
+    auto lead = [&](uint64_t* b) { return CG == 2 ? mapa0(su32(b)) : su32(b); };
     const CUtensorMap* tmx = &tm_x;
 
     if (warp == W_PROD) {
-        if (lane == 0) {                                           // ---- TMA producer (C operands)
+        if (lane == 0) {                                           // ---- TMA producer (C operands, this CTA's half)
             int s = 0; uint32_t ph = 0;
-            for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            for (long long it = 0; live(it); ++it) {
                 for (int nt = 0; nt < NT; ++nt) {
+                    const int ntl = (d.dbg & 1) ? 0 : nt;          // debug: re-load one C tile (L2-feed probe)
+                    const int crow = (ntl * CG + (int)rank) * TC_BN;   // first centroid of this CTA's half
                     for (int a = 0; a < NATOM; ++a) {
                         mbar_wait(empty + s, ph ^ 1);
-                        mbar_expect_tx(full + s, a == 0 ? STAGE_BYTES : STAGE_MAIN);
+                        if (leader) mbar_expect_tx(full + s, CG * (a == 0 ? STAGE_BYTES : STAGE_MAIN));
                         uint8_t* st = stg + (size_t)s * STAGE_BYTES;
-                        const int ntl = (d.dbg & 1) ? 0 : nt;     // debug: re-load one C tile (L2-feed probe)
-                        tma_load_2d(st, &tm_chi, full + s, a * AELEM, ntl * TC_BN);
-                        tma_load_2d(st + TC_BN * 128, &tm_clo, full + s, a * AELEM, ntl * TC_BN);
-                        if (a == 0)
-                            bulk_load(st + STAGE_MAIN, d.cnimg + (size_t)ntl * AAKM_CNIMG_BYTES, AAKM_CNIMG_BYTES, full + s);
+                        const uint32_t fb = lead(full + s);
+                        tma_load_2d_cg<CG>(st, &tm_chi, fb, a * AELEM, crow);
+                        tma_load_2d_cg<CG>(st + TC_BN * 128, &tm_clo, fb, a * AELEM, crow);
+                        if (a == 0) tma_load_2d_cg<CG>(st + STAGE_MAIN, &tm_cn, fb, 0, (ntl * CG + (int)rank) * 4);
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                 }
             }
+            for (int i = 0; i < S; ++i) {                          // drain: every commit to this CTA has landed
+                mbar_wait(empty + s, ph ^ 1);
+                if (++s == S) { s = 0; ph ^= 1; }
+            }
         }
     } else if (warp == W_MMA) {
-        if (lane == 0) {                                           // ---- MMA issuer
+        if (lane == 0 && leader) {                                 // ---- MMA issuer (the pair's leader)
             int s = 0, acc = 0; uint32_t ph = 0, aph = 0;
             uint32_t oph = 0;                                      // phase bit per operand buffer
             const uint32_t opb_a = su32(opb), stg_a = su32(stg), ablk_a = su32(ablk);
             int xb = 0;
-            for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            for (long long it = 0; live(it); ++it) {
                 mbar_wait(opready + xb, (oph >> xb) & 1u);
                 oph ^= 1u << xb;
                 tc_fence_after();
@@ -344,13 +439,13 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 for (int nt = 0; nt < NT; ++nt) {
                     mbar_wait(acce + acc, aph ^ 1);
                     tc_fence_after();
-                    const uint32_t dt = tmem + (uint32_t)(acc * TC_BN);
+                    const uint32_t dt = tmem + (uint32_t)(acc * AW);
                     for (int a = 0; a < NATOM; ++a) {
                         mbar_wait(full + s, ph);
                         tc_fence_after();
                         const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
                         if (a == 0 && !(d.dbg & 4))                // folded ||c||^2 block starts the sum
-                            mma_k<KIND>(dt, sdesc_ns(ablk_a), sdesc_ns(sb + STAGE_MAIN), 0u);
+                            mma_cg<KIND, CG>(dt, sdesc_ns(ablk_a), sdesc_ns(sb + STAGE_MAIN), 0u, IDESC_CG);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if (d.dbg & 4) break;                   // debug: no MMAs (feed/epilogue probe)
@@ -359,17 +454,17 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             const uint64_t al = sdesc(xlo_a + a * ATOM_BYTES_X + ko);
                             const uint64_t bh = sdesc(sb + ko);
                             const uint64_t bl = sdesc(sb + TC_BN * 128 + ko);
-                            mma_k<KIND>(dt, al, bh, 1u);               // small terms first
-                            mma_k<KIND>(dt, ah, bl, 1u);
-                            mma_k<KIND>(dt, ah, bh, 1u);
+                            mma_cg<KIND, CG>(dt, al, bh, 1u, IDESC_CG);   // small terms first
+                            mma_cg<KIND, CG>(dt, ah, bl, 1u, IDESC_CG);
+                            mma_cg<KIND, CG>(dt, ah, bh, 1u, IDESC_CG);
                         }
-                        mma_commit(empty + s);                     // frees the C stage when done
+                        commit_cg<CG>(empty + s);                  // frees the stage (both halves) when done
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
-                    mma_commit(accf + acc);                        // accumulator ready
-                    if (++acc == NACC) { acc = 0; aph ^= 1; }
+                    commit_cg<CG>(accf + acc);                     // accumulator ready in both CTAs
+                    if (++acc == NACC_) { acc = 0; aph ^= 1; }
                 }
-                mma_commit(opempty + xb);                          // operand buffer no longer read
+                commit_cg<CG>(opempty + xb);                       // operand buffers no longer read
                 if (++xb == nxb) xb = 0;
             }
         }
@@ -380,13 +475,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         uint32_t sph = 0;
         uint32_t eph = 0;                                          // phase bit per operand buffer
         int xb = 0;
-        long long tile = blockIdx.x;
-        if (t == 0 && tile < n_tiles) {
+        if (t == 0 && live(0)) {
             mbar_expect_tx(stfull, A * ATOM_BYTES_X);
-            for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile * TC_BM));
+            for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(0) * TC_BM));
         }
         const float inv_sx = KIND ? d.x_inv_scale : 1.0f;
-        for (int it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+        for (long long it = 0; live(it); ++it) {
             mbar_wait(stfull, sph);
             sph ^= 1;
             if (!inplace) {
@@ -447,19 +541,28 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) { mbar_arrive(opready + xb); mbar_arrive(xready + it % XR); }
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cl(lead(opready + xb));   // once per row tile: release.cluster is affordable
+                else mbar_arrive(opready + xb);
+                mbar_arrive(xready + it % XR);
+            }
             // both splitter warps are done with the staging tile: prefetch the next one
             // (in place: only once the MMAs have consumed the tile)
             asm volatile("bar.sync 5, 64;" ::: "memory");
-            const long long nxt = tile + gridDim.x;
-            if (inplace && nxt < n_tiles) {
+            if (inplace && live(it + 1)) {
                 mbar_wait(opempty, eph & 1u);
                 eph ^= 1u;
             }
-            if (t == 0 && nxt < n_tiles) {
+            if (t == 0 && live(it + 1)) {
                 mbar_expect_tx(stfull, A * ATOM_BYTES_X);
-                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(nxt * TC_BM));
+                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(it + 1) * TC_BM));
             }
+            if (++xb == nxb) xb = 0;
+        }
+        // drain: the operand-buffer commits of the last tiles have landed here
+        for (int i = 0; i < nxb; ++i) {
+            mbar_wait(opempty + xb, ((eph >> xb) & 1u) ^ 1u);
+            eph ^= 1u << xb;
             if (++xb == nxb) xb = 0;
         }
     } else {                                                       // ---- epilogue (warps 0..15)
@@ -470,10 +573,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
         const float gam = d.tau_gamma;
         const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;    // score units
-        const uint32_t k32 = d.key_mul;
         const float tau_abs = KIND ? d.st->tau_abs : 0.0f;
+        const uint32_t k32 = d.key_mul;
         int acc = 0; uint32_t aph = 0;
-        for (long long tile = blockIdx.x, it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+        for (long long it = 0; live(it); ++it) {
             // ||x||^2 of this row from its ring slot.  The splitter runs at most
             // 2 + NACC tiles ahead of the epilogue (operand buffers + accumulators),
             // so a ring of XR = 8 slots neither aliases a phase nor overwrites an unread slot.
@@ -487,55 +590,63 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             int BB[NTRK];
 #pragma unroll
             for (int u = 0; u < NTRK; ++u) { B1[u] = INFINITY; B2[u] = INFINITY; BB[u] = 0; }
-            const long long frow = tile * TC_BM + r;
+            const long long frow = tile_of(it) * TC_BM + r;
             float lim = -INFINITY;
             int cnt = 0;
             if (MODE == 1 && frow < n_rows) lim = d.flag_b1[frow] + d.flag_tau[frow];
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(accf + acc, aph);
                 tc_fence_after();
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_BN + cq * 32), v);
-                // the scores are in registers: hand the accumulator back to the MMA warp
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(acce + acc);
-                if (++acc == NACC) { acc = 0; aph ^= 1; }
-                if (d.dbg & 2) continue;                            // debug: no epilogue math
-                const int j0 = nt * TC_BN + cq * 32;
-                if (j0 + 32 > K) {                                  // ragged last tile: padded columns lose
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : 0x7F7FFFFFu;
-                }
-                float O1[NTRK];
-#pragma unroll
-                for (int u = 0; u < NTRK; ++u) O1[u] = B1[u];
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    if (MODE == 0) {
-                        // two pairs -> trackers u = (j/2 + pp) mod NTRK
-#pragma unroll
-                        for (int pp = 0; pp < 2; ++pp) {
-                            const int u = ((j >> 1) + pp) & (NTRK - 1);
-                            const float ka = pack_key(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
-                            const float kb = pack_key(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
-                            const float m = fminf(ka, kb), M = fmaxf(ka, kb);
-                            B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
-                            B1[u] = fminf(B1[u], m);
+#pragma unroll 1
+                for (int b = 0; b < CG; ++b) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * AW + (cq * CG + b) * 32), v);
+                    if (b == CG - 1) {
+                        // the scores are in registers: hand the accumulator back to the MMA warp
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (CG == 2) mbar_arrive_cl_relaxed(lead(acce + acc));
+                            else mbar_arrive(acce + acc);
                         }
-                    } else {
+                        if (++acc == NACC_) { acc = 0; aph ^= 1; }
+                    }
+                    if (d.dbg & 2) continue;                        // debug: no epilogue math
+                    const int j0 = nt * AW + (cq * CG + b) * 32;
+                    if (j0 + 32 > K) {                              // ragged last tile: padded columns lose
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            if (__uint_as_float(v[j + u]) <= lim) {
-                                if (cnt < MAXCH) d.cand[(frow * NQ + cq) * MAXCH + cnt] = j0 + j + u;
-                                ++cnt;
+                        for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : 0x7F7FFFFFu;
+                    }
+                    float O1[NTRK];
+#pragma unroll
+                    for (int u = 0; u < NTRK; ++u) O1[u] = B1[u];
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        if (MODE == 0) {
+                            // two pairs -> trackers u = (j/2 + pp) mod NTRK
+#pragma unroll
+                            for (int pp = 0; pp < 2; ++pp) {
+                                const int u = ((j >> 1) + pp) & (NTRK - 1);
+                                const float ka = pack_key(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
+                                const float kb = pack_key(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
+                                const float m = fminf(ka, kb), M = fmaxf(ka, kb);
+                                B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
+                                B1[u] = fminf(B1[u], m);
+                            }
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                if (__uint_as_float(v[j + u]) <= lim) {
+                                    if (cnt < MAXCH) d.cand[(frow * NQ + cq) * MAXCH + cnt] = j0 + j + u;
+                                    ++cnt;
+                                }
                             }
                         }
                     }
-                }
-                if (MODE == 0) {
+                    if (MODE == 0) {
 #pragma unroll
-                    for (int u = 0; u < NTRK; ++u) BB[u] = B1[u] != O1[u] ? j0 : BB[u];
+                        for (int u = 0; u < NTRK; ++u) BB[u] = B1[u] != O1[u] ? j0 : BB[u];
+                    }
                 }
             }
             if (MODE == 0) {
@@ -579,9 +690,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync();                                   // no CTA leaves while its peer may still signal it
     if (warp == W_SPLIT) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * TC_BN));
+        if (CG == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
@@ -598,9 +711,15 @@ static size_t smem_need(int kind, int A, int S, int NT, int NXB) {
 
 // stages S and operand buffers NXB: prefer double-buffered X operands while
 // keeping >= 3 C stages, else single-buffer (>= 2 stages)
+// AAKM_TC_MAXS / AAKM_TC_MAXNXB: perf-experiment caps (unset in normal runs)
+static int env_cap(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
 static void pick_pipe(int kind, int A, int NT, int& S, int& NXB) {
-    for (NXB = 2; NXB >= (kind == 0 ? 0 : 1); --NXB)
-        for (S = 6; S >= (NXB == 2 ? 3 : 2); --S)
+    static const int maxs = env_cap("AAKM_TC_MAXS", 6), maxnxb = env_cap("AAKM_TC_MAXNXB", 2);
+    for (NXB = maxnxb; NXB >= (kind == 0 ? 0 : 1); --NXB)
+        for (S = maxs; S >= (NXB == 2 ? 3 : 2); --S)
             if (smem_need(kind, A, S, NT, NXB) <= (size_t)SMEM_LIMIT) return;
     S = 0; NXB = -1;
 }
@@ -628,18 +747,19 @@ bool tc16_supported(int d, int K) {
 // k-steps (+16 for the internal 16-term dot) at <= 2^-22 each.
 float tau_gamma_tc16(int d) { return 4.0f * (3.0f * 2.3841858e-7f + (3.0f * d / 16.0f + 16.0f) * 2.3841858e-7f); }
 
+#define AAKM_TC_INSTANCES(X, CG)                                                                     \
+    X(1, 0, 0, CG) X(2, 0, 0, CG) X(3, 0, 0, CG) X(4, 0, 0, CG) X(1, 1, 0, CG) X(2, 1, 0, CG) X(3, 1, 0, CG) \
+    X(4, 1, 0, CG) X(2, 0, 1, CG) X(4, 0, 1, CG) X(2, 1, 1, CG) X(4, 1, 1, CG)
+
 cudaError_t setup_tc() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    const void* fns[] = {(const void*)k_assign_tc<1, 0, 0>, (const void*)k_assign_tc<2, 0, 0>,
-                         (const void*)k_assign_tc<3, 0, 0>, (const void*)k_assign_tc<4, 0, 0>,
-                         (const void*)k_assign_tc<1, 1, 0>, (const void*)k_assign_tc<2, 1, 0>,
-                         (const void*)k_assign_tc<3, 1, 0>, (const void*)k_assign_tc<4, 1, 0>,
-                         (const void*)k_assign_tc<2, 0, 1>, (const void*)k_assign_tc<4, 0, 1>,
-                         (const void*)k_assign_tc<2, 1, 1>, (const void*)k_assign_tc<4, 1, 1>};
+#define AAKM_FN(A_, M_, K_, C_) (const void*)k_assign_tc<A_, M_, K_, C_>,
+    const void* fns[] = {AAKM_TC_INSTANCES(AAKM_FN, 1) AAKM_TC_INSTANCES(AAKM_FN, 2)};
+#undef AAKM_FN
     for (auto f : fns) {
         e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
         if (e != cudaSuccess) return e;
@@ -678,6 +798,21 @@ static bool encode_rows(CUtensorMap* m, const void* base, long long rows, int d,
     return r == CUDA_SUCCESS;
 }
 
+// The folded ||c||^2 image (AAKM_CNIMG_BYTES per 128 centroids, already in the
+// UMMA no-swizzle layout) as a plain 2-D array of 1-KB rows, copied verbatim.
+static bool encode_cnimg(CUtensorMap* m, const void* base, int tiles) {
+    PFN_encodeTiled enc = encoder();
+    if (!enc || !base) return false;
+    cuuint64_t dims[2] = {256, (cuuint64_t)tiles * (AAKM_CNIMG_BYTES / 1024)};
+    cuuint64_t strides[1] = {1024};
+    cuuint32_t box[2] = {256, AAKM_CNIMG_BYTES / 1024};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Tensor maps for one Dev (X shard, C operand buffers, gathered rows); opaque to the runtime.
 void* tc_make_maps(const Dev& d) {
     const bool f16 = d.tc_kind == 1;
@@ -687,38 +822,78 @@ void* tc_make_maps(const Dev& d) {
     const void* chi = f16 ? (const void*)d.Chi16 : (const void*)d.Chi;
     const void* clo = f16 ? (const void*)d.Clo16 : (const void*)d.Clo;
     bool ok = encode_rows(&m->x, d.X, d.n, d.d, TC_BM, false) && encode_rows(&m->chi, chi, d.K, d.d, TC_BN, f16) &&
-              encode_rows(&m->clo, clo, d.K, d.d, TC_BN, f16) && encode_rows(&m->xf, d.Xf, d.fcap, d.d, TC_BM, false);
+              encode_rows(&m->clo, clo, d.K, d.d, TC_BN, f16) && encode_rows(&m->xf, d.Xf, d.fcap, d.d, TC_BM, false) &&
+              encode_cnimg(&m->cn, d.cnimg, (d.K + TC_BN - 1) / TC_BN);
     if (!ok) { free(m); return nullptr; }
     return m;
 }
 
 void tc_free_maps(void* m) { free(m); }
 
-template <int MODE, int KIND>
-static void launch_tc_kind(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
+// CTAs per MMA: 2 (cta_group::2 pairs: half the shared-memory operand traffic and
+// half the C-tile L2 reads per SM) unless AAKM_TC_CG=1 (experiments / fallback).
+static int tc_cg() {
+    static const int cg = getenv("AAKM_TC_CG") && atoi(getenv("AAKM_TC_CG")) == 1 ? 1 : 2;
+    return cg;
+}
+
+template <int A, int MODE, int KIND, int CG>
+static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, const GEval& g, int S, int NT, int NXB,
+                       long long n_tiles, size_t smem, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    int grid = g_num_sms;
+    if (CG == 2) {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        // pairs that can be co-resident (a persistent grid must not wait on itself)
+        static int max_clusters[2] = {0, 0};
+        int& mc = max_clusters[smem > 200 * 1024 ? 1 : 0];
+        if (mc == 0) {
+            cfg.gridDim = dim3(g_num_sms & ~1);
+            if (cudaOccupancyMaxActiveClusters(&mc, (const void*)k_assign_tc<A, MODE, KIND, CG>, &cfg) != cudaSuccess || mc < 1)
+                mc = g_num_sms / 2;
+            cudaGetLastError();
+        }
+        grid = 2 * mc;
+    }
+    if (MODE == 0 && n_tiles < grid) grid = (int)n_tiles;
+    if (CG == 2) grid = (grid + 1) & ~1;
+    if (grid < CG) grid = CG;
+    cfg.gridDim = dim3(grid);
+    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB);
+}
+
+template <int MODE, int KIND, int CG>
+static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
     const int A = d.d / 32;
-    const int NT = (d.K + TC_BN - 1) / TC_BN;
+    const int NT = (d.K + TC_BN * CG - 1) / (TC_BN * CG);
     int S, NXB;
     pick_pipe(KIND, A, NT, S, NXB);
     const size_t smem = smem_need(KIND, A, S, NT, NXB);
-    int grid = g_num_sms;
     const CUtensorMap& xm = MODE == 0 ? m->x : m->xf;
-    if (MODE == 0) {
-        const long long n_tiles = (d.n + TC_BM - 1) / TC_BM;
-        if (n_tiles < grid) grid = (int)n_tiles;
-    }
-    if (grid < 1) grid = 1;
+    const long long n_tiles = MODE == 0 ? (d.n + TC_BM - 1) / TC_BM : 1ll << 40;
     if (KIND == 0) {
         switch (A) {
-            case 1: k_assign_tc<1, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
-            case 2: k_assign_tc<2, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
-            case 3: k_assign_tc<3, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
-            default: k_assign_tc<4, MODE, 0><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB); break;
+            case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
+            case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
+            case 3: launch_one<3, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
+            default: launch_one<4, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
         }
     } else {
-        if (A == 2) k_assign_tc<2, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB);
-        else k_assign_tc<4, MODE, 1><<<grid, TC_THREADS, smem, s>>>(xm, m->chi, m->clo, d, g, S, NT, NXB);
+        if (A == 2) launch_one<2, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s);
+        else launch_one<4, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s);
     }
+}
+
+template <int MODE, int KIND>
+static void launch_tc_kind(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
+    if (tc_cg() == 2) launch_tc_cg<MODE, KIND, 2>(d, g, m, s);
+    else launch_tc_cg<MODE, KIND, 1>(d, g, m, s);
 }
 
 template <int MODE>
