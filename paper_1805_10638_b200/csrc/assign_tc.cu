@@ -98,6 +98,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     while (!mbar_try(b, parity))
         if (clock64() - t0 > (1ll << 32)) __trap();
 }
+// Same with a sleep between polls: for warps off the critical path (producer,
+// splitter), whose spinning would otherwise take issue slots from the epilogue.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, uint32_t ns) {
+    if (mbar_try(b, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try(b, parity)) {
+        __nanosleep(ns);
+        if (clock64() - t0 > (1ll << 32)) __trap();
+    }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
@@ -408,7 +418,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     const int ntl = (d.dbg & 1) ? 0 : nt;          // debug: re-load one C tile (L2-feed probe)
                     const int crow = (ntl * CG + (int)rank) * TC_BN;   // first centroid of this CTA's half
                     for (int a = 0; a < NATOM; ++a) {
-                        mbar_wait(empty + s, ph ^ 1);
+                        mbar_wait_sleep(empty + s, ph ^ 1, 32);
                         if (leader) mbar_expect_tx(full + s, CG * (a == 0 ? STAGE_BYTES : STAGE_MAIN));
                         uint8_t* st = stg + (size_t)s * STAGE_BYTES;
                         const uint32_t fb = lead(full + s);
@@ -481,10 +491,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         }
         const float inv_sx = KIND ? d.x_inv_scale : 1.0f;
         for (long long it = 0; live(it); ++it) {
-            mbar_wait(stfull, sph);
+            mbar_wait_sleep(stfull, sph, 128);
             sph ^= 1;
             if (!inplace) {
-                mbar_wait(opempty + xb, ((eph >> xb) & 1u) ^ 1u);  // the MMAs of tile - NXB are done
+                mbar_wait_sleep(opempty + xb, ((eph >> xb) & 1u) ^ 1u, 256);  // the MMAs of tile - NXB are done
                 eph ^= 1u << xb;
             }
             uint8_t* xhi = opb + xb * OPB;
@@ -597,20 +607,23 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(accf + acc, aph);
                 tc_fence_after();
-#pragma unroll 1
+                // all CG 32-column batches of this warp in flight at once, one wait, then
+                // the accumulator goes back to the MMA warp before any math
+                uint32_t vv[CG][32];
+#pragma unroll
+                for (int b = 0; b < CG; ++b)
+                    tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * AW + (cq * CG + b) * 32), vv[b]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cl_relaxed(lead(acce + acc));
+                    else mbar_arrive(acce + acc);
+                }
+                if (++acc == NACC_) { acc = 0; aph ^= 1; }
+#pragma unroll
                 for (int b = 0; b < CG; ++b) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * AW + (cq * CG + b) * 32), v);
-                    if (b == CG - 1) {
-                        // the scores are in registers: hand the accumulator back to the MMA warp
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (CG == 2) mbar_arrive_cl_relaxed(lead(acce + acc));
-                            else mbar_arrive(acce + acc);
-                        }
-                        if (++acc == NACC_) { acc = 0; aph ^= 1; }
-                    }
+                    uint32_t* v = vv[b];
                     if (d.dbg & 2) continue;                        // debug: no epilogue math
                     const int j0 = nt * AW + (cq * CG + b) * 32;
                     if (j0 + 32 > K) {                              // ragged last tile: padded columns lose
