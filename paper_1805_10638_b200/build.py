@@ -3,6 +3,7 @@ linked against the torch-wheel NCCL (the same libnccl.so.2 torch loads)."""
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -26,16 +27,23 @@ def nccl_dir():
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "aakm.h")]
-    newest = max(os.path.getmtime(p) for p in srcs + hdrs)
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "aakm.h")]
     nd = nccl_dir()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     flags = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
              "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include"),
              "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+    # content stamp (sources + flags): mtimes alone missed edits made while a build ran
+    h = hashlib.sha256(" ".join(flags).encode())
+    for p in srcs + hdrs:
+        h.update(p.encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    stamp = os.path.join(BUILD, "stamp")
+    digest = h.hexdigest()
+    if not force and os.path.exists(OUT) and os.path.exists(stamp) and open(stamp).read() == digest:
+        return OUT
+    os.makedirs(BUILD, exist_ok=True)
     objs = []
     procs = []
     for s in srcs:
@@ -57,6 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xlinker", "-rpath=" + lib]
     subprocess.check_call(cmd)
     os.replace(tmp, OUT)
+    with open(stamp, "w") as f:
+        f.write(digest)
     return OUT
 
 
