@@ -14,7 +14,10 @@ e2e    = the same metric through the C ABI with HOST inputs: every step copies
          reads C^{t+1} and E back.
 roofline = the dominant kernel (the assignment engine), algorithmic flops
          2 N K d per launch over its CUDA-event duration inside the timed
-         steps, against the tensor (3xTF32, fp32-equivalent) or FP32 peak.
+         steps, against the tensor (three MMAs per product, fp32-equivalent)
+         or FP32 peak.
+time_to_converge = Algorithm 1 and plain Lloyd run to convergence on
+         --ttc-config (default c3; c5 does not converge within 5000 passes).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
        python bench.py --impl reference ...   (the CPU oracle arm)
@@ -146,6 +149,40 @@ def run_reference(args):
     return 0
 
 
+# --------------------------------------------------------------------- time to converge
+def time_to_converge(cfgname, rank, world, barrier):
+    """Algorithm 1 (dynamic m, m0 = 5) and plain Lloyd (m = 0) run to convergence
+    (rule R3) through kmeans_run on the sharded config, C^0 resident; CUDA events
+    around the call, max over ranks.  (c5 itself does not converge within 5000
+    passes under either variant, see profiles/r01_converge_gpu.jsonl.)"""
+    import torch
+    import torch.distributed as dist
+    from paper_1805_10638_b200 import aakm, synthetic
+    X, C0, cfg = synthetic.make(cfgname, seed=0)
+    lo, hi = synthetic.shard_bounds(cfg.N, rank, world)
+    Xs = torch.from_numpy(X[lo:hi]).cuda()
+    C0d = torch.from_numpy(C0).cuda()
+    out = {"config": cfgname, "N": cfg.N, "d": cfg.d, "K": cfg.K}
+    for name, kw in (("aa", dict(m0=cfg.m0)), ("lloyd", dict(m0=0, dynamic_m=False))):
+        km = aakm.KMeans(Xs, cfg.K, aakm.config(max_iters=20000, **kw), n_global=cfg.N, rank=rank, nranks=world)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(km.stream)
+        _, _, rep = km.run(C0d)
+        e1.record(km.stream)
+        barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        km.close()
+        pre = "" if name == "aa" else "lloyd_"
+        out.update({pre + "seconds": float(t.item()), pre + "iters": rep["iters"], pre + "n_assign": rep["n_assign"],
+                    pre + "converged": bool(rep["converged"]), pre + "energy": rep["energy"]})
+        if name == "aa":
+            out.update({"accepted": rep["n_accepted"], "rejected": rep["n_rejected"], "m_final": rep["m_final"]})
+    return out
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -157,6 +194,7 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "tc16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ttc-config", default="c3", help="config run to convergence for time_to_converge ('none' skips)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -279,9 +317,11 @@ def main():
                      "kernel": f"assign_{path}", "avg_launch_ms": avg_ms, "launches": a_n},
         "clocks": clk.summary(),
     }
+    km.close()
+    if args.ttc_config != "none":
+        line["time_to_converge"] = time_to_converge(args.ttc_config, rank, world, barrier)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(X, C0, args.config)
-    km.close()
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

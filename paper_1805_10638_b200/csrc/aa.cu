@@ -248,29 +248,33 @@ void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0,
 // Lane r owns row r of the Cholesky factor in registers (compile-time
 // indexed, fully unrolled); columns move between lanes with shuffles.
 #define FULL 0xffffffffu
-__global__ void __launch_bounds__(32) k_solve(Dev d) {
+__global__ void __launch_bounds__(1024) k_solve(Dev d) {
     DevState* st = d.st;
     if (st->done) return;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int H = d.H;
     const long long t = st->t;
     const int init = st->init_mode;
     const int W = init ? 0 : (int)(t < H - 1 ? t : H - 1);
     const int ts = (int)(t % H);
-    // fixed-order reduction of the Gram partials of this pass
-    for (int q = lane; q < 2 * W; q += 32) {
+    // fixed-order reduction of the Gram partials of this pass: one warp per entry,
+    // lanes stride over the blocks, then a fixed xor tree (same bytes on every rank)
+    for (int q = warp; q < 2 * W; q += 32) {
         double v = 0.0;
-        for (int b = 0; b < d.gram_blocks; ++b) v += d.gram_part[(long long)b * 2 * H + q];
-        if (q < W) {
-            const int s2 = (int)((t - q) % H);
-            st->gram[ts * H + s2] = v;
-            st->gram[s2 * H + ts] = v;
-        } else {
-            st->bvec[q - W] = v;
+        for (int b = lane; b < d.gram_blocks; b += 32) v += d.gram_part[(long long)b * 2 * H + q];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+            if (q < W) {
+                const int s2 = (int)((t - q) % H);
+                st->gram[ts * H + s2] = v;
+                st->gram[s2 * H + ts] = v;
+            } else {
+                st->bvec[q - W] = v;
+            }
         }
     }
-    __threadfence_block();
-    __syncwarp();
+    __syncthreads();
+    if (warp != 0) return;                          // the solve itself is one warp
     int m_t = init ? 0 : (st->m < t ? st->m : (int)t);
     if (m_t > W) m_t = W;
     // column a <-> dF(t - a); lane a holds column a's scale and rhs
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(32) k_solve(Dev d) {
 }
 #undef FULL
 
-void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 32, 0, s>>>(d); }
+void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 1024, 0, s>>>(d); }
 
 // ---------------------------------------------------------------- advance
 __global__ void k_advance(Dev d) {

@@ -199,10 +199,10 @@ kmeans_status validate(long long n_local, int d, int k, const kmeans_config* cfg
     if (!(cfg->ridge >= 0.0)) { why = "ridge < 0"; return KMEANS_ERR_INVALID; }
     if (cfg->assign_path < 0 || cfg->assign_path > 3) { why = "bad assign_path"; return KMEANS_ERR_INVALID; }
     if (cfg->assign_path == KMEANS_PATH_TC && !tc_supported(d, k)) {
-        why = "tensor-core path needs d % 32 == 0, d <= 128, K <= ~8192"; return KMEANS_ERR_INVALID;
+        why = "tensor-core path needs d % 32 == 0 and d <= 128"; return KMEANS_ERR_INVALID;
     }
     if (cfg->assign_path == KMEANS_PATH_TC16 && !tc16_supported(d, k)) {
-        why = "2xFP16 tensor-core path needs d in {64, 128}, K <= ~8192"; return KMEANS_ERR_INVALID;
+        why = "2xFP16 tensor-core path needs d in {64, 128}"; return KMEANS_ERR_INVALID;
     }
     return KMEANS_OK;
 }

@@ -1,0 +1,72 @@
+"""-m gpu: the tensor-core assignment engines at shapes the main parity cases do
+not reach -- ragged K (partial 256-centroid pair tiles and 128-centroid halves
+past K), n with a partial last row-tile pair, the single-SM (cta_group::1)
+variant -- each against the CPU oracle under the north-star tie rule."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+from gpu_helpers import check_assign, dev, make, require_gpu
+from paper_1805_10638_b200 import aakm
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    require_gpu()
+
+
+@pytest.mark.parametrize("path,cfg", [("tc", "c3"), ("tc", "c5"), ("tc16", "c5"), ("tc16", "c4")])
+@pytest.mark.parametrize("K", [1, 100, 129, 257, 300, 1000])
+def test_ragged_k(path, cfg, K):
+    X, C0, c = make(cfg, N=3001, K=K)
+    km = aakm.KMeans(dev(X), c.K, aakm.config(assign_path=path))
+    rng = np.random.default_rng(K)
+    C = C0 + rng.normal(0, 0.01, C0.shape).astype(np.float32)
+    lab, E, _ = km.assign(dev(C))
+    lab = lab.cpu().numpy()
+    assert lab.min() >= 0 and lab.max() < c.K
+    check_assign(X, C, lab, msg=f"{path}/{cfg}/K={K}")
+    E_ora = oracle.energy(X, C.astype(np.float64), lab)
+    assert abs(E - E_ora) <= 1e-6 * E_ora
+    km.close()
+
+
+@pytest.mark.parametrize("n", [128, 129, 255, 256, 257, 383, 385])
+def test_row_tile_pairs(n):
+    # 2-CTA pairs take row tiles two at a time: odd tile counts leave the partner
+    # of the last pair with an all-out-of-bounds tile
+    X, C0, c = make("c5", N=max(n, 300), K=100)
+    X = X[:n]
+    km = aakm.KMeans(dev(X), c.K, aakm.config(assign_path="tc16"))
+    lab, _, _ = km.assign(dev(C0))
+    check_assign(X, C0, lab.cpu().numpy(), msg=f"n={n}")
+    km.close()
+
+
+def test_single_sm_variant_subprocess():
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle
+from gpu_helpers import check_assign, dev, make
+from paper_1805_10638_b200 import aakm
+for path, cfg in (("tc16", "c5"), ("tc", "c3")):
+    X, C0, c = make(cfg, N=5003, K=300)
+    km = aakm.KMeans(dev(X), c.K, aakm.config(assign_path=path))
+    lab, E, _ = km.assign(dev(C0))
+    check_assign(X, C0, lab.cpu().numpy(), msg=path)
+    C, lab, rep = km.run(dev(C0))
+    assert rep["converged"], rep
+    km.close()
+print("ok")
+""" % (ROOT, os.path.join(ROOT, "tests"))
+    env = dict(os.environ, AAKM_TC_CG="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
