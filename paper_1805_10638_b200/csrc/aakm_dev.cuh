@@ -40,7 +40,7 @@ struct alignas(16) DevState {
     int n_alpha, fb_slot, final_traced, pad0;
     unsigned int cmax2_bits;     // max_j ||c_j||^2 of the centroids being assigned (float bits)
     unsigned int cmax2_tmp, comb_ctr, upd_ctr, hist_ctr;
-    float c_scale;               // 2xFP16 engine: power-of-two scale of C
+    float c_scale;               // 2xFP16 engine: common power-of-two operand scale s (x/s, c/s)
     float tau_abs;               // 2xFP16 engine: absolute term of the near-tie bound
     float cn_amul;               // 2xFP16 engine: power-of-two A-side factor of the folded ||c||^2 column
     unsigned int x_amax_bits;    // create-time scratch: max |x| over the shard (2xFP16 X scale)
@@ -69,9 +69,10 @@ struct Dev {
     void* Chi16;          // 2xFP16 engine: fp16 hi of C / s_c
     void* Clo16;          // 2xFP16 engine: fp16 lo
     int tc_kind;          // 0 = 3xTF32, 1 = 2xFP16
-    float x_scale;        // 2xFP16: power-of-two scale of X (|x|/s_x <= 2^13)
+    float x_scale;        // 2xFP16: create-time scale from max |x| (informational)
     float x_inv_scale;
-    float x_absmax;
+    float x_absmax;       // 2xFP16: max |x_ik| over the shard (subnormal part of the error bound)
+    float x_nmax;         // 2xFP16: max ||x_i|| over the shard (fixes the common operand scale)
     int* lab[2];          // label ping-pong, lab[cur] = P^t, lab[cur^1] = P^{t-1}
     int* flag_rows;       // near-tie row list (capacity n)
     float* flag_b1;       // best fp32/3xTF32 score of each flagged row (capacity fcap)
@@ -131,6 +132,7 @@ __host__ __device__ inline unsigned int cnimg_off(int r, int byte) {   // (row, 
     return (unsigned)((r >> 3) * 256 + (byte >> 4) * 128 + (r & 7) * 16 + (byte & 15));
 }
 void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s);
+void launch_xnmax(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
 void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
 void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 void launch_update(const Dev& d, const GEval& g, cudaStream_t s);

@@ -214,6 +214,20 @@ __device__ __forceinline__ float pack_key(uint32_t sc_bits, uint32_t j, uint32_t
     return __uint_as_float(k + j);
 }
 
+// Window key (2xFP16 engine): the accumulator a = ||x - c||^2 / (2 s^2) + 6 lies in
+// [4, 134], so its float bits are 0 1000 0eee m..m (biased exponent 129..134) and
+// bits << 5 keeps the order: the dropped top 5 bits are constant, the new sign
+// bit (exponent bit 3) is 0, the new exponent field is never all-ones.  The low 5
+// bits take the column's position: ONE IMAD per score, and the key is exact.
+__device__ __forceinline__ float wkey(uint32_t a_bits, uint32_t j, uint32_t k32) {
+    uint32_t k;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(a_bits), "r"(k32), "n"(0));
+    return __uint_as_float(k + j);
+}
+__device__ __forceinline__ float wdecode(float key) {
+    return __uint_as_float((__float_as_uint(key) >> 5) | 0x40000000u);
+}
+
 __device__ __forceinline__ float4 lds128(uint32_t saddr) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
@@ -331,7 +345,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     }
     constexpr int NATOM = KIND ? A / 2 : A;        // 128-B operand K-atoms per row
     constexpr int AELEM = KIND ? 64 : 32;          // elements per operand atom
-    constexpr int OPB = 2 * NATOM * ATOM_BYTES_X;  // one operand buffer: hi + lo
+    // one operand buffer: hi + lo (+ KIND 1: this row tile's A side of the folded block)
+    constexpr int OPB = 2 * NATOM * ATOM_BYTES_X + (KIND ? AAKM_CNIMG_BYTES : 0);
     constexpr int AW = TC_BN * CG;                 // accumulator columns = centroids per pair tile
     constexpr int NACC_ = 4 / CG;                  // accumulator buffers (512 TMEM columns)
     constexpr uint32_t IDESC_ = (KIND ? IDESC16 : IDESC) & ~((0x3Fu << 17) | (0x1Fu << 24));
@@ -345,8 +360,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint8_t* xst = smem;                                           // fp32 X tile (TMA target, splitter-owned)
     uint8_t* opb = inplace ? smem : xst + A * ATOM_BYTES_X;        // operand buffers [hi | lo]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
-    uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // constant A side of the folded ||c||^2 block
-    float* xnorm = reinterpret_cast<float*>(ablk + AAKM_CNIMG_BYTES); // [XR][128] ||x||^2 ring, slot = tile iteration % XR
+    uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // KIND 0: constant A side of the folded block
+    float* xnorm = reinterpret_cast<float*>(ablk + (KIND ? 0 : AAKM_CNIMG_BYTES)); // [XR][128] ||x||^2 ring (slot = iteration % XR)
     float4* mrg = reinterpret_cast<float4*>(xnorm + XR * TC_BM);      // [NQ-1][128] partial results of quarters 1..3
     uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + (NQ - 1) * TC_BM);
     uint64_t* full = bars;                                         // [S]  stage landed (leader: both halves)
@@ -363,19 +378,14 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     const int K = d.K;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;          // position in the CTA pair
     const bool leader = rank == 0;
-    // scores in units of U = 1 / (2 s_x s_c) (KIND 1) or 1/2 (KIND 0): the accumulator is
-    // s' = U cn - x.c/(s_x s_c) (power-of-two scaling: exact).  A side of the folded block:
-    // every row (1, 1, 1, 0, ...) in tf32 (KIND 0) or (2^p, 2^p, 0, ...) in fp16 (KIND 1).
-    {
-        uint32_t aw0 = 0x3F800000u;
-        if (KIND) {
-            const uint32_t hb = __half_as_ushort(__float2half_rn(d.st->cn_amul));
-            aw0 = hb | (hb << 16);
-        }
+    // KIND 0: the accumulator is the score ||c||^2/2 - x.c; the constant A side of the folded
+    // block is (1, 1, 1, 0, ...) in every row.  KIND 1 ("window keys"): with the common scale
+    // s the accumulator is ||x - c||^2 / (2 s^2) + 6 in [4, 134]; its A side is per row tile
+    // (1, 1, h_i, l_i, 0, ...) with h_i + l_i = ||x_i||^2 / (2 s^2) + 6, written by the splitter.
+    if (KIND == 0) {
         for (int i = threadIdx.x; i < TC_BM * 8; i += TC_THREADS) {
             const int r = i >> 3, w = i & 7;
-            const uint32_t val = KIND ? (w == 0 ? aw0 : 0u) : (w < 3 ? aw0 : 0u);
-            *reinterpret_cast<uint32_t*>(ablk + cnimg_off(r, w * 4)) = val;
+            *reinterpret_cast<uint32_t*>(ablk + cnimg_off(r, w * 4)) = w < 3 ? 0x3F800000u : 0u;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
     }
@@ -454,8 +464,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         mbar_wait(full + s, ph);
                         tc_fence_after();
                         const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
-                        if (a == 0 && !(d.dbg & 4))                // folded ||c||^2 block starts the sum
-                            mma_cg<KIND, CG>(dt, sdesc_ns(ablk_a), sdesc_ns(sb + STAGE_MAIN), 0u, IDESC_CG);
+                        if (a == 0 && !(d.dbg & 4)) {              // folded block starts the sum
+                            const uint32_t fa = KIND ? xhi_a + (uint32_t)(2 * NATOM * ATOM_BYTES_X) : ablk_a;
+                            mma_cg<KIND, CG>(dt, sdesc_ns(fa), sdesc_ns(sb + STAGE_MAIN), 0u, IDESC_CG);
+                        }
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if (d.dbg & 4) break;                   // debug: no MMAs (feed/epilogue probe)
@@ -489,7 +501,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             mbar_expect_tx(stfull, A * ATOM_BYTES_X);
             for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(0) * TC_BM));
         }
-        const float inv_sx = KIND ? d.x_inv_scale : 1.0f;
+        const float inv_sx = KIND ? 1.0f / d.st->c_scale : 1.0f;     // exact (power of 2)
+        const float hxs = 0.5f * inv_sx * inv_sx;
         for (long long it = 0; live(it); ++it) {
             mbar_wait_sleep(stfull, sph, 128);
             sph ^= 1;
@@ -548,6 +561,17 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     }
                 }
                 xnorm[(it % XR) * TC_BM + r] = xn;
+                if (KIND) {                                        // A side of the folded block, row r
+                    uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
+                    const float v = fmaf(xn, hxs, 6.0f);
+                    const __half h = __float2half_rn(v);
+                    const __half l = __float2half_rn(v - __half2float(h));
+                    *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, 0)) = 0x3C003C00u;            // (1, 1)
+                    *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, 4)) =
+                        (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(l) << 16);
+#pragma unroll
+                    for (int b = 8; b < 32; b += 4) *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, b)) = 0u;
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -582,7 +606,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
         const float gam = d.tau_gamma;
-        const float Usc = KIND ? 0.5f / (d.x_scale * d.st->c_scale) : 0.5f;    // score units
+        const float Usc = KIND ? 0.5f / (d.st->c_scale * d.st->c_scale) : 0.5f;  // accumulator units per distance unit
         const float tau_abs = KIND ? d.st->tau_abs : 0.0f;
         const uint32_t k32 = d.key_mul;
         int acc = 0; uint32_t aph = 0;
@@ -628,7 +652,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     const int j0 = nt * AW + (cq * CG + b) * 32;
                     if (j0 + 32 > K) {                              // ragged last tile: padded columns lose
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : 0x7F7FFFFFu;
+                        for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : (KIND ? 0x437A0000u : 0x7F7FFFFFu);
                     }
                     float O1[NTRK];
 #pragma unroll
@@ -640,8 +664,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 #pragma unroll
                             for (int pp = 0; pp < 2; ++pp) {
                                 const int u = ((j >> 1) + pp) & (NTRK - 1);
-                                const float ka = pack_key(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
-                                const float kb = pack_key(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
+                                const float ka = KIND ? wkey(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32)
+                                                      : pack_key(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
+                                const float kb = KIND ? wkey(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32)
+                                                      : pack_key(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
                                 const float m = fminf(ka, kb), M = fmaxf(ka, kb);
                                 B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
                                 B1[u] = fminf(B1[u], m);
@@ -688,10 +714,17 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     }
                     const long long row = frow;
                     const bool ok = row < d.n;
-                    // tau in score units (the folded ||c||^2 term adds cmax2 to the accumulated
-                    // magnitude), + 2 key quanta (32 ulps each) of the larger-magnitude key
-                    const float tau = Usc * (gam * (xn + 2.0f * cmax2) + tau_abs) +
-                                      7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
+                    float tau;
+                    if (KIND) {
+                        // window keys are exact accumulator values: decode; the accumulated
+                        // magnitude is <= (||x||^2 + ||c||^2) U 2 + 6 (folded terms first)
+                        b1 = wdecode(b1); b2 = wdecode(b2);
+                        tau = Usc * (gam * 2.0f * (xn + cmax2) + tau_abs) + gam * 8.0f;
+                    } else {
+                        // score units (the folded ||c||^2 term adds cmax2 to the accumulated
+                        // magnitude), + 2 key quanta (32 ulps each) of the larger-magnitude key
+                        tau = Usc * (gam * (xn + 2.0f * cmax2) + tau_abs) + 7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
+                    }
                     if (ok) lab_out[row] = i1;
                     push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
                 }
@@ -718,8 +751,9 @@ static size_t smem_need(int kind, int A, int S, int NT, int NXB) {
     const int natom = kind ? A / 2 : A;
     const int staging = NXB == 0 ? 0 : A;                  // NXB == 0: in place, one operand buffer
     const int nb = NXB == 0 ? 1 : NXB;
-    return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * 2 * natom * ATOM_BYTES_X + (size_t)S * STAGE_BYTES +
-           AAKM_CNIMG_BYTES + XR * TC_BM * 4 + (NQ - 1) * TC_BM * 16 + 512;
+    const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + (kind ? AAKM_CNIMG_BYTES : 0);
+    return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
+           (kind ? 0 : AAKM_CNIMG_BYTES) + XR * TC_BM * 4 + (NQ - 1) * TC_BM * 16 + 512;
 }
 
 // stages S and operand buffers NXB: prefer double-buffered X operands while
@@ -928,22 +962,19 @@ __global__ void __launch_bounds__(256) k_csplit16(Dev d, int mode) {
     if (mode == 1 && (st->done || !st->reject)) return;
     const float cmax2 = __uint_as_float(st->cmax2_bits);
     const float cmax = sqrtf(cmax2);
-    const float sc = cmax > 0.f ? exp2f(ceilf(log2f(cmax)) - 13.0f) : 1.0f;   // |c|/s_c <= 2^13 (< 65504)
+    // one power-of-two scale s for both operands with ||x||/s, ||c||/s <= 8, so every
+    // window-key accumulator ||x - c||^2 / (2 s^2) + 6 lies in [4, 134] (see the kernel)
+    const float M = fmaxf(cmax, d.x_nmax);
+    const float sc = M > 0.f ? exp2f(ceilf(log2f(M)) - 3.0f) : 1.0f;
     const float inv = 1.0f / sc;                                                // exact (power of 2)
-    // folded ||c||^2 column: score units U = 1 / (2 s_x s_c), cn U = amul (h + l) with h, l fp16
-    // and amul = 2^p (exact in fp16, p <= 15) keeping cn U / amul <= 2^14
-    const float U = 0.5f / (d.x_scale * sc);
-    const float cnu_max = cmax2 * U;
-    const float p = cnu_max > 16384.f ? fminf(ceilf(log2f(cnu_max)) - 14.0f, 15.0f) : 0.0f;
-    const float amul = exp2f(p), ainv = 1.0f / amul;
+    const float U = 0.5f * inv * inv;                                           // accumulator units / distance unit
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->c_scale = sc;
-        st->cn_amul = amul;
+        st->cn_amul = 1.0f;
         const float D = (float)d.d;
-        // split subnormals of x and c, plus the fp16 subnormal floor of the folded column (amul 2^-24 in
-        // score units, i.e. amul 2^-24 / U in distance units)
-        st->tau_abs = 8.0f * 2.9802322e-8f * (D * sc * d.x_absmax + sqrtf(D) * d.x_scale * cmax) +
-                      amul * 5.9604645e-8f / U;
+        // fp16 subnormal floors (absolute 2^-25 in operand units) of the split x and c
+        // parts and of the folded ||c||^2/(2 s^2) column, in distance units
+        st->tau_abs = 8.0f * 2.9802322e-8f * (D * sc * d.x_absmax + sqrtf(D) * sc * cmax) + 5.9604645e-8f / U;
     }
     const long long KD = (long long)d.K * d.d;
     __half* hi = reinterpret_cast<__half*>(d.Chi16);
@@ -955,15 +986,18 @@ __global__ void __launch_bounds__(256) k_csplit16(Dev d, int mode) {
         lo[e] = __float2half_rn(v - __half2float(h));
     }
     if (d.cnimg) {
+        // B side of the folded block: (h, l) of ||c_j||^2 / (2 s^2) <= 32, then (1, 1) which
+        // pairs with the per-row (h, l) of ||x_i||^2 / (2 s^2) + 6 written by the splitter
         for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x) {
-            const float v = d.cn[j] * U * ainv;
+            const float v = d.cn[j] * U;
             const __half h = __float2half_rn(v);
             const __half l = __float2half_rn(v - __half2float(h));
             uint8_t* row = d.cnimg + (size_t)(j >> 7) * AAKM_CNIMG_BYTES;
             const int r = (int)(j & 127);
             *reinterpret_cast<uint32_t*>(row + cnimg_off(r, 0)) =
                 (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(l) << 16);
-            for (int b = 4; b < 32; b += 4) *reinterpret_cast<uint32_t*>(row + cnimg_off(r, b)) = 0u;
+            *reinterpret_cast<uint32_t*>(row + cnimg_off(r, 4)) = 0x3C003C00u;          // (1.0, 1.0)
+            for (int b = 8; b < 32; b += 4) *reinterpret_cast<uint32_t*>(row + cnimg_off(r, b)) = 0u;
         }
     }
 }
@@ -986,6 +1020,24 @@ __global__ void k_absmax(const float* X, long long n, unsigned int* out) {
 
 void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s) {
     k_absmax<<<2 * (g_num_sms > 0 ? g_num_sms : 148), 256, 0, s>>>(X, n, out);
+}
+
+// max_i ||x_i||^2 over the shard (one warp per row, fp32; the caller adds a margin)
+__global__ void k_xnmax(const float* X, long long n, int d, unsigned int* out) {
+    const int lane = threadIdx.x & 31;
+    float m = 0.f;
+    for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((long long)gridDim.x * blockDim.x) >> 5) {
+        float s = 0.f;
+        for (int k = lane; k < d; k += 32) { const float v = X[i * d + k]; s = fmaf(v, v, s); }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        m = fmaxf(m, s);
+    }
+    if (lane == 0) atomicMax(out, __float_as_uint(m));
+}
+
+void launch_xnmax(const float* X, long long n, int d, unsigned int* out, cudaStream_t s) {
+    k_xnmax<<<4 * (g_num_sms > 0 ? g_num_sms : 148), 256, 0, s>>>(X, n, d, out);
 }
 
 // ---- refine for the tensor-core engine: gather -> candidate pass -> exact fp64

@@ -477,7 +477,17 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         float m;
         memcpy(&m, &bits, 4);
         const float sx = m > 0.f ? exp2f(ceilf(log2f(m)) - 13.0f) : 1.0f;
-        for (Dev* dv : {&h->d, &h->da}) { dv->x_absmax = m; dv->x_scale = sx; dv->x_inv_scale = 1.0f / sx; }
+        // max ||x_i||^2 (float bits of non-negative values order as uints)
+        CKC(cudaMemsetAsync(amax, 0, 4, h->stream));
+        if (n_local > 0) launch_xnmax(X, n_local, d, amax, h->stream);
+        CKC(cudaMemcpyAsync(&bits, amax, 4, cudaMemcpyDeviceToHost, h->stream));
+        CKC(cudaStreamSynchronize(h->stream));
+        float xn2;
+        memcpy(&xn2, &bits, 4);
+        const float xnm = sqrtf(xn2) * (1.0f + 1e-6f);   // upward margin for the fp32 norm
+        for (Dev* dv : {&h->d, &h->da}) {
+            dv->x_absmax = m; dv->x_scale = sx; dv->x_inv_scale = 1.0f / sx; dv->x_nmax = xnm;
+        }
     }
     if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16) {
         h->tcm = tc_make_maps(h->d);
