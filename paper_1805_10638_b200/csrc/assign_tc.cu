@@ -50,7 +50,6 @@ constexpr int MAXCH = AAKM_MAXC / NQ;              // candidate slots per row pe
 constexpr int W_PROD = NQ * 4;                     // warp roles: epilogue warps 0..15 first, so the
 constexpr int W_MMA = W_PROD + 1;                  // SMSP arbiter (highest warp id first) never starves
 constexpr int W_SPLIT = W_PROD + 2;                // the producer / MMA issuer behind busy epilogue warps
-constexpr int XR = 8;                              // ||x||^2 ring depth (> max splitter lead of 2 + NACC tiles)
 constexpr int ATOM_BYTES_X = TC_BM * 128;          // one 32-element K-atom of the X tile
 constexpr int STAGE_MAIN = 2 * TC_BN * 128;        // C_hi atom + C_lo atom
 constexpr int STAGE_BYTES = STAGE_MAIN + AAKM_CNIMG_BYTES;   // + the folded ||c||^2 block (first atom only)
@@ -286,6 +285,10 @@ __device__ __forceinline__ void tma_load_2d_cg(void* dst, const CUtensorMap* map
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
             ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1) : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1) : "memory");
+}
 template <int KIND, int CG>
 __device__ __forceinline__ void mma_cg(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum, uint32_t idesc) {
     if (CG == 2) {
@@ -333,7 +336,7 @@ template <int A, int MODE, int KIND, int CG>   // d = 32 * A (KIND 1: A even); C
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
             const __grid_constant__ CUtensorMap tm_clo, const __grid_constant__ CUtensorMap tm_cn, Dev d, GEval g,
-            int S, int NT, int NXB) {
+            int S, int NT, int NXB, int XRr) {
     // Every CTA of a pair must run the same pipeline (barriers are shared), so the
     // early exits depend only on grid-uniform device state.
     if (!geval_active(d, g)) return;
@@ -355,14 +358,18 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     // NXB == 0: in-place mode (KIND 0, no room for a staging tile): the TMA
     // target is operand buffer 0's hi half and the split runs in place.
+    // DX (KIND 1): no staging tile; the splitter reads its rows straight from
+    // global memory (L2-prefetched one row tile ahead by TMA), which leaves room
+    // for a fourth C stage.
+    constexpr bool DX = KIND == 1;
     const bool inplace = NXB == 0;
     const int nxb = inplace ? 1 : NXB;
     uint8_t* xst = smem;                                           // fp32 X tile (TMA target, splitter-owned)
-    uint8_t* opb = inplace ? smem : xst + A * ATOM_BYTES_X;        // operand buffers [hi | lo]
+    uint8_t* opb = (inplace || DX) ? smem : xst + A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
     uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // KIND 0: constant A side of the folded block
-    float* xnorm = reinterpret_cast<float*>(ablk + (KIND ? 0 : AAKM_CNIMG_BYTES)); // [XR][128] ||x||^2 ring (slot = iteration % XR)
-    float4* mrg = reinterpret_cast<float4*>(xnorm + XR * TC_BM);      // [NQ-1][128] partial results of quarters 1..3
+    float* xnorm = reinterpret_cast<float*>(ablk + (KIND ? 0 : AAKM_CNIMG_BYTES)); // [XRr][128] ||x||^2 ring (slot = iteration % XRr)
+    float4* mrg = reinterpret_cast<float4*>(xnorm + XRr * TC_BM);     // [NQ-1][128] partial results of quarters 1..3
     uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + (NQ - 1) * TC_BM);
     uint64_t* full = bars;                                         // [S]  stage landed (leader: both halves)
     uint64_t* empty = bars + S;                                    // [S]  stage consumed (multicast commit)
@@ -371,8 +378,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint64_t* stfull = acce + 4;                                   // X staging landed
     uint64_t* opready = stfull + 1;                                // [2] operand buffer split (leader: both CTAs)
     uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
-    uint64_t* xready = opempty + 2;                                // [XR] ||x||^2 slot written (epilogue side)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XR);
+    uint64_t* xready = opempty + 2;                                // [XRr] ||x||^2 slot written (epilogue side)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XRr);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = d.K;
@@ -394,7 +401,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         for (int b = 0; b < 4; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4 * CG); }
         for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2 * CG); mbar_init(opempty + b, 1); }
         mbar_init(stfull, 1);
-        for (int b = 0; b < XR; ++b) mbar_init(xready + b, 2);
+        for (int b = 0; b < XRr; ++b) mbar_init(xready + b, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_SPLIT) {
@@ -498,14 +505,24 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         uint32_t eph = 0;                                          // phase bit per operand buffer
         int xb = 0;
         if (t == 0 && live(0)) {
-            mbar_expect_tx(stfull, A * ATOM_BYTES_X);
-            for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(0) * TC_BM));
+            if (DX) {
+                for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(0) * TC_BM));
+            } else {
+                mbar_expect_tx(stfull, A * ATOM_BYTES_X);
+                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(0) * TC_BM));
+            }
         }
         const float inv_sx = KIND ? 1.0f / d.st->c_scale : 1.0f;     // exact (power of 2)
         const float hxs = 0.5f * inv_sx * inv_sx;
+        const float* Xsrc = MODE == 0 ? d.X : d.Xf;
         for (long long it = 0; live(it); ++it) {
-            mbar_wait_sleep(stfull, sph, 128);
-            sph ^= 1;
+            if (DX) {
+                if (t == 0 && live(it + 1))                        // next row tile -> L2
+                    for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(it + 1) * TC_BM));
+            } else {
+                mbar_wait_sleep(stfull, sph, 128);
+                sph ^= 1;
+            }
             if (!inplace) {
                 mbar_wait_sleep(opempty + xb, ((eph >> xb) & 1u) ^ 1u, 256);  // the MMAs of tile - NXB are done
                 eph ^= 1u << xb;
@@ -538,10 +555,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     for (int a16 = 0; a16 < NATOM; ++a16) {
 #pragma unroll
                         for (int c16 = 0; c16 < 8; ++c16) {
-                            const int a32 = 2 * a16 + (c16 >> 2);
-                            const int c32 = (c16 & 3) * 2;
-                            const float4 v0 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + ((c32 ^ (r & 7)) << 4));
-                            const float4 v1 = *reinterpret_cast<const float4*>(xst + a32 * ATOM_BYTES_X + r * 128 + (((c32 + 1) ^ (r & 7)) << 4));
+                            // columns 64 a16 + 8 c16 .. + 8 of row r (zeros past the last row)
+                            const long long grow = tile_of(it) * TC_BM + r;
+                            const float4* src = reinterpret_cast<const float4*>(Xsrc + grow * A * 32) + a16 * 16 + c16 * 2;
+                            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+                            if (grow < n_rows) { v0 = __ldg(src); v1 = __ldg(src + 1); }
                             const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
                             uint32_t hp[4], lp[4];
 #pragma unroll
@@ -560,7 +578,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         }
                     }
                 }
-                xnorm[(it % XR) * TC_BM + r] = xn;
+                xnorm[(it & (XRr - 1)) * TC_BM + r] = xn;
                 if (KIND) {                                        // A side of the folded block, row r
                     uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
                     const float v = fmaf(xn, hxs, 6.0f);
@@ -578,7 +596,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             if (lane == 0) {
                 if (CG == 2) mbar_arrive_cl(lead(opready + xb));   // once per row tile: release.cluster is affordable
                 else mbar_arrive(opready + xb);
-                mbar_arrive(xready + it % XR);
+                mbar_arrive(xready + (it & (XRr - 1)));
+            }
+            if (DX) {
+                if (++xb == nxb) xb = 0;
+                continue;
             }
             // both splitter warps are done with the staging tile: prefetch the next one
             // (in place: only once the MMAs have consumed the tile)
@@ -612,10 +634,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         int acc = 0; uint32_t aph = 0;
         for (long long it = 0; live(it); ++it) {
             // ||x||^2 of this row from its ring slot.  The splitter runs at most
-            // 2 + NACC tiles ahead of the epilogue (operand buffers + accumulators),
-            // so a ring of XR = 8 slots neither aliases a phase nor overwrites an unread slot.
-            mbar_wait(xready + it % XR, (uint32_t)(it / XR) & 1u);
-            const float xn = cq == 0 ? xnorm[(it % XR) * TC_BM + r] : 0.f;
+            // NXB + ceil(NACC / NT) row tiles ahead of the epilogue (operand buffers +
+            // accumulators); the ring has one slot more (xr_of), so it neither
+            // aliases a phase nor overwrites an unread slot.
+            mbar_wait(xready + (it & (XRr - 1)), (uint32_t)(it / XRr) & 1u);
+            const float xn = cq == 0 ? xnorm[(it & (XRr - 1)) * TC_BM + r] : 0.f;
             // NTRK independent top-2 trackers.  MODE 0 keys pack the column's position
             // inside its 32-column batch into the 5 low mantissa bits of the score (a
             // <= 2^-18 |s| perturbation, added to tau), so one FMNMX carries value and
@@ -747,13 +770,25 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 // ------------------------------------------------------------------ host side
 static int g_num_sms = 0;
 
-static size_t smem_need(int kind, int A, int S, int NT, int NXB) {
+// ||x||^2 ring depth: the splitter runs at most NXB + ceil(NACC/NT) row tiles ahead
+// of the epilogue, so the ring needs one slot more than that (power of two)
+static int xr_of(int NT, int NXB, int cg) {
+    const int nacc = 4 / cg;
+    const int lead = (NXB < 1 ? 1 : NXB) + (nacc + NT - 1) / NT;
+    int xr = 2;
+    while (xr < lead + 1) xr *= 2;
+    return xr;
+}
+
+static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2) {
     const int natom = kind ? A / 2 : A;
-    const int staging = NXB == 0 ? 0 : A;                  // NXB == 0: in place, one operand buffer
+    const int staging = (NXB == 0 || kind == 1) ? 0 : A;   // in place / direct X: no staging tile
     const int nb = NXB == 0 ? 1 : NXB;
     const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + (kind ? AAKM_CNIMG_BYTES : 0);
+    const int xr = xr_of(NT, NXB, cg);
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
-           (kind ? 0 : AAKM_CNIMG_BYTES) + XR * TC_BM * 4 + (NQ - 1) * TC_BM * 16 + 512;
+           (kind ? 0 : AAKM_CNIMG_BYTES) + (size_t)xr * TC_BM * 4 + (NQ - 1) * TC_BM * 16 +
+           (size_t)(2 * S + 13 + xr) * 8 + 16;
 }
 
 // stages S and operand buffers NXB: prefer double-buffered X operands while
@@ -763,18 +798,19 @@ static int env_cap(const char* name, int dflt) {
     const char* v = getenv(name);
     return v ? atoi(v) : dflt;
 }
-static void pick_pipe(int kind, int A, int NT, int& S, int& NXB) {
+static void pick_pipe(int kind, int A, int NT, int& S, int& NXB, int cg = 2) {
     static const int maxs = env_cap("AAKM_TC_MAXS", 6), maxnxb = env_cap("AAKM_TC_MAXNXB", 2);
     for (NXB = maxnxb; NXB >= (kind == 0 ? 0 : 1); --NXB)
-        for (S = maxs; S >= (NXB == 2 ? 3 : 2); --S)
-            if (smem_need(kind, A, S, NT, NXB) <= (size_t)SMEM_LIMIT) return;
+        for (S = maxs; S >= 2; --S)
+            if (smem_need(kind, A, S, NT, NXB, cg) <= (size_t)SMEM_LIMIT) return;
     S = 0; NXB = -1;
 }
 
 static int pick_stages(int kind, int A, int NT) {
-    int S, NXB;
-    pick_pipe(kind, A, NT, S, NXB);
-    return S;
+    int S, NXB, S1, NXB1;
+    pick_pipe(kind, A, NT, S, NXB, 2);
+    pick_pipe(kind, A, NT, S1, NXB1, 1);
+    return S < S1 ? S : S1;
 }
 
 bool tc_supported(int d, int K) {
@@ -886,7 +922,7 @@ static int tc_cg() {
 
 template <int A, int MODE, int KIND, int CG>
 static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, const GEval& g, int S, int NT, int NXB,
-                       long long n_tiles, size_t smem, cudaStream_t s) {
+                       int XRr, long long n_tiles, size_t smem, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(TC_THREADS);
     cfg.dynamicSmemBytes = smem;
@@ -912,7 +948,7 @@ static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, con
     if (CG == 2) grid = (grid + 1) & ~1;
     if (grid < CG) grid = CG;
     cfg.gridDim = dim3(grid);
-    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB);
+    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB, XRr);
 }
 
 template <int MODE, int KIND, int CG>
@@ -920,20 +956,21 @@ static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStre
     const int A = d.d / 32;
     const int NT = (d.K + TC_BN * CG - 1) / (TC_BN * CG);
     int S, NXB;
-    pick_pipe(KIND, A, NT, S, NXB);
-    const size_t smem = smem_need(KIND, A, S, NT, NXB);
+    pick_pipe(KIND, A, NT, S, NXB, CG);
+    const size_t smem = smem_need(KIND, A, S, NT, NXB, CG);
+    const int xr = xr_of(NT, NXB, CG);
     const CUtensorMap& xm = MODE == 0 ? m->x : m->xf;
     const long long n_tiles = MODE == 0 ? (d.n + TC_BM - 1) / TC_BM : 1ll << 40;
     if (KIND == 0) {
         switch (A) {
-            case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
-            case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
-            case 3: launch_one<3, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
-            default: launch_one<4, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s); break;
+            case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
+            case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
+            case 3: launch_one<3, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
+            default: launch_one<4, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
         }
     } else {
-        if (A == 2) launch_one<2, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s);
-        else launch_one<4, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, n_tiles, smem, s);
+        if (A == 2) launch_one<2, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s);
+        else launch_one<4, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s);
     }
 }
 
