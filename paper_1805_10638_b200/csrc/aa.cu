@@ -248,7 +248,9 @@ void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0,
 // Lane r owns row r of the Cholesky factor in registers (compile-time
 // indexed, fully unrolled); columns move between lanes with shuffles.
 #define FULL 0xffffffffu
-__global__ void __launch_bounds__(1024) k_solve(Dev d) {
+// Fixed-order reduction of this pass's Gram partials: one warp per entry, lanes
+// stride over the blocks, then a fixed xor tree (same bytes on every rank).
+__global__ void __launch_bounds__(1024) k_gram_reduce(Dev d) {
     DevState* st = d.st;
     if (st->done) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -257,8 +259,6 @@ __global__ void __launch_bounds__(1024) k_solve(Dev d) {
     const int init = st->init_mode;
     const int W = init ? 0 : (int)(t < H - 1 ? t : H - 1);
     const int ts = (int)(t % H);
-    // fixed-order reduction of the Gram partials of this pass: one warp per entry,
-    // lanes stride over the blocks, then a fixed xor tree (same bytes on every rank)
     for (int q = warp; q < 2 * W; q += 32) {
         double v = 0.0;
         for (int b = lane; b < d.gram_blocks; b += 32) v += d.gram_part[(long long)b * 2 * H + q];
@@ -273,8 +273,17 @@ __global__ void __launch_bounds__(1024) k_solve(Dev d) {
             }
         }
     }
-    __syncthreads();
-    if (warp != 0) return;                          // the solve itself is one warp
+}
+
+__global__ void __launch_bounds__(32) k_solve(Dev d) {
+    DevState* st = d.st;
+    if (st->done) return;
+    const int lane = threadIdx.x;
+    const int H = d.H;
+    const long long t = st->t;
+    const int init = st->init_mode;
+    const int W = init ? 0 : (int)(t < H - 1 ? t : H - 1);
+    const int ts = (int)(t % H);
     int m_t = init ? 0 : (st->m < t ? st->m : (int)t);
     if (m_t > W) m_t = W;
     // column a <-> dF(t - a); lane a holds column a's scale and rhs
@@ -299,69 +308,55 @@ __global__ void __launch_bounds__(1024) k_solve(Dev d) {
     const int my_slot = col >= 0 ? (int)((((t - col) % H) + H) % H) : 0;
     const double my_s = __shfl_sync(FULL, s_a, col >= 0 ? col : 0);
     const double my_b = __shfl_sync(FULL, b_a, col >= 0 ? col : 0);
+    // The compacted, scaled, ridged normal matrix in shared memory (lane i = row i):
+    // all loads issued at once, then a right-looking Cholesky in which each lane
+    // updates its own row.  Every entry sees the same subtraction sequence as the
+    // dot-product form (q ascending), so theta is unchanged bit for bit.
+    __shared__ double sA[AAKM_H_SLOTS][AAKM_H_SLOTS + 1];    // scaled matrix (kept for restarts)
+    __shared__ double sL[AAKM_H_SLOTS][AAKM_H_SLOTS + 1];    // factor, built in place
+    __shared__ double s_s[AAKM_H_SLOTS];
+    __shared__ int s_slot[AAKM_H_SLOTS];
+    if (lane < na) { s_slot[lane] = my_slot; s_s[lane] = my_s; }
+    __syncwarp();
+    if (lane < na) {
+        for (int c = 0; c <= lane; ++c) sA[lane][c] = st->gram[my_slot * H + s_slot[c]];
+        for (int c = 0; c <= lane; ++c) sA[lane][c] = sA[lane][c] / (my_s * s_s[c]) + (c == lane ? d.ridge : 0.0);
+    }
+    __syncwarp();
     double phi_mine = 0.0;
-    const double ridge = d.ridge;
     while (na > 0) {
-        double Lr[AAKM_H_SLOTS];                    // row `lane` of L
-#pragma unroll
-        for (int q = 0; q < AAKM_H_SLOTS; ++q) Lr[q] = 0.0;
+        if (lane < na)
+            for (int c = 0; c <= lane; ++c) sL[lane][c] = sA[lane][c];
+        __syncwarp();
         bool ok = true;
-#pragma unroll
-        for (int c = 0; c < AAKM_H_SLOTS; ++c) {
-            if (c < na) {
-                const int slot_c = __shfl_sync(FULL, my_slot, c);
-                const double s_c = __shfl_sync(FULL, my_s, c);
-                // A[lane][c] of the scaled, ridged normal matrix
-                double v = 0.0;
-                if (lane >= c && lane < na) {
-                    v = st->gram[my_slot * H + slot_c] / (my_s * s_c);
-                    if (lane == c) v += ridge;
-                }
-#pragma unroll
-                for (int q = 0; q < AAKM_H_SLOTS; ++q) {
-                    if (q < c) {
-                        const double Lcq = __shfl_sync(FULL, Lr[q], c);
-                        v -= Lr[q] * Lcq;
-                    }
-                }
-                const double diag = __shfl_sync(FULL, v, c);
-                if (!(diag > 0.0) || !isfinite(diag)) { ok = false; break; }
-                const double Lcc = sqrt(diag);
-                if (lane == c) Lr[c] = Lcc;
-                else if (lane > c && lane < na) Lr[c] = v / Lcc;
-            }
+        for (int c = 0; c < na; ++c) {
+            const double diag = sL[c][c];
+            if (!(diag > 0.0) || !isfinite(diag)) { ok = false; break; }
+            const double Lcc = sqrt(diag);
+            double Lic = 0.0;
+            if (lane > c && lane < na) { Lic = sL[lane][c] / Lcc; sL[lane][c] = Lic; }
+            __syncwarp();
+            if (lane == c) sL[c][c] = Lcc;
+            if (lane > c && lane < na)
+                for (int j = c + 1; j <= lane; ++j) sL[lane][j] -= Lic * sL[j][c];
+            __syncwarp();
         }
-        if (!ok) { --na; continue; }                 // drop the oldest active column
-        // forward: L y = bh   (y replicated in every lane via broadcast)
+        if (!ok) { --na; __syncwarp(); continue; }   // drop the oldest active column
+        // forward: L y = bh (lane a ends up holding y_a)
         double y_mine = 0.0;
-#pragma unroll
-        for (int a = 0; a < AAKM_H_SLOTS; ++a) {
-            if (a < na) {
-                double v = my_b;
-#pragma unroll
-                for (int q = 0; q < AAKM_H_SLOTS; ++q) {
-                    if (q < a) v -= Lr[q] * __shfl_sync(FULL, y_mine, q);
-                }
-                v = v / Lr[a < AAKM_H_SLOTS ? a : 0];
-                const double ya = __shfl_sync(FULL, v, a);
-                if (lane == a) y_mine = ya;
-            }
+        double bres = my_b;                          // b_i - sum_{q < a} L_iq y_q, q ascending
+        for (int a = 0; a < na; ++a) {
+            const double ya = __shfl_sync(FULL, bres, a) / sL[a][a];
+            if (lane == a) y_mine = ya;
+            if (lane > a && lane < na) bres -= sL[lane][a] * ya;
         }
-        // backward: L^T phi = y
+        // backward: L^T phi = y (fixed xor-tree sums)
         phi_mine = 0.0;
         for (int a = na - 1; a >= 0; --a) {
-            double contrib = 0.0;
-#pragma unroll
-            for (int q = 0; q < AAKM_H_SLOTS; ++q) {
-                if (q == a && lane > a && lane < na) contrib = Lr[q] * phi_mine;
-            }
+            double contrib = (lane > a && lane < na) ? sL[lane][a] * phi_mine : 0.0;
             for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(FULL, contrib, o);
-            double Laa = 0.0;
-#pragma unroll
-            for (int q = 0; q < AAKM_H_SLOTS; ++q) if (q == a) Laa = Lr[q];
-            Laa = __shfl_sync(FULL, Laa, a);
             const double ya = __shfl_sync(FULL, y_mine, a);
-            const double pa = (ya - contrib) / Laa;
+            const double pa = (ya - contrib) / sL[a][a];
             if (lane == a) phi_mine = pa;
         }
         break;
@@ -398,7 +393,10 @@ __global__ void __launch_bounds__(1024) k_solve(Dev d) {
 }
 #undef FULL
 
-void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 1024, 0, s>>>(d); }
+void launch_solve(const Dev& d, cudaStream_t s) {
+    k_gram_reduce<<<1, 1024, 0, s>>>(d);
+    k_solve<<<1, 32, 0, s>>>(d);
+}
 
 // ---------------------------------------------------------------- advance
 __global__ void k_advance(Dev d) {

@@ -303,7 +303,7 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
     dbg("combine_mix", s);
     launch_advance(d, s);
     dbg("advance", s);
-    h->launches += 5;
+    h->launches += 6;
     CK(h, cudaGetLastError());
     return KMEANS_OK;
 }
