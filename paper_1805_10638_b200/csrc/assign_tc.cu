@@ -436,12 +436,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     const int crow = (ntl * CG + (int)rank) * TC_BN;   // first centroid of this CTA's half
                     for (int a = 0; a < NATOM; ++a) {
                         mbar_wait_sleep(empty + s, ph ^ 1, 32);
-                        if (leader) mbar_expect_tx(full + s, CG * (a == 0 ? STAGE_BYTES : STAGE_MAIN));
+                        if (leader) mbar_expect_tx(full + s, CG * (a == NATOM - 1 ? STAGE_BYTES : STAGE_MAIN));
                         uint8_t* st = stg + (size_t)s * STAGE_BYTES;
                         const uint32_t fb = lead(full + s);
                         tma_load_2d_cg<CG>(st, &tm_chi, fb, a * AELEM, crow);
                         tma_load_2d_cg<CG>(st + TC_BN * 128, &tm_clo, fb, a * AELEM, crow);
-                        if (a == 0) tma_load_2d_cg<CG>(st + STAGE_MAIN, &tm_cn, fb, 0, (ntl * CG + (int)rank) * 4);
+                        if (a == NATOM - 1) tma_load_2d_cg<CG>(st + STAGE_MAIN, &tm_cn, fb, 0, (ntl * CG + (int)rank) * 4);
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                 }
@@ -471,10 +471,6 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         mbar_wait(full + s, ph);
                         tc_fence_after();
                         const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
-                        if (a == 0 && !(d.dbg & 4)) {              // folded block starts the sum
-                            const uint32_t fa = KIND ? xhi_a + (uint32_t)(2 * NATOM * ATOM_BYTES_X) : ablk_a;
-                            mma_cg<KIND, CG>(dt, sdesc_ns(fa), sdesc_ns(sb + STAGE_MAIN), 0u, IDESC_CG);
-                        }
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if (d.dbg & 4) break;                   // debug: no MMAs (feed/epilogue probe)
@@ -483,9 +479,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             const uint64_t al = sdesc(xlo_a + a * ATOM_BYTES_X + ko);
                             const uint64_t bh = sdesc(sb + ko);
                             const uint64_t bl = sdesc(sb + TC_BN * 128 + ko);
-                            mma_cg<KIND, CG>(dt, al, bh, 1u, IDESC_CG);   // small terms first
+                            mma_cg<KIND, CG>(dt, al, bh, (a | kk) ? 1u : 0u, IDESC_CG);   // small terms first
                             mma_cg<KIND, CG>(dt, ah, bl, 1u, IDESC_CG);
                             mma_cg<KIND, CG>(dt, ah, bh, 1u, IDESC_CG);
+                        }
+                        // the folded block closes the sum: during the 3d/16 (3d/8) product steps
+                        // the running sum stays within 2U sum|x_k c_k| <= U(||x||^2 + ||c||^2)
+                        if (a == NATOM - 1 && !(d.dbg & 4)) {
+                            const uint32_t fa = KIND ? xhi_a + (uint32_t)(2 * NATOM * ATOM_BYTES_X) : ablk_a;
+                            mma_cg<KIND, CG>(dt, sdesc_ns(fa), sdesc_ns(sb + STAGE_MAIN), 1u, IDESC_CG);
                         }
                         commit_cg<CG>(empty + s);                  // frees the stage (both halves) when done
                         if (++s == S) { s = 0; ph ^= 1; }
@@ -739,10 +741,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     const bool ok = row < d.n;
                     float tau;
                     if (KIND) {
-                        // window keys are exact accumulator values: decode; the accumulated
-                        // magnitude is <= (||x||^2 + ||c||^2) U 2 + 6 (folded terms first)
+                        // window keys are exact accumulator values: decode.  The folded terms
+                        // enter last, so every partial sum is <= U (||x||^2 + ||c||^2) + 6
                         b1 = wdecode(b1); b2 = wdecode(b2);
-                        tau = Usc * (gam * 2.0f * (xn + cmax2) + tau_abs) + gam * 8.0f;
+                        tau = Usc * (gam * (xn + cmax2) + tau_abs) + gam * 8.0f;
                     } else {
                         // score units (the folded ||c||^2 term adds cmax2 to the accumulated
                         // magnitude), + 2 key quanta (32 ulps each) of the larger-magnitude key
