@@ -245,8 +245,7 @@ void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0,
 // ---------------------------------------------------------------- solve
 // One warp.  Eq. (7) under reading R-A14 (see oracle ora_ls_solve for the
 // plain statement): unit-diagonal scaling, ridge, Cholesky, drop-oldest.
-// Lane r owns row r of the Cholesky factor in registers (compile-time
-// indexed, fully unrolled); columns move between lanes with shuffles.
+// Lane r owns row r of the matrix / Cholesky factor in shared memory.
 #define FULL 0xffffffffu
 // Fixed-order reduction of this pass's Gram partials: one warp per entry, lanes
 // stride over the blocks, then a fixed xor tree (same bytes on every rank).

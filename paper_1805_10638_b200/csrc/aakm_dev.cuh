@@ -133,9 +133,10 @@ __host__ __device__ inline unsigned int cnimg_off(int r, int byte) {   // (row, 
 }
 void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s);
 void launch_xnmax(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
-void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
-void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
-void launch_update(const Dev& d, const GEval& g, cudaStream_t s);
+// the launchers below return how many kernels they enqueued (the gpu_launches count)
+int launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
+int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
+int launch_update(const Dev& d, const GEval& g, cudaStream_t s);
 bool update_sorted(const Dev& d);
 void launch_control(const Dev& d, int stage, cudaStream_t s);
 void launch_finalize(const Dev& d, cudaStream_t s);

@@ -1144,10 +1144,11 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
     }
 }
 
-void launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
+int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
     k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
     k_refine_exact<<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    return 3;
 }
 
 }  // namespace aakm

@@ -98,9 +98,10 @@ cudaError_t setup_refine() {
     return cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (4096 + CAND) * 4);
 }
 
-void launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first) {
+int launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first) {
     size_t smem = (size_t)8 * (d.d + CAND) * 4;
     k_refine<<<296, 256, smem, s>>>(d, g, first);
+    return 1;
 }
 
 }  // namespace aakm

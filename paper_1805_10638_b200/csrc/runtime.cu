@@ -228,11 +228,10 @@ static void combine(kmeans_handle* h, const Dev& d, int mode, const float* src, 
 // rows beyond the candidate capacity (and the SIMT engine) use the SIMT refine.
 static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
     if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16) {
-        launch_refine_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
-        launch_refine(d, g, s, d.fcap);
-        h->launches += 3;
+        h->launches += launch_refine_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
+        h->launches += launch_refine(d, g, s, d.fcap);
     } else {
-        launch_refine(d, g, s, 0);
+        h->launches += launch_refine(d, g, s, 0);
     }
 }
 
@@ -272,9 +271,8 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     dbg("assign", s);
     refine_engine(h, d, g, s);
     dbg("refine", s);
-    launch_update(d, g, s);
+    h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
     dbg("update", s);
-    h->launches += 3;
     st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
     if (h->nranks > 1) dbg("allreduce", s);
@@ -303,7 +301,7 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
     dbg("combine_mix", s);
     launch_advance(d, s);
     dbg("advance", s);
-    h->launches += 6;
+    h->launches += 5;                               // finalize, gram, gram_reduce + solve, advance
     CK(h, cudaGetLastError());
     return KMEANS_OK;
 }
@@ -537,8 +535,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     kmeans_status st = timed_assign(h, d, g, s, h->cfg.timing != 0);
     if (st != KMEANS_OK) return st;
     refine_engine(h, d, g, s);
-    launch_update(d, g, s);
-    h->launches += 4;
+    h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
     st = allreduce(h, d.packed[0], s);
     if (st != KMEANS_OK) return st;
     const long long KD = (long long)d.K * d.d;
@@ -561,8 +558,7 @@ kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const float
     CK(h, cudaMemsetAsync(&d.st->label_error, 0, sizeof(int), s));
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels); g.prev_mode = 1; g.Cassign = C_prev;
-    launch_update(d, g, s);
-    h->launches += 1;
+    h->launches += launch_update(d, g, s);
     kmeans_status st = allreduce(h, d.packed[0], s);
     if (st != KMEANS_OK) return st;
     launch_update_G(d, d.packed[0], C_prev, G_out, (long long*)counts_out, s);
@@ -585,8 +581,7 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels);
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev; g.Cassign = C; g.packed_out = packed_out;
-    launch_update(d, g, s);
-    h->launches += 1;
+    h->launches += launch_update(d, g, s);
     CK(h, cudaStreamSynchronize(s));
     CK(h, cudaGetLastError());
     return KMEANS_OK;

@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 // instead of d per row.  X is read exactly once, as contiguous row segments;
 // the energy uses the chunk's centroid kept in registers.
 //   k_hist     N_j (block histograms in smem) + #changed + label check
-//   k_scan     offsets, per-cluster chunk counts, cursors, N_j -> packed
+//   k_scan_a   per cluster: N_j -> packed, per-(block, cluster) offsets within the cluster
+//   k_scan_b   exclusive scans over clusters, chunk counts, chunk -> cluster map
 //   k_scatter  perm[offset_j + rank] = row (warp-aggregated cursors)
 //   k_segsum   S_j += sum of the chunk's rows, E += sum (x - c_j)^2
 
@@ -167,7 +168,7 @@ __device__ __forceinline__ void finish_changed(const Dev& d, double* out, long l
 }
 
 // Block b histograms its contiguous row range [b*R, (b+1)*R) into smem and
-// stores it to seg_bh[b][K]; k_scan turns counts into per-(block, cluster)
+// stores it to seg_bh[b][K]; k_scan_a/b turn counts into per-(block, cluster)
 // base offsets, and k_scatter re-walks the same rows placing each at
 // base + local rank (shared-memory counters): no global atomics on the
 // contended per-cluster cursors.
@@ -188,7 +189,22 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     block_rows(d, r0, r1);
     long long ch = 0;
     int bad = 0;
-    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    // 4 labels per thread per step (more loads in flight: the pass is latency-bound)
+    const long long nv = (r1 - r0) / 4;
+    for (long long v = threadIdx.x; v < nv; v += blockDim.x) {
+        const long long i = r0 + 4 * v;
+        int l4[4], p4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { l4[u] = p.lab[i + u]; p4[u] = p.prev ? p.prev[i + u] : l4[u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = l4[u];
+            if (j < 0 || j >= K) { bad = 1; continue; }
+            ch += (p4[u] != j);
+            atomicAdd(&hs[j], 1);
+        }
+    }
+    for (long long i = r0 + 4 * nv + threadIdx.x; i < r1; i += blockDim.x) {
         const int j = p.lab[i];
         if (j < 0 || j >= K) { bad = 1; continue; }
         if (p.prev) ch += (p.prev[i] != j);
@@ -201,13 +217,37 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     finish_changed(d, p.out, ch);
 }
 
-// one block: per-cluster totals over blocks, exclusive scans over clusters,
-// per-(block, cluster) scatter bases, chunk offsets and chunk -> cluster map.
-__global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g, int nblk) {
+// Phase A (one thread per cluster, many blocks): N_j = sum over row blocks, and
+// the per-(block, cluster) offsets within cluster j (exclusive scan over blocks).
+__global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     const int K = d.K;
-    const long long KD = (long long)K * d.d;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= K) return;
+    long long o = 0;
+    int b = 0;
+    for (; b + 8 <= nblk; b += 8) {
+        int t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = d.seg_bh[(long long)(b + u) * K + j];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { d.seg_bh[(long long)(b + u) * K + j] = (int)o; o += t[u]; }
+    }
+    for (; b < nblk; ++b) {
+        const int t = d.seg_bh[(long long)b * K + j];
+        d.seg_bh[(long long)b * K + j] = (int)o;
+        o += t;
+    }
+    d.seg_off[j] = (int)o;                               // count for now; phase B makes it an offset
+    p.out[(long long)K * d.d + j] = (double)o;           // N_j
+}
+
+// Phase B (one block): exclusive scans over clusters of the counts and of the
+// chunk counts, chunk -> cluster map.  k_scatter adds seg_off[j] to the bases.
+__global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    const int K = d.K;
     __shared__ long long wsum[2][32];
     __shared__ long long carry[2];
     if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
@@ -215,18 +255,7 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g, int nblk) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int base = 0; base < K; base += blockDim.x) {
         const int j = base + threadIdx.x;
-        long long c = 0;
-        if (j < K) {
-            int b = 0;
-            for (; b + 8 <= nblk; b += 8) {
-                int t[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) t[u] = d.seg_bh[(long long)(b + u) * K + j];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) c += t[u];
-            }
-            for (; b < nblk; ++b) c += d.seg_bh[(long long)b * K + j];
-        }
+        const long long c = j < K ? d.seg_off[j] : 0;
         const long long nc = (c + SEG_ROWS - 1) / SEG_ROWS;
         long long a = c, bb = nc;
         for (int o = 1; o < 32; o <<= 1) {
@@ -247,19 +276,12 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, GEval g, int nblk) {
         __syncthreads();
         const long long pa = (w ? wsum[0][w - 1] : 0) + a - c + carry[0];
         const long long pb = (w ? wsum[1][w - 1] : 0) + bb - nc + carry[1];
+        __syncthreads();                                 // every thread has read its count
         if (j < K) {
             d.seg_off[j] = (int)pa;
             d.seg_chunk[j] = (int)pb;
-            p.out[KD + j] = (double)c;                  // N_j
-            long long o = pa;                            // scatter base of (block b, cluster j)
-            for (int b = 0; b < nblk; ++b) {
-                const int v = d.seg_bh[(long long)b * K + j];
-                d.seg_bh[(long long)b * K + j] = (int)o;
-                o += v;
-            }
             for (long long q = 0; q < nc; ++q) d.seg_cmap[pb + q] = j;
         }
-        __syncthreads();
         if (threadIdx.x == blockDim.x - 1) { carry[0] = pa + c; carry[1] = pb + nc; }
         __syncthreads();
     }
@@ -272,11 +294,21 @@ __global__ void __launch_bounds__(1024) k_scatter(Dev d, GEval g) {
     extern __shared__ int cur[];
     const int K = d.K;
     const int* bh = d.seg_bh + (long long)blockIdx.x * K;
-    for (int j = threadIdx.x; j < K; j += blockDim.x) cur[j] = bh[j];
+    for (int j = threadIdx.x; j < K; j += blockDim.x) cur[j] = bh[j] + d.seg_off[j];
     __syncthreads();
     long long r0, r1;
     block_rows(d, r0, r1);
-    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const long long nv = (r1 - r0) / 4;
+    for (long long v = threadIdx.x; v < nv; v += blockDim.x) {
+        const long long i = r0 + 4 * v;
+        int l4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) l4[u] = p.lab[i + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (l4[u] >= 0 && l4[u] < K) d.perm[atomicAdd(&cur[l4[u]], 1)] = (int)(i + u);
+    }
+    for (long long i = r0 + 4 * nv + threadIdx.x; i < r1; i += blockDim.x) {
         const int j = p.lab[i];
         if (j < 0 || j >= K) continue;
         d.perm[atomicAdd(&cur[j], 1)] = (int)i;
@@ -429,23 +461,24 @@ cudaError_t setup_update() {
 
 bool update_sorted(const Dev& d) { return d.n >= AAKM_SORTED_MIN_ROWS && d.d <= 128 && d.K <= AAKM_SORTED_MAX_K; }
 
-void launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
+int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     if (!update_sorted(d)) {
         k_update<<<d.upd_blocks, 256, 0, s>>>(d, g);
-        return;
+        return 1;
     }
     const size_t hs = (size_t)d.K * 4;
     k_hist<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
-    k_scan<<<1, 1024, 0, s>>>(d, g, AAKM_SEG_BLOCKS);
+    k_scan_a<<<(d.K + 255) / 256, 256, 0, s>>>(d, g, AAKM_SEG_BLOCKS);
+    k_scan_b<<<1, 1024, 0, s>>>(d, g);
     k_scatter<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
     if (d.d % 4 == 0 && (d.d / 4) <= 32 && ((d.d / 4) & (d.d / 4 - 1)) == 0) {
         switch (d.d / 4) {
-            case 1: k_segsum4<1><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
-            case 2: k_segsum4<2><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
-            case 4: k_segsum4<4><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
-            case 8: k_segsum4<8><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
-            case 16: k_segsum4<16><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
-            default: k_segsum4<32><<<d.upd_blocks, 256, 0, s>>>(d, g); return;
+            case 1: k_segsum4<1><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
+            case 2: k_segsum4<2><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
+            case 4: k_segsum4<4><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
+            case 8: k_segsum4<8><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
+            case 16: k_segsum4<16><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
+            default: k_segsum4<32><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
         }
     }
     const int V = (d.d + 31) / 32;
@@ -455,6 +488,7 @@ void launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
         case 3: k_segsum<3><<<d.upd_blocks, 256, 0, s>>>(d, g); break;
         default: k_segsum<4><<<d.upd_blocks, 256, 0, s>>>(d, g); break;
     }
+    return 5;
 }
 
 // kmeans_update API: G = S / N (empty -> C_prev row, R-A15), counts.
