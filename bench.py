@@ -158,9 +158,8 @@ def time_to_converge(cfgname, rank, world, barrier):
     import torch
     import torch.distributed as dist
     from paper_1805_10638_b200 import aakm, synthetic
-    X, C0, cfg = synthetic.make(cfgname, seed=0)
-    lo, hi = synthetic.shard_bounds(cfg.N, rank, world)
-    Xs = torch.from_numpy(X[lo:hi]).cuda()
+    X, C0, cfg = synthetic.make_shard(cfgname, rank, world, seed=0)
+    Xs = torch.from_numpy(X).cuda()
     C0d = torch.from_numpy(C0).cuda()
     out = {"config": cfgname, "N": cfg.N, "d": cfg.d, "K": cfg.K}
     for name, kw in (("aa", dict(m0=cfg.m0)), ("lloyd", dict(m0=0, dynamic_m=False))):
@@ -209,10 +208,10 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    X, C0, cfg = synthetic.make(args.config, seed=0)
+    X, C0, cfg = synthetic.make_shard(args.config, rank, world, seed=0)     # this rank's rows only
     lo, hi = synthetic.shard_bounds(cfg.N, rank, world)
-    Xs = torch.from_numpy(X[lo:hi]).cuda()
-    X_host = torch.from_numpy(X[lo:hi]).pin_memory()
+    Xs = torch.from_numpy(X).cuda()
+    X_host = torch.from_numpy(X).pin_memory()
     C0d = torch.from_numpy(C0).cuda()
     km = aakm.KMeans(Xs, cfg.K, aakm.config(m0=cfg.m0, assign_path=args.path, timing=True),
                      n_global=cfg.N, rank=rank, nranks=world)

@@ -151,6 +151,43 @@ def make(cfg: str, seed: int = 0, N: int | None = None, K: int | None = None,
     return X, C0, dataclasses.replace(base, N=N, K=K)
 
 
+def make_shard(cfg: str, rank: int, world: int, seed: int = 0, N: int | None = None, K: int | None = None):
+    """(X[lo:hi] of shard_bounds(N, rank, world), C0, Config): the same bytes as
+    make(...) restricted to this rank's rows, without holding the full X (each
+    chunk is drawn, its shard rows and C^0 rows are kept, the rest dropped)."""
+    base = CONFIGS[cfg]
+    N = base.N if N is None else int(N)
+    K = base.K if K is None else int(K)
+    d = base.d
+    if K > N:
+        raise ValueError("K > N")
+    lo, hi = shard_bounds(N, rank, world)
+    p = _params(cfg, seed, N, d, K)
+    idx = _rng(cfg, seed, 1).choice(N, K, replace=False)
+    Xs = np.empty((hi - lo, d), dtype=np.float32)
+    C0 = np.empty((K, d), dtype=np.float32)
+    bounds = [(c, r0, min(r0 + CHUNK, N)) for c, r0 in enumerate(range(0, N, CHUNK))]
+    need = [b for b in bounds if (b[1] < hi and b[2] > lo) or np.any((idx >= b[1]) & (idx < b[2]))]
+    nthreads = max(1, min(len(need), (os.cpu_count() or 1) // max(world, 1), 16))
+
+    def work(b):
+        c, r0, r1 = b
+        x = _chunk(cfg, seed, c, r0, r1, d, p)
+        a0, a1 = max(r0, lo), min(r1, hi)
+        if a0 < a1:
+            Xs[a0 - lo:a1 - lo] = x[a0 - r0:a1 - r0]
+        sel = np.nonzero((idx >= r0) & (idx < r1))[0]
+        C0[sel] = x[idx[sel] - r0]
+
+    if nthreads > 1 and len(need) > 1:
+        with cf.ThreadPoolExecutor(nthreads) as ex:
+            list(ex.map(work, need))
+    else:
+        for b in need:
+            work(b)
+    return Xs, C0, dataclasses.replace(base, N=N, K=K)
+
+
 def shard_bounds(N: int, rank: int, world: int):
     """Contiguous row block of `rank` (data-parallel sharding over samples)."""
     q, r = divmod(N, world)

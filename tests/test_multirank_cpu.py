@@ -80,3 +80,17 @@ def test_gloo_two_rank_decomposition(tmp_path, cfg):
     N = got[K * d:K * d + K]
     G = np.where(N[:, None] > 0, got[:K * d].reshape(K, d) / np.maximum(N, 1)[:, None], C)
     np.testing.assert_allclose(G, G_ref, rtol=1e-12, atol=1e-12)
+
+
+def test_make_shard_matches_make():
+    # each rank draws only its rows (bench.py at N > 1); bytes equal make()'s slice
+    from paper_1805_10638_b200 import synthetic as S
+    for cfg, N, K in (("c3", 70_000, 32), ("c5", 1_200_000, 64)):
+        X, C0, _ = S.make(cfg, N=N, K=K)
+        for world in (1, 2, 3):
+            parts = []
+            for r in range(world):
+                Xs, C0s, _ = S.make_shard(cfg, r, world, N=N, K=K)
+                assert np.array_equal(C0s, C0)
+                parts.append(Xs)
+            assert np.array_equal(np.concatenate(parts), X)
