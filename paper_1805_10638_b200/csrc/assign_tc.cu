@@ -508,7 +508,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         int xb = 0;
         if (t == 0 && live(0)) {
             if (DX) {
-                for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(0) * TC_BM));
+                if (MODE == 0)
+                    for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(0) * TC_BM));
             } else {
                 mbar_expect_tx(stfull, A * ATOM_BYTES_X);
                 for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(0) * TC_BM));
@@ -516,10 +517,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         }
         const float inv_sx = KIND ? 1.0f / d.st->c_scale : 1.0f;     // exact (power of 2)
         const float hxs = 0.5f * inv_sx * inv_sx;
-        const float* Xsrc = MODE == 0 ? d.X : d.Xf;
+        // DX candidate pass (MODE 1): the flagged rows are read in place through the
+        // flag list (no gathered copy), so there is nothing to prefetch by TMA
+        const float* Xsrc = (MODE == 0 || DX) ? d.X : d.Xf;
         for (long long it = 0; live(it); ++it) {
             if (DX) {
-                if (t == 0 && live(it + 1))                        // next row tile -> L2
+                if (MODE == 0 && t == 0 && live(it + 1))           // next row tile -> L2
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(it + 1) * TC_BM));
             } else {
                 mbar_wait_sleep(stfull, sph, 128);
@@ -559,9 +562,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         for (int c16 = 0; c16 < 8; ++c16) {
                             // columns 64 a16 + 8 c16 .. + 8 of row r (zeros past the last row)
                             const long long grow = tile_of(it) * TC_BM + r;
-                            const float4* src = reinterpret_cast<const float4*>(Xsrc + grow * A * 32) + a16 * 16 + c16 * 2;
                             float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-                            if (grow < n_rows) { v0 = __ldg(src); v1 = __ldg(src + 1); }
+                            if (grow < n_rows) {
+                                const long long xrow = MODE == 1 ? (long long)d.flag_rows[grow] : grow;
+                                const float4* src = reinterpret_cast<const float4*>(Xsrc + xrow * A * 32) + a16 * 16 + c16 * 2;
+                                v0 = __ldg(src); v1 = __ldg(src + 1);
+                            }
                             const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
                             uint32_t hp[4], lp[4];
 #pragma unroll
@@ -1145,10 +1151,12 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
 }
 
 int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
-    k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    // the 2xFP16 engine reads the flagged rows in place (DX splitter); 3xTF32 TMAs a gathered copy
+    const int gather = d.tc_kind == 1 ? 0 : 1;
+    if (gather) k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
     k_refine_exact<<<4 * g_num_sms, 256, 0, s>>>(d, g);
-    return 3;
+    return 2 + gather;
 }
 
 }  // namespace aakm
