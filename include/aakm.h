@@ -50,7 +50,7 @@ extern "C" {
 #endif
 
 #define KMEANS_M_MAX 30          /* m_bar of PAPER.md:177; ring = m_max + 1 slots */
-#define KMEANS_ABI_VERSION 1
+#define KMEANS_ABI_VERSION 2
 
 typedef struct kmeans_handle kmeans_handle;
 typedef struct CUstream_st *kmeans_stream_t;   /* == cudaStream_t */
@@ -84,6 +84,16 @@ typedef struct {
     double ridge;        /* lambda on the unit-diagonal scaled Gram (R-A14)       */
     int32_t assign_path; /* KMEANS_PATH_*                                        */
     int32_t timing;      /* 1 = record CUDA events around each assignment launch  */
+    int32_t bounded;     /* 1 = Hamerly-bounded assignment in the Algorithm 1
+                            passes (aa_step / run; 2xFP16 engine only, otherwise
+                            ignored): per row an upper bound on the distance to
+                            its centroid and a lower bound on every other one,
+                            moved by the centroid shifts (the paper's Assignment-
+                            Step is Hamerly-pruned); rows the
+                            bounds prove unchanged keep their label, the rest run
+                            through the tensor engine as a gathered row list.
+                            Labels stay exact.  Default 0 (dense: bench.py's
+                            dist-evals/s metric counts N*K per pass).            */
 } kmeans_config;
 
 /* Result of kmeans_run (fields per DESIGN.md R-A19). */
@@ -209,6 +219,12 @@ AAKM_API int64_t kmeans_launch_count(const kmeans_handle *h);
 
 /* Rows flagged as near-ties (re-decided in fp64) by the last assignment. */
 AAKM_API kmeans_status kmeans_last_flagged(kmeans_handle *h, int64_t *flagged /*host*/);
+
+/* Assignment work since the last Algorithm 1 line 1 (kmeans_aa_step(C0) /
+ * kmeans_run): rows run through the assignment engine vs rows assigned
+ * (local to this rank).  Equal unless cfg.bounded proved rows unchanged. */
+AAKM_API kmeans_status kmeans_bounded_stats(kmeans_handle *h, int64_t *rows_scored /*host*/,
+                                            int64_t *rows_total /*host*/);
 
 /* Name of the assignment engine the handle selected ("simt"/"tc"). */
 AAKM_API const char *kmeans_assign_path_name(const kmeans_handle *h);

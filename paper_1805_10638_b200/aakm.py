@@ -34,7 +34,7 @@ class AAKMError(RuntimeError):
 class Config(ct.Structure):
     _fields_ = [("m0", ct.c_int32), ("m_max", ct.c_int32), ("eps1", ct.c_double), ("eps2", ct.c_double),
                 ("dynamic_m", ct.c_int32), ("max_iters", ct.c_int32), ("ridge", ct.c_double),
-                ("assign_path", ct.c_int32), ("timing", ct.c_int32)]
+                ("assign_path", ct.c_int32), ("timing", ct.c_int32), ("bounded", ct.c_int32)]
 
 
 class Report(ct.Structure):
@@ -88,6 +88,7 @@ def lib():
                 "kmeans_assign_timing": ([P, ct.POINTER(D), ct.POINTER(I64)], I32),
                 "kmeans_launch_count": ([P], I64),
                 "kmeans_last_flagged": ([P, ct.POINTER(I64)], I32),
+                "kmeans_bounded_stats": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
                 "kmeans_assign_path_name": ([P], ct.c_char_p),
                 "kmeans_destroy": ([P], I32),
                 "kmeans_last_error": ([P], ct.c_char_p),
@@ -108,13 +109,14 @@ def header_symbols():
 
 
 def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000, ridge=1e-10,
-           assign_path="auto", timing=False) -> Config:
+           assign_path="auto", timing=False, bounded=False) -> Config:
     """Algorithm 1 settings (m0 = 5 per BASELINE configs, reading R-A18)."""
     c = Config()
     c.m0, c.m_max, c.eps1, c.eps2 = m0, m_max, eps1, eps2
     c.dynamic_m, c.max_iters, c.ridge = int(dynamic_m), max_iters, ridge
     c.assign_path = PATHS[assign_path] if isinstance(assign_path, str) else int(assign_path)
     c.timing = int(timing)
+    c.bounded = int(bounded)
     return c
 
 
@@ -283,6 +285,12 @@ class KMeans:
         ms, n = ct.c_double(), ct.c_int64()
         self._c(lib().kmeans_assign_timing(self.h, ct.byref(ms), ct.byref(n)))
         return ms.value, n.value
+
+    def bounded_stats(self):
+        """(rows run through the assignment engine, rows assigned) since line 1."""
+        a, b = ct.c_int64(), ct.c_int64()
+        self._c(lib().kmeans_bounded_stats(self.h, ct.byref(a), ct.byref(b)))
+        return a.value, b.value
 
     def last_flagged(self) -> int:
         v = ct.c_int64()

@@ -131,6 +131,8 @@ __global__ void k_control(Dev d, int stage) {
         const long long ch = (long long)pk[KD + d.K + 1];
         st->n_assign += 1;
         st->last_flag[0] = d.flag_count[0];
+        st->rows_total += d.n;
+        st->rows_scored += (d.ub && st->bnd_use) ? d.act_count[0] : d.n;
         st->reject = 0; st->accepted_now = 0; st->rejected_now = 0;
         st->E_cand = E; st->E_final = E; st->changed = ch;
         if (st->init_mode) return;                              // line 1: E^0 = +inf regardless
@@ -154,6 +156,8 @@ __global__ void k_control(Dev d, int stage) {
         const long long ch = (long long)pk[KD + d.K + 1];
         st->n_assign += 1;
         st->last_flag[1] = d.flag_count[1];
+        st->rows_total += d.n;
+        st->rows_scored += (d.ub && st->bnd_use) ? d.act_count[1] : d.n;
         st->E_final = E; st->changed = ch;
         st->lloyd = 1;
         if (ch == 0) { st->done = 1; st->converged = 1; }       // R3: re-test after the fallback
@@ -444,6 +448,8 @@ __global__ void k_reset(Dev d) {
     st->done = 0; st->converged = 0; st->init_mode = 1;
     st->hist_count = 0; st->accepted_now = 0; st->rejected_now = 0; st->label_error = 0;
     st->n_alpha = 1; st->fb_slot = 0; st->final_traced = 0;
+    st->bnd_ready = 0; st->bnd_use = 0;                         // bounded engine: recompute every row first
+    st->rows_scored = 0; st->rows_total = 0;
 }
 
 void launch_reset(const Dev& d, cudaStream_t s) { k_reset<<<1, 1, 0, s>>>(d); }

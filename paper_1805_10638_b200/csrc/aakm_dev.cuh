@@ -44,6 +44,9 @@ struct alignas(16) DevState {
     float tau_abs;               // 2xFP16 engine: absolute term of the near-tie bound
     float cn_amul;               // 2xFP16 engine: power-of-two A-side factor of the folded ||c||^2 column
     unsigned int x_amax_bits;    // create-time scratch: max |x| over the shard (2xFP16 X scale)
+    int bnd_ready, bnd_use;      // bounded engine: bounds valid for the next / this assignment
+    long long rows_scored, rows_total;   // bounded engine: rows run through the tensor engine / all rows
+    unsigned int shift_max_bits, shift_tmp, shift_ctr, pad3;   // max_j ||c_j - c_ref_j|| (float bits)
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -89,6 +92,12 @@ struct Dev {
     int* seg_chunk;       // chunk offsets (K+1)
     int* seg_cmap;        // chunk -> cluster (n/SEG_ROWS + K)
     int* perm;            // rows bucketed by label (n)
+    float* ub;            // bounded engine (nullptr = dense): per row, upper bound on ||x_i - c_{rho_i}||
+    float* lb;            //   ... and lower bound on min_{j != rho_i} ||x_i - c_j||, w.r.t. C_ref
+    int* act_rows;        //   rows the bounds could not prove unchanged (capacity n)
+    long long* act_count; //   [2] their counts, branch A / B (zeroed per pass with packed)
+    float* C_ref;         //   centroids the bounds refer to (the last assigned set)
+    float* shift;         //   ||c_j - c_ref_j|| of the set being assigned (K)
     float* Gring;         // H x K*d
     float* Fring;         // H x K*d
     double* gram_part;    // AAKM_GRAM_BLOCKS x (2*H)
@@ -128,6 +137,8 @@ bool tc_supported(int d, int K);
 bool tc16_supported(int d, int K);
 float tau_gamma_tc16(int d);
 void launch_csplit16(const Dev& d, int mode, cudaStream_t s);
+int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s);   // k_shift + k_bounds
+void launch_assign_tc_bounded(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 __host__ __device__ inline unsigned int cnimg_off(int r, int byte) {   // (row, byte in its 32-B K row)
     return (unsigned)((r >> 3) * 256 + (byte >> 4) * 128 + (r & 7) * 16 + (byte & 15));
 }

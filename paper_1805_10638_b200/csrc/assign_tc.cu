@@ -346,6 +346,14 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         if (n_rows > d.fcap) n_rows = d.fcap;
         if (n_rows == 0) return;
     }
+    // MODE 2 (bounded, 2xFP16 only): once the Hamerly bounds are live, only the rows
+    // k_bounds could not prove unchanged, through the gathered list act_rows
+    const bool use_list = MODE == 2 && d.st->bnd_use;
+    const int* rows_of = MODE == 1 ? d.flag_rows : d.act_rows;
+    if (use_list) {
+        n_rows = d.act_count[g.branch];
+        if (n_rows == 0) return;
+    }
     constexpr int NATOM = KIND ? A / 2 : A;        // 128-B operand K-atoms per row
     constexpr int AELEM = KIND ? 64 : 32;          // elements per operand atom
     // one operand buffer: hi + lo (+ KIND 1: this row tile's A side of the folded block)
@@ -508,7 +516,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         int xb = 0;
         if (t == 0 && live(0)) {
             if (DX) {
-                if (MODE == 0)
+                if (MODE != 1 && !use_list)
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(0) * TC_BM));
             } else {
                 mbar_expect_tx(stfull, A * ATOM_BYTES_X);
@@ -522,7 +530,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         const float* Xsrc = (MODE == 0 || DX) ? d.X : d.Xf;
         for (long long it = 0; live(it); ++it) {
             if (DX) {
-                if (MODE == 0 && t == 0 && live(it + 1))           // next row tile -> L2
+                if (MODE != 1 && !use_list && t == 0 && live(it + 1))   // next row tile -> L2
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(it + 1) * TC_BM));
             } else {
                 mbar_wait_sleep(stfull, sph, 128);
@@ -564,7 +572,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             const long long grow = tile_of(it) * TC_BM + r;
                             float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
                             if (grow < n_rows) {
-                                const long long xrow = MODE == 1 ? (long long)d.flag_rows[grow] : grow;
+                                const long long xrow = (MODE == 1 || use_list) ? (long long)rows_of[grow] : grow;
                                 const float4* src = reinterpret_cast<const float4*>(Xsrc + xrow * A * 32) + a16 * 16 + c16 * 2;
                                 v0 = __ldg(src); v1 = __ldg(src + 1);
                             }
@@ -690,7 +698,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     for (int u = 0; u < NTRK; ++u) O1[u] = B1[u];
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {
-                        if (MODE == 0) {
+                        if (MODE != 1) {
                             // two pairs -> trackers u = (j/2 + pp) mod NTRK
 #pragma unroll
                             for (int pp = 0; pp < 2; ++pp) {
@@ -713,13 +721,13 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             }
                         }
                     }
-                    if (MODE == 0) {
+                    if (MODE != 1) {
 #pragma unroll
                         for (int u = 0; u < NTRK; ++u) BB[u] = B1[u] != O1[u] ? j0 : BB[u];
                     }
                 }
             }
-            if (MODE == 0) {
+            if (MODE != 1) {
                 // merge the trackers, then the column quarters (ties -> lower column index)
                 float b1 = B1[0], b2 = B2[0];
                 int i1 = BB[0] + (int)(__float_as_uint(B1[0]) & 31u);
@@ -743,8 +751,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         i1 = tk ? oi1 : i1;
                         b1 = fminf(b1, m.x);
                     }
-                    const long long row = frow;
-                    const bool ok = row < d.n;
+                    const bool ok = frow < n_rows;
+                    const long long row = (use_list && ok) ? (long long)d.act_rows[frow] : frow;
                     float tau;
                     if (KIND) {
                         // window keys are exact accumulator values: decode.  The folded terms
@@ -756,8 +764,21 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         // magnitude), + 2 key quanta (32 ulps each) of the larger-magnitude key
                         tau = Usc * (gam * (xn + 2.0f * cmax2) + tau_abs) + 7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
                     }
+                    const bool flag = ok && (b2 - b1 <= tau);
                     if (ok) lab_out[row] = i1;
-                    push_flag_tc(d, g.branch, ok && (b2 - b1 <= tau), row, b1, tau);
+                    if (KIND && ok && d.ub) {
+                        // Hamerly bounds for the next assignment (distance units, rounded
+                        // outward): each accumulator is within tau of its exact value;
+                        // near-tie rows are left for the exact refine and always recomputed
+                        float u = INFINITY, l = 0.f;
+                        if (!flag) {
+                            u = __fsqrt_ru(__fdiv_ru(fmaxf(b1 + tau - 6.0f, 0.0f), Usc)) * 1.000001f;
+                            l = __fsqrt_rd(__fdiv_rd(fmaxf(b2 - tau - 6.0f, 0.0f), Usc)) * 0.999999f;
+                        }
+                        d.ub[row] = u;
+                        d.lb[row] = l;
+                    }
+                    push_flag_tc(d, g.branch, flag, row, b1, tau);
                 }
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
             } else if (frow < n_rows) {
@@ -840,7 +861,7 @@ float tau_gamma_tc16(int d) { return 4.0f * (3.0f * 2.3841858e-7f + (3.0f * d / 
 
 #define AAKM_TC_INSTANCES(X, CG)                                                                     \
     X(1, 0, 0, CG) X(2, 0, 0, CG) X(3, 0, 0, CG) X(4, 0, 0, CG) X(1, 1, 0, CG) X(2, 1, 0, CG) X(3, 1, 0, CG) \
-    X(4, 1, 0, CG) X(2, 0, 1, CG) X(4, 0, 1, CG) X(2, 1, 1, CG) X(4, 1, 1, CG)
+    X(4, 1, 0, CG) X(2, 0, 1, CG) X(4, 0, 1, CG) X(2, 1, 1, CG) X(4, 1, 1, CG) X(2, 2, 1, CG) X(4, 2, 1, CG)
 
 cudaError_t setup_tc() {
     int dev = 0;
@@ -967,9 +988,9 @@ static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStre
     pick_pipe(KIND, A, NT, S, NXB, CG);
     const size_t smem = smem_need(KIND, A, S, NT, NXB, CG);
     const int xr = xr_of(NT, NXB, CG);
-    const CUtensorMap& xm = MODE == 0 ? m->x : m->xf;
+    const CUtensorMap& xm = MODE == 1 ? m->xf : m->x;
     const long long n_tiles = MODE == 0 ? (d.n + TC_BM - 1) / TC_BM : 1ll << 40;
-    if (KIND == 0) {
+    if constexpr (KIND == 0) {
         switch (A) {
             case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
             case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
@@ -996,6 +1017,14 @@ static void launch_tc_mode(const Dev& d, const GEval& g, const TcMaps* m, cudaSt
 
 void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
     launch_tc_mode<0>(d, g, static_cast<const TcMaps*>(maps), s);
+}
+
+// Bounded engine (2xFP16 only): MODE 2 over the rows k_bounds left unproven
+// (all rows, writing fresh bounds, until the bounds are live).
+void launch_assign_tc_bounded(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
+    const TcMaps* m = static_cast<const TcMaps*>(maps);
+    if (tc_cg() == 2) launch_tc_cg<2, 1, 2>(d, g, m, s);
+    else launch_tc_cg<2, 1, 1>(d, g, m, s);
 }
 
 // ---- 2xFP16 operand prep of the centroids (after every k_combine): power-of-two

@@ -1,0 +1,115 @@
+// bounds.cu -- Hamerly-bounded assignment for the 2xFP16 tensor engine (f2).
+//
+// The paper's Assignment-Step is Hamerly-pruned: per sample
+// an upper bound u_i on the distance to its own centroid and a lower bound l_i
+// on the distance to every other one.  When the centroids move by
+// s_j = ||c_j - c_ref_j||, u_i + s_{rho_i} and l_i - max_j s_j remain bounds, and
+// u_i < l_i proves the label is unchanged (the exact argmin is still rho_i).
+// Here the surviving rows are not scanned one by one: the unproven rows form a
+// gathered list that the tensor engine runs in MODE 2, which writes fresh
+// bounds (from its exact window keys and error bound) for every row it scores.
+//   k_shift   s_j and max_j s_j for the set about to be assigned; C_ref <- it
+//   k_bounds  per row: the Hamerly test; proven rows keep (copy) their label and
+//             move their bounds, the rest are appended to act_rows
+// AA jumps are handled by construction: the shifts are measured between
+// whichever two sets are assigned consecutively (C^t, then C_AU^t on a
+// rejection, then C^{t+1}).  All bound arithmetic rounds outward.
+#include <math.h>
+
+#include "aakm_dev.cuh"
+
+namespace aakm {
+
+__global__ void __launch_bounds__(256) k_shift(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    DevState* st = d.st;
+    const float* C = g.Cassign ? g.Cassign : d.C;
+    const int D = d.d;
+    const int lane = threadIdx.x & 31;
+    float bmax = 0.f;
+    for (long long j = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < d.K;
+         j += (long long)gridDim.x * (blockDim.x >> 5)) {
+        double s = 0.0;
+        for (int k = lane; k < D; k += 32) {
+            const float c = C[j * D + k];
+            const double df = (double)c - (double)d.C_ref[j * D + k];
+            s = fma(df, df, s);
+            d.C_ref[j * D + k] = c;
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const float sh = (float)(sqrt(s) * (1.0 + 1e-12)) * 1.000001f;   // upward
+        if (lane == 0) d.shift[j] = sh;
+        bmax = fmaxf(bmax, sh);
+    }
+    for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    __shared__ float wm[32];
+    __shared__ bool last;
+    if (lane == 0) wm[threadIdx.x >> 5] = bmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, wm[i]);
+        atomicMax(&st->shift_tmp, __float_as_uint(m));          // non-negative floats order as uints
+        __threadfence();
+        last = atomicAdd(&st->shift_ctr, 1u) == gridDim.x - 1;
+        if (last) {
+            __threadfence();
+            st->shift_max_bits = atomicExch(&st->shift_tmp, 0u);
+            st->shift_ctr = 0;
+            st->bnd_use = st->bnd_ready;                        // bounds valid for this assignment?
+            st->bnd_ready = 1;                                  // ... and (fresh or moved) for the next
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    const DevState* st = d.st;
+    if (!st->bnd_use) return;                                   // first assignment: dense
+    const float smax = __uint_as_float(st->shift_max_bits);
+    const int cur = st->cur;
+    int* lab_out = g.lab_out ? g.lab_out : d.lab[cur];
+    // labels the bounds refer to: the previous pass's final labels (branch A), or
+    // branch A's labels of this pass (branch B assigns the fallback after it)
+    const int* lab_ref = g.branch == 0 ? d.lab[cur ^ 1] : lab_out;
+    const int lane = threadIdx.x & 31;
+    const long long n = d.n;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool unsafe = false;
+        if (i < n) {
+            const int a = lab_ref[i];
+            const float u = __fadd_ru(d.ub[i], d.shift[a]);
+            const float l = __fsub_rd(d.lb[i], smax);
+            if (u < l) {
+                d.ub[i] = u;
+                d.lb[i] = l;
+                if (g.branch == 0) lab_out[i] = a;
+            } else {
+                unsafe = true;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, unsafe);
+        if (m) {
+            long long base = 0;
+            if (lane == 0) base = (long long)atomicAdd((unsigned long long*)&d.act_count[g.branch],
+                                                       (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (unsafe) d.act_rows[base + __popc(m & ((1u << lane) - 1))] = (int)i;
+        }
+    }
+}
+
+int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s) {
+    int kb = (int)((d.K + 7) / 8);
+    if (kb > 1184) kb = 1184;
+    if (kb < 1) kb = 1;
+    k_shift<<<kb, 256, 0, s>>>(d, g);
+    long long rb = (d.n + 255) / 256;
+    if (rb > 4 * 1184) rb = 4 * 1184;
+    if (rb < 1) rb = 1;
+    k_bounds<<<(int)rb, 256, 0, s>>>(d, g);
+    return 2;
+}
+
+}  // namespace aakm

@@ -133,7 +133,8 @@ namespace {
 struct Layout {
     size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
         scratch, packed1,
-        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, perm, Gring, Fring, gram_part, trace, total,
+        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, perm, Gring, Fring, gram_part, trace,
+        ub, lb, act_rows, C_ref, shift, total,
         scratch_bytes;
 };
 
@@ -142,7 +143,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 // rows the tensor-core candidate refine can hold (more -> SIMT refine for the rest)
 long long fcap_of(long long n) { return n / 4 + 4096; }
 
-Layout layout(long long n, int d, int K, int m_max) {
+Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     Layout L;
     size_t o = 0;
     const size_t KD = (size_t)K * d;
@@ -181,6 +182,10 @@ Layout layout(long long n, int d, int K, int m_max) {
     L.Fring = take((size_t)H * KD * 4);
     L.gram_part = take((size_t)AAKM_GRAM_BLOCKS * 2 * AAKM_H_SLOTS * 8);
     L.trace = take((size_t)AAKM_TRACE_CAP * sizeof(TraceRec));
+    // bounded engine (2xFP16, cfg.bounded): 12 B per row + 2 centroid-sized arrays
+    const size_t nb = bounded ? (size_t)n : 0;
+    L.ub = take(nb * 4 + 4); L.lb = take(nb * 4 + 4); L.act_rows = take(nb * 4 + 4);
+    L.C_ref = take(bounded ? KD * 4 : 4); L.shift = take(bounded ? (size_t)K * 4 : 4);
     L.total = o;
     return L;
 }
@@ -210,9 +215,14 @@ kmeans_status validate(long long n_local, int d, int k, const kmeans_config* cfg
 
 // ------------------------------------------------------------------ enqueue helpers
 static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaStream_t s) {
-    if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16)
+    if (d.ub) {                                   // bounded engine: Hamerly test, then the gathered rows
+        h->launches += launch_bounds_prep(d, g, s);
+        launch_assign_tc_bounded(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
+    } else if (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16) {
         launch_assign_tc(d, g, d.st == h->d.st ? h->tcm : h->tcm_api, s);
-    else launch_assign_simt(d, g, s);
+    } else {
+        launch_assign_simt(d, g, s);
+    }
 }
 
 // Centroid prep after every change of C (a1 / a13): ||c||^2, tf32 split, and
@@ -343,7 +353,7 @@ kmeans_status kmeans_config_default(kmeans_config* cfg) {
     memset(cfg, 0, sizeof(*cfg));
     cfg->m0 = 2; cfg->m_max = 30; cfg->eps1 = 0.02; cfg->eps2 = 0.5;
     cfg->dynamic_m = 1; cfg->max_iters = 10000; cfg->ridge = 1e-10;
-    cfg->assign_path = KMEANS_PATH_AUTO; cfg->timing = 0;
+    cfg->assign_path = KMEANS_PATH_AUTO; cfg->timing = 0; cfg->bounded = 0;
     return KMEANS_OK;
 }
 
@@ -353,7 +363,7 @@ kmeans_status kmeans_workspace_size(int64_t n_local, int32_t d, int32_t k, const
     if (!bytes) return KMEANS_ERR_INVALID;
     kmeans_status s = validate(n_local, d, k, cfg, why);
     if (s != KMEANS_OK) { g_create_err = why; return s; }
-    *bytes = layout(n_local, d, k, cfg->m_max).total;
+    *bytes = layout(n_local, d, k, cfg->m_max, cfg->bounded != 0).total;
     return KMEANS_OK;
 }
 
@@ -380,7 +390,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     if ((nranks == 1) != (uid128 == nullptr)) { g_create_err = "uid128 must be NULL iff nranks == 1"; return KMEANS_ERR_INVALID; }
     if (n_global < n_local || k > n_global) { g_create_err = "need n_local <= n_global and k <= n_global"; return KMEANS_ERR_INVALID; }
     if (((uintptr_t)workspace & 255) != 0) { g_create_err = "workspace must be 256-byte aligned"; return KMEANS_ERR_INVALID; }
-    Layout L = layout(n_local, d, k, cfg->m_max);
+    Layout L = layout(n_local, d, k, cfg->m_max, cfg->bounded != 0);
     if (workspace_bytes < L.total) { g_create_err = "workspace too small"; return KMEANS_ERR_INVALID; }
 
     kmeans_handle* h = new kmeans_handle();
@@ -409,6 +419,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.cand_cnt = (int*)(w + L.cand_cnt);
     D.fcap = fcap_of(n_local);
     D.flag_count = (long long*)(w + L.scratch);
+    D.act_count = (long long*)(w + L.scratch + 32);                   // [2], zeroed per pass with the flags
     D.packed[0] = (double*)(w + L.scratch + 256);
     D.packed[1] = (double*)(w + L.packed1);
     D.upd_part = (double*)(w + L.upd_part);
@@ -433,12 +444,18 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     const bool tcpath = h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16;
     D.cnimg = tcpath ? (uint8_t*)(w + L.cnimg) : nullptr;
     D.key_mul = 32u;
+    if (h->path == KMEANS_PATH_TC16 && cfg->bounded) {                 // bounded engine (Algorithm 1 passes)
+        D.ub = (float*)(w + L.ub); D.lb = (float*)(w + L.lb); D.act_rows = (int*)(w + L.act_rows);
+        D.C_ref = (float*)(w + L.C_ref); D.shift = (float*)(w + L.shift);
+    }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
     D.x_scale = 1.f; D.x_inv_scale = 1.f; D.x_absmax = 0.f;
     D.tau_gamma = h->path == KMEANS_PATH_TC ? tau_gamma_tc(d)
                 : h->path == KMEANS_PATH_TC16 ? tau_gamma_tc16(d) : tau_gamma_simt(d);
     h->da = D;
+    h->da.ub = nullptr; h->da.lb = nullptr; h->da.act_rows = nullptr;    // the API calls stay dense
+    h->da.C_ref = nullptr; h->da.shift = nullptr;
     h->da.st = (DevState*)(w + L.st_api);
     h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
     h->da.cn = (float*)(w + L.cna);
@@ -737,6 +754,16 @@ kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* 
 }
 
 int64_t kmeans_launch_count(const kmeans_handle* h) { return h ? h->launches : 0; }
+
+kmeans_status kmeans_bounded_stats(kmeans_handle* h, int64_t* rows_scored, int64_t* rows_total) {
+    LIVE(h);
+    if (!rows_scored || !rows_total) FAIL(h, KMEANS_ERR_INVALID, "NULL output");
+    CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    *rows_scored = h->st_host->rows_scored;
+    *rows_total = h->st_host->rows_total;
+    return KMEANS_OK;
+}
 
 kmeans_status kmeans_last_flagged(kmeans_handle* h, int64_t* flagged) {
     LIVE(h);

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from gpu_helpers import check_assign, dev, make, require_gpu
+from gpu_helpers import check_assign, dev, make, require_gpu, torch
 from paper_1805_10638_b200 import aakm
 
 pytestmark = pytest.mark.gpu
@@ -70,3 +70,42 @@ print("ok")
     env = dict(os.environ, AAKM_TC_CG="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# ---------------------------------------------------------------- bounded engine (f2)
+@pytest.mark.parametrize("cfg,N,K", [("c5", 40_000, 256), ("c4", 30_000, 256)])
+def test_bounded_matches_dense_passes(cfg, N, K):
+    """Hamerly-bounded assignment (cfg.bounded) against the dense engine, pass by
+    pass from the same C^0: identical decisions and labels; energies to 1e-9."""
+    X, C0, c = make(cfg, N=N, K=K)
+    Xd = dev(X)
+    kd = aakm.KMeans(Xd, c.K, aakm.config(m0=5, assign_path="tc16"))
+    kb = aakm.KMeans(Xd, c.K, aakm.config(m0=5, assign_path="tc16", bounded=True))
+    kd.aa_step(dev(C0)); kb.aa_step(dev(C0))
+    for p in range(60):
+        a, b = kd.aa_step(), kb.aa_step()
+        for k in ("t", "m", "m_t", "accepted", "rejected", "converged", "changed"):
+            assert a[k] == b[k], (p, k, a, b)
+        assert abs(a["energy"] - b["energy"]) <= 1e-9 * a["energy"], (p, a, b)
+        _, la = kd.centroids(); _, lb = kb.centroids()
+        assert torch.equal(la, lb), p
+        if a["converged"]:
+            break
+    scored, total = kb.bounded_stats()
+    assert 0 < scored < total, (scored, total)      # the bounds did prove rows unchanged
+    s0, t0 = kd.bounded_stats()
+    assert s0 == t0
+    kd.close(); kb.close()
+
+
+@pytest.mark.parametrize("cfg,N,K,seed", [("c4", 8_000, 256, 0), ("c5", 20_000, 256, 1)])
+def test_bounded_end_to_end_vs_oracle(cfg, N, K, seed):
+    X, C0, c = make(cfg, seed=seed, N=N, K=K)
+    km = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, assign_path="tc16", bounded=True))
+    C, lab, rep = km.run(dev(C0))
+    ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=5, parity=True))
+    assert rep["converged"] and ref["converged"]
+    assert rep["iters"] == ref["iters"], (rep, ref["iters"])
+    assert abs(rep["energy"] - ref["energy"]) <= 1e-4 * ref["energy"]
+    check_assign(X, C.cpu().numpy(), lab.cpu().numpy())
+    km.close()
