@@ -16,8 +16,9 @@ roofline = the dominant kernel (the assignment engine), algorithmic flops
          2 N K d per launch over its CUDA-event duration inside the timed
          steps, against the tensor (three MMAs per product, fp32-equivalent)
          or FP32 peak.
-time_to_converge = Algorithm 1 and plain Lloyd run to convergence on
-         --ttc-config (default c3; c5 does not converge within 5000 passes).
+time_to_converge = Algorithm 1 (bounded and dense assignment) and Lloyd run to
+         convergence on --ttc-config (default c4; c5 does not converge within
+         5000 passes under Algorithm 1).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
        python bench.py --impl reference ...   (the CPU oracle arm)
@@ -151,10 +152,12 @@ def run_reference(args):
 
 # --------------------------------------------------------------------- time to converge
 def time_to_converge(cfgname, rank, world, barrier):
-    """Algorithm 1 (dynamic m, m0 = 5) and plain Lloyd (m = 0) run to convergence
+    """Algorithm 1 (dynamic m, m0 = 5) with the Hamerly-bounded assignment
+    (cfg.bounded, the paper's own pruned Assignment-Step), the same with the
+    dense assignment, and plain Lloyd (m = 0, bounded), each run to convergence
     (rule R3) through kmeans_run on the sharded config, C^0 resident; CUDA events
-    around the call, max over ranks.  (c5 itself does not converge within 5000
-    passes under either variant, see profiles/r01_converge_gpu.jsonl.)"""
+    around the call, max over ranks.  (c5 does not converge within 5000 passes
+    under Algorithm 1, see profiles/r01_converge_gpu.jsonl.)"""
     import torch
     import torch.distributed as dist
     from paper_1805_10638_b200 import aakm, synthetic
@@ -162,7 +165,9 @@ def time_to_converge(cfgname, rank, world, barrier):
     Xs = torch.from_numpy(X).cuda()
     C0d = torch.from_numpy(C0).cuda()
     out = {"config": cfgname, "N": cfg.N, "d": cfg.d, "K": cfg.K}
-    for name, kw in (("aa", dict(m0=cfg.m0)), ("lloyd", dict(m0=0, dynamic_m=False))):
+    variants = (("", dict(m0=cfg.m0, bounded=True)), ("dense_", dict(m0=cfg.m0, bounded=False)),
+                ("lloyd_", dict(m0=0, dynamic_m=False, bounded=True)))
+    for pre, kw in variants:
         km = aakm.KMeans(Xs, cfg.K, aakm.config(max_iters=20000, **kw), n_global=cfg.N, rank=rank, nranks=world)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -173,12 +178,14 @@ def time_to_converge(cfgname, rank, world, barrier):
         t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        scored, total = km.bounded_stats()
         km.close()
-        pre = "" if name == "aa" else "lloyd_"
         out.update({pre + "seconds": float(t.item()), pre + "iters": rep["iters"], pre + "n_assign": rep["n_assign"],
-                    pre + "converged": bool(rep["converged"]), pre + "energy": rep["energy"]})
-        if name == "aa":
-            out.update({"accepted": rep["n_accepted"], "rejected": rep["n_rejected"], "m_final": rep["m_final"]})
+                    pre + "converged": bool(rep["converged"]), pre + "energy": rep["energy"],
+                    pre + "rows_scored_frac": scored / max(total, 1)})
+        if pre == "":
+            out.update({"accepted": rep["n_accepted"], "rejected": rep["n_rejected"], "m_final": rep["m_final"],
+                        "assign_engine": "bounded 2xFP16" if kw.get("bounded") and cfg.d in (64, 128) else "dense"})
     return out
 
 
@@ -193,7 +200,7 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "tc16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ttc-config", default="c3", help="config run to convergence for time_to_converge ('none' skips)")
+    ap.add_argument("--ttc-config", default="c4", help="config run to convergence for time_to_converge ('none' skips)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
