@@ -140,6 +140,11 @@ typedef struct {
     int64_t t;
     double E1, E2;       /* E^{t-1}, E^{t-2} (post-guard)                         */
     int64_t n_accepted, n_rejected, n_assign;
+    double *gram;        /* (m_max+1)^2 doubles, nullable: the cached Gram entries
+                            <dF(a), dF(b)> indexed by ring slot (a mod (m_max+1));
+                            opaque -- export fills it, import restores it so a
+                            resumed run repeats the uninterrupted one; NULL on
+                            import recomputes it from Fhist on the host          */
 } kmeans_state;
 
 /* Fill cfg with the defaults above.  Errors: INVALID if cfg is NULL. */
@@ -197,7 +202,13 @@ AAKM_API kmeans_status kmeans_run(kmeans_handle *h, const float *C0, float *C_ou
  * Asynchronous. */
 AAKM_API kmeans_status kmeans_get_centroids(kmeans_handle *h, float *C_out, int32_t *labels_out);
 
-/* Checkpoint / lockstep hooks (host buffers, see kmeans_state).  Synchronise. */
+/* Checkpoint / lockstep hooks (host buffers, see kmeans_state).  Synchronise.
+ * export: the state between two passes (after kmeans_aa_step / kmeans_run).
+ * import: replaces the Algorithm 1 state of this handle (same X, K, d and
+ * m_max as the exporter; nranks > 1: every rank imports its own export); the
+ * next kmeans_aa_step(NULL) continues pass t.  Errors: INVALID for NULL C /
+ * fallback / history buffers, hist_count outside [0, m_max + 1], m outside
+ * [0, m_max], t < 1. */
 AAKM_API kmeans_status kmeans_state_export(kmeans_handle *h, kmeans_state *st /*host*/);
 AAKM_API kmeans_status kmeans_state_import(kmeans_handle *h, const kmeans_state *st /*host*/);
 

@@ -54,7 +54,7 @@ class State(ct.Structure):
                 ("labels_prev", ct.c_void_p), ("hist_count", ct.c_int32), ("m", ct.c_int32),
                 ("lloyd", ct.c_int32), ("done", ct.c_int32), ("t", ct.c_int64), ("E1", ct.c_double),
                 ("E2", ct.c_double), ("n_accepted", ct.c_int64), ("n_rejected", ct.c_int64),
-                ("n_assign", ct.c_int64)]
+                ("n_assign", ct.c_int64), ("gram", ct.c_void_p)]
 
 
 def _struct(s):
@@ -268,18 +268,41 @@ class KMeans:
         C = np.zeros(KD, np.float32); fb = np.zeros(KD, np.float32)
         Gh = np.zeros(H * KD, np.float32); Fh = np.zeros(H * KD, np.float32)
         lp = np.zeros(max(self.n, 1), np.int32)
+        gr = np.zeros(H * H, np.float64)
         s = State()
         s.C, s.fallback, s.Ghist, s.Fhist, s.labels_prev = (C.ctypes.data, fb.ctypes.data, Gh.ctypes.data,
                                                             Fh.ctypes.data, lp.ctypes.data)
+        s.gram = gr.ctypes.data
         self._c(lib().kmeans_state_export(self.h, ct.byref(s)))
         r = _struct(s)
-        for k in ("C", "fallback", "Ghist", "Fhist", "labels_prev"):
+        for k in ("C", "fallback", "Ghist", "Fhist", "labels_prev", "gram"):
             r.pop(k)
         hc = r["hist_count"]
         r.update(C=C.reshape(self.K, self.d), fallback=fb.reshape(self.K, self.d),
                  Ghist=Gh.reshape(H, self.K, self.d)[:hc], Fhist=Fh.reshape(H, self.K, self.d)[:hc],
-                 labels_prev=lp[: self.n])
+                 labels_prev=lp[: self.n], gram=gr)
         return r
+
+    def state_import(self, st, with_gram=True):
+        """Resume Algorithm 1 from a state_export() dict (checkpoint/resume)."""
+        KD = self.K * self.d
+        hc = int(st["hist_count"])
+        H = self.cfg.m_max + 1
+        C = np.ascontiguousarray(st["C"], np.float32).reshape(KD)
+        fb = np.ascontiguousarray(st["fallback"], np.float32).reshape(KD)
+        Gh = np.zeros(H * KD, np.float32); Fh = np.zeros(H * KD, np.float32)
+        Gh[: hc * KD] = np.ascontiguousarray(st["Ghist"], np.float32).reshape(-1)[: hc * KD]
+        Fh[: hc * KD] = np.ascontiguousarray(st["Fhist"], np.float32).reshape(-1)[: hc * KD]
+        lp = np.ascontiguousarray(st["labels_prev"], np.int32).reshape(-1)
+        gr = np.ascontiguousarray(st["gram"], np.float64) if with_gram else None
+        s = State()
+        s.C, s.fallback, s.Ghist, s.Fhist = C.ctypes.data, fb.ctypes.data, Gh.ctypes.data, Fh.ctypes.data
+        s.labels_prev = lp.ctypes.data if self.n > 0 else None
+        s.gram = gr.ctypes.data if gr is not None else None
+        s.hist_count, s.m, s.lloyd, s.done, s.t = hc, int(st["m"]), int(st["lloyd"]), int(st["done"]), int(st["t"])
+        s.E1, s.E2 = float(st["E1"]), float(st["E2"])
+        s.n_accepted, s.n_rejected, s.n_assign = int(st["n_accepted"]), int(st["n_rejected"]), int(st["n_assign"])
+        self._c(lib().kmeans_state_import(self.h, ct.byref(s)))
 
     def assign_timing(self):
         ms, n = ct.c_double(), ct.c_int64()

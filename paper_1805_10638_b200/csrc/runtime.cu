@@ -729,13 +729,64 @@ kmeans_status kmeans_state_export(kmeans_handle* h, kmeans_state* out) {
         const int which = S.done ? (S.cur ^ 1) : (S.cur ^ 1);
         CK(h, cudaMemcpy(out->labels_prev, d.lab[which], (size_t)d.n * 4, cudaMemcpyDeviceToHost));
     }
+    if (out->gram)
+        for (int a = 0; a < d.H; ++a)
+            for (int b = 0; b < d.H; ++b) out->gram[a * d.H + b] = S.gram[a * d.H + b];
     return KMEANS_OK;
 }
 
 kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
     LIVE(h);
-    (void)st;
-    FAIL(h, KMEANS_ERR_INVALID, "kmeans_state_import is not implemented in this build");
+    const Dev& d = h->d;
+    if (!st || !st->C || (st->hist_count > 0 && (!st->Ghist || !st->Fhist)) || (d.n > 0 && !st->labels_prev))
+        FAIL(h, KMEANS_ERR_INVALID, "NULL state buffer");
+    if (st->hist_count < 0 || st->hist_count > d.H) FAIL(h, KMEANS_ERR_INVALID, "hist_count outside [0, m_max + 1]");
+    if (st->m < 0 || st->m > d.m_max) FAIL(h, KMEANS_ERR_INVALID, "m outside [0, m_max]");
+    if (st->t < 1) FAIL(h, KMEANS_ERR_INVALID, "t < 1 (export after Algorithm 1 line 1)");
+    cudaStream_t s = h->stream;
+    const size_t KD = (size_t)d.K * d.d;
+    CK(h, cudaStreamSynchronize(s));
+    // history into the ring slots it came from: entry j = (G^{t-1-j}, F^{t-1-j})
+    for (int j = 0; j < st->hist_count; ++j) {
+        const long long slot = ((st->t - 1 - j) % d.H + d.H) % d.H;
+        CK(h, cudaMemcpy(d.Gring + slot * KD, st->Ghist + j * KD, KD * 4, cudaMemcpyHostToDevice));
+        CK(h, cudaMemcpy(d.Fring + slot * KD, st->Fhist + j * KD, KD * 4, cudaMemcpyHostToDevice));
+    }
+    CK(h, cudaMemcpy(d.C, st->C, KD * 4, cudaMemcpyHostToDevice));
+    if (d.n > 0) CK(h, cudaMemcpy(d.lab[1], st->labels_prev, (size_t)d.n * 4, cudaMemcpyHostToDevice));
+    // the control state, on top of the current device state (keeps engine-side fields)
+    CK(h, cudaMemcpy(h->st_host, d.st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    DevState S = *h->st_host;
+    S.t = st->t; S.m = st->m; S.lloyd = st->lloyd; S.E1 = st->E1; S.E2 = st->E2;
+    S.E_final = st->E1; S.E_cand = st->E1;
+    S.done = st->done; S.converged = 0; S.cur = 0; S.init_mode = 0; S.reject = 0;
+    S.hist_count = st->hist_count; S.n_accepted = st->n_accepted; S.n_rejected = st->n_rejected;
+    S.n_assign = st->n_assign; S.trace_len = 0; S.final_traced = 0; S.label_error = 0;
+    S.bnd_ready = 0; S.bnd_use = 0; S.rows_scored = 0; S.rows_total = 0;
+    if (st->gram) {
+        for (int a = 0; a < d.H; ++a)
+            for (int b = 0; b < d.H; ++b) S.gram[a * d.H + b] = st->gram[a * d.H + b];
+    } else {
+        // recompute <dF(a), dF(b)> for the window from the host history (fp64)
+        const int W = st->hist_count - 1;                         // differences available
+        for (int a = 0; a < W; ++a)
+            for (int b = 0; b <= a; ++b) {
+                double v = 0.0;
+                for (size_t e = 0; e < KD; ++e) {
+                    const double da = (double)st->Fhist[a * KD + e] - (double)st->Fhist[(a + 1) * KD + e];
+                    const double db = (double)st->Fhist[b * KD + e] - (double)st->Fhist[(b + 1) * KD + e];
+                    v += da * db;
+                }
+                const long long sa = ((st->t - 1 - a) % d.H + d.H) % d.H, sb = ((st->t - 1 - b) % d.H + d.H) % d.H;
+                S.gram[sa * d.H + sb] = v;
+                S.gram[sb * d.H + sa] = v;
+            }
+    }
+    CK(h, cudaMemcpy(d.st, &S, sizeof(DevState), cudaMemcpyHostToDevice));
+    combine(h, d, 2, d.C, s);                                     // operand prep of C^t
+    CK(h, cudaStreamSynchronize(s));
+    CK(h, cudaGetLastError());
+    return KMEANS_OK;
 }
 
 kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* launches) {

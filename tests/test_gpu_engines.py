@@ -109,3 +109,43 @@ def test_bounded_end_to_end_vs_oracle(cfg, N, K, seed):
     assert abs(rep["energy"] - ref["energy"]) <= 1e-4 * ref["energy"]
     check_assign(X, C.cpu().numpy(), lab.cpu().numpy())
     km.close()
+
+
+# ---------------------------------------------------------------- checkpoint / resume
+@pytest.mark.parametrize("cfg,N,K,path", [("c5", 30_000, 256, "auto"), ("c2", None, None, "auto"),
+                                          ("c3", 20_000, 64, "tc")])
+def test_checkpoint_resume(cfg, N, K, path):
+    """kmeans_state_export after pass t, kmeans_state_import into a fresh handle on
+    the same data: the resumed passes repeat the uninterrupted ones."""
+    X, C0, c = make(cfg, N=N, K=K)
+    Xd = dev(X)
+    a = aakm.KMeans(Xd, c.K, aakm.config(m0=5, assign_path=path))
+    a.aa_step(dev(C0))
+    for _ in range(8):
+        if a.aa_step()["converged"]:
+            pytest.skip("converged before the checkpoint")
+    snap = a.state_export()
+    ref = [a.aa_step() for _ in range(6)]
+    b = aakm.KMeans(Xd, c.K, aakm.config(m0=5, assign_path=path))
+    b.state_import(snap)
+    got = [b.aa_step() for _ in range(6)]
+    for p, (x, y) in enumerate(zip(ref, got)):
+        for k in ("t", "m", "m_t", "accepted", "rejected", "converged", "changed"):
+            assert x[k] == y[k], (p, k, x, y)
+        assert abs(x["energy"] - y["energy"]) <= 1e-9 * x["energy"], (p, x, y)
+        if x["converged"]:
+            break
+    sa, sb = a.state_export(), b.state_export()
+    assert np.allclose(sa["C"], sb["C"], rtol=1e-6, atol=1e-6)
+    a.close(); b.close()
+
+
+def test_state_import_validation():
+    X, C0, c = make("c1")
+    km = aakm.KMeans(dev(X), c.K, aakm.config(m0=2))
+    km.aa_step(dev(C0)); km.aa_step()
+    snap = km.state_export()
+    bad = dict(snap, m=31)
+    with pytest.raises(aakm.AAKMError):
+        km.state_import(bad)
+    km.close()
