@@ -126,9 +126,9 @@ __global__ void k_control(Dev d, int stage) {
     if (st->done) return;
     const long long KD = (long long)d.K * d.d;
     if (stage == 0) {
-        const double* pk = d.packed[0];
-        const double E = pk[KD + d.K];
-        const long long ch = (long long)pk[KD + d.K + 1];
+        const long long* pk = d.packed[0];
+        const double E = __longlong_as_double(pk[2 * KD + d.K]);   // k_energy, after the allreduce
+        const long long ch = pk[2 * KD + d.K + 1];
         st->n_assign += 1;
         st->last_flag[0] = d.flag_count[0];
         st->rows_total += d.n;
@@ -151,9 +151,9 @@ __global__ void k_control(Dev d, int stage) {
         }
     } else {
         if (!st->reject) return;
-        const double* pk = d.packed[1];
-        const double E = pk[KD + d.K];
-        const long long ch = (long long)pk[KD + d.K + 1];
+        const long long* pk = d.packed[1];
+        const double E = __longlong_as_double(pk[2 * KD + d.K]);
+        const long long ch = pk[2 * KD + d.K + 1];
         st->n_assign += 1;
         st->last_flag[1] = d.flag_count[1];
         st->rows_total += d.n;
@@ -172,15 +172,15 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
     if (st->done) return;
     const int D = d.d;
     const long long KD = (long long)d.K * D;
-    const double* pk = st->reject ? d.packed[1] : d.packed[0];
+    const long long* pk = st->reject ? d.packed[1] : d.packed[0];
     const long long slot = st->t % d.H;
     float* G = d.Gring + slot * KD;
     float* F = d.Fring + slot * KD;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
          e += (long long)gridDim.x * blockDim.x) {
-        const double nj = pk[KD + e / D];
+        const long long nj = pk[2 * KD + e / D];
         const float c = d.C[e];
-        const float g = nj > 0.0 ? (float)(pk[e] / nj) : c;        // G = S / N (Eq. 4)
+        const float g = nj > 0 ? (float)(fx_value(pk[e], pk[KD + e], d.fx_inv) / (double)nj) : c;   // G = S / N (Eq. 4)
         G[e] = g;
         F[e] = g - c;                                            // F^t = G^t - C^t (fp32)
     }

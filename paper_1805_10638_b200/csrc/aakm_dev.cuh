@@ -85,7 +85,11 @@ struct Dev {
     int* cand_cnt;        // candidate counts per flagged row and epilogue half (> AAKM_MAXC/2 = overflow)
     long long fcap;       // capacity of the candidate path (rows beyond -> SIMT refine)
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
-    double* packed[2];    // [S (K*d) | N (K) | E | changed], branch A / B
+    long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E (fp64 bits) | changed], branch A / B
+    float fx_scale;       // 2^(22-e), |x| <= 2^e over all ranks: S in exact fixed point (update.cu)
+    double fx_inv;        // 2^(e-22)
+    double xn_total;      // sum_i ||x_i||^2 over all ranks (fixed-point exact, create time)
+    double xn_local;      // ... over this rank's rows
     double* upd_part;     // per-block (E, changed) partials
     int* seg_bh;          // sorted update engine: per-block histograms -> scatter bases (SEG_BLOCKS x K)
     int* seg_off;         // row offsets of cluster j in perm (K+1)
@@ -117,7 +121,7 @@ struct GEval {
     const int* lab_prev;  // used when prev_mode == 2
     int prev_mode;        // 0 = d.lab[st->cur ^ 1], 1 = none, 2 = lab_prev
     const float* Cassign; // nullptr -> d.C
-    double* packed_out;   // nullptr -> d.packed[branch]
+    long long* packed_out;// nullptr -> d.packed[branch]
 };
 
 __device__ __forceinline__ bool geval_active(const Dev& d, const GEval& g) {
@@ -142,8 +146,6 @@ void launch_assign_tc_bounded(const Dev& d, const GEval& g, const void* maps, cu
 __host__ __device__ inline unsigned int cnimg_off(int r, int byte) {   // (row, byte in its 32-B K row)
     return (unsigned)((r >> 3) * 256 + (byte >> 4) * 128 + (r & 7) * 16 + (byte & 15));
 }
-void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s);
-void launch_xnmax(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
 // the launchers below return how many kernels they enqueued (the gpu_launches count)
 int launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
 int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
@@ -155,8 +157,16 @@ void launch_gram(const Dev& d, cudaStream_t s);
 void launch_solve(const Dev& d, cudaStream_t s);
 void launch_advance(const Dev& d, cudaStream_t s);
 void launch_reset(const Dev& d, cudaStream_t s);
-void launch_update_G(const Dev& d, const double* packed, const float* Cprev, float* G,
+void launch_update_G(const Dev& d, const long long* packed, const float* Cprev, float* G,
                      long long* counts, cudaStream_t s);
+void launch_energy(const Dev& d, const GEval& g, cudaStream_t s);       // E after the allreduce
+void launch_partials_out(const Dev& d, const long long* packed, const float* C, double* out, cudaStream_t s);
+void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
+void launch_xstats_sum(const float* X, long long n, int d, double q, long long* out, cudaStream_t s);
+// fixed-point sums (update.cu) -> fp64: (hi + lo 2^-22) 2^(e-22), exact conversions
+__host__ __device__ inline double fx_value(long long hi, long long lo, double fx_inv) {
+    return ((double)hi + (double)lo * 2.384185791015625e-07) * fx_inv;
+}
 
 // one-time kernel attribute setup (max dynamic smem); never during stream capture
 cudaError_t setup_simt();

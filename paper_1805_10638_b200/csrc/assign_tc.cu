@@ -1053,37 +1053,6 @@ void launch_csplit16(const Dev& d, int mode, cudaStream_t s) {
     k_csplit16<<<blocks, 256, 0, s>>>(d, mode);
 }
 
-// max |x| over the shard (float bits of non-negative values order as uints)
-__global__ void k_absmax(const float* X, long long n, unsigned int* out) {
-    float m = 0.f;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-        m = fmaxf(m, fabsf(X[e]));
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
-}
-
-void launch_absmax(const float* X, long long n, unsigned int* out, cudaStream_t s) {
-    k_absmax<<<2 * (g_num_sms > 0 ? g_num_sms : 148), 256, 0, s>>>(X, n, out);
-}
-
-// max_i ||x_i||^2 over the shard (one warp per row, fp32; the caller adds a margin)
-__global__ void k_xnmax(const float* X, long long n, int d, unsigned int* out) {
-    const int lane = threadIdx.x & 31;
-    float m = 0.f;
-    for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
-         i += ((long long)gridDim.x * blockDim.x) >> 5) {
-        float s = 0.f;
-        for (int k = lane; k < d; k += 32) { const float v = X[i * d + k]; s = fmaf(v, v, s); }
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        m = fmaxf(m, s);
-    }
-    if (lane == 0) atomicMax(out, __float_as_uint(m));
-}
-
-void launch_xnmax(const float* X, long long n, int d, unsigned int* out, cudaStream_t s) {
-    k_xnmax<<<4 * (g_num_sms > 0 ? g_num_sms : 148), 256, 0, s>>>(X, n, d, out);
-}
-
 // ---- refine for the tensor-core engine: gather -> candidate pass -> exact fp64
 // one warp per flagged row, float4 lanes (d % 32 == 0 on this engine)
 __global__ void __launch_bounds__(256) k_gather_flagged(Dev d, GEval g) {

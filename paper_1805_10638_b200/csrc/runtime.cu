@@ -165,7 +165,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.Xf = take((size_t)fc * d * 4 + 16);
     L.cand = take((size_t)fc * AAKM_MAXC * 4 + 4);
     L.cand_cnt = take((size_t)fc * 16 + 16);
-    const size_t pk = (KD + K + 2) * 8;
+    const size_t pk = (2 * KD + K + 2) * 8;     // [S_hi | S_lo | N | E | changed], int64 words
     L.scratch = o;
     size_t s0 = take(256);                 // flag counts
     (void)s0;
@@ -245,10 +245,13 @@ static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
     }
 }
 
-static kmeans_status allreduce(kmeans_handle* h, double* buf, cudaStream_t s) {
+// One integer allreduce of the packed partials: exact and order-free, so every
+// rank (and every rank count) sees the same bytes.  The E slot is still zero
+// here; k_energy fills it from the reduced sums afterwards.
+static kmeans_status allreduce(kmeans_handle* h, long long* buf, cudaStream_t s) {
     if (h->nranks <= 1) return KMEANS_OK;
-    const size_t cnt = (size_t)h->d.K * h->d.d + h->d.K + 2;
-    NK(h, ncclAllReduce(buf, buf, cnt, ncclFloat64, ncclSum, h->comm, s));
+    const size_t cnt = 2 * (size_t)h->d.K * h->d.d + h->d.K + 2;
+    NK(h, ncclAllReduce(buf, buf, cnt, ncclInt64, ncclSum, h->comm, s));
     return KMEANS_OK;
 }
 
@@ -286,9 +289,11 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
     if (h->nranks > 1) dbg("allreduce", s);
+    launch_energy(d, g, s);
+    dbg("energy", s);
     launch_control(d, branch, s);
     dbg("control", s);
-    h->launches += 1;
+    h->launches += 2;
     return KMEANS_OK;
 }
 
@@ -420,8 +425,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.fcap = fcap_of(n_local);
     D.flag_count = (long long*)(w + L.scratch);
     D.act_count = (long long*)(w + L.scratch + 32);                   // [2], zeroed per pass with the flags
-    D.packed[0] = (double*)(w + L.scratch + 256);
-    D.packed[1] = (double*)(w + L.packed1);
+    D.packed[0] = (long long*)(w + L.scratch + 256);
+    D.packed[1] = (long long*)(w + L.packed1);
     D.upd_part = (double*)(w + L.upd_part);
     D.seg_bh = (int*)(w + L.seg_bh);
     D.seg_off = (int*)(w + L.seg_off);
@@ -481,25 +486,21 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         }
     }
     CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    // this rank's max |x_ik| and max ||x_i||^2 (one pass; float bits of non-negative
+    // values order as uints): the 2xFP16 operand scale (rank-local) and, reduced
+    // over the ranks below, the scales of the exact update sums
+    float mloc[2] = {0.f, 0.f};
+    {
+        unsigned int* mx = (unsigned int*)(w + L.scratch);
+        CKC(cudaMemsetAsync(mx, 0, 8, h->stream));
+        launch_xstats_max(X, n_local, d, mx, h->stream);
+        CKC(cudaMemcpyAsync(mloc, mx, 8, cudaMemcpyDeviceToHost, h->stream));
+        CKC(cudaStreamSynchronize(h->stream));
+    }
     if (h->path == KMEANS_PATH_TC16) {
-        // power-of-two scale of X for the fp16 split: |x| / s_x <= 2^13
-        unsigned int* amax = &((DevState*)(w + L.st))->x_amax_bits;
-        CKC(cudaMemsetAsync(amax, 0, 4, h->stream));
-        if (n_local > 0) launch_absmax(X, n_local * (long long)d, amax, h->stream);
-        unsigned int bits = 0;
-        CKC(cudaMemcpyAsync(&bits, amax, 4, cudaMemcpyDeviceToHost, h->stream));
-        CKC(cudaStreamSynchronize(h->stream));
-        float m;
-        memcpy(&m, &bits, 4);
+        const float m = mloc[0];
         const float sx = m > 0.f ? exp2f(ceilf(log2f(m)) - 13.0f) : 1.0f;
-        // max ||x_i||^2 (float bits of non-negative values order as uints)
-        CKC(cudaMemsetAsync(amax, 0, 4, h->stream));
-        if (n_local > 0) launch_xnmax(X, n_local, d, amax, h->stream);
-        CKC(cudaMemcpyAsync(&bits, amax, 4, cudaMemcpyDeviceToHost, h->stream));
-        CKC(cudaStreamSynchronize(h->stream));
-        float xn2;
-        memcpy(&xn2, &bits, 4);
-        const float xnm = sqrtf(xn2) * (1.0f + 1e-6f);   // upward margin for the fp32 norm
+        const float xnm = sqrtf(mloc[1]) * (1.0f + 1e-6f);   // (already rounded up in fp32) margin
         for (Dev* dv : {&h->d, &h->da}) {
             dv->x_absmax = m; dv->x_scale = sx; dv->x_inv_scale = 1.0f / sx; dv->x_nmax = xnm;
         }
@@ -532,6 +533,43 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             return KMEANS_ERR_NCCL;
         }
     }
+    // Scales of the exact fixed-point update sums (update.cu) and sum_i ||x_i||^2,
+    // from statistics of X over ALL ranks, so every rank forms identical bytes.
+    {
+        unsigned int* mx = (unsigned int*)(w + L.scratch);            // scratch is free until the first pass
+        long long* xs = (long long*)(w + L.scratch + 64);
+        CKC(cudaMemsetAsync(w + L.scratch, 0, 128, h->stream));
+        CKC(cudaMemcpyAsync(mx, mloc, 8, cudaMemcpyHostToDevice, h->stream));
+        if (nranks > 1) {
+            ncclResult_t r = ncclAllReduce(mx, mx, 2, ncclFloat32, ncclMax, h->comm, h->stream);
+            if (r != ncclSuccess) { g_create_err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); delete h; return KMEANS_ERR_NCCL; }
+        }
+        unsigned int mb[2];
+        CKC(cudaMemcpyAsync(mb, mx, 8, cudaMemcpyDeviceToHost, h->stream));
+        CKC(cudaStreamSynchronize(h->stream));
+        float mf[2];
+        memcpy(mf, mb, 8);
+        int ex = 0, en = 0;
+        if (mf[0] > 0.f) frexpf(mf[0], &ex);                           // max |x| < 2^ex
+        if (mf[1] > 0.f) frexpf(mf[1], &en);                           // max ||x||^2 < 2^en
+        const double q = ldexp(1.0, 22 - en);                          // row ||x||^2 q <= 2^22
+        launch_xstats_sum(X, n_local, d, q, xs, h->stream);
+        long long loc[2] = {0, 0}, tot[2] = {0, 0};
+        CKC(cudaMemcpyAsync(loc, xs, 16, cudaMemcpyDeviceToHost, h->stream));
+        if (nranks > 1) {
+            ncclResult_t r = ncclAllReduce(xs, xs, 2, ncclInt64, ncclSum, h->comm, h->stream);
+            if (r != ncclSuccess) { g_create_err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); delete h; return KMEANS_ERR_NCCL; }
+        }
+        CKC(cudaMemcpyAsync(tot, xs, 16, cudaMemcpyDeviceToHost, h->stream));
+        CKC(cudaStreamSynchronize(h->stream));
+        for (Dev* dv : {&h->d, &h->da}) {
+            dv->fx_scale = ldexpf(1.0f, 22 - ex);
+            dv->fx_inv = ldexp(1.0, ex - 22);
+            dv->xn_local = ((double)loc[0] + (double)loc[1] * 9.313225746154785e-10) / q;   // 2^-30
+            dv->xn_total = ((double)tot[0] + (double)tot[1] * 9.313225746154785e-10) / q;
+        }
+        CKC(cudaMemsetAsync(w + L.scratch, 0, 128, h->stream));
+    }
     CKC(cudaStreamSynchronize(h->stream));
 #undef CKC
     *out = h;
@@ -555,13 +593,17 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
     st = allreduce(h, d.packed[0], s);
     if (st != KMEANS_OK) return st;
+    launch_energy(d, g, s);
+    h->launches += 1;
     const long long KD = (long long)d.K * d.d;
-    CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + KD + d.K, 16, cudaMemcpyDeviceToHost, s));
+    CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + 2 * KD + d.K, 16, cudaMemcpyDeviceToHost, s));
     CK(h, cudaMemcpyAsync(h->scal_host + 2, d.flag_count, 8, cudaMemcpyDeviceToHost, s));
     CK(h, cudaStreamSynchronize(s));
     CK(h, cudaGetLastError());
-    if (energy_out) *energy_out = h->scal_host[0];
-    if (changed_out) *changed_out = labels_prev ? (int64_t)h->scal_host[1] : 0;
+    long long raw[2];
+    memcpy(raw, h->scal_host, 16);
+    if (energy_out) memcpy(energy_out, &raw[0], 8);                  // fp64 bits (k_energy)
+    if (changed_out) *changed_out = labels_prev ? (int64_t)raw[1] : 0;
     return KMEANS_OK;
 }
 
@@ -593,12 +635,13 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     if ((!labels && h->d.n > 0) || !C || !packed_out) FAIL(h, KMEANS_ERR_INVALID, "NULL argument");
     cudaStream_t s = h->stream;
     const Dev& d = h->da;
-    const size_t bytes = ((size_t)d.K * d.d + d.K + 2) * 8;
-    CK(h, cudaMemsetAsync(packed_out, 0, bytes, s));
+    CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels);
-    g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev; g.Cassign = C; g.packed_out = packed_out;
+    g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev; g.Cassign = C;
     h->launches += launch_update(d, g, s);
+    launch_partials_out(d, d.packed[0], C, packed_out, s);            // unreduced, as doubles
+    h->launches += 1;
     CK(h, cudaStreamSynchronize(s));
     CK(h, cudaGetLastError());
     return KMEANS_OK;

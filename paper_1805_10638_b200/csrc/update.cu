@@ -1,16 +1,19 @@
-// update.cu -- update step partials + exact energy + convergence count.
+// update.cu -- update step partials + convergence count.
 //
 // Update step, Eq. (4): c_j = (1/N_j) sum_{rho_i = j} x_i.
-// One pass over the local shard produces the packed vector that the ranks
-// allreduce (SURVEY §8a rows a4-a7):
-//   S_j  = sum_{rho_i = j} x_i           (fp64; the mean is G_j = S_j / N_j)
+// One pass over the local shard produces the packed int64 vector the ranks
+// allreduce (SURVEY §8a rows a5-a7):
+//   S_j  = sum_{rho_i = j} x_i  as two fixed-point integers per coordinate:
+//          x 2^(22-e) = hi + lo 2^-22 (|x| <= 2^e over all ranks, hi/lo rounded
+//          to nearest), so every x with |x| >= 2^(e-23) is carried exactly and
+//          the rest to 2^(e-45); integer sums are exact and order-free, so S
+//          (and everything downstream) is bitwise identical run to run and for
+//          any number of ranks
 //   N_j  = #{i : rho_i = j}
-//   E    = sum_i ||x_i - c_{rho_i}||^2  (Eq. 1 with the given P, PAPER.md:113;
-//                                         fp64 direct differences)
 //   changed = #{i : rho_i != rho_i^{prev}}
-// The energy reuses the same loads of x_i and c_{rho_i}, so X is read once.
-// E/changed: fixed-order per-block partials, reduced by the last block in a
-// fixed tree -> bitwise reproducible for a fixed launch geometry.
+// The energy E(P, C) (Eq. 1) is formed after the allreduce from
+// the same exact sums, E = sum_i ||x_i||^2 - 2 sum_j S_j.c_j + sum_j N_j ||c_j||^2,
+// by one fixed-order kernel (aa.cu k_energy).
 #include "aakm_dev.cuh"
 
 namespace aakm {
@@ -23,7 +26,7 @@ struct Pick {
     const int* lab;
     const int* prev;
     const float* C;
-    double* out;
+    long long* out;       // packed [S_hi | S_lo | N | E | changed]
 };
 
 __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
@@ -36,51 +39,22 @@ __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
     return p;
 }
 
-// Block reduction of (E, changed) and the deterministic last-block finish.
-__device__ void finish_scalars(const Dev& d, double* out, double e, long long ch) {
-    __shared__ double se[32];
-    __shared__ long long sc[32];
-    __shared__ bool last;
-    for (int o = 16; o; o >>= 1) {
-        e += __shfl_xor_sync(0xffffffffu, e, o);
-        ch += __shfl_xor_sync(0xffffffffu, ch, o);
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if (l == 0) { se[w] = e; sc[w] = ch; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double be = 0.0; long long bc = 0;
-        for (int i = 0; i < nw; ++i) { be += se[i]; bc += sc[i]; }
-        d.upd_part[2 * blockIdx.x] = be;
-        d.upd_part[2 * blockIdx.x + 1] = __longlong_as_double(bc);
-        __threadfence();
-        unsigned prevc = atomicAdd(&d.st->upd_ctr, 1u);
-        last = (prevc == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    double te = 0.0; long long tc = 0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-        te += __ldcg(d.upd_part + 2 * b);
-        tc += __double_as_longlong(__ldcg(d.upd_part + 2 * b + 1));
-    }
-    for (int o = 16; o; o >>= 1) {
-        te += __shfl_xor_sync(0xffffffffu, te, o);
-        tc += __shfl_xor_sync(0xffffffffu, tc, o);
-    }
-    __syncthreads();
-    if (l == 0) { se[w] = te; sc[w] = tc; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double be = 0.0; long long bc = 0;
-        for (int i = 0; i < nw; ++i) { be += se[i]; bc += sc[i]; }
-        const long long KD = (long long)d.K * d.d;
-        out[KD + d.K] += be;            // packed was zeroed before the launch
-        out[KD + d.K + 1] += (double)bc;
-        d.st->upd_ctr = 0;
-    }
+// x -> (hi, lo) with x 2^(22-e) = hi + lo 2^-22 (+ |residual| <= 2^-23), both
+// rounded to nearest through the 1.5 * 2^23 magic (fp32 only; |x 2^(22-e)| <= 2^22).
+__device__ __forceinline__ void fx_add(float x, float sc, int& hi, int& lo) {
+    const float M = 12582912.0f;
+    const float t = fmaf(x, sc, M);
+    const float hv = t - M;
+    const float r = fmaf(x, sc, -hv);                 // exact
+    const float t2 = fmaf(r, 4194304.0f, M);
+    hi += __float_as_int(t) - 0x4B400000;
+    lo += __float_as_int(t2) - 0x4B400000;
 }
+__device__ __forceinline__ void red_add_s64(long long* p, long long v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+__device__ void finish_changed(const Dev& d, long long* out, long long ch);
 
 // Lanes are grouped per row (group = next pow2 >= d, <= 32) so a row's d
 // coordinates are read and reduced as one coalesced segment; S_j and N_j go
@@ -98,7 +72,7 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
     const int groups_per_block = blockDim.x / GS;
     const long long gid = (long long)blockIdx.x * groups_per_block + threadIdx.x / GS;
     const long long ngroups = (long long)gridDim.x * groups_per_block;
-    double e_acc = 0.0;
+    const float sc = d.fx_scale;
     long long ch = 0;
     int bad = 0;
     for (long long row = gid; row < d.n; row += ngroups) {
@@ -106,19 +80,18 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
         if (j < 0 || j >= K) { bad = 1; continue; }
         if (gl == 0) {
             if (p.prev) ch += (p.prev[row] != j);
-            red_add_f64(p.out + KD + j, 1.0);
+            red_add_s64(p.out + 2 * KD + j, 1);
         }
         const float* x = d.X + row * D;
-        const float* c = p.C + (long long)j * D;
         for (int k = gl; k < D; k += GS) {
-            const float xv = __ldcs(x + k);
-            const double diff = (double)xv - (double)__ldg(c + k);   // exact in fp64
-            e_acc = fma(diff, diff, e_acc);
-            red_add_f64(p.out + (long long)j * D + k, (double)xv);
+            int hi = 0, lo = 0;
+            fx_add(__ldcs(x + k), sc, hi, lo);
+            red_add_s64(p.out + (long long)j * D + k, hi);
+            red_add_s64(p.out + KD + (long long)j * D + k, lo);
         }
     }
     if (bad) d.st->label_error = 1;
-    finish_scalars(d, p.out, e_acc, ch);
+    finish_changed(d, p.out, ch);
 }
 
 // ------------------------------------------------------------------
@@ -135,7 +108,7 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 
 constexpr int SEG_ROWS = 256;
 
-__device__ __forceinline__ void finish_changed(const Dev& d, double* out, long long ch) {
+__device__ void finish_changed(const Dev& d, long long* out, long long ch) {
     __shared__ long long sc[32];
     __shared__ bool last;
     for (int o = 16; o; o >>= 1) ch += __shfl_xor_sync(0xffffffffu, ch, o);
@@ -162,7 +135,7 @@ __device__ __forceinline__ void finish_changed(const Dev& d, double* out, long l
     if (threadIdx.x == 0) {
         long long bc = 0;
         for (int i = 0; i < nw; ++i) bc += sc[i];
-        out[(long long)d.K * d.d + d.K + 1] += (double)bc;
+        out[2 * (long long)d.K * d.d + d.K + 1] += bc;     // changed (packed was zeroed)
         d.st->hist_ctr = 0;
     }
 }
@@ -240,7 +213,7 @@ __global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
         o += t;
     }
     d.seg_off[j] = (int)o;                               // count for now; phase B makes it an offset
-    p.out[(long long)K * d.d + j] = (double)o;           // N_j
+    p.out[2 * (long long)K * d.d + j] = o;               // N_j
 }
 
 // Phase B (one block): exclusive scans over clusters of the counts and of the
@@ -320,9 +293,10 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     const int D = d.d, K = d.K;
+    const long long KD = (long long)K * D;
     const int lane = threadIdx.x & 31;
     const long long nchunks = d.seg_chunk[K];
-    double e_acc = 0.0;
+    const float sc = d.fx_scale;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
         const int j = d.seg_cmap[w];
@@ -335,14 +309,9 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             const int q = u * 32 + lane;
             rid[u] = q < cnt ? d.perm[r0 + q] : -1;
         }
-        float c[V];
-        double s[V];
+        int hi[V], lo[V];                         // <= 256 rows per chunk: int32 cannot overflow
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const int k = lane + 32 * v;
-            c[v] = k < D ? __ldg(p.C + (long long)j * D + k) : 0.f;
-            s[v] = 0.0;
-        }
+        for (int v = 0; v < V; ++v) { hi[v] = 0; lo[v] = 0; }
 #pragma unroll
         for (int u = 0; u < SEG_ROWS / 32; ++u) {
             if (u * 32 < cnt) {                   // predicate, not break: keeps rid[] in registers
@@ -360,17 +329,8 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
                 }
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
-                    const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
-                    if (row < 0) continue;
 #pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        const int k = lane + 32 * v;
-                        if (k < D) {
-                            s[v] += (double)xv[t][v];
-                            const double df = (double)xv[t][v] - (double)c[v];
-                            e_acc = fma(df, df, e_acc);
-                        }
-                    }
+                    for (int v = 0; v < V; ++v) fx_add(xv[t][v], sc, hi[v], lo[v]);   // zeros add nothing
                 }
             }
             }
@@ -378,10 +338,12 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int k = lane + 32 * v;
-            if (k < D) red_add_f64(p.out + (long long)j * D + k, s[v]);
+            if (k < D) {
+                red_add_s64(p.out + (long long)j * D + k, hi[v]);
+                red_add_s64(p.out + KD + (long long)j * D + k, lo[v]);
+            }
         }
     }
-    finish_scalars(d, p.out, e_acc, 0);
 }
 
 // float4 variant (d = 4 * LPR, LPR in {1,2,4,8,16,32}): LPR lanes cover one
@@ -394,11 +356,12 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
     constexpr int ROUND = U * RPW;                       // rows per round (16, or 32 when RPW = 32)
     const Pick p = pick(d, g);
     const int D = d.d, K = d.K;
+    const long long KD = (long long)K * D;
     const int lane = threadIdx.x & 31;
     const int h = lane / LPR, c4i = lane % LPR;          // row slot within the instruction, float4 index
     const long long nchunks = d.seg_chunk[K];
     const float4* X4 = reinterpret_cast<const float4*>(d.X);
-    double e_acc = 0.0;
+    const float sc = d.fx_scale;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
         const int j = d.seg_cmap[w];
@@ -410,47 +373,41 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
             const int q = t * 32 + lane;
             rid[t] = q < cnt ? d.perm[r0 + q] : -1;
         }
-        const float4 c = __ldg(reinterpret_cast<const float4*>(p.C + (long long)j * D) + c4i);
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        // fixed-point parts of the 4 coordinates, int32 per chunk (<= 256 rows / lane)
+        int h0 = 0, h1 = 0, h2 = 0, h3 = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
 #pragma unroll
         for (int t = 0; t < SEG_ROWS / 32; ++t) {
             if (t * 32 < cnt) {
 #pragma unroll
                 for (int r = 0; r < 32; r += ROUND) {
                     float4 xv[U];
-                    int rw[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        rw[u] = __shfl_sync(0xffffffffu, rid[t], (r + u * RPW + h) & 31);
-                        xv[u] = rw[u] >= 0 ? __ldcs(X4 + (long long)rw[u] * LPR + c4i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const int rw = __shfl_sync(0xffffffffu, rid[t], (r + u * RPW + h) & 31);
+                        xv[u] = rw >= 0 ? __ldcs(X4 + (long long)rw * LPR + c4i) : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        if (rw[u] >= 0) {
-                            s0 += (double)xv[u].x; s1 += (double)xv[u].y; s2 += (double)xv[u].z; s3 += (double)xv[u].w;
-                            double df = (double)xv[u].x - (double)c.x; e_acc = fma(df, df, e_acc);
-                            df = (double)xv[u].y - (double)c.y; e_acc = fma(df, df, e_acc);
-                            df = (double)xv[u].z - (double)c.z; e_acc = fma(df, df, e_acc);
-                            df = (double)xv[u].w - (double)c.w; e_acc = fma(df, df, e_acc);
-                        }
+                        fx_add(xv[u].x, sc, h0, l0); fx_add(xv[u].y, sc, h1, l1);
+                        fx_add(xv[u].z, sc, h2, l2); fx_add(xv[u].w, sc, h3, l3);
                     }
                 }
             }
         }
-        // combine the RPW row slots (lanes with equal c4i), fixed xor order
+        // combine the RPW row slots (lanes with equal c4i): exact int64 sums
+        long long s[8] = {h0, h1, h2, h3, l0, l1, l2, l3};
 #pragma unroll
         for (int o = LPR; o < 32; o <<= 1) {
-            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-            s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
         }
         if (h == 0) {
-            double* out = p.out + (long long)j * D + 4 * c4i;
-            red_add_f64(out, s0); red_add_f64(out + 1, s1); red_add_f64(out + 2, s2); red_add_f64(out + 3, s3);
+            long long* oh = p.out + (long long)j * D + 4 * c4i;
+            long long* ol = oh + KD;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { red_add_s64(oh + q, s[q]); red_add_s64(ol + q, s[4 + q]); }
         }
     }
-    finish_scalars(d, p.out, e_acc, 0);
 }
 
 cudaError_t setup_update() {
@@ -492,23 +449,175 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
 }
 
 // kmeans_update API: G = S / N (empty -> C_prev row, R-A15), counts.
-__global__ void k_update_G(long long KD, int D, int K, const double* packed, const float* Cprev,
-                           float* G, long long* counts) {
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int j = (int)(e / D);
-        const double nj = packed[KD + j];
-        G[e] = nj > 0.0 ? (float)(packed[e] / nj) : Cprev[e];
-        if (counts && e % D == 0) counts[j] = (long long)nj;
+__global__ void k_update_G(Dev d, const long long* packed, const float* Cprev, float* G, long long* counts) {
+    const long long KD = (long long)d.K * d.d;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
+        const long long j = e / d.d;
+        const long long nj = packed[2 * KD + j];
+        G[e] = nj > 0 ? (float)(fx_value(packed[e], packed[KD + e], d.fx_inv) / (double)nj) : Cprev[e];
+        if (counts && e % d.d == 0) counts[j] = nj;
     }
 }
 
-void launch_update_G(const Dev& d, const double* packed, const float* Cprev, float* G,
+void launch_update_G(const Dev& d, const long long* packed, const float* Cprev, float* G,
                      long long* counts, cudaStream_t s) {
     long long KD = (long long)d.K * d.d;
     int blocks = (int)((KD + 255) / 256);
     if (blocks > 1184) blocks = 1184;
-    k_update_G<<<blocks, 256, 0, s>>>(KD, d.d, d.K, packed, Cprev, G, counts);
+    k_update_G<<<blocks, 256, 0, s>>>(d, packed, Cprev, G, counts);
+}
+
+}  // namespace aakm
+
+namespace aakm {
+
+// ------------------------------------------------------------------
+// Energy E(P, C) (Eq. 1) from the exact sums, after the allreduce:
+//   E = sum_i ||x_i||^2 - 2 sum_j S_j.c_j + sum_j N_j ||c_j||^2,
+// one block, each thread a fixed set of clusters in order, a fixed tree: the
+// same bytes on every rank and for every rank count.
+__device__ double energy_terms(const Dev& d, const long long* pk, const float* C) {
+    const long long KD = (long long)d.K * d.d;
+    double acc = 0.0;
+    for (int j = threadIdx.x; j < d.K; j += blockDim.x) {
+        const long long nj = pk[2 * KD + j];
+        if (nj == 0) continue;
+        double cc = 0.0, sx = 0.0;
+        for (int k = 0; k < d.d; ++k) {
+            const long long e = (long long)j * d.d + k;
+            const double c = (double)C[e];
+            cc = fma(c, c, cc);
+            sx = fma(fx_value(pk[e], pk[KD + e], d.fx_inv), c, sx);
+        }
+        acc += (double)nj * cc - 2.0 * sx;
+    }
+    __shared__ double sw[32];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    double tot = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sw[w];
+    return tot;                                   // valid in thread 0
+}
+
+// Grid version for the Algorithm 1 passes: a warp per cluster (lanes over the
+// coordinates, coalesced), fixed xor trees, per-block partials in a fixed grid,
+// summed in block order by the last block -- deterministic for a fixed K, d.
+constexpr int EN_BLOCKS = 148;
+__global__ void __launch_bounds__(256) k_energy(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    const Pick p = pick(d, g);
+    const long long KD = (long long)d.K * d.d;
+    const long long* pk = p.out;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double wacc = 0.0;
+    for (long long j = (long long)blockIdx.x * 8 + w; j < d.K; j += (long long)gridDim.x * 8) {
+        const long long nj = pk[2 * KD + j];
+        double cc = 0.0, sx = 0.0;
+        if (nj != 0) {
+            for (int k = lane; k < d.d; k += 32) {
+                const long long e = j * d.d + k;
+                const double c = (double)p.C[e];
+                cc = fma(c, c, cc);
+                sx = fma(fx_value(pk[e], pk[KD + e], d.fx_inv), c, sx);
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            cc += __shfl_xor_sync(0xffffffffu, cc, o);
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        }
+        wacc += (double)nj * cc - 2.0 * sx;
+    }
+    __shared__ double sw[8];
+    __shared__ bool last;
+    if (lane == 0) sw[w] = wacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bs = 0.0;
+        for (int i = 0; i < 8; ++i) bs += sw[i];
+        d.upd_part[2048 + blockIdx.x] = bs;          // past finish_changed's slots
+        __threadfence();
+        last = atomicAdd(&d.st->upd_ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    double tot = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) tot += __ldcg(d.upd_part + 2048 + b);
+    p.out[2 * KD + d.K] = __double_as_longlong(d.xn_total + tot);
+    d.st->upd_ctr = 0;
+}
+
+void launch_energy(const Dev& d, const GEval& g, cudaStream_t s) {
+    int blocks = (int)((d.K + 7) / 8);
+    if (blocks > EN_BLOCKS) blocks = EN_BLOCKS;
+    k_energy<<<blocks, 256, 0, s>>>(d, g);
+}
+
+// kmeans_update_partials: this rank's unreduced [S | N | E_local | changed] as doubles.
+__global__ void __launch_bounds__(1024) k_partials_out(Dev d, const long long* pk, const float* C, double* out) {
+    const long long KD = (long long)d.K * d.d;
+    for (long long e = threadIdx.x; e < KD; e += blockDim.x) out[e] = fx_value(pk[e], pk[KD + e], d.fx_inv);
+    for (int j = threadIdx.x; j < d.K; j += blockDim.x) out[KD + j] = (double)pk[2 * KD + j];
+    const double t = energy_terms(d, pk, C);
+    if (threadIdx.x == 0) {
+        out[KD + d.K] = d.xn_local + t;
+        out[KD + d.K + 1] = (double)pk[2 * KD + d.K + 1];
+    }
+}
+
+void launch_partials_out(const Dev& d, const long long* packed, const float* C, double* out, cudaStream_t s) {
+    k_partials_out<<<1, 1024, 0, s>>>(d, packed, C, out);
+}
+
+// ------------------------------------------------------------------ create-time statistics of X
+// out4[0] = max |x| (float bits), out4[1] = max ||x_i||^2 (float bits, rounded up)
+__global__ void k_xstats_max(const float* X, long long n, int D, unsigned int* out) {
+    const int lane = threadIdx.x & 31;
+    float am = 0.f, nm = 0.f;
+    for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((long long)gridDim.x * blockDim.x) >> 5) {
+        double s = 0.0;
+        for (int k = lane; k < D; k += 32) {
+            const float v = X[i * D + k];
+            am = fmaxf(am, fabsf(v));
+            s = fma((double)v, (double)v, s);
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        nm = fmaxf(nm, __double2float_ru(s));
+    }
+    for (int o = 16; o; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+    if (lane == 0) { atomicMax(out, __float_as_uint(am)); atomicMax(out + 1, __float_as_uint(nm)); }
+}
+
+// sum_i ||x_i||^2 q = sum hi + 2^-30 sum lo, both int64 (exact, order-free);
+// ||x_i||^2 in fp64 with k ascending, q = 2^(22-en) so each row is <= 2^22
+__global__ void k_xstats_sum(const float* X, long long n, int D, double q, long long* out) {
+    long long ahi = 0, alo = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < D; ++k) { const double v = (double)X[i * D + k]; s = fma(v, v, s); }
+        const double v = s * q;                                   // exact (power of 2)
+        const double h = rint(v);
+        ahi += (long long)h;
+        alo += llrint((v - h) * 1073741824.0);                    // 2^30
+    }
+    for (int o = 16; o; o >>= 1) {
+        ahi += __shfl_xor_sync(0xffffffffu, ahi, o);
+        alo += __shfl_xor_sync(0xffffffffu, alo, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)ahi);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)alo);
+    }
+}
+
+void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s) {
+    if (n > 0) k_xstats_max<<<592, 256, 0, s>>>(X, n, d, out);
+}
+void launch_xstats_sum(const float* X, long long n, int d, double q, long long* out, cudaStream_t s) {
+    if (n > 0) k_xstats_sum<<<592, 256, 0, s>>>(X, n, d, q, out);
 }
 
 }  // namespace aakm

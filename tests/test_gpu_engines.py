@@ -149,3 +149,25 @@ def test_state_import_validation():
     with pytest.raises(aakm.AAKMError):
         km.state_import(bad)
     km.close()
+
+
+# ---------------------------------------------------------------- reproducibility
+@pytest.mark.parametrize("cfg,N,K,bounded", [("c4", 40_000, 256, False), ("c5", 60_000, 512, True),
+                                             ("c3", 50_000, 64, False)])
+def test_runs_are_bitwise_reproducible(cfg, N, K, bounded):
+    """The update sums are exact integers (order-free), the energy and the
+    Anderson step fixed-order: two runs from the same C^0 agree bit for bit."""
+    X, C0, c = make(cfg, N=N, K=K)
+    Xd = dev(X)
+    out = []
+    for _ in range(2):
+        km = aakm.KMeans(Xd, c.K, aakm.config(m0=5, bounded=bounded, max_iters=400))
+        C, lab, rep = km.run(dev(C0))
+        out.append((C.cpu().numpy().copy(), lab.cpu().numpy().copy(), rep))
+        km.close()
+    (C1, l1, r1), (C2, l2, r2) = out
+    assert np.array_equal(C1.view(np.uint32), C2.view(np.uint32))
+    assert np.array_equal(l1, l2)
+    for k in ("iters", "n_assign", "n_accepted", "n_rejected", "converged", "m_final"):
+        assert r1[k] == r2[k], k
+    assert r1["energy"] == r2["energy"]
