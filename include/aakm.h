@@ -213,8 +213,11 @@ AAKM_API kmeans_status kmeans_state_export(kmeans_handle *h, kmeans_state *st /*
 AAKM_API kmeans_status kmeans_state_import(kmeans_handle *h, const kmeans_state *st /*host*/);
 
 /* Test hook for the data-parallel partition logic: this rank's UNREDUCED
- * packed partials [S (K*d, sum of x_i - C_{rho_i}) | N (K) | E | changed]
- * as K*d + K + 2 doubles (device).  Synchronises. */
+ * partials [S (K*d, S_j = sum of x_i over rho_i = j) | N (K) | E_local |
+ * changed] as K*d + K + 2 doubles (device): S from the exact fixed-point sums,
+ * E_local = sum over this rank's rows of ||x_i - c_{rho_i}||^2 (so the ranks'
+ * values sum to the global E).  labels_prev nullable (changed = 0).
+ * Synchronises. */
 AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *labels,
                                      const int32_t *labels_prev, const float *C,
                                      double *packed_out);
@@ -237,7 +240,7 @@ AAKM_API kmeans_status kmeans_last_flagged(kmeans_handle *h, int64_t *flagged /*
 AAKM_API kmeans_status kmeans_bounded_stats(kmeans_handle *h, int64_t *rows_scored /*host*/,
                                             int64_t *rows_total /*host*/);
 
-/* Name of the assignment engine the handle selected ("simt"/"tc"). */
+/* Name of the assignment engine the handle selected ("simt"/"tc"/"tc16"). */
 AAKM_API const char *kmeans_assign_path_name(const kmeans_handle *h);
 
 AAKM_API kmeans_status kmeans_destroy(kmeans_handle *h);
