@@ -171,3 +171,34 @@ def test_runs_are_bitwise_reproducible(cfg, N, K, bounded):
     for k in ("iters", "n_assign", "n_accepted", "n_rejected", "converged", "m_final"):
         assert r1[k] == r2[k], k
     assert r1["energy"] == r2["energy"]
+
+
+# ---------------------------------------------------------------- odd dimensions
+@pytest.mark.parametrize("d", [1, 3, 7, 24, 33, 100])
+def test_odd_d_assign_update_and_run(d):
+    """d outside the synthetic configs: SIMT / 3xTF32 engines, the generic
+    (non-float4) segmented sums at n >= 65 536 rows, and a short run vs the oracle."""
+    rng = np.random.default_rng(d)
+    n, K = 70_000, 37
+    means = rng.normal(0, 4, (K, d))
+    X = (means[rng.integers(0, K, n)] + rng.normal(0, 1, (n, d))).astype(np.float32)
+    C0 = X[rng.choice(n, K, replace=False)].copy()
+    km = aakm.KMeans(dev(X), K, aakm.config(m0=5))
+    lab, E, _ = km.assign(dev(C0))
+    lab = lab.cpu().numpy()
+    check_assign(X, C0, lab, msg=f"d={d}")
+    E_ora = oracle.energy(X, C0.astype(np.float64), lab)
+    assert abs(E - E_ora) <= 1e-6 * E_ora
+    G, cnt = km.update(dev(lab), dev(C0))
+    G_ora, cnt_ora = oracle.update(X, lab, C0.astype(np.float64))
+    np.testing.assert_array_equal(cnt.cpu().numpy(), cnt_ora)
+    scale = np.maximum(np.abs(G_ora), np.sqrt(np.mean(G_ora ** 2)))
+    assert (np.abs(G.cpu().numpy() - G_ora) / scale).max() <= 1e-6
+    km.close()
+    Xs, C0s = X[:4000], C0[:8]
+    km = aakm.KMeans(dev(Xs), 8, aakm.config(m0=5))
+    C, labs, rep = km.run(dev(C0s))
+    ref = oracle.run(Xs, C0s.astype(np.float64), oracle.OracleConfig(m0=5, parity=True))
+    assert rep["converged"] and ref["converged"]
+    assert rep["iters"] == ref["iters"] and abs(rep["energy"] - ref["energy"]) <= 1e-4 * ref["energy"]
+    km.close()
