@@ -127,8 +127,8 @@ __global__ void k_control(Dev d, int stage) {
     const long long KD = (long long)d.K * d.d;
     if (stage == 0) {
         const long long* pk = d.packed[0];
-        const double E = __longlong_as_double(pk[2 * KD + d.K]);   // k_energy, after the allreduce
-        const long long ch = pk[2 * KD + d.K + 1];
+        const double E = __longlong_as_double(pk[pk_e(d)]);   // k_energy, after the allreduce
+        const long long ch = pk[pk_ch(d)];
         st->n_assign += 1;
         st->last_flag[0] = d.flag_count[0];
         st->rows_total += d.n;
@@ -152,8 +152,8 @@ __global__ void k_control(Dev d, int stage) {
     } else {
         if (!st->reject) return;
         const long long* pk = d.packed[1];
-        const double E = __longlong_as_double(pk[2 * KD + d.K]);
-        const long long ch = pk[2 * KD + d.K + 1];
+        const double E = __longlong_as_double(pk[pk_e(d)]);
+        const long long ch = pk[pk_ch(d)];
         st->n_assign += 1;
         st->last_flag[1] = d.flag_count[1];
         st->rows_total += d.n;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
     float* F = d.Fring + slot * KD;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
          e += (long long)gridDim.x * blockDim.x) {
-        const long long nj = pk[2 * KD + e / D];
+        const long long nj = pk[pk_n(d) + e / D];
         const float c = d.C[e];
         const float g = nj > 0 ? (float)(fx_value(pk[e], pk[KD + e], d.fx_inv) / (double)nj) : c;   // G = S / N (Eq. 4)
         G[e] = g;

@@ -85,11 +85,10 @@ struct Dev {
     int* cand_cnt;        // candidate counts per flagged row and epilogue half (> AAKM_MAXC/2 = overflow)
     long long fcap;       // capacity of the candidate path (rows beyond -> SIMT refine)
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
-    long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E (fp64 bits) | changed], branch A / B
+    long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E_hi | E_lo | E (fp64 bits) | changed]
     float fx_scale;       // 2^(22-e), |x| <= 2^e over all ranks: S in exact fixed point (update.cu)
     double fx_inv;        // 2^(e-22)
-    double xn_total;      // sum_i ||x_i||^2 over all ranks (fixed-point exact, create time)
-    double xn_local;      // ... over this rank's rows
+    double xn_gmax;       // max_i ||x_i|| over all ranks (rounded up): bounds every ||x_i - c||
     double* upd_part;     // per-block (E, changed) partials
     int* seg_bh;          // sorted update engine: per-block histograms -> scatter bases (SEG_BLOCKS x K)
     int* seg_off;         // row offsets of cluster j in perm (K+1)
@@ -108,6 +107,7 @@ struct Dev {
     TraceRec* trace;
     int nranks;
     int upd_blocks;
+    int upd_sorted;       // label-sorted update engine (chosen from n_global, d, K: the same on every rank)
     int gram_blocks;
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
@@ -150,7 +150,7 @@ __host__ __device__ inline unsigned int cnimg_off(int r, int byte) {   // (row, 
 int launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first = 0);
 int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 int launch_update(const Dev& d, const GEval& g, cudaStream_t s);
-bool update_sorted(const Dev& d);
+bool update_sorted(long long n_global, int dd, int K);
 void launch_control(const Dev& d, int stage, cudaStream_t s);
 void launch_finalize(const Dev& d, cudaStream_t s);
 void launch_gram(const Dev& d, cudaStream_t s);
@@ -162,10 +162,32 @@ void launch_update_G(const Dev& d, const long long* packed, const float* Cprev, 
 void launch_energy(const Dev& d, const GEval& g, cudaStream_t s);       // E after the allreduce
 void launch_partials_out(const Dev& d, const long long* packed, const float* C, double* out, cudaStream_t s);
 void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
-void launch_xstats_sum(const float* X, long long n, int d, double q, long long* out, cudaStream_t s);
+
 // fixed-point sums (update.cu) -> fp64: (hi + lo 2^-22) 2^(e-22), exact conversions
 __host__ __device__ inline double fx_value(long long hi, long long lo, double fx_inv) {
     return ((double)hi + (double)lo * 2.384185791015625e-07) * fx_inv;
+}
+// packed-vector word offsets
+__host__ __device__ inline long long pk_n(const Dev& d) { return 2LL * d.K * d.d; }           // N_j at + j
+__host__ __device__ inline long long pk_ehi(const Dev& d) { return 2LL * d.K * d.d + d.K; }   // E_hi, E_lo
+__host__ __device__ inline long long pk_e(const Dev& d) { return pk_ehi(d) + 2; }             // E (fp64 bits)
+__host__ __device__ inline long long pk_ch(const Dev& d) { return pk_ehi(d) + 3; }            // changed
+__host__ __device__ inline long long pk_words(const Dev& d) { return pk_ehi(d) + 4; }
+// Per-row energies e_i = ||x_i - c_rho_i||^2 go into the packed vector as a two-part
+// fixed point with quantum 1/q: q = 2^(22 - eb), 2^eb >= 2 (max||x|| + max||c||)^2 >=
+// every e_i, so each row is carried to 2^-52 of the bound and an exact 0 stays 0.
+__device__ inline double energy_q(const Dev& d) {
+    const double cm = sqrt((double)__uint_as_float(d.st->cmax2_bits));
+    const double B = 2.0 * (d.xn_gmax + cm) * (d.xn_gmax + cm);
+    int eb = 0;
+    frexp(B > 0.0 ? B : 1.0, &eb);
+    return ldexp(1.0, 22 - eb);
+}
+__device__ inline void energy_add(double e, double q, long long& hi, long long& lo) {
+    const double v = e * q;                                  // exact (power of 2), <= 2^22
+    const double h = rint(v);
+    hi += (long long)h;
+    lo += llrint((v - h) * 1073741824.0);                    // 2^30
 }
 
 // one-time kernel attribute setup (max dynamic smem); never during stream capture

@@ -165,7 +165,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.Xf = take((size_t)fc * d * 4 + 16);
     L.cand = take((size_t)fc * AAKM_MAXC * 4 + 4);
     L.cand_cnt = take((size_t)fc * 16 + 16);
-    const size_t pk = (2 * KD + K + 2) * 8;     // [S_hi | S_lo | N | E | changed], int64 words
+    const size_t pk = (2 * KD + K + 4) * 8;     // [S_hi | S_lo | N | E_hi | E_lo | E | changed], int64 words (pk_words)
     L.scratch = o;
     size_t s0 = take(256);                 // flag counts
     (void)s0;
@@ -250,7 +250,7 @@ static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
 // here; k_energy fills it from the reduced sums afterwards.
 static kmeans_status allreduce(kmeans_handle* h, long long* buf, cudaStream_t s) {
     if (h->nranks <= 1) return KMEANS_OK;
-    const size_t cnt = 2 * (size_t)h->d.K * h->d.d + h->d.K + 2;
+    const size_t cnt = (size_t)pk_words(h->d);     // the E slot is still 0 here (k_energy runs after)
     NK(h, ncclAllReduce(buf, buf, cnt, ncclInt64, ncclSum, h->comm, s));
     return KMEANS_OK;
 }
@@ -533,12 +533,10 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             return KMEANS_ERR_NCCL;
         }
     }
-    // Scales of the exact fixed-point update sums (update.cu) and sum_i ||x_i||^2,
-    // from statistics of X over ALL ranks, so every rank forms identical bytes.
+    // Scales of the exact fixed-point update and energy sums (update.cu), from
+    // statistics of X over ALL ranks, so every rank forms identical bytes.
     {
         unsigned int* mx = (unsigned int*)(w + L.scratch);            // scratch is free until the first pass
-        long long* xs = (long long*)(w + L.scratch + 64);
-        CKC(cudaMemsetAsync(w + L.scratch, 0, 128, h->stream));
         CKC(cudaMemcpyAsync(mx, mloc, 8, cudaMemcpyHostToDevice, h->stream));
         if (nranks > 1) {
             ncclResult_t r = ncclAllReduce(mx, mx, 2, ncclFloat32, ncclMax, h->comm, h->stream);
@@ -549,24 +547,14 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         CKC(cudaStreamSynchronize(h->stream));
         float mf[2];
         memcpy(mf, mb, 8);
-        int ex = 0, en = 0;
+        int ex = 0;
         if (mf[0] > 0.f) frexpf(mf[0], &ex);                           // max |x| < 2^ex
-        if (mf[1] > 0.f) frexpf(mf[1], &en);                           // max ||x||^2 < 2^en
-        const double q = ldexp(1.0, 22 - en);                          // row ||x||^2 q <= 2^22
-        launch_xstats_sum(X, n_local, d, q, xs, h->stream);
-        long long loc[2] = {0, 0}, tot[2] = {0, 0};
-        CKC(cudaMemcpyAsync(loc, xs, 16, cudaMemcpyDeviceToHost, h->stream));
-        if (nranks > 1) {
-            ncclResult_t r = ncclAllReduce(xs, xs, 2, ncclInt64, ncclSum, h->comm, h->stream);
-            if (r != ncclSuccess) { g_create_err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); delete h; return KMEANS_ERR_NCCL; }
-        }
-        CKC(cudaMemcpyAsync(tot, xs, 16, cudaMemcpyDeviceToHost, h->stream));
-        CKC(cudaStreamSynchronize(h->stream));
+        const bool srt = update_sorted(n_global, d, k);
         for (Dev* dv : {&h->d, &h->da}) {
             dv->fx_scale = ldexpf(1.0f, 22 - ex);
             dv->fx_inv = ldexp(1.0, ex - 22);
-            dv->xn_local = ((double)loc[0] + (double)loc[1] * 9.313225746154785e-10) / q;   // 2^-30
-            dv->xn_total = ((double)tot[0] + (double)tot[1] * 9.313225746154785e-10) / q;
+            dv->xn_gmax = sqrt((double)mf[1]) * (1.0 + 1e-6);          // max_i ||x_i||, rounded up
+            dv->upd_sorted = srt ? 1 : 0;
         }
         CKC(cudaMemsetAsync(w + L.scratch, 0, 128, h->stream));
     }
@@ -595,8 +583,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     if (st != KMEANS_OK) return st;
     launch_energy(d, g, s);
     h->launches += 1;
-    const long long KD = (long long)d.K * d.d;
-    CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + 2 * KD + d.K, 16, cudaMemcpyDeviceToHost, s));
+    CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + pk_e(d), 16, cudaMemcpyDeviceToHost, s));   // E, changed
     CK(h, cudaMemcpyAsync(h->scal_host + 2, d.flag_count, 8, cudaMemcpyDeviceToHost, s));
     CK(h, cudaStreamSynchronize(s));
     CK(h, cudaGetLastError());
@@ -617,6 +604,7 @@ kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const float
     CK(h, cudaMemsetAsync(&d.st->label_error, 0, sizeof(int), s));
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels); g.prev_mode = 1; g.Cassign = C_prev;
+    combine(h, d, 2, C_prev, s);                          // max ||c||^2 of C_prev (the energy scale)
     h->launches += launch_update(d, g, s);
     kmeans_status st = allreduce(h, d.packed[0], s);
     if (st != KMEANS_OK) return st;
@@ -639,6 +627,7 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels);
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev; g.Cassign = C;
+    combine(h, d, 2, C, s);                               // max ||c||^2 of C (the energy scale)
     h->launches += launch_update(d, g, s);
     launch_partials_out(d, d.packed[0], C, packed_out, s);            // unreduced, as doubles
     h->launches += 1;

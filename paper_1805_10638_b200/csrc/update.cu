@@ -10,10 +10,11 @@
 //          (and everything downstream) is bitwise identical run to run and for
 //          any number of ranks
 //   N_j  = #{i : rho_i = j}
+//   E    = sum_i ||x_i - c_{rho_i}||^2  (Eq. 1 with the given P):
+//          each row by direct differences in fp64 (fixed order), then the same
+//          kind of two-part fixed point (energy_q): exact zeros stay zero
 //   changed = #{i : rho_i != rho_i^{prev}}
-// The energy E(P, C) (Eq. 1) is formed after the allreduce from
-// the same exact sums, E = sum_i ||x_i||^2 - 2 sum_j S_j.c_j + sum_j N_j ||c_j||^2,
-// by one fixed-order kernel (aa.cu k_energy).
+// X is read once.
 #include "aakm_dev.cuh"
 
 namespace aakm {
@@ -69,28 +70,47 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
     while (GS < D && GS < 32) GS <<= 1;
     const int lane = threadIdx.x & 31;
     const int gl = lane % GS;                     // lane within the row group
-    const int groups_per_block = blockDim.x / GS;
-    const long long gid = (long long)blockIdx.x * groups_per_block + threadIdx.x / GS;
-    const long long ngroups = (long long)gridDim.x * groups_per_block;
+    const int gpw = 32 / GS;                      // row groups per warp
+    // warp-uniform trip count (the energy shuffles need the whole warp)
+    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const float sc = d.fx_scale;
-    long long ch = 0;
+    const double q = energy_q(d);
+    long long ch = 0, ehi = 0, elo = 0;
     int bad = 0;
-    for (long long row = gid; row < d.n; row += ngroups) {
-        const int j = p.lab[row];
-        if (j < 0 || j >= K) { bad = 1; continue; }
-        if (gl == 0) {
-            if (p.prev) ch += (p.prev[row] != j);
-            red_add_s64(p.out + 2 * KD + j, 1);
+    for (long long base = wid * gpw; base < d.n; base += nw * gpw) {
+        const long long row = base + lane / GS;
+        const bool live = row < d.n;
+        const int j = live ? p.lab[row] : 0;
+        const bool okj = live && j >= 0 && j < K;   // uniform within the row group
+        if (live && !okj) bad = 1;
+        double e = 0.0;
+        if (okj) {
+            if (gl == 0) {
+                if (p.prev) ch += (p.prev[row] != j);
+                red_add_s64(p.out + pk_n(d) + j, 1);
+            }
+            const float* x = d.X + row * D;
+            const float* c = p.C + (long long)j * D;
+            for (int k = gl; k < D; k += GS) {
+                const float xv = __ldcs(x + k);
+                int hi = 0, lo = 0;
+                fx_add(xv, sc, hi, lo);
+                red_add_s64(p.out + (long long)j * D + k, hi);
+                red_add_s64(p.out + KD + (long long)j * D + k, lo);
+                const double df = (double)xv - (double)__ldg(c + k);
+                e = fma(df, df, e);
+            }
         }
-        const float* x = d.X + row * D;
-        for (int k = gl; k < D; k += GS) {
-            int hi = 0, lo = 0;
-            fx_add(__ldcs(x + k), sc, hi, lo);
-            red_add_s64(p.out + (long long)j * D + k, hi);
-            red_add_s64(p.out + KD + (long long)j * D + k, lo);
-        }
+        for (int o = 1; o < GS; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);   // fixed tree
+        if (okj && gl == 0) energy_add(e, q, ehi, elo);
     }
     if (bad) d.st->label_error = 1;
+    for (int o = 16; o; o >>= 1) {
+        ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
+        elo += __shfl_xor_sync(0xffffffffu, elo, o);
+    }
+    if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
     finish_changed(d, p.out, ch);
 }
 
@@ -135,7 +155,7 @@ __device__ void finish_changed(const Dev& d, long long* out, long long ch) {
     if (threadIdx.x == 0) {
         long long bc = 0;
         for (int i = 0; i < nw; ++i) bc += sc[i];
-        out[2 * (long long)d.K * d.d + d.K + 1] += bc;     // changed (packed was zeroed)
+        out[pk_ch(d)] += bc;                              // changed (packed was zeroed)
         d.st->hist_ctr = 0;
     }
 }
@@ -213,7 +233,7 @@ __global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
         o += t;
     }
     d.seg_off[j] = (int)o;                               // count for now; phase B makes it an offset
-    p.out[2 * (long long)K * d.d + j] = o;               // N_j
+    p.out[pk_n(d) + j] = o;                              // N_j
 }
 
 // Phase B (one block): exclusive scans over clusters of the counts and of the
@@ -297,6 +317,8 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     const int lane = threadIdx.x & 31;
     const long long nchunks = d.seg_chunk[K];
     const float sc = d.fx_scale;
+    const double q = energy_q(d);
+    long long ehi = 0, elo = 0;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
         const int j = d.seg_cmap[w];
@@ -306,12 +328,17 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
         int rid[SEG_ROWS / 32];
 #pragma unroll
         for (int u = 0; u < SEG_ROWS / 32; ++u) {
-            const int q = u * 32 + lane;
-            rid[u] = q < cnt ? d.perm[r0 + q] : -1;
+            const int qi = u * 32 + lane;
+            rid[u] = qi < cnt ? d.perm[r0 + qi] : -1;
         }
         int hi[V], lo[V];                         // <= 256 rows per chunk: int32 cannot overflow
+        float cj[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) { hi[v] = 0; lo[v] = 0; }
+        for (int v = 0; v < V; ++v) {
+            hi[v] = 0; lo[v] = 0;
+            const int k = lane + 32 * v;
+            cj[v] = k < D ? __ldg(p.C + (long long)j * D + k) : 0.f;
+        }
 #pragma unroll
         for (int u = 0; u < SEG_ROWS / 32; ++u) {
             if (u * 32 < cnt) {                   // predicate, not break: keeps rid[] in registers
@@ -329,8 +356,16 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
                 }
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
+                    double e = 0.0;
 #pragma unroll
-                    for (int v = 0; v < V; ++v) fx_add(xv[t][v], sc, hi[v], lo[v]);   // zeros add nothing
+                    for (int v = 0; v < V; ++v) {
+                        fx_add(xv[t][v], sc, hi[v], lo[v]);   // zeros add nothing
+                        const int k = lane + 32 * v;
+                        if (k < D) { const double df = (double)xv[t][v] - (double)cj[v]; e = fma(df, df, e); }
+                    }
+                    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+                    const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
+                    if (lane == 0 && row >= 0) energy_add(e, q, ehi, elo);
                 }
             }
             }
@@ -344,6 +379,7 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             }
         }
     }
+    if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
 }
 
 // float4 variant (d = 4 * LPR, LPR in {1,2,4,8,16,32}): LPR lanes cover one
@@ -362,6 +398,8 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
     const long long nchunks = d.seg_chunk[K];
     const float4* X4 = reinterpret_cast<const float4*>(d.X);
     const float sc = d.fx_scale;
+    const double q = energy_q(d);
+    long long ehi = 0, elo = 0;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
         const int j = d.seg_cmap[w];
@@ -370,9 +408,11 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
         int rid[SEG_ROWS / 32];
 #pragma unroll
         for (int t = 0; t < SEG_ROWS / 32; ++t) {
-            const int q = t * 32 + lane;
-            rid[t] = q < cnt ? d.perm[r0 + q] : -1;
+            const int qi = t * 32 + lane;
+            rid[t] = qi < cnt ? d.perm[r0 + qi] : -1;
         }
+        const float4 c = __ldg(reinterpret_cast<const float4*>(p.C + (long long)j * D) + c4i);
+        const double cx = c.x, cy = c.y, cz = c.z, cw = c.w;
         // fixed-point parts of the 4 coordinates, int32 per chunk (<= 256 rows / lane)
         int h0 = 0, h1 = 0, h2 = 0, h3 = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
 #pragma unroll
@@ -390,6 +430,15 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
                     for (int u = 0; u < U; ++u) {
                         fx_add(xv[u].x, sc, h0, l0); fx_add(xv[u].y, sc, h1, l1);
                         fx_add(xv[u].z, sc, h2, l2); fx_add(xv[u].w, sc, h3, l3);
+                        // e_i by direct differences: 4 coordinates here, then the row's LPR lanes
+                        double df = (double)xv[u].x - cx, e = df * df;
+                        df = (double)xv[u].y - cy; e = fma(df, df, e);
+                        df = (double)xv[u].z - cz; e = fma(df, df, e);
+                        df = (double)xv[u].w - cw; e = fma(df, df, e);
+#pragma unroll
+                        for (int o = 1; o < LPR; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+                        const int rw = __shfl_sync(0xffffffffu, rid[t], (r + u * RPW + h) & 31);
+                        if (c4i == 0 && rw >= 0) energy_add(e, q, ehi, elo);
                     }
                 }
             }
@@ -399,15 +448,20 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
 #pragma unroll
         for (int o = LPR; o < 32; o <<= 1) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+            for (int qq = 0; qq < 8; ++qq) s[qq] += __shfl_xor_sync(0xffffffffu, s[qq], o);
         }
         if (h == 0) {
             long long* oh = p.out + (long long)j * D + 4 * c4i;
             long long* ol = oh + KD;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { red_add_s64(oh + q, s[q]); red_add_s64(ol + q, s[4 + q]); }
+            for (int qq = 0; qq < 4; ++qq) { red_add_s64(oh + qq, s[qq]); red_add_s64(ol + qq, s[4 + qq]); }
         }
     }
+    for (int o = 16; o; o >>= 1) {
+        ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
+        elo += __shfl_xor_sync(0xffffffffu, elo, o);
+    }
+    if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
 }
 
 cudaError_t setup_update() {
@@ -416,10 +470,14 @@ cudaError_t setup_update() {
     return cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
 }
 
-bool update_sorted(const Dev& d) { return d.n >= AAKM_SORTED_MIN_ROWS && d.d <= 128 && d.K <= AAKM_SORTED_MAX_K; }
+// Chosen from global quantities so every rank runs the same per-row energy order
+// (E is then identical for every rank count).
+bool update_sorted(long long n_global, int dd, int K) {
+    return n_global >= AAKM_SORTED_MIN_ROWS && dd <= 128 && K <= AAKM_SORTED_MAX_K;
+}
 
 int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
-    if (!update_sorted(d)) {
+    if (!d.upd_sorted) {
         k_update<<<d.upd_blocks, 256, 0, s>>>(d, g);
         return 1;
     }
@@ -453,7 +511,7 @@ __global__ void k_update_G(Dev d, const long long* packed, const float* Cprev, f
     const long long KD = (long long)d.K * d.d;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
         const long long j = e / d.d;
-        const long long nj = packed[2 * KD + j];
+        const long long nj = packed[pk_n(d) + j];
         G[e] = nj > 0 ? (float)(fx_value(packed[e], packed[KD + e], d.fx_inv) / (double)nj) : Cprev[e];
         if (counts && e % d.d == 0) counts[j] = nj;
     }
@@ -472,103 +530,35 @@ void launch_update_G(const Dev& d, const long long* packed, const float* Cprev, 
 namespace aakm {
 
 // ------------------------------------------------------------------
-// Energy E(P, C) (Eq. 1) from the exact sums, after the allreduce:
-//   E = sum_i ||x_i||^2 - 2 sum_j S_j.c_j + sum_j N_j ||c_j||^2,
-// one block, each thread a fixed set of clusters in order, a fixed tree: the
-// same bytes on every rank and for every rank count.
-__device__ double energy_terms(const Dev& d, const long long* pk, const float* C) {
-    const long long KD = (long long)d.K * d.d;
-    double acc = 0.0;
-    for (int j = threadIdx.x; j < d.K; j += blockDim.x) {
-        const long long nj = pk[2 * KD + j];
-        if (nj == 0) continue;
-        double cc = 0.0, sx = 0.0;
-        for (int k = 0; k < d.d; ++k) {
-            const long long e = (long long)j * d.d + k;
-            const double c = (double)C[e];
-            cc = fma(c, c, cc);
-            sx = fma(fx_value(pk[e], pk[KD + e], d.fx_inv), c, sx);
-        }
-        acc += (double)nj * cc - 2.0 * sx;
-    }
-    __shared__ double sw[32];
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    double tot = 0.0;
-    if (threadIdx.x == 0)
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sw[w];
-    return tot;                                   // valid in thread 0
-}
-
-// Grid version for the Algorithm 1 passes: a warp per cluster (lanes over the
-// coordinates, coalesced), fixed xor trees, per-block partials in a fixed grid,
-// summed in block order by the last block -- deterministic for a fixed K, d.
-constexpr int EN_BLOCKS = 148;
-__global__ void __launch_bounds__(256) k_energy(Dev d, GEval g) {
+// E from its reduced fixed-point parts (after the allreduce): identical bytes on
+// every rank and for every rank count.
+__global__ void k_energy(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
-    const long long KD = (long long)d.K * d.d;
-    const long long* pk = p.out;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double wacc = 0.0;
-    for (long long j = (long long)blockIdx.x * 8 + w; j < d.K; j += (long long)gridDim.x * 8) {
-        const long long nj = pk[2 * KD + j];
-        double cc = 0.0, sx = 0.0;
-        if (nj != 0) {
-            for (int k = lane; k < d.d; k += 32) {
-                const long long e = j * d.d + k;
-                const double c = (double)p.C[e];
-                cc = fma(c, c, cc);
-                sx = fma(fx_value(pk[e], pk[KD + e], d.fx_inv), c, sx);
-            }
-        }
-        for (int o = 16; o; o >>= 1) {
-            cc += __shfl_xor_sync(0xffffffffu, cc, o);
-            sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        }
-        wacc += (double)nj * cc - 2.0 * sx;
-    }
-    __shared__ double sw[8];
-    __shared__ bool last;
-    if (lane == 0) sw[w] = wacc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double bs = 0.0;
-        for (int i = 0; i < 8; ++i) bs += sw[i];
-        d.upd_part[2048 + blockIdx.x] = bs;          // past finish_changed's slots
-        __threadfence();
-        last = atomicAdd(&d.st->upd_ctr, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last || threadIdx.x != 0) return;
-    __threadfence();
-    double tot = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) tot += __ldcg(d.upd_part + 2048 + b);
-    p.out[2 * KD + d.K] = __double_as_longlong(d.xn_total + tot);
-    d.st->upd_ctr = 0;
+    const double q = energy_q(d);
+    const long long* e = p.out + pk_ehi(d);
+    p.out[pk_e(d)] = __double_as_longlong(((double)e[0] + (double)e[1] * 9.313225746154785e-10) / q);
 }
 
-void launch_energy(const Dev& d, const GEval& g, cudaStream_t s) {
-    int blocks = (int)((d.K + 7) / 8);
-    if (blocks > EN_BLOCKS) blocks = EN_BLOCKS;
-    k_energy<<<blocks, 256, 0, s>>>(d, g);
-}
+void launch_energy(const Dev& d, const GEval& g, cudaStream_t s) { k_energy<<<1, 1, 0, s>>>(d, g); }
 
 // kmeans_update_partials: this rank's unreduced [S | N | E_local | changed] as doubles.
-__global__ void __launch_bounds__(1024) k_partials_out(Dev d, const long long* pk, const float* C, double* out) {
+__global__ void k_partials_out(Dev d, const long long* pk, double* out) {
     const long long KD = (long long)d.K * d.d;
-    for (long long e = threadIdx.x; e < KD; e += blockDim.x) out[e] = fx_value(pk[e], pk[KD + e], d.fx_inv);
-    for (int j = threadIdx.x; j < d.K; j += blockDim.x) out[KD + j] = (double)pk[2 * KD + j];
-    const double t = energy_terms(d, pk, C);
-    if (threadIdx.x == 0) {
-        out[KD + d.K] = d.xn_local + t;
-        out[KD + d.K + 1] = (double)pk[2 * KD + d.K + 1];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x)
+        out[e] = fx_value(pk[e], pk[KD + e], d.fx_inv);
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x)
+        out[KD + j] = (double)pk[pk_n(d) + j];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const long long* e = pk + pk_ehi(d);
+        out[KD + d.K] = ((double)e[0] + (double)e[1] * 9.313225746154785e-10) / energy_q(d);
+        out[KD + d.K + 1] = (double)pk[pk_ch(d)];
     }
 }
 
 void launch_partials_out(const Dev& d, const long long* packed, const float* C, double* out, cudaStream_t s) {
-    k_partials_out<<<1, 1024, 0, s>>>(d, packed, C, out);
+    (void)C;
+    k_partials_out<<<64, 256, 0, s>>>(d, packed, out);
 }
 
 // ------------------------------------------------------------------ create-time statistics of X
@@ -591,33 +581,8 @@ __global__ void k_xstats_max(const float* X, long long n, int D, unsigned int* o
     if (lane == 0) { atomicMax(out, __float_as_uint(am)); atomicMax(out + 1, __float_as_uint(nm)); }
 }
 
-// sum_i ||x_i||^2 q = sum hi + 2^-30 sum lo, both int64 (exact, order-free);
-// ||x_i||^2 in fp64 with k ascending, q = 2^(22-en) so each row is <= 2^22
-__global__ void k_xstats_sum(const float* X, long long n, int D, double q, long long* out) {
-    long long ahi = 0, alo = 0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int k = 0; k < D; ++k) { const double v = (double)X[i * D + k]; s = fma(v, v, s); }
-        const double v = s * q;                                   // exact (power of 2)
-        const double h = rint(v);
-        ahi += (long long)h;
-        alo += llrint((v - h) * 1073741824.0);                    // 2^30
-    }
-    for (int o = 16; o; o >>= 1) {
-        ahi += __shfl_xor_sync(0xffffffffu, ahi, o);
-        alo += __shfl_xor_sync(0xffffffffu, alo, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)ahi);
-        atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)alo);
-    }
-}
-
 void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s) {
     if (n > 0) k_xstats_max<<<592, 256, 0, s>>>(X, n, d, out);
-}
-void launch_xstats_sum(const float* X, long long n, int d, double q, long long* out, cudaStream_t s) {
-    if (n > 0) k_xstats_sum<<<592, 256, 0, s>>>(X, n, d, q, out);
 }
 
 }  // namespace aakm

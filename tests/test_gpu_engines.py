@@ -202,3 +202,28 @@ def test_odd_d_assign_update_and_run(d):
     assert rep["converged"] and ref["converged"]
     assert rep["iters"] == ref["iters"] and abs(rep["energy"] - ref["energy"]) <= 1e-4 * ref["energy"]
     km.close()
+
+
+# ---------------------------------------------------------------- degenerate shapes
+def test_empty_shard_and_k_equals_n():
+    """A rank with no rows (N < ranks) contributes nothing; K = n puts every
+    sample on its own centroid (E = 0, labels = identity for distinct rows)."""
+    X, C0, c = make("c4", N=300, K=300)
+    X = np.unique(X, axis=0)[:256]
+    n = len(X)
+    # empty shard: partials are all zero, labels_prev/labels of length 0
+    empty = np.zeros((0, X.shape[1]), np.float32)
+    km = aakm.KMeans(dev(empty) if False else torch.zeros((0, X.shape[1]), dtype=torch.float32, device="cuda"),
+                     8, aakm.config(), n_global=n)
+    part = km.update_partials(torch.zeros(0, dtype=torch.int32, device="cuda"), dev(X[:8])).cpu().numpy()
+    assert not part.any()
+    km.close()
+    # K = n with C = X: exact identity labels, zero energy, G = X
+    km = aakm.KMeans(dev(X), n, aakm.config(assign_path="tc16"))
+    lab, E, _ = km.assign(dev(X))
+    assert np.array_equal(lab.cpu().numpy(), np.arange(n)) and E == 0.0
+    G, cnt = km.update(lab, dev(X))
+    assert np.array_equal(G.cpu().numpy(), X) and (cnt.cpu().numpy() == 1).all()
+    C, labs, rep = km.run(dev(X))
+    assert rep["converged"] and rep["energy"] == 0.0 and rep["iters"] == 2
+    km.close()
