@@ -124,7 +124,6 @@ __device__ int adjust_m(int m, int m_max, double Et, double E1, double E2, doubl
 __global__ void k_control(Dev d, int stage) {
     DevState* st = d.st;
     if (st->done) return;
-    const long long KD = (long long)d.K * d.d;
     if (stage == 0) {
         const long long* pk = d.packed[0];
         const double E = __longlong_as_double(pk[pk_e(d)]);   // k_energy, after the allreduce

@@ -93,7 +93,8 @@ struct Dev {
     int* seg_bh;          // sorted update engine: per-block histograms -> scatter bases (SEG_BLOCKS x K)
     int* seg_off;         // row offsets of cluster j in perm (K+1)
     int* seg_chunk;       // chunk offsets (K+1)
-    int* seg_cmap;        // chunk -> cluster (n/SEG_ROWS + K)
+    const void* xg_map;   // device copy of the gather4 map of X (nullptr: generic segmented sums)
+    int4* seg_cmap;       // chunk -> {cluster j, first sorted row, rows, 0} (n/SEG_ROWS + K)
     int* perm;            // rows bucketed by label (n)
     float* ub;            // bounded engine (nullptr = dense): per row, upper bound on ||x_i - c_{rho_i}||
     float* lb;            //   ... and lower bound on min_{j != rho_i} ||x_i - c_j||, w.r.t. C_ref
@@ -120,7 +121,6 @@ struct GEval {
     int* lab_out;         // nullptr -> d.lab[st->cur]
     const int* lab_prev;  // used when prev_mode == 2
     int prev_mode;        // 0 = d.lab[st->cur ^ 1], 1 = none, 2 = lab_prev
-    const float* Cassign; // nullptr -> d.C
     long long* packed_out;// nullptr -> d.packed[branch]
 };
 
@@ -137,6 +137,9 @@ void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s);
 void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 void* tc_make_maps(const Dev& d);   // TMA tensor maps of (X, C_hi, C_lo); nullptr if unsupported
 void tc_free_maps(void* m);
+// 128-byte TMA map of X (n x d fp32) with a {d, 1} box for tile::gather4 row gathers
+// (the update's segmented sums); false if d is not a multiple of 4 in [4, 128].
+bool encode_gather_rows(void* map128, const float* X, long long n, int d);
 bool tc_supported(int d, int K);
 bool tc16_supported(int d, int K);
 float tau_gamma_tc16(int d);
@@ -173,21 +176,28 @@ __host__ __device__ inline long long pk_ehi(const Dev& d) { return 2LL * d.K * d
 __host__ __device__ inline long long pk_e(const Dev& d) { return pk_ehi(d) + 2; }             // E (fp64 bits)
 __host__ __device__ inline long long pk_ch(const Dev& d) { return pk_ehi(d) + 3; }            // changed
 __host__ __device__ inline long long pk_words(const Dev& d) { return pk_ehi(d) + 4; }
-// Per-row energies e_i = ||x_i - c_rho_i||^2 go into the packed vector as a two-part
-// fixed point with quantum 1/q: q = 2^(22 - eb), 2^eb >= 2 (max||x|| + max||c||)^2 >=
-// every e_i, so each row is carried to 2^-52 of the bound and an exact 0 stays 0.
+// Energies e_i = ||x_i - c_rho_i||^2 go into the packed vector as a two-part fixed
+// point [E_hi (units 1/q) | E_lo (units 2^-30/q)]. q = 2^(21 - eb) with
+// 2^eb > B = 2 (max||x|| + max||c||)^2 >= every e_i, so any partial e of one row
+// scales to v = e q < 2^21; energy_fx rounds v to a multiple of 2^-30 (adding
+// 1.5*2^22, whose ulp is 2^-30, rounds exactly) and returns it as an integer < 2^51.
+// A lane sums at most 256 of them in an int64 (< 2^59) and moves the sum into the
+// two parts with energy_flush. Each partial carries 2^-52 of B; an exact 0 stays 0;
+// the integer sums do not depend on order.
 __device__ inline double energy_q(const Dev& d) {
     const double cm = sqrt((double)__uint_as_float(d.st->cmax2_bits));
     const double B = 2.0 * (d.xn_gmax + cm) * (d.xn_gmax + cm);
     int eb = 0;
     frexp(B > 0.0 ? B : 1.0, &eb);
-    return ldexp(1.0, 22 - eb);
+    return ldexp(1.0, 21 - eb);
 }
-__device__ inline void energy_add(double e, double q, long long& hi, long long& lo) {
-    const double v = e * q;                                  // exact (power of 2), <= 2^22
-    const double h = rint(v);
-    hi += (long long)h;
-    lo += llrint((v - h) * 1073741824.0);                    // 2^30
+__device__ inline long long energy_fx(double v) {
+    return __double_as_longlong(v + 6291456.0) - 0x4158000000000000LL;
+}
+__device__ inline void energy_flush(long long& acc, long long& hi, long long& lo) {
+    hi += acc >> 30;
+    lo += acc & 0x3fffffffLL;
+    acc = 0;
 }
 
 // one-time kernel attribute setup (max dynamic smem); never during stream capture

@@ -895,6 +895,19 @@ static bool encode_cnimg(CUtensorMap* m, const void* base, int tiles) {
     return r == CUDA_SUCCESS;
 }
 
+bool encode_gather_rows(void* map128, const float* X, long long n, int d) {
+    PFN_encodeTiled enc = encoder();
+    if (!enc || d % 4 != 0 || d < 4 || d > 128 || ((uintptr_t)X & 15) != 0) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)(n > 0 ? n : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {(cuuint32_t)d, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap*>(map128), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X),
+                     dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Tensor maps for one Dev (X shard, C operand buffers, gathered rows); opaque to the runtime.
 void* tc_make_maps(const Dev& d) {
     const bool f16 = d.tc_kind == 1;

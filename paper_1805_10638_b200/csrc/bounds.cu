@@ -23,7 +23,7 @@ namespace aakm {
 __global__ void __launch_bounds__(256) k_shift(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     DevState* st = d.st;
-    const float* C = g.Cassign ? g.Cassign : d.C;
+    const float* C = d.C;
     const int D = d.d;
     const int lane = threadIdx.x & 31;
     float bmax = 0.f;

@@ -133,7 +133,7 @@ namespace {
 struct Layout {
     size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
         scratch, packed1,
-        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, perm, Gring, Fring, gram_part, trace,
+        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, perm, Gring, Fring, gram_part, trace,
         ub, lb, act_rows, C_ref, shift, total,
         scratch_bytes;
 };
@@ -176,8 +176,9 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.seg_bh = take((size_t)AAKM_SEG_BLOCKS * K * 4);
     L.seg_off = take((size_t)K * 4 + 4);
     L.seg_chunk = take((size_t)K * 4 + 4);
-    L.seg_cmap = take(((size_t)n / 256 + K + 1) * 4);
+    L.seg_cmap = take(((size_t)n / 256 + K + 1) * 16);
     L.perm = take((size_t)n * 4 + 4);
+    L.xg_map = take(128);
     L.Gring = take((size_t)H * KD * 4);
     L.Fring = take((size_t)H * KD * 4);
     L.gram_part = take((size_t)AAKM_GRAM_BLOCKS * 2 * AAKM_H_SLOTS * 8);
@@ -431,7 +432,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.seg_bh = (int*)(w + L.seg_bh);
     D.seg_off = (int*)(w + L.seg_off);
     D.seg_chunk = (int*)(w + L.seg_chunk);
-    D.seg_cmap = (int*)(w + L.seg_cmap);
+    D.seg_cmap = (int4*)(w + L.seg_cmap);
     D.perm = (int*)(w + L.perm);
     D.Gring = (float*)(w + L.Gring); D.Fring = (float*)(w + L.Fring);
     D.gram_part = (double*)(w + L.gram_part);
@@ -512,6 +513,15 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             g_create_err = "cuTensorMapEncodeTiled failed for the tensor-core engine";
             delete h;
             return KMEANS_ERR_CUDA;
+        }
+    }
+    {   // gather4 map of X for the update's segmented sums (generic kernel if unavailable)
+        alignas(64) unsigned char map[128];
+        const int lpr = d / 4;
+        if (d % 4 == 0 && lpr <= 32 && (lpr & (lpr - 1)) == 0 && encode_gather_rows(map, X, n_local, d)) {
+            CKC(cudaMemcpyAsync(w + L.xg_map, map, 128, cudaMemcpyHostToDevice, h->stream));
+            CKC(cudaStreamSynchronize(h->stream));
+            h->d.xg_map = w + L.xg_map; h->da.xg_map = w + L.xg_map;
         }
     }
     CKC(cudaMallocHost(&h->st_host, sizeof(DevState)));
@@ -603,7 +613,7 @@ kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const float
     CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
     CK(h, cudaMemsetAsync(&d.st->label_error, 0, sizeof(int), s));
     GEval g{};
-    g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels); g.prev_mode = 1; g.Cassign = C_prev;
+    g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels); g.prev_mode = 1;
     combine(h, d, 2, C_prev, s);                          // max ||c||^2 of C_prev (the energy scale)
     h->launches += launch_update(d, g, s);
     kmeans_status st = allreduce(h, d.packed[0], s);
@@ -626,7 +636,7 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
     GEval g{};
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels);
-    g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev; g.Cassign = C;
+    g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
     combine(h, d, 2, C, s);                               // max ||c||^2 of C (the energy scale)
     h->launches += launch_update(d, g, s);
     launch_partials_out(d, d.packed[0], C, packed_out, s);            // unreduced, as doubles

@@ -35,7 +35,7 @@ __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
     const int cur = d.st->cur;
     p.lab = g.lab_out ? g.lab_out : d.lab[cur];
     p.prev = g.prev_mode == 0 ? d.lab[cur ^ 1] : (g.prev_mode == 2 ? g.lab_prev : nullptr);
-    p.C = g.Cassign ? g.Cassign : d.C;
+    p.C = d.C;
     p.out = g.packed_out ? g.packed_out : d.packed[g.branch];
     return p;
 }
@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
                 e = fma(df, df, e);
             }
         }
-        for (int o = 1; o < GS; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);   // fixed tree
-        if (okj && gl == 0) energy_add(e, q, ehi, elo);
+        long long ea = okj ? energy_fx(e * q) : 0;   // this lane's part of e_row
+        energy_flush(ea, ehi, elo);
     }
     if (bad) d.st->label_error = 1;
     for (int o = 16; o; o >>= 1) {
@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
         if (j < K) {
             d.seg_off[j] = (int)pa;
             d.seg_chunk[j] = (int)pb;
-            for (long long q = 0; q < nc; ++q) d.seg_cmap[pb + q] = j;
+            for (long long q = 0; q < nc; ++q)
+                d.seg_cmap[pb + q] = make_int4(j, (int)(pa + q * SEG_ROWS), (int)min((long long)SEG_ROWS, c - q * SEG_ROWS), 0);
         }
         if (threadIdx.x == blockDim.x - 1) { carry[0] = pa + c; carry[1] = pb + nc; }
         __syncthreads();
@@ -318,12 +319,13 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     const long long nchunks = d.seg_chunk[K];
     const float sc = d.fx_scale;
     const double q = energy_q(d);
-    long long ehi = 0, elo = 0;
+    long long ehi = 0, elo = 0, ea = 0;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
-        const int j = d.seg_cmap[w];
-        const long long r0 = d.seg_off[j] + (w - d.seg_chunk[j]) * SEG_ROWS;
-        const int cnt = (int)min((long long)SEG_ROWS, (long long)d.seg_off[j + 1] - r0);
+        const int4 ci = d.seg_cmap[w];
+        const int j = ci.x;
+        const long long r0 = ci.y;
+        const int cnt = ci.z;
         // the chunk's row ids, 8 per lane, fetched up front (one round trip)
         int rid[SEG_ROWS / 32];
 #pragma unroll
@@ -343,11 +345,13 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
         for (int u = 0; u < SEG_ROWS / 32; ++u) {
             if (u * 32 < cnt) {                   // predicate, not break: keeps rid[] in registers
             float xv[8][V];
+            bool ok[8];
 #pragma unroll
             for (int b8 = 0; b8 < 32; b8 += 8) {
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
+                    ok[t] = row >= 0;
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
                         const int k = lane + 32 * v;
@@ -363,13 +367,12 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
                         const int k = lane + 32 * v;
                         if (k < D) { const double df = (double)xv[t][v] - (double)cj[v]; e = fma(df, df, e); }
                     }
-                    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-                    const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
-                    if (lane == 0 && row >= 0) energy_add(e, q, ehi, elo);
+                    if (ok[t]) ea += energy_fx(e * q);   // this lane's part of e_row
                 }
             }
             }
         }
+        energy_flush(ea, ehi, elo);              // <= 256 rows per chunk
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int k = lane + 32 * v;
@@ -379,83 +382,190 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             }
         }
     }
+    for (int o = 16; o; o >>= 1) {
+        ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
+        elo += __shfl_xor_sync(0xffffffffu, elo, o);
+    }
     if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
 }
 
-// float4 variant (d = 4 * LPR, LPR in {1,2,4,8,16,32}): LPR lanes cover one
-// row, RPW = 32 / LPR rows per warp instruction, 16 rows in flight per warp.
+// ------------------------------------------------------------------
+// Segmented sums with the rows gathered by bulk asynchronous copies (the sorted
+// engine's production kernel for d = 4 LPR, LPR a power of two <= 32).
+// Each warp walks its chunks (<= SEG_ROWS rows of one cluster j) as items of
+// <= SEG_SR rows. Producer side: lanes 0..3 each start one TMA tile::gather4
+// (4 rows by index from the X map) and lane 31 a cp.async.bulk of the centroid
+// row c_j into a slot of the warp's SEG_NS-deep shared-memory ring, all
+// completing on the slot's mbarrier; the item's {j, rows, last} go to the
+// slot's record. Row ids
+// are loaded two items ahead and chunk records one chunk ahead, so no global
+// load sits on the consumer's path. Consumer side: LPR lanes per row (float4
+// each), RPW = 32 / LPR rows per shared-memory instruction. The sums are the
+// same exact fixed point as the other engines; the energy parts are this
+// lane's 4 coordinates by direct fp64 differences (energy_fx).
+constexpr int SEG_SR = 16;         // rows per item
+constexpr int SEG_NS = 3;          // ring depth (items per warp)
+constexpr int SEG_SMEM = 215040;   // shared memory budget per block
+
+template <int LPR> struct SegBulk {
+    static constexpr int RB = 16 * LPR;                               // row bytes
+    static constexpr int GP = 4 * RB > 128 ? 4 * RB : 128;            // gather4 group pitch (TMA dst: 128 B aligned)
+    static constexpr int CO = SEG_SR / 4 * GP;                         // c_j row offset
+    static constexpr int SLOT = (CO + RB + 127) / 128 * 128;           // rows + c_j
+    static constexpr int WARP = (SEG_NS * SLOT + SEG_NS * 16 + SEG_NS * 8 + 127) / 128 * 128;
+    static constexpr int WPB = SEG_SMEM / WARP > 16 ? 16 : SEG_SMEM / WARP;
+    static constexpr int SMEM = WPB * WARP;
+};
+
+__device__ __forceinline__ void sb_init(uint64_t* bar) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void sb_expect(uint64_t* bar, unsigned bytes) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void sb_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    const unsigned da = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned ba = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(da), "l"(src), "r"(bytes), "r"(ba) : "memory");
+}
+// 4 rows (box {d, 1} of the X map) -> 4 consecutive d x 4 B rows at dst
+__device__ __forceinline__ void sb_gather4(void* dst, const void* map, int r0, int r1, int r2, int r3, uint64_t* bar) {
+    const unsigned da = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned ba = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                 ::"r"(da), "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(ba) : "memory");
+}
+__device__ __forceinline__ void sb_wait(uint64_t* bar, unsigned phase) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(a), "r"(phase) : "memory");
+    }
+}
+
+// lane g < 4 holds the ids of rows 4g..4g+3 of the item (past the end: repeats of its last row)
+struct SegItem { int i0, i1, i2, i3, j, nr, last; };
+
 template <int LPR>
-__global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
+__global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
-    constexpr int RPW = 32 / LPR;
-    constexpr int U = (16 / RPW) > 0 ? 16 / RPW : 1;     // instructions per round
-    constexpr int ROUND = U * RPW;                       // rows per round (16, or 32 when RPW = 32)
+    using SB = SegBulk<LPR>;
+    constexpr int RB = SB::RB, RPW = 32 / LPR;
+    constexpr int IT = (SEG_SR + RPW - 1) / RPW;                       // consumer instructions per item
+    extern __shared__ __align__(128) unsigned char sm[];
     const Pick p = pick(d, g);
     const int D = d.d, K = d.K;
     const long long KD = (long long)K * D;
-    const int lane = threadIdx.x & 31;
-    const int h = lane / LPR, c4i = lane % LPR;          // row slot within the instruction, float4 index
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = lane / LPR, c4i = lane % LPR;
+    unsigned char* ring = sm + warp * SB::WARP;
+    int4* rec = reinterpret_cast<int4*>(ring + SEG_NS * SB::SLOT);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rec + SEG_NS);
+    if (lane < SEG_NS) sb_init(bar + lane);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
     const long long nchunks = d.seg_chunk[K];
-    const float4* X4 = reinterpret_cast<const float4*>(d.X);
+    const long long TW = (long long)gridDim.x * SB::WPB;
+    const char* Cb = reinterpret_cast<const char*>(p.C);
+    const int4 none = make_int4(0, 0, 0, 0);
+
+    // item generator ("ahead" cursor): chunk aw, its record and the next one's
+    long long aw = (long long)blockIdx.x * SB::WPB + warp;
+    int4 ai = aw < nchunks ? d.seg_cmap[aw] : none;
+    int4 an = aw + TW < nchunks ? d.seg_cmap[aw + TW] : none;
+    int ast = 0;
+    auto gen = [&](SegItem& o) {
+        if (aw >= nchunks) { o.nr = 0; o.i0 = o.i1 = o.i2 = o.i3 = 0; o.j = 0; o.last = 0; return; }
+        const int base = ast * SEG_SR;
+        o.j = ai.x;
+        o.nr = min(SEG_SR, ai.z - base);
+        const int* pr = d.perm + ai.y + base;
+        const int g4 = 4 * (lane & 3), lst = o.nr - 1;
+        o.i0 = pr[min(g4, lst)]; o.i1 = pr[min(g4 + 1, lst)];
+        o.i2 = pr[min(g4 + 2, lst)]; o.i3 = pr[min(g4 + 3, lst)];
+        o.last = base + SEG_SR >= ai.z;
+        if (o.last) {
+            aw += TW; ai = an; ast = 0;
+            an = aw + TW < nchunks ? d.seg_cmap[aw + TW] : none;
+        } else {
+            ++ast;
+        }
+    };
+    SegItem qa, qb;
+    gen(qa);
+    gen(qb);
+    int ps = 0;                                                        // producer slot
+    int inflight = 0;
+    auto produce = [&]() {
+        if (qa.nr == 0) return;
+        uint64_t* b = bar + ps;
+        unsigned char* slot = ring + ps * SB::SLOT;
+        const int ng = (qa.nr + 3) >> 2;                               // gather4 instructions
+        if (lane == 0) { rec[ps] = make_int4(qa.j, qa.nr, qa.last, 0); sb_expect(b, (unsigned)((4 * ng + 1) * RB)); }
+        __syncwarp();
+        if (lane < ng) sb_gather4(slot + lane * SB::GP, d.xg_map, qa.i0, qa.i1, qa.i2, qa.i3, b);
+        if (lane == 31) sb_copy(slot + SB::CO, Cb + (long long)qa.j * RB, RB, b);
+        ps = ps + 1 == SEG_NS ? 0 : ps + 1;
+        ++inflight;
+        qa = qb;
+        gen(qb);
+    };
+#pragma unroll
+    for (int i = 0; i < SEG_NS; ++i) produce();
+
     const float sc = d.fx_scale;
     const double q = energy_q(d);
-    long long ehi = 0, elo = 0;
-    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
-         w += (long long)gridDim.x * (blockDim.x >> 5)) {
-        const int j = d.seg_cmap[w];
-        const long long r0 = d.seg_off[j] + (w - d.seg_chunk[j]) * SEG_ROWS;
-        const int cnt = (int)min((long long)SEG_ROWS, (long long)d.seg_off[j + 1] - r0);
-        int rid[SEG_ROWS / 32];
-#pragma unroll
-        for (int t = 0; t < SEG_ROWS / 32; ++t) {
-            const int qi = t * 32 + lane;
-            rid[t] = qi < cnt ? d.perm[r0 + qi] : -1;
-        }
-        const float4 c = __ldg(reinterpret_cast<const float4*>(p.C + (long long)j * D) + c4i);
+    long long ehi = 0, elo = 0, ea = 0;
+    unsigned phase = 0;                                                // bit b: parity of slot b
+    int cs = 0;                                                        // consumer slot
+    int h0 = 0, h1 = 0, h2 = 0, h3 = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
+    while (inflight > 0) {
+        sb_wait(bar + cs, (phase >> cs) & 1u);
+        phase ^= 1u << cs;
+        const int4 r = rec[cs];                                        // {j, rows, last}
+        const unsigned char* slot = ring + cs * SB::SLOT;
+        const float4 c = *reinterpret_cast<const float4*>(slot + SB::CO + 16 * c4i);
         const double cx = c.x, cy = c.y, cz = c.z, cw = c.w;
-        // fixed-point parts of the 4 coordinates, int32 per chunk (<= 256 rows / lane)
-        int h0 = 0, h1 = 0, h2 = 0, h3 = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
 #pragma unroll
-        for (int t = 0; t < SEG_ROWS / 32; ++t) {
-            if (t * 32 < cnt) {
-#pragma unroll
-                for (int r = 0; r < 32; r += ROUND) {
-                    float4 xv[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int rw = __shfl_sync(0xffffffffu, rid[t], (r + u * RPW + h) & 31);
-                        xv[u] = rw >= 0 ? __ldcs(X4 + (long long)rw * LPR + c4i) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        fx_add(xv[u].x, sc, h0, l0); fx_add(xv[u].y, sc, h1, l1);
-                        fx_add(xv[u].z, sc, h2, l2); fx_add(xv[u].w, sc, h3, l3);
-                        // e_i by direct differences: 4 coordinates here, then the row's LPR lanes
-                        double df = (double)xv[u].x - cx, e = df * df;
-                        df = (double)xv[u].y - cy; e = fma(df, df, e);
-                        df = (double)xv[u].z - cz; e = fma(df, df, e);
-                        df = (double)xv[u].w - cw; e = fma(df, df, e);
-#pragma unroll
-                        for (int o = 1; o < LPR; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-                        const int rw = __shfl_sync(0xffffffffu, rid[t], (r + u * RPW + h) & 31);
-                        if (c4i == 0 && rw >= 0) energy_add(e, q, ehi, elo);
-                    }
-                }
+        for (int i = 0; i < IT; ++i) {
+            const int rr = i * RPW + h;
+            if (rr < r.y) {
+                const float4 xv = *reinterpret_cast<const float4*>(slot + (rr >> 2) * SB::GP + (rr & 3) * RB + 16 * c4i);
+                fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
+                fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
+                double df = (double)xv.x - cx, e = df * df;                // this lane's part of e_row
+                df = (double)xv.y - cy; e = fma(df, df, e);
+                df = (double)xv.z - cz; e = fma(df, df, e);
+                df = (double)xv.w - cw; e = fma(df, df, e);
+                ea += energy_fx(e * q);
             }
         }
-        // combine the RPW row slots (lanes with equal c4i): exact int64 sums
-        long long s[8] = {h0, h1, h2, h3, l0, l1, l2, l3};
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads done before the slot refills
+        cs = cs + 1 == SEG_NS ? 0 : cs + 1;
+        --inflight;
+        produce();
+        if (!r.z) continue;
+        // chunk done: combine the RPW row slots (lanes with equal c4i), exact int64 sums
+        energy_flush(ea, ehi, elo);                                    // <= SEG_ROWS rows
+        long long s8[8] = {h0, h1, h2, h3, l0, l1, l2, l3};
 #pragma unroll
         for (int o = LPR; o < 32; o <<= 1) {
 #pragma unroll
-            for (int qq = 0; qq < 8; ++qq) s[qq] += __shfl_xor_sync(0xffffffffu, s[qq], o);
+            for (int t = 0; t < 8; ++t) s8[t] += __shfl_xor_sync(0xffffffffu, s8[t], o);
         }
         if (h == 0) {
-            long long* oh = p.out + (long long)j * D + 4 * c4i;
+            long long* oh = p.out + (long long)r.x * D + 4 * c4i;
             long long* ol = oh + KD;
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) { red_add_s64(oh + qq, s[qq]); red_add_s64(ol + qq, s[4 + qq]); }
+            for (int t = 0; t < 4; ++t) { red_add_s64(oh + t, s8[t]); red_add_s64(ol + t, s8[4 + t]); }
         }
+        h0 = h1 = h2 = h3 = l0 = l1 = l2 = l3 = 0;
     }
     for (int o = 16; o; o >>= 1) {
         ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
@@ -464,10 +574,23 @@ __global__ void __launch_bounds__(256) k_segsum4(Dev d, GEval g) {
     if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
 }
 
+template <int LPR> static cudaError_t seg_attr() {
+    return cudaFuncSetAttribute(k_segsum_bulk<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SegBulk<LPR>::SMEM);
+}
+template <int LPR> static void seg_launch(const Dev& d, const GEval& g, cudaStream_t s) {
+    using SB = SegBulk<LPR>;
+    const int per_sm = SB::SMEM <= 113 * 1024 ? 2 : 1;
+    k_segsum_bulk<LPR><<<AAKM_SEG_BLOCKS * per_sm, 32 * SB::WPB, SB::SMEM, s>>>(d, g);
+}
+
 cudaError_t setup_update() {
     cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
+    e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
+    if (e != cudaSuccess) return e;
+    for (cudaError_t f : {seg_attr<1>(), seg_attr<2>(), seg_attr<4>(), seg_attr<8>(), seg_attr<16>(), seg_attr<32>()})
+        if (f != cudaSuccess) return f;
+    return cudaSuccess;
 }
 
 // Chosen from global quantities so every rank runs the same per-row energy order
@@ -486,14 +609,14 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     k_scan_a<<<(d.K + 255) / 256, 256, 0, s>>>(d, g, AAKM_SEG_BLOCKS);
     k_scan_b<<<1, 1024, 0, s>>>(d, g);
     k_scatter<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
-    if (d.d % 4 == 0 && (d.d / 4) <= 32 && ((d.d / 4) & (d.d / 4 - 1)) == 0) {
+    if (d.xg_map) {
         switch (d.d / 4) {
-            case 1: k_segsum4<1><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
-            case 2: k_segsum4<2><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
-            case 4: k_segsum4<4><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
-            case 8: k_segsum4<8><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
-            case 16: k_segsum4<16><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
-            default: k_segsum4<32><<<d.upd_blocks, 256, 0, s>>>(d, g); return 5;
+            case 1: seg_launch<1>(d, g, s); return 5;
+            case 2: seg_launch<2>(d, g, s); return 5;
+            case 4: seg_launch<4>(d, g, s); return 5;
+            case 8: seg_launch<8>(d, g, s); return 5;
+            case 16: seg_launch<16>(d, g, s); return 5;
+            default: seg_launch<32>(d, g, s); return 5;
         }
     }
     const int V = (d.d + 31) / 32;

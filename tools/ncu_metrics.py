@@ -20,3 +20,13 @@ for r in rows[2:]:
     st = sorted(((float(d[k].replace(',', '') or 0), k) for k in hdr if k.startswith(STALL) and k.endswith("_per_issue_active.ratio")), reverse=True)
     for v, k in st[:8]:
         print(f"  stall {k[len(STALL):-len('_per_issue_active.ratio')]:30s} {v:.3f}")
+    # busiest pipes (any pipe metric reported as % of peak)
+    pipes = []
+    for k in hdr:
+        if (k.startswith("sm__pipe_") or k.startswith("sm__inst_executed_pipe_")) and "pct_of_peak" in k:
+            try:
+                pipes.append((float(d[k].replace(',', '')), k))
+            except ValueError:
+                pass
+    for v, k in sorted(pipes, reverse=True)[:10]:
+        print(f"  pipe {k:76s} {v:.1f}")
