@@ -212,9 +212,7 @@ def test_empty_shard_and_k_equals_n():
     X = np.unique(X, axis=0)[:256]
     n = len(X)
     # empty shard: partials are all zero, labels_prev/labels of length 0
-    empty = np.zeros((0, X.shape[1]), np.float32)
-    km = aakm.KMeans(dev(empty) if False else torch.zeros((0, X.shape[1]), dtype=torch.float32, device="cuda"),
-                     8, aakm.config(), n_global=n)
+    km = aakm.KMeans(torch.zeros((0, X.shape[1]), dtype=torch.float32, device="cuda"), 8, aakm.config(), n_global=n)
     part = km.update_partials(torch.zeros(0, dtype=torch.int32, device="cuda"), dev(X[:8])).cpu().numpy()
     assert not part.any()
     km.close()
@@ -226,4 +224,38 @@ def test_empty_shard_and_k_equals_n():
     assert np.array_equal(G.cpu().numpy(), X) and (cnt.cpu().numpy() == 1).all()
     C, labs, rep = km.run(dev(X))
     assert rep["converged"] and rep["energy"] == 0.0 and rep["iters"] == 2
+    km.close()
+
+
+@pytest.mark.parametrize("d", [4, 8, 16, 32, 64, 128])
+def test_sorted_update_engine(d):
+    """The label-sorted update (n >= 65 536: histogram, scans, scatter, TMA
+    gather4 segmented sums) for every float4 width: one cluster holding 40 % of
+    the rows (hundreds of 256-row chunks), tiny and empty clusters, rows equal to
+    their centroid (exact zero energy parts); S/N, E and #changed against the
+    oracle (E to 1e-12: direct differences on both sides)."""
+    rng = np.random.default_rng(100 + d)
+    n, K = 70_001, 50
+    X = rng.normal(0, 3, (n, d)).astype(np.float32)
+    C = rng.normal(0, 3, (K, d)).astype(np.float32)
+    lab = rng.integers(1, K - 3, n).astype(np.int32)              # K-3..K-1 stay empty
+    lab[rng.random(n) < 0.4] = 0
+    lab[:500] = 7
+    X[:500] = C[7]                                                 # e_i = 0 exactly
+    prev = lab.copy()
+    prev[rng.random(n) < 0.1] = 1
+    km = aakm.KMeans(dev(X), K, aakm.config())
+    part = km.update_partials(dev(lab), dev(C), labels_prev=dev(prev)).cpu().numpy()
+    G_ora, cnt = oracle.update(X, lab, C.astype(np.float64))
+    np.testing.assert_array_equal(part[K * d:K * d + K], cnt)
+    S = part[:K * d].reshape(K, d)
+    G = np.where(cnt[:, None] > 0, S / np.maximum(cnt, 1)[:, None], C)
+    np.testing.assert_allclose(G, G_ora, rtol=1e-12, atol=1e-12)
+    E_ora = oracle.energy(X, C.astype(np.float64), lab)
+    assert abs(part[-2] - E_ora) <= 1e-12 * E_ora, (part[-2], E_ora)
+    assert part[-1] == float((lab != prev).sum())
+    # the same through kmeans_update + kmeans_assign's energy on C itself
+    G2, cnt2 = km.update(dev(lab), dev(C))
+    np.testing.assert_array_equal(cnt2.cpu().numpy(), cnt)
+    assert np.abs(G2.cpu().numpy() - G_ora.astype(np.float32)).max() <= 1e-6 * max(1.0, np.abs(G_ora).max())
     km.close()
