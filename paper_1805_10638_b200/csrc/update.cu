@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
 // Segmented sums with the rows gathered by bulk asynchronous copies (the sorted
 // engine's production kernel for d = 4 LPR, LPR a power of two <= 32).
 // Each warp walks its chunks (<= SEG_ROWS rows of one cluster j) as items of
-// <= SEG_SR rows. Producer side: lanes 0..3 each start one TMA tile::gather4
+// <= SR rows (32, or 16 for d = 128). Producer side: lanes 0..SR/4-1 each start one TMA tile::gather4
 // (4 rows by index from the X map) and lane 31 a cp.async.bulk of the centroid
 // row c_j into a slot of the warp's SEG_NS-deep shared-memory ring, all
 // completing on the slot's mbarrier; the item's {j, rows, last} go to the
@@ -403,14 +403,14 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
 // each), RPW = 32 / LPR rows per shared-memory instruction. The sums are the
 // same exact fixed point as the other engines; the energy parts are this
 // lane's 4 coordinates by direct fp64 differences (energy_fx).
-constexpr int SEG_SR = 16;         // rows per item
 constexpr int SEG_NS = 3;          // ring depth (items per warp)
 constexpr int SEG_SMEM = 215040;   // shared memory budget per block
 
 template <int LPR> struct SegBulk {
     static constexpr int RB = 16 * LPR;                               // row bytes
+    static constexpr int SR = 16;                                      // rows per item
     static constexpr int GP = 4 * RB > 128 ? 4 * RB : 128;            // gather4 group pitch (TMA dst: 128 B aligned)
-    static constexpr int CO = SEG_SR / 4 * GP;                         // c_j row offset
+    static constexpr int CO = SR / 4 * GP;                         // c_j row offset
     static constexpr int SLOT = (CO + RB + 127) / 128 * 128;           // rows + c_j
     static constexpr int WARP = (SEG_NS * SLOT + SEG_NS * 16 + SEG_NS * 8 + 127) / 128 * 128;
     static constexpr int WPB = SEG_SMEM / WARP > 16 ? 16 : SEG_SMEM / WARP;
@@ -448,7 +448,7 @@ __device__ __forceinline__ void sb_wait(uint64_t* bar, unsigned phase) {
     }
 }
 
-// lane g < 4 holds the ids of rows 4g..4g+3 of the item (past the end: repeats of its last row)
+// lane g < SR/4 holds the ids of rows 4g..4g+3 of the item (past the end: repeats of its last row)
 struct SegItem { int i0, i1, i2, i3, j, nr, last; };
 
 template <int LPR>
@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
     if (!geval_active(d, g)) return;
     using SB = SegBulk<LPR>;
     constexpr int RB = SB::RB, RPW = 32 / LPR;
-    constexpr int IT = (SEG_SR + RPW - 1) / RPW;                       // consumer instructions per item
+    constexpr int SR = SB::SR;
+    constexpr int IT = (SR + RPW - 1) / RPW;                       // consumer instructions per item
     extern __shared__ __align__(128) unsigned char sm[];
     const Pick p = pick(d, g);
     const int D = d.d, K = d.K;
@@ -481,14 +482,14 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
     int ast = 0;
     auto gen = [&](SegItem& o) {
         if (aw >= nchunks) { o.nr = 0; o.i0 = o.i1 = o.i2 = o.i3 = 0; o.j = 0; o.last = 0; return; }
-        const int base = ast * SEG_SR;
+        const int base = ast * SR;
         o.j = ai.x;
-        o.nr = min(SEG_SR, ai.z - base);
+        o.nr = min(SR, ai.z - base);
         const int* pr = d.perm + ai.y + base;
-        const int g4 = 4 * (lane & 3), lst = o.nr - 1;
+        const int g4 = 4 * (lane & (SR / 4 - 1)), lst = o.nr - 1;
         o.i0 = pr[min(g4, lst)]; o.i1 = pr[min(g4 + 1, lst)];
         o.i2 = pr[min(g4 + 2, lst)]; o.i3 = pr[min(g4 + 3, lst)];
-        o.last = base + SEG_SR >= ai.z;
+        o.last = base + SR >= ai.z;
         if (o.last) {
             aw += TW; ai = an; ast = 0;
             an = aw + TW < nchunks ? d.seg_cmap[aw + TW] : none;
@@ -532,18 +533,22 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         const float4 c = *reinterpret_cast<const float4*>(slot + SB::CO + 16 * c4i);
         const double cx = c.x, cy = c.y, cz = c.z, cw = c.w;
 #pragma unroll
-        for (int i = 0; i < IT; ++i) {
+        for (int i = 0; i < IT; ++i) {                                 // branch-free: rows past r.y read as 0
             const int rr = i * RPW + h;
-            if (rr < r.y) {
-                const float4 xv = *reinterpret_cast<const float4*>(slot + (rr >> 2) * SB::GP + (rr & 3) * RB + 16 * c4i);
-                fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
-                fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
-                double df = (double)xv.x - cx, e = df * df;                // this lane's part of e_row
-                df = (double)xv.y - cy; e = fma(df, df, e);
-                df = (double)xv.z - cz; e = fma(df, df, e);
-                df = (double)xv.w - cw; e = fma(df, df, e);
-                ea += energy_fx(e * q);
-            }
+            const int ra = RPW > SR ? min(rr, SR - 1) : rr;                // stay inside the slot
+            const unsigned char* a = SB::GP == 4 * RB ? slot + ra * RB + 16 * c4i
+                                                      : slot + (ra >> 2) * SB::GP + (ra & 3) * RB + 16 * c4i;
+            float4 xv = *reinterpret_cast<const float4*>(a);
+            const bool ok = rr < r.y;
+            if (!ok) xv = make_float4(0.f, 0.f, 0.f, 0.f);              // adds nothing to the sums
+            fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
+            fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
+            double df = (double)xv.x - cx, e = df * df;                    // this lane's part of e_row
+            df = (double)xv.y - cy; e = fma(df, df, e);
+            df = (double)xv.z - cz; e = fma(df, df, e);
+            df = (double)xv.w - cw; e = fma(df, df, e);
+            const long long v = energy_fx(e * q);
+            ea += ok ? v : 0;
         }
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads done before the slot refills
