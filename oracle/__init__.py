@@ -8,5 +8,5 @@ its citations, and DESIGN.md §3 for the pins.
 """
 from .oracle import (  # noqa: F401
     build, lib, assign, best2, energy, update, ls_solve, adjust_m, sqdist,
-    OracleConfig, AAState, run, lloyd,
+    OracleConfig, AAState, run, lloyd, seed_pp, seed_scale, SeedError,
 )

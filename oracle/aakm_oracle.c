@@ -382,3 +382,83 @@ int ora_pass(ora_state *s)
 }
 
 int ora_state_size(void) { return (int)sizeof(ora_state); }
+
+/* ------------------------------------------------------------------------ */
+/* K-Means++ seeding (the paper seeds with K-Means++ among others,
+ * PAPER.md:44,347, citing Arthur & Vassilvitskii), with the
+ * caller's uniforms u[0..k-1] in [0,1) and the D^2 weights in fixed point
+ * (reading R-A27), step by step:
+ *   t     = 50 - e with (2 max|x_ik|)^2 < 2^e: every squared coordinate
+ *           difference scaled by 2^t is < 2^50;
+ *   dist_i(c) = sum_k rint(((double)x_ik - (double)c_k)^2 * 2^t)   (int64,
+ *           each term rounded to nearest-even; the sum is exact);
+ *   center 0 = sample floor(u_0 N);  D2_i = dist_i(center 0);
+ *   for r = 1..k-1:  M = max_i D2_i (M = 0: fewer than k distinct samples ->
+ *           return 2);  sh = max(0, bitlen(M) + ceil(log2 N) - 62);
+ *           w_i = D2_i >> sh;  T = sum_i w_i;  tau = min(T - 1, floor(u_r T));
+ *           center r = the smallest i with w_0 + ... + w_i > tau  (inverse CDF:
+ *           P(i) = w_i / T, proportional to D^2; w_i = 0 is never drawn);
+ *           D2_i = min(D2_i, dist_i(center r)).
+ * idx[k] receives the sample indices; D2_out (optional, N) the final D2.
+ * Returns 0, 1 (a u outside [0,1) or k outside [1, N]) or 2.               */
+static int64_t ora_q(double v, int t) { return (int64_t)nearbyint(ldexp(v, t)); }
+
+static int64_t ora_qdist(const float *x, const float *c, int d, int t)
+{
+    int64_t s = 0;
+    for (int k = 0; k < d; ++k) {
+        double diff = (double)x[k] - (double)c[k];
+        s += ora_q(diff * diff, t);
+    }
+    return s;
+}
+
+int ora_seed_pp(const float *X, int64_t N, int d, int k, const double *u,
+                int64_t *idx, int64_t *D2_out)
+{
+    if (k < 1 || (int64_t)k > N) return 1;
+    for (int r = 0; r < k; ++r)
+        if (!(u[r] >= 0.0 && u[r] < 1.0)) return 1;
+    double amax = 0.0;
+    for (int64_t i = 0; i < N * (int64_t)d; ++i)
+        if (fabs((double)X[i]) > amax) amax = fabs((double)X[i]);
+    int e = 0;
+    if (amax > 0.0) frexp(4.0 * amax * amax, &e);       /* (2 amax)^2 < 2^e */
+    const int t = 50 - e;
+    int L = 0;
+    while (((int64_t)1 << L) < N) ++L;                  /* ceil(log2 N) */
+    int64_t *D2 = (int64_t *)malloc((size_t)N * sizeof(int64_t));
+    int64_t i0 = (int64_t)floor(u[0] * (double)N);
+    if (i0 > N - 1) i0 = N - 1;
+    idx[0] = i0;
+    for (int64_t i = 0; i < N; ++i)
+        D2[i] = ora_qdist(X + i * (int64_t)d, X + i0 * (int64_t)d, d, t);
+    int status = 0;
+    for (int r = 1; r < k; ++r) {
+        int64_t M = 0;
+        for (int64_t i = 0; i < N; ++i)
+            if (D2[i] > M) M = D2[i];
+        if (M == 0) { status = 2; break; }
+        int bl = 0;
+        while (bl < 63 && (M >> bl) != 0) ++bl;         /* M < 2^bl */
+        int sh = bl + L - 62;
+        if (sh < 0) sh = 0;
+        int64_t T = 0;
+        for (int64_t i = 0; i < N; ++i) T += D2[i] >> sh;
+        int64_t tau = (int64_t)floor(u[r] * (double)T);
+        if (tau > T - 1) tau = T - 1;
+        int64_t acc = 0, pick = -1;
+        for (int64_t i = 0; i < N; ++i) {
+            acc += D2[i] >> sh;
+            if (acc > tau) { pick = i; break; }
+        }
+        idx[r] = pick;
+        for (int64_t i = 0; i < N; ++i) {
+            int64_t v = ora_qdist(X + i * (int64_t)d, X + pick * (int64_t)d, d, t);
+            if (v < D2[i]) D2[i] = v;
+        }
+    }
+    if (D2_out) memcpy(D2_out, D2, (size_t)N * sizeof(int64_t));
+    free(D2);
+    return status;
+}

@@ -71,6 +71,7 @@ def lib():
             L.ora_init.argtypes = [ct.POINTER(_State), P, I32]; L.ora_init.restype = None
             L.ora_pass.argtypes = [ct.POINTER(_State)]; L.ora_pass.restype = I32
             L.ora_state_size.restype = I32
+            L.ora_seed_pp.argtypes = [P, I64, I32, I32, P, P, P]; L.ora_seed_pp.restype = I32
             assert L.ora_state_size() == ct.sizeof(_State), "ora_state layout mismatch"
             _lib = L
     return _lib
@@ -247,3 +248,33 @@ def run(X, C0, cfg: OracleConfig | None = None, trace=False):
 def lloyd(X, C0, max_iters=10000, trace=False):
     """Plain Lloyd = Algorithm 1 with fixed m = 0 (every iterate is a Lloyd iterate)."""
     return run(X, C0, OracleConfig(m0=0, dynamic_m=False, max_iters=max_iters), trace=trace)
+
+
+class SeedError(ValueError):
+    """ora_seed_pp status 1 (bad u or k) or 2 (fewer than k distinct samples)."""
+
+
+def seed_pp(X, k, u, return_d2=False):
+    """K-Means++ seeding with the caller's uniforms u[0..k-1] (oracle/aakm_oracle.c
+    ora_seed_pp: fixed-point D^2 weights, reading R-A27). Returns the k sample
+    indices (int64), and the final fixed-point D2 if asked."""
+    X = _f32(X)
+    N, d = X.shape
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if u.shape != (k,):
+        raise SeedError("u must hold k uniforms")
+    idx = np.zeros(k, dtype=np.int64)
+    d2 = np.zeros(N, dtype=np.int64) if return_d2 else None
+    st = lib().ora_seed_pp(_p(X), N, d, int(k), _p(u), _p(idx), _p(d2) if d2 is not None else None)
+    if st != 0:
+        raise SeedError({1: "u outside [0,1) or k outside [1, N]", 2: "fewer than k distinct samples"}[st])
+    return (idx, d2) if return_d2 else idx
+
+
+def seed_scale(X):
+    """t of R-A27: 2^t scales every squared coordinate difference below 2^50."""
+    a = float(np.abs(np.asarray(X, dtype=np.float64)).max()) if np.size(X) else 0.0
+    if a == 0.0:
+        return 50
+    return 50 - int(np.frexp(4.0 * a * a)[1])
+
