@@ -50,7 +50,7 @@ extern "C" {
 #endif
 
 #define KMEANS_M_MAX 30          /* m_bar of PAPER.md:177; ring = m_max + 1 slots */
-#define KMEANS_ABI_VERSION 2
+#define KMEANS_ABI_VERSION 3
 
 typedef struct kmeans_handle kmeans_handle;
 typedef struct CUstream_st *kmeans_stream_t;   /* == cudaStream_t */
@@ -221,6 +221,23 @@ AAKM_API kmeans_status kmeans_state_import(kmeans_handle *h, const kmeans_state 
 AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *labels,
                                      const int32_t *labels_prev, const float *C,
                                      double *packed_out);
+
+/* K-Means++ seeding (Arthur & Vassilvitskii 2007, which the paper uses among
+ * its seeders: PAPER.md:44,347) of the handle's K centers.
+ *   u       host, K uniforms in [0, 1) (the caller's random numbers): center 0
+ *           is global sample floor(u[0] N); center r >= 1 is drawn by inverse
+ *           CDF with u[r] from weights w_i proportional to D(x_i)^2, the squared
+ *           distance to the nearest chosen center, in the fixed point of
+ *           DESIGN.md reading R-A27 (so every rank count draws the same
+ *           samples, and samples with D = 0 are never drawn).
+ *   C_out   device, K x d fp32 row-major, caller-owned: the chosen samples.
+ *   idx_out host, K int64 (nullable): their global row indices.
+ * Collective when nranks > 1 (three small allreduces per center). Uses the
+ * handle's X and workspace; does not touch the Algorithm 1 state.
+ * Synchronises. Errors: INVALID for NULL u / C_out, a u outside [0, 1), or
+ * fewer than K distinct samples (every remaining D^2 = 0). */
+AAKM_API kmeans_status kmeans_seed_pp(kmeans_handle *h, const double *u /*host*/, float *C_out,
+                                      int64_t *idx_out /*host*/);
 
 /* Sum of CUDA-event durations (ms) of the assignment launches recorded since
  * the last call (config.timing = 1), and their count.  Synchronises. */

@@ -89,6 +89,7 @@ def lib():
                 "kmeans_launch_count": ([P], I64),
                 "kmeans_last_flagged": ([P, ct.POINTER(I64)], I32),
                 "kmeans_bounded_stats": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
+                "kmeans_seed_pp": ([P, P, P, P], I32),
                 "kmeans_assign_path_name": ([P], ct.c_char_p),
                 "kmeans_destroy": ([P], I32),
                 "kmeans_last_error": ([P], ct.c_char_p),
@@ -314,6 +315,20 @@ class KMeans:
         a, b = ct.c_int64(), ct.c_int64()
         self._c(lib().kmeans_bounded_stats(self.h, ct.byref(a), ct.byref(b)))
         return a.value, b.value
+
+    def seed_pp(self, u):
+        """K-Means++ seeding (kmeans_seed_pp) with the caller's K uniforms in [0, 1):
+        returns (C0 as a K x d device tensor, the K global sample indices)."""
+        import numpy as np
+        t = self.torch
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.shape != (self.K,):
+            raise ValueError("u must hold K uniforms")
+        C = t.empty((self.K, self.d), dtype=t.float32, device=self.device)
+        idx = np.zeros(self.K, dtype=np.int64)
+        self._c(lib().kmeans_seed_pp(self.h, u.ctypes.data_as(ct.c_void_p), _ptr(C),
+                                     idx.ctypes.data_as(ct.c_void_p)))
+        return C, idx
 
     def last_flagged(self) -> int:
         v = ct.c_int64()

@@ -12,6 +12,8 @@
 #define AAKM_SORTED_MIN_ROWS 65536  // label-sorted update engine from this many rows
 #define AAKM_SORTED_MAX_K 16384     // ... and up to this many clusters (smem histograms)
 #define AAKM_SEG_BLOCKS 148         // row blocks of the histogram / scatter
+#define AAKM_MAX_RANKS 1024         // NCCL ranks per communicator this build sizes for
+#define AAKM_SEED_BLOCKS 1184      // row blocks of the K-Means++ passes (8 x 148)
 #define AAKM_CNIMG_BYTES 4096       // folded ||c||^2 block of one 128-centroid tile (128 rows x 32 B)
 
 namespace aakm {
@@ -47,6 +49,8 @@ struct alignas(16) DevState {
     int bnd_ready, bnd_use;      // bounded engine: bounds valid for the next / this assignment
     long long rows_scored, rows_total;   // bounded engine: rows run through the tensor engine / all rows
     unsigned int shift_max_bits, shift_tmp, shift_ctr, pad3;   // max_j ||c_j - c_ref_j|| (float bits)
+    long long seed_max;          // K-Means++: max_i D2_i of the current round (fixed point)
+    int seed_err, pad4;          // K-Means++: 2 = fewer distinct samples than K
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -93,6 +97,12 @@ struct Dev {
     int* seg_bh;          // sorted update engine: per-block histograms -> scatter bases (SEG_BLOCKS x K)
     int* seg_off;         // row offsets of cluster j in perm (K+1)
     int* seg_chunk;       // chunk offsets (K+1)
+    long long* seed_d2;   // K-Means++: D2_i (n, fixed point, seed.cu)
+    long long* seed_part; // K-Means++: per-block weight sums (AAKM_SEED_BLOCKS)
+    long long* seed_T;    // K-Means++: every rank's weight total (nranks)
+    int* seed_x;          // K-Means++: exchange row (d fp32 bits + global index)
+    long long* seed_idx;  // K-Means++: chosen global indices (K)
+    double* seed_u;       // K-Means++: the caller's uniforms (K)
     const void* xg_map;   // device copy of the gather4 map of X (nullptr: generic segmented sums)
     int4* seg_cmap;       // chunk -> {cluster j, first sorted row, rows, 0} (n/SEG_ROWS + K)
     int* perm;            // rows bucketed by label (n)
@@ -140,6 +150,13 @@ void tc_free_maps(void* m);
 // 128-byte TMA map of X (n x d fp32) with a {d, 1} box for tile::gather4 row gathers
 // (the update's segmented sums); false if d is not a multiple of 4 in [4, 128].
 bool encode_gather_rows(void* map128, const float* X, long long n, int d);
+// K-Means++ seeding (seed.cu)
+int seed_blocks(const Dev& d);
+void launch_seed_first(const Dev& d, long long row_local, long long gi, cudaStream_t s);
+void launch_seed_dist(const Dev& d, const float* c, int first, double scale, cudaStream_t s);
+void launch_seed_weights(const Dev& d, int log2n, int rank, int nranks, cudaStream_t s);
+void launch_seed_select(const Dev& d, int r, int log2n, int rank, int nranks, long long row_offset, cudaStream_t s);
+void launch_seed_commit(const Dev& d, float* C_out, int r, cudaStream_t s);
 bool tc_supported(int d, int K);
 bool tc16_supported(int d, int K);
 float tau_gamma_tc16(int d);

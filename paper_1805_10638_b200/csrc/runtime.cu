@@ -45,6 +45,7 @@ struct kmeans_handle {
     DevState* st_host = nullptr;                             // pinned
     TraceRec* tr_host = nullptr;                             // pinned
     double* scal_host = nullptr;                             // pinned (E, changed)
+    float x_gamax = 0.f;                                     // max |x_ik| over all ranks (K-Means++ scale)
     cudaEvent_t run_ev[2] = {nullptr, nullptr};
     int* done_host = nullptr;                                // pinned
 };
@@ -133,7 +134,7 @@ namespace {
 struct Layout {
     size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
         scratch, packed1,
-        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, perm, Gring, Fring, gram_part, trace,
+        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
         ub, lb, act_rows, C_ref, shift, total,
         scratch_bytes;
 };
@@ -179,6 +180,12 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.seg_cmap = take(((size_t)n / 256 + K + 1) * 16);
     L.perm = take((size_t)n * 4 + 4);
     L.xg_map = take(128);
+    L.seed_d2 = take((size_t)n * 8 + 8);
+    L.seed_part = take((size_t)AAKM_SEED_BLOCKS * 8);
+    L.seed_T = take((size_t)AAKM_MAX_RANKS * 8);
+    L.seed_x = take((size_t)(d + 2) * 4);
+    L.seed_idx = take((size_t)K * 8);
+    L.seed_u = take((size_t)K * 8);
     L.Gring = take((size_t)H * KD * 4);
     L.Fring = take((size_t)H * KD * 4);
     L.gram_part = take((size_t)AAKM_GRAM_BLOCKS * 2 * AAKM_H_SLOTS * 8);
@@ -392,7 +399,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     kmeans_status vs = validate(n_local, d, k, cfg, why);
     if (vs != KMEANS_OK) { g_create_err = why; return vs; }
     if ((!X && n_local > 0) || !workspace) { g_create_err = "X or workspace is NULL"; return KMEANS_ERR_INVALID; }
-    if (nranks < 1 || rank < 0 || rank >= nranks) { g_create_err = "bad rank/nranks"; return KMEANS_ERR_INVALID; }
+    if (nranks < 1 || nranks > AAKM_MAX_RANKS || rank < 0 || rank >= nranks) { g_create_err = "bad rank/nranks"; return KMEANS_ERR_INVALID; }
     if ((nranks == 1) != (uid128 == nullptr)) { g_create_err = "uid128 must be NULL iff nranks == 1"; return KMEANS_ERR_INVALID; }
     if (n_global < n_local || k > n_global) { g_create_err = "need n_local <= n_global and k <= n_global"; return KMEANS_ERR_INVALID; }
     if (((uintptr_t)workspace & 255) != 0) { g_create_err = "workspace must be 256-byte aligned"; return KMEANS_ERR_INVALID; }
@@ -433,6 +440,9 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.seg_off = (int*)(w + L.seg_off);
     D.seg_chunk = (int*)(w + L.seg_chunk);
     D.seg_cmap = (int4*)(w + L.seg_cmap);
+    D.seed_d2 = (long long*)(w + L.seed_d2); D.seed_part = (long long*)(w + L.seed_part);
+    D.seed_T = (long long*)(w + L.seed_T); D.seed_x = (int*)(w + L.seed_x);
+    D.seed_idx = (long long*)(w + L.seed_idx); D.seed_u = (double*)(w + L.seed_u);
     D.perm = (int*)(w + L.perm);
     D.Gring = (float*)(w + L.Gring); D.Fring = (float*)(w + L.Fring);
     D.gram_part = (double*)(w + L.gram_part);
@@ -566,6 +576,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             dv->xn_gmax = sqrt((double)mf[1]) * (1.0 + 1e-6);          // max_i ||x_i||, rounded up
             dv->upd_sorted = srt ? 1 : 0;
         }
+        h->x_gamax = mf[0];
         CKC(cudaMemsetAsync(w + L.scratch, 0, 128, h->stream));
     }
     CKC(cudaStreamSynchronize(h->stream));
@@ -847,6 +858,64 @@ kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* 
 }
 
 int64_t kmeans_launch_count(const kmeans_handle* h) { return h ? h->launches : 0; }
+
+// K-Means++ seeding (seed.cu, reading R-A27): K rounds, each one pass over X
+// plus three small kernels; with nranks > 1 three tiny allreduces per round
+// (max D2, the ranks' weight totals, the chosen row).
+kmeans_status kmeans_seed_pp(kmeans_handle* h, const double* u, float* C_out, int64_t* idx_out) {
+    LIVE(h);
+    const Dev& d = h->d;
+    const int K = d.K;
+    if (!u || !C_out) FAIL(h, KMEANS_ERR_INVALID, "NULL u or C_out");
+    for (int r = 0; r < K; ++r)
+        if (!(u[r] >= 0.0 && u[r] < 1.0)) FAIL(h, KMEANS_ERR_INVALID, "u outside [0, 1)");
+    cudaStream_t s = h->stream;
+    const long long N = h->n_global;
+    long long offset = 0;                               // this rank's first global row
+    if (h->nranks > 1) {
+        std::vector<long long> nl(h->nranks, 0);
+        nl[h->rank] = d.n;
+        CK(h, cudaMemcpyAsync(d.seed_T, nl.data(), 8 * h->nranks, cudaMemcpyHostToDevice, s));
+        NK(h, ncclAllReduce(d.seed_T, d.seed_T, h->nranks, ncclInt64, ncclSum, h->comm, s));
+        CK(h, cudaMemcpyAsync(nl.data(), d.seed_T, 8 * h->nranks, cudaMemcpyDeviceToHost, s));
+        CK(h, cudaStreamSynchronize(s));
+        for (int q = 0; q < h->rank; ++q) offset += nl[q];
+    }
+    CK(h, cudaMemcpyAsync(d.seed_u, u, 8 * (size_t)K, cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemsetAsync(&d.st->seed_max, 0, 16, s));   // seed_max, seed_err
+    const double a = h->x_gamax;
+    int e = 0;
+    if (a > 0.0) frexp(4.0 * a * a, &e);                 // (2 max|x|)^2 < 2^e
+    const double scale = ldexp(1.0, 50 - e);
+    int log2n = 0;
+    while ((1LL << log2n) < N) ++log2n;
+    long long i0 = (long long)floor(u[0] * (double)N);
+    if (i0 > N - 1) i0 = N - 1;
+    const long long loc = (i0 >= offset && i0 < offset + d.n) ? i0 - offset : -1;
+    launch_seed_first(d, loc, i0, s);
+    if (h->nranks > 1) NK(h, ncclAllReduce(d.seed_x, d.seed_x, d.d + 2, ncclInt32, ncclSum, h->comm, s));
+    launch_seed_commit(d, C_out, 0, s);
+    h->launches += 2;
+    for (int r = 1; r < K; ++r) {
+        launch_seed_dist(d, C_out + (long long)(r - 1) * d.d, r == 1, scale, s);
+        if (h->nranks > 1)
+            NK(h, ncclAllReduce(&d.st->seed_max, &d.st->seed_max, 1, ncclInt64, ncclMax, h->comm, s));
+        launch_seed_weights(d, log2n, h->rank, h->nranks, s);
+        if (h->nranks > 1) NK(h, ncclAllReduce(d.seed_T, d.seed_T, h->nranks, ncclInt64, ncclSum, h->comm, s));
+        launch_seed_select(d, r, log2n, h->rank, h->nranks, offset, s);
+        if (h->nranks > 1) NK(h, ncclAllReduce(d.seed_x, d.seed_x, d.d + 2, ncclInt32, ncclSum, h->comm, s));
+        launch_seed_commit(d, C_out, r, s);
+        h->launches += 5;
+        if ((r & 255) == 0) CK(h, cudaGetLastError());
+    }
+    int err = 0;
+    CK(h, cudaMemcpyAsync(&err, &d.st->seed_err, 4, cudaMemcpyDeviceToHost, s));
+    if (idx_out) CK(h, cudaMemcpyAsync(idx_out, d.seed_idx, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    CK(h, cudaGetLastError());
+    if (err) FAIL(h, KMEANS_ERR_INVALID, "fewer distinct samples than K (every remaining D^2 is 0)");
+    return KMEANS_OK;
+}
 
 kmeans_status kmeans_bounded_stats(kmeans_handle* h, int64_t* rows_scored, int64_t* rows_total) {
     LIVE(h);

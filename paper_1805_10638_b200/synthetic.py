@@ -193,3 +193,10 @@ def shard_bounds(N: int, rank: int, world: int):
     q, r = divmod(N, world)
     lo = rank * q + min(rank, r)
     return lo, lo + q + (1 if rank < r else 0)
+
+
+def seed_uniforms(cfg: str, K: int, seed: int = 0) -> np.ndarray:
+    """K uniforms in [0, 1) for K-Means++ seeding (kmeans_seed_pp / oracle.seed_pp),
+    from their own stream (3) of the config's seed sequence."""
+    return _rng(cfg, seed, 3).random(K)
+

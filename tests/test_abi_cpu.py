@@ -44,7 +44,7 @@ def test_links_wheel_nccl_only(L):
 
 
 def test_abi_version_and_defaults(L):
-    assert L.kmeans_abi_version() == 2
+    assert L.kmeans_abi_version() == 3
     c = aakm.Config()
     c.bounded = 7
     assert L.kmeans_config_default(ct.byref(c)) == 0
