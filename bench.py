@@ -189,6 +189,40 @@ def time_to_converge(cfgname, rank, world, barrier):
     return out
 
 
+# --------------------------------------------------------------------- K-Means++ seeding (f3)
+def seed_pp_bench(cfgname, rank, world, barrier, peaks):
+    """kmeans_seed_pp for all K centers of the sharded config (C ABI, X resident),
+    CUDA events around the call, max over ranks. Per center one pass over X
+    (k_seed_dist: X + D2 read/write) and one over D2 (k_seed_weights): the
+    algorithmic bytes are n (4d + 24) per center."""
+    import torch
+    import torch.distributed as dist
+    from paper_1805_10638_b200 import aakm, synthetic
+    X, _, cfg = synthetic.make_shard(cfgname, rank, world, seed=0)
+    Xs = torch.from_numpy(X).cuda()
+    km = aakm.KMeans(Xs, cfg.K, aakm.config(), n_global=cfg.N, rank=rank, nranks=world)
+    u = synthetic.seed_uniforms(cfgname, cfg.K)
+    barrier()
+    L0 = km.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(km.stream)
+    _, idx = km.seed_pp(u)
+    e1.record(km.stream)
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    launches = km.launch_count() - L0
+    km.close()
+    n = X.shape[0]
+    gbs = cfg.K * n * (4.0 * cfg.d + 24.0) / sec / 1e9
+    return {"config": cfgname, "N": cfg.N, "d": cfg.d, "K": cfg.K, "seconds": sec,
+            "centers_per_s": cfg.K / sec, "gpu_launches": launches,
+            "hbm_gbs_algorithmic": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+            "first_indices": [int(v) for v in idx[:4]]}
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -201,6 +235,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ttc-config", default="c4", help="config run to convergence for time_to_converge ('none' skips)")
+    ap.add_argument("--seed-config", default="c5", help="config seeded by kmeans_seed_pp for seed_pp ('none' skips)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -326,6 +361,8 @@ def main():
     km.close()
     if args.ttc_config != "none":
         line["time_to_converge"] = time_to_converge(args.ttc_config, rank, world, barrier)
+    if args.seed_config != "none":
+        line["seed_pp"] = seed_pp_bench(args.seed_config, rank, world, barrier, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(X, C0, args.config)
     if rank == 0:

@@ -151,6 +151,7 @@ void tc_free_maps(void* m);
 // (the update's segmented sums); false if d is not a multiple of 4 in [4, 128].
 bool encode_gather_rows(void* map128, const float* X, long long n, int d);
 // K-Means++ seeding (seed.cu)
+cudaError_t setup_seed();
 int seed_blocks(const Dev& d);
 void launch_seed_first(const Dev& d, long long row_local, long long gi, cudaStream_t s);
 void launch_seed_dist(const Dev& d, const float* c, int first, double scale, cudaStream_t s);

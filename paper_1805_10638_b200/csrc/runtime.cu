@@ -180,7 +180,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.seg_cmap = take(((size_t)n / 256 + K + 1) * 16);
     L.perm = take((size_t)n * 4 + 4);
     L.xg_map = take(128);
-    L.seed_d2 = take((size_t)n * 8 + 8);
+    L.seed_d2 = take((size_t)n * 8 + 16);           // + the 16-B tail of a bulk-copied odd run
     L.seed_part = take((size_t)AAKM_SEED_BLOCKS * 8);
     L.seed_T = take((size_t)AAKM_MAX_RANKS * 8);
     L.seed_x = take((size_t)(d + 2) * 4);
@@ -492,7 +492,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     {
         static bool once = false;
         if (!once) {
-            CKC(setup_simt()); CKC(setup_refine()); CKC(setup_update()); CKC(setup_tc());
+            CKC(setup_simt()); CKC(setup_refine()); CKC(setup_update()); CKC(setup_tc()); CKC(setup_seed());
             once = true;
         }
     }

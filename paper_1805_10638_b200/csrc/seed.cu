@@ -23,12 +23,14 @@ namespace aakm {
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ long long seed_term(float x, double c, double scale) {
     const double df = __dsub_rn((double)x, c);
-    const double v = __dmul_rn(__dmul_rn(df, df), scale);               // exact power-of-two scaling
-    return __double_as_longlong(__dadd_rn(v, 6755399441055744.0)) - 0x4338000000000000LL;   // rint, v < 2^51
+    // rint(fl(df^2) 2^t): the scaling is exact, so one fma with 1.5 2^52 rounds
+    // fl(df^2) 2^t to the nearest integer (< 2^51) exactly as the oracle's nearbyint
+    const double v = __fma_rn(__dmul_rn(df, df), scale, 6755399441055744.0);
+    return __double_as_longlong(v) - 0x4338000000000000LL;
 }
 
 __device__ __forceinline__ void seed_block_rows(long long n, int nb, int b, long long& r0, long long& r1) {
-    const long long per = (n + nb - 1) / nb;
+    const long long per = ((n + nb - 1) / nb + 15) / 16 * 16;       // multiples of 16 rows (16-B aligned D2 runs)
     r0 = min(n, (long long)b * per);
     r1 = min(n, r0 + per);
 }
@@ -45,31 +47,96 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 // ---------------------------------------------------------------- k_seed_dist
 // D2_i = min(D2_i, dist_i(c)) for the newest center c = C_out[r] (first round:
 // D2_i = dist_i(c)), and the block maxima -> atomicMax(seed_max).
-// float4 layout: LPR = d/4 lanes per row, RPW = 32/LPR rows per warp step.
+// A block's rows are contiguous, so thread 0 streams them (and their D2) into a
+// SEED_NS-deep shared-memory ring with 1-D bulk copies (16 KB of X per stage,
+// mbarrier completion); the 8 warps read rows from shared memory: LPR = d/4
+// lanes per row (float4 each), RPW = 32/LPR rows per instruction.
+constexpr int SEED_STAGE = 16384;
+constexpr int SEED_NS = 4;
+
+template <int LPR> struct SeedRing {
+    static constexpr int RB = 16 * LPR;
+    static constexpr int TR = SEED_STAGE / RB;                        // rows per stage
+    static constexpr int SLOT = SEED_STAGE + TR * 8;                  // X rows + their D2
+    static constexpr int SMEM = SEED_NS * SLOT + SEED_NS * 8;
+};
+
+__device__ __forceinline__ void sd_wait(uint64_t* bar, unsigned phase) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(a), "r"(phase) : "memory");
+    }
+}
+__device__ __forceinline__ void sd_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                   "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
 template <int LPR>
 __global__ void __launch_bounds__(256) k_seed_dist(Dev d, const float* c, int first, double scale, int nb) {
     if (d.st->seed_err) return;
-    constexpr int RPW = 32 / LPR;
+    using SR = SeedRing<LPR>;
+    constexpr int RB = SR::RB, TR = SR::TR, RPW = 32 / LPR;
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + SEED_NS * SR::SLOT);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int h = lane / LPR, c4i = lane % LPR;
-    const float4 cf = reinterpret_cast<const float4*>(c)[c4i];
-    const double c0 = cf.x, c1 = cf.y, c2 = cf.z, c3 = cf.w;
     long long r0, r1;
     seed_block_rows(d.n, nb, blockIdx.x, r0, r1);
+    const int nst = (int)((r1 - r0 + TR - 1) / TR);
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < SEED_NS; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(full + q)) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    const char* Xb = reinterpret_cast<const char*>(d.X);
+    auto issue = [&](int st) {                                         // thread 0 only
+        const long long a = r0 + (long long)st * TR;
+        const int rows = (int)min((long long)TR, r1 - a);
+        unsigned char* slot = sm + (st % SEED_NS) * SR::SLOT;
+        uint64_t* b = full + st % SEED_NS;
+        const unsigned xb = (unsigned)(rows * RB);
+        const unsigned db = first ? 0u : (unsigned)((rows * 8 + 15) & ~15);   // r0 is a multiple of 16 rows
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(xb + db) : "memory");
+        sd_copy(slot, Xb + a * RB, xb, b);
+        if (db) sd_copy(slot + SEED_STAGE, d.seed_d2 + a, db, b);
+    };
+    if (threadIdx.x == 0)
+        for (int st = 0; st < min(SEED_NS, nst); ++st) issue(st);
+    const float4 cf = reinterpret_cast<const float4*>(c)[c4i];
+    const double c0 = cf.x, c1 = cf.y, c2 = cf.z, c3 = cf.w;
     long long mx = 0;
-    const float4* X4 = reinterpret_cast<const float4*>(d.X);
-    for (long long base = r0 + (long long)warp * RPW; base < r1; base += (long long)nw * RPW) {
-        const long long row = base + h;
-        const bool ok = row < r1;
-        const float4 x = ok ? __ldcs(X4 + row * LPR + c4i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        long long s = seed_term(x.x, c0, scale) + seed_term(x.y, c1, scale) +
-                      seed_term(x.z, c2, scale) + seed_term(x.w, c3, scale);
+    for (int st = 0; st < nst; ++st) {
+        const int q = st % SEED_NS;
+        sd_wait(full + q, (unsigned)(st / SEED_NS) & 1u);
+        const unsigned char* slot = sm + q * SR::SLOT;
+        const long long* d2s = reinterpret_cast<const long long*>(slot + SEED_STAGE);
+        const long long a = r0 + (long long)st * TR;
+        const int rows = (int)min((long long)TR, r1 - a);
+#pragma unroll 4
+        for (int ib = warp * RPW; ib < TR; ib += nw * RPW) {           // uniform trip count
+            const int i = ib + h;
+            const bool ok = i < rows;
+            const float4 x = *reinterpret_cast<const float4*>(slot + (ok ? i : 0) * RB + 16 * c4i);
+            long long s = seed_term(x.x, c0, scale) + seed_term(x.y, c1, scale) +
+                          seed_term(x.z, c2, scale) + seed_term(x.w, c3, scale);
 #pragma unroll
-        for (int o = 1; o < LPR; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (ok && c4i == 0) {
-            const long long v = first ? s : min(s, d.seed_d2[row]);
-            d.seed_d2[row] = v;
-            mx = max(mx, v);
+            for (int o = 1; o < LPR; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (ok && c4i == 0) {
+                const long long v = first ? s : min(s, d2s[i]);
+                d.seed_d2[a + i] = v;
+                mx = max(mx, v);
+            }
+        }
+        __syncthreads();                                               // the slot is consumed
+        if (threadIdx.x == 0 && st + SEED_NS < nst) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(st + SEED_NS);
         }
     }
     mx = warp_max_ll(mx);
@@ -264,6 +331,15 @@ __global__ void k_seed_commit(Dev d, float* C_out, int r) {
 }
 
 // ---------------------------------------------------------------- launchers
+template <int LPR> static cudaError_t seed_attr() {
+    return cudaFuncSetAttribute(k_seed_dist<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SeedRing<LPR>::SMEM);
+}
+cudaError_t setup_seed() {
+    for (cudaError_t e : {seed_attr<1>(), seed_attr<2>(), seed_attr<4>(), seed_attr<8>(), seed_attr<16>(), seed_attr<32>()})
+        if (e != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
 int seed_blocks(const Dev& d) {
     long long nb = (d.n + 4095) / 4096;
     if (nb > AAKM_SEED_BLOCKS) nb = AAKM_SEED_BLOCKS;
@@ -279,12 +355,12 @@ void launch_seed_dist(const Dev& d, const float* c, int first, double scale, cud
     const int lpr = d.d / 4;
     if (d.d % 4 == 0 && lpr <= 32 && (lpr & (lpr - 1)) == 0) {
         switch (lpr) {
-            case 1: k_seed_dist<1><<<nb, 256, 0, s>>>(d, c, first, scale, nb); return;
-            case 2: k_seed_dist<2><<<nb, 256, 0, s>>>(d, c, first, scale, nb); return;
-            case 4: k_seed_dist<4><<<nb, 256, 0, s>>>(d, c, first, scale, nb); return;
-            case 8: k_seed_dist<8><<<nb, 256, 0, s>>>(d, c, first, scale, nb); return;
-            case 16: k_seed_dist<16><<<nb, 256, 0, s>>>(d, c, first, scale, nb); return;
-            default: k_seed_dist<32><<<nb, 256, 0, s>>>(d, c, first, scale, nb); return;
+            case 1: k_seed_dist<1><<<nb, 256, SeedRing<1>::SMEM, s>>>(d, c, first, scale, nb); return;
+            case 2: k_seed_dist<2><<<nb, 256, SeedRing<2>::SMEM, s>>>(d, c, first, scale, nb); return;
+            case 4: k_seed_dist<4><<<nb, 256, SeedRing<4>::SMEM, s>>>(d, c, first, scale, nb); return;
+            case 8: k_seed_dist<8><<<nb, 256, SeedRing<8>::SMEM, s>>>(d, c, first, scale, nb); return;
+            case 16: k_seed_dist<16><<<nb, 256, SeedRing<16>::SMEM, s>>>(d, c, first, scale, nb); return;
+            default: k_seed_dist<32><<<nb, 256, SeedRing<32>::SMEM, s>>>(d, c, first, scale, nb); return;
         }
     }
     k_seed_dist_any<<<nb, 256, 0, s>>>(d, c, first, scale, nb);
