@@ -239,6 +239,20 @@ AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *l
 AAKM_API kmeans_status kmeans_seed_pp(kmeans_handle *h, const double *u /*host*/, float *C_out,
                                       int64_t *idx_out /*host*/);
 
+/* One loop pass of Algorithm 1 (as kmeans_aa_step(h, NULL, info, theta))
+ * whose input X is first refreshed from host memory: X_host (host, pinned
+ * for overlap; n_local x d fp32 row-major) is copied into the device buffer
+ * given to kmeans_create (which this call overwrites) in `chunks` row blocks
+ * (clamped to [1, 64]) on a private copy stream, and the dense tensor-core
+ * assignment starts on each block as soon as it has landed, so the transfer
+ * overlaps the contraction. Other engines (SIMT, cfg.bounded) copy first,
+ * then run the pass. Requires a started run (kmeans_aa_step with C0).
+ * Asynchronous unless info/theta are requested; X_host must stay valid until
+ * the stream has passed this call. Collective when nranks > 1. Errors: INVALID
+ * for a NULL X_host with n_local > 0. */
+AAKM_API kmeans_status kmeans_aa_step_host(kmeans_handle *h, const float *X_host /*host*/, int32_t chunks,
+                                           kmeans_step_info *info /*host*/, double *theta_out /*host*/);
+
 /* Sum of CUDA-event durations (ms) of the assignment launches recorded since
  * the last call (config.timing = 1), and their count.  Synchronises. */
 AAKM_API kmeans_status kmeans_assign_timing(kmeans_handle *h, double *ms_total /*host*/,

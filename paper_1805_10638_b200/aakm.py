@@ -90,6 +90,7 @@ def lib():
                 "kmeans_last_flagged": ([P, ct.POINTER(I64)], I32),
                 "kmeans_bounded_stats": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
                 "kmeans_seed_pp": ([P, P, P, P], I32),
+                "kmeans_aa_step_host": ([P, P, I32, P, P], I32),
                 "kmeans_assign_path_name": ([P], ct.c_char_p),
                 "kmeans_destroy": ([P], I32),
                 "kmeans_last_error": ([P], ct.c_char_p),
@@ -241,6 +242,26 @@ class KMeans:
         inf = StepInfo()
         theta = (ct.c_double * KMEANS_M_MAX)()
         self._c(lib().kmeans_aa_step(self.h, _ptr(C0), ct.byref(inf), theta))
+        r = _struct(inf)
+        r["theta"] = list(theta)[: r["m_t"]]
+        return r
+
+    def aa_step_host(self, X_host, chunks=8, info=True):
+        """One loop pass with X refreshed from host memory (kmeans_aa_step_host):
+        X_host is a CPU float32 tensor of this handle's shape (pin it for overlap);
+        the copy streams in `chunks` row blocks under the assignment."""
+        t = self.torch
+        if not isinstance(X_host, t.Tensor) or X_host.device.type != "cpu":
+            raise TypeError("X_host must be a CPU torch tensor")
+        if X_host.dtype != t.float32 or not X_host.is_contiguous() or tuple(X_host.shape) != (self.n, self.d):
+            raise ValueError("X_host must be a contiguous float32 (n_local, d) tensor")
+        self._keep_host = X_host                    # valid until the stream passes this call
+        if not info:
+            self._c(lib().kmeans_aa_step_host(self.h, ct.c_void_p(X_host.data_ptr()), int(chunks), None, None))
+            return None
+        inf = StepInfo()
+        theta = (ct.c_double * KMEANS_M_MAX)()
+        self._c(lib().kmeans_aa_step_host(self.h, ct.c_void_p(X_host.data_ptr()), int(chunks), ct.byref(inf), theta))
         r = _struct(inf)
         r["theta"] = list(theta)[: r["m_t"]]
         return r

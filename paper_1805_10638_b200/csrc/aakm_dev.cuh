@@ -132,6 +132,7 @@ struct GEval {
     const int* lab_prev;  // used when prev_mode == 2
     int prev_mode;        // 0 = d.lab[st->cur ^ 1], 1 = none, 2 = lab_prev
     long long* packed_out;// nullptr -> d.packed[branch]
+    long long tile0, tile1;  // MODE 0 dense engine: row tiles [tile0, tile1) only (tile1 = 0: all)
 };
 
 __device__ __forceinline__ bool geval_active(const Dev& d, const GEval& g) {

@@ -395,11 +395,14 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     if (CG == 2) cluster_sync(); else __syncthreads();              // barrier inits visible to the peer
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const long long n_tiles = (n_rows + TC_BM - 1) / TC_BM;
-    // pair p processes row tiles (p + it * P) * CG + rank; both CTAs run the same
-    // iteration count (a partner past the end works on an all-OOB tile: zeros, no output)
+    long long n_tiles = (n_rows + TC_BM - 1) / TC_BM;
+    long long tbase = 0;                                            // MODE 0 row-tile range (streamed X)
+    if (MODE == 0 && g.tile1 > 0) { tbase = g.tile0; n_tiles = min(n_tiles, g.tile1) - g.tile0; }
+    // pair p processes row tiles tbase + (p + it * P) * CG + rank; both CTAs run the same
+    // iteration count (a partner past the end works on an all-OOB tile: zeros, no output;
+    // streamed ranges hold an even number of tiles except the last)
     const long long pair0 = blockIdx.x / CG, npairs = gridDim.x / CG;
-    auto tile_of = [&](long long it) { return (pair0 + it * npairs) * CG + rank; };
+    auto tile_of = [&](long long it) { return tbase + (pair0 + it * npairs) * CG + rank; };
     auto live = [&](long long it) { return (pair0 + it * npairs) * CG < n_tiles; };
     // the leader's copy of a barrier (cluster address) -- where remote arrivals go
     auto lead = [&](uint64_t* b) { return CG == 2 ? mapa0(su32(b)) : su32(b); };
@@ -972,7 +975,8 @@ static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStre
     const size_t smem = smem_need(KIND, A, S, NT, NXB, CG);
     const int xr = xr_of(NT, NXB, CG);
     const CUtensorMap& xm = MODE == 1 ? m->xf : m->x;
-    const long long n_tiles = MODE == 0 ? (d.n + TC_BM - 1) / TC_BM : 1ll << 40;
+    long long n_tiles = MODE == 0 ? (d.n + TC_BM - 1) / TC_BM : 1ll << 40;
+    if (MODE == 0 && g.tile1 > 0) n_tiles = min(n_tiles, g.tile1) - g.tile0;
     if constexpr (KIND == 0) {
         switch (A) {
             case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;

@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/aakm.h"
@@ -46,6 +47,12 @@ struct kmeans_handle {
     TraceRec* tr_host = nullptr;                             // pinned
     double* scal_host = nullptr;                             // pinned (E, changed)
     float x_gamax = 0.f;                                     // max |x_ik| over all ranks (K-Means++ scale)
+    // streamed X (kmeans_aa_step_host): H2D row chunks on copy_stream, one event each
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> feed_ev;
+    cudaEvent_t feed_gate = nullptr, feed_all = nullptr;
+    int feed_chunks = 0;                                     // > 0 while a streamed pass is enqueued
+    long long feed_tiles = 0;                                // row tiles per chunk (even)
     cudaEvent_t run_ev[2] = {nullptr, nullptr};
     int* done_host = nullptr;                                // pinned
 };
@@ -287,7 +294,20 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     GEval g{};
     g.branch = branch; g.force = 0; g.prev_mode = 0;
     if (branch == 1) { combine(h, d, 1, nullptr, s); dbg("combine_fb", s); }
-    kmeans_status st = timed_assign(h, d, g, s, timing && branch == 0);
+    kmeans_status st = KMEANS_OK;
+    if (branch == 0 && h->feed_chunks > 0) {                // streamed X: each row chunk once it landed
+        const long long T = (d.n + 127) / 128;
+        for (int c = 0; c < h->feed_chunks; ++c) {
+            CK(h, cudaStreamWaitEvent(s, h->feed_ev[c], 0));
+            GEval gc = g;
+            gc.tile0 = c * h->feed_tiles;
+            gc.tile1 = std::min(T, (c + 1) * h->feed_tiles);
+            launch_assign_tc(d, gc, h->tcm, s);
+        }
+        h->launches += h->feed_chunks - 1;
+    } else {
+        st = timed_assign(h, d, g, s, timing && branch == 0);
+    }
     if (st != KMEANS_OK) return st;
     dbg("assign", s);
     refine_engine(h, d, g, s);
@@ -676,12 +696,7 @@ static void fill_info(kmeans_handle* h, kmeans_step_info* info, double* theta) {
     }
 }
 
-kmeans_status kmeans_aa_step(kmeans_handle* h, const float* C0, kmeans_step_info* info, double* theta_out) {
-    LIVE(h);
-    kmeans_status st;
-    if (C0) st = start(h, C0);
-    else st = enqueue_pass(h, h->stream, h->cfg.timing != 0);
-    if (st != KMEANS_OK) return st;
+static kmeans_status step_info(kmeans_handle* h, kmeans_step_info* info, double* theta_out) {
     if (info || theta_out) {
         cudaStream_t s = h->stream;
         CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -692,6 +707,62 @@ kmeans_status kmeans_aa_step(kmeans_handle* h, const float* C0, kmeans_step_info
         fill_info(h, info, theta_out);
     }
     return KMEANS_OK;
+}
+
+kmeans_status kmeans_aa_step(kmeans_handle* h, const float* C0, kmeans_step_info* info, double* theta_out) {
+    LIVE(h);
+    kmeans_status st;
+    if (C0) st = start(h, C0);
+    else st = enqueue_pass(h, h->stream, h->cfg.timing != 0);
+    if (st != KMEANS_OK) return st;
+    return step_info(h, info, theta_out);
+}
+
+// One loop pass with X refreshed from pinned host memory: the H2D copy runs in
+// row chunks on a copy stream and the dense tensor-core assignment consumes
+// each chunk as it lands, so the transfer overlaps the contraction.
+kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t chunks, kmeans_step_info* info,
+                                  double* theta_out) {
+    LIVE(h);
+    const Dev& d = h->d;
+    if (!X_host && d.n > 0) FAIL(h, KMEANS_ERR_INVALID, "X_host is NULL");
+    if (chunks < 1) chunks = 1;
+    if (chunks > 64) chunks = 64;
+    cudaStream_t s = h->stream;
+    if (!h->copy_stream) {
+        CK(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        CK(h, cudaEventCreateWithFlags(&h->feed_gate, cudaEventDisableTiming));
+        CK(h, cudaEventCreateWithFlags(&h->feed_all, cudaEventDisableTiming));
+        h->feed_ev.resize(64);
+        for (auto& e : h->feed_ev) CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const long long T = (d.n + 127) / 128;
+    const long long ct = ((T + chunks - 1) / chunks + 1) & ~1LL;      // even: CTA pairs stay inside a chunk
+    const int nc = T > 0 ? (int)((T + ct - 1) / ct) : 0;
+    CK(h, cudaEventRecord(h->feed_gate, s));                           // earlier work on X is done
+    CK(h, cudaStreamWaitEvent(h->copy_stream, h->feed_gate, 0));
+    float* X = const_cast<float*>(d.X);
+    for (int c = 0; c < nc; ++c) {
+        const long long r0 = c * ct * 128, r1 = std::min(d.n, (c + 1) * ct * 128);
+        CK(h, cudaMemcpyAsync(X + r0 * d.d, X_host + r0 * d.d, (size_t)(r1 - r0) * d.d * 4, cudaMemcpyHostToDevice,
+                              h->copy_stream));
+        CK(h, cudaEventRecord(h->feed_ev[c], h->copy_stream));
+    }
+    CK(h, cudaEventRecord(h->feed_all, h->copy_stream));
+    const bool streamed = nc > 0 && !d.ub && (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16);
+    if (!streamed) {
+        CK(h, cudaStreamWaitEvent(s, h->feed_all, 0));
+        kmeans_status st = enqueue_pass(h, s, h->cfg.timing != 0);
+        if (st != KMEANS_OK) return st;
+        return step_info(h, info, theta_out);
+    }
+    h->feed_chunks = nc;
+    h->feed_tiles = ct;
+    kmeans_status st = enqueue_pass(h, s, false);
+    h->feed_chunks = 0;
+    CK(h, cudaStreamWaitEvent(s, h->feed_all, 0));
+    if (st != KMEANS_OK) return st;
+    return step_info(h, info, theta_out);
 }
 
 kmeans_status kmeans_run(kmeans_handle* h, const float* C0, float* C_out, int32_t* labels_out, kmeans_report* rep) {
@@ -948,6 +1019,13 @@ kmeans_status kmeans_destroy(kmeans_handle* h) {
     if (!h->poisoned) cudaStreamSynchronize(h->stream);
     if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    if (h->copy_stream) {
+        if (!h->poisoned) cudaStreamSynchronize(h->copy_stream);
+        cudaStreamDestroy(h->copy_stream);
+        for (auto e : h->feed_ev) cudaEventDestroy(e);
+        cudaEventDestroy(h->feed_gate);
+        cudaEventDestroy(h->feed_all);
+    }
     if (h->tcm) tc_free_maps(h->tcm);
     if (h->tcm_api) tc_free_maps(h->tcm_api);
     for (auto& e : h->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }

@@ -20,6 +20,8 @@ import concurrent.futures as cf
 import dataclasses
 import os
 
+import threading
+
 import numpy as np
 
 TAG = 180510638
@@ -44,6 +46,11 @@ CONFIGS = {
     "c5": Config("c5", 16_000_000, 64, 4096, well_separated=False),
 }
 CFG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
+
+
+# numpy's BLAS (OpenBLAS) corrupted c4 rows when the chunk threads multiplied
+# concurrently (different bytes run to run); the matmuls are serialised.
+_BLAS_LOCK = threading.Lock()
 
 
 def _rng(cfg: str, seed: int, *stream):
@@ -112,8 +119,10 @@ def _chunk(cfg: str, seed: int, c: int, r0: int, r1: int, d: int, p: dict) -> np
         z = p["z"][r0:r1]
         a = r.standard_normal((n, 16))
         b = r.standard_normal((n, d))
-        off = b - (b @ Q) @ Q.T                               # (I - Q Q^T) b
-        x = p["mu"][z] + a @ Q.T + 0.1 * off
+        with _BLAS_LOCK:                                      # BLAS is not safe under concurrent callers here
+            off = b - (b @ Q) @ Q.T                           # (I - Q Q^T) b
+            aq = a @ Q.T
+        x = p["mu"][z] + aq + 0.1 * off
     elif cfg == "c5":
         return r.random((n, d), dtype=np.float32)
     return x.astype(np.float32)

@@ -259,3 +259,31 @@ def test_sorted_update_engine(d):
     np.testing.assert_array_equal(cnt2.cpu().numpy(), cnt)
     assert np.abs(G2.cpu().numpy() - G_ora.astype(np.float32)).max() <= 1e-6 * max(1.0, np.abs(G_ora).max())
     km.close()
+
+
+@pytest.mark.parametrize("cfg,N,K,chunks", [("c5", 70_000, 512, 8), ("c4", 33_000, 256, 3),
+                                            ("c3", 50_001, 64, 64), ("c2", None, None, 4)])
+def test_streamed_host_pass_matches_resident(cfg, N, K, chunks):
+    """kmeans_aa_step_host (X streamed from pinned host memory in row chunks under
+    the assignment) repeats the resident passes bit for bit, even when the device
+    copy of X was scrambled in between (the assignment must read the new rows)."""
+    X, C0, c = make(cfg, N=N, K=K)
+    a = aakm.KMeans(dev(X), c.K, aakm.config(m0=5))
+    a.aa_step(dev(C0))
+    ref = [a.aa_step() for _ in range(5)]
+    sa = a.state_export()
+    a.close()
+    Xd = dev(X)
+    b = aakm.KMeans(Xd, c.K, aakm.config(m0=5))
+    b.aa_step(dev(C0))
+    Xh = torch.from_numpy(X).pin_memory()
+    got = []
+    for _ in range(5):
+        Xd.copy_(torch.randn_like(Xd))               # stale device rows: the pass must wait for the copy
+        torch.cuda.synchronize()
+        got.append(b.aa_step_host(Xh, chunks=chunks))
+    sb = b.state_export()
+    b.close()
+    for x, y in zip(ref, got):
+        assert x == y, (x, y)
+    assert np.array_equal(sa["C"], sb["C"])
