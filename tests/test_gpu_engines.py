@@ -261,20 +261,21 @@ def test_sorted_update_engine(d):
     km.close()
 
 
-@pytest.mark.parametrize("cfg,N,K,chunks", [("c5", 70_000, 512, 8), ("c4", 33_000, 256, 3),
-                                            ("c3", 50_001, 64, 64), ("c2", None, None, 4)])
-def test_streamed_host_pass_matches_resident(cfg, N, K, chunks):
+@pytest.mark.parametrize("cfg,N,K,chunks,bounded", [("c5", 70_000, 512, 8, False), ("c4", 33_000, 256, 3, False),
+                                                    ("c3", 50_001, 64, 64, False), ("c2", None, None, 4, False),
+                                                    ("c5", 70_000, 512, 5, True)])
+def test_streamed_host_pass_matches_resident(cfg, N, K, chunks, bounded):
     """kmeans_aa_step_host (X streamed from pinned host memory in row chunks under
     the assignment) repeats the resident passes bit for bit, even when the device
     copy of X was scrambled in between (the assignment must read the new rows)."""
     X, C0, c = make(cfg, N=N, K=K)
-    a = aakm.KMeans(dev(X), c.K, aakm.config(m0=5))
+    a = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, bounded=bounded))
     a.aa_step(dev(C0))
     ref = [a.aa_step() for _ in range(5)]
     sa = a.state_export()
     a.close()
     Xd = dev(X)
-    b = aakm.KMeans(Xd, c.K, aakm.config(m0=5))
+    b = aakm.KMeans(Xd, c.K, aakm.config(m0=5, bounded=bounded))
     b.aa_step(dev(C0))
     Xh = torch.from_numpy(X).pin_memory()
     got = []
