@@ -273,8 +273,6 @@ __global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
         if (j < K) {
             d.seg_off[j] = (int)pa;
             d.seg_chunk[j] = (int)pb;
-            for (long long q = 0; q < nc; ++q)
-                d.seg_cmap[pb + q] = make_int4(j, (int)(pa + q * SEG_ROWS), (int)min((long long)SEG_ROWS, c - q * SEG_ROWS), 0);
         }
         if (threadIdx.x == blockDim.x - 1) { carry[0] = pa + c; carry[1] = pb + nc; }
         __syncthreads();
@@ -287,6 +285,18 @@ __global__ void __launch_bounds__(1024) k_scatter(Dev d, GEval g) {
     const Pick p = pick(d, g);
     extern __shared__ int cur[];
     const int K = d.K;
+    // chunk table {j, first sorted row, rows}: chunk w belongs to the last cluster
+    // whose first chunk is <= w (binary search; empty clusters share starts)
+    const long long nch = d.seg_chunk[K];
+    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < nch; w += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = K - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (d.seg_chunk[mid] <= w) lo = mid; else hi = mid - 1;
+        }
+        const long long r0 = d.seg_off[lo] + (w - d.seg_chunk[lo]) * SEG_ROWS;
+        d.seg_cmap[w] = make_int4(lo, (int)r0, (int)min((long long)SEG_ROWS, (long long)d.seg_off[lo + 1] - r0), 0);
+    }
     const int* bh = d.seg_bh + (long long)blockIdx.x * K;
     for (int j = threadIdx.x; j < K; j += blockDim.x) cur[j] = bh[j] + d.seg_off[j];
     __syncthreads();
