@@ -89,6 +89,9 @@ struct Dev {
     int* cand_cnt;        // candidate counts per flagged row and epilogue half (> AAKM_MAXC/2 = overflow)
     long long fcap;       // capacity of the candidate path (rows beyond -> SIMT refine)
     long long* flag_count;// [2] near-tie counts of branch A / B (zeroed per pass with packed)
+    int* pair_rows;       // near-tie rows whose window holds exactly two centroids (capacity fcap)
+    int2* pair_j;         //   their two centroids (best key, runner-up)
+    long long* pair_count;//   [2] counts, branch A / B (zeroed per pass with the flags)
     long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E_hi | E_lo | E (fp64 bits) | changed]
     float fx_scale;       // 2^(22-e), |x| <= 2^e over all ranks: S in exact fixed point (update.cu)
     double fx_inv;        // 2^(e-22)

@@ -219,6 +219,51 @@ __device__ __forceinline__ void push_flag_tc(const Dev& d, int branch, bool flag
     }
 }
 
+// Near-tie rows whose window [b1, b1 + tau] provably holds two centroids only
+// (best key i1 and runner-up i2): k_refine_pair decides them without the
+// candidate pass. Past the list's capacity they join the flag list.
+__device__ __forceinline__ void push_pair_tc(const Dev& d, int branch, bool pair, long long row, int i1, int i2,
+                                             float b1, float tau) {
+    unsigned mask = __ballot_sync(0xffffffffu, pair);
+    if (mask == 0) return;
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(mask) - 1;
+    long long base = 0;
+    if (lane == leader)
+        base = (long long)atomicAdd((unsigned long long*)&d.pair_count[branch], (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pair) {
+        const long long f = base + __popc(mask & ((1u << lane) - 1));
+        if (f < d.fcap) {
+            d.pair_rows[f] = (int)row;
+            d.pair_j[f] = make_int2(i1, i2);
+        } else {
+            const long long g = (long long)atomicAdd((unsigned long long*)&d.flag_count[branch], 1ull);
+            d.flag_rows[g] = (int)row;
+            if (g < d.fcap) { d.flag_b1[g] = b1; d.flag_tau[g] = tau; }
+        }
+    }
+}
+
+// Top-2 keys with indices plus a lower bound L on every other key, merged from
+// two such summaries (KIND 1 window keys: positive, order-preserving floats).
+// i2 = -1 when the runner-up's index is unknown (then L <= b2 as well).
+struct Top2L { float b1, b2, L; int i1, i2; };
+__device__ __forceinline__ void top2l_merge(Top2L& a, float v1, int j1, float v2, int j2, float Lv) {
+    const float t3 = fminf(fmaxf(a.b2, v1), fmaxf(a.b1, v2));       // third smallest of the four
+    a.L = fminf(fminf(a.L, Lv), t3);
+    if (v1 < a.b1 || (v1 == a.b1 && j1 < a.i1)) {
+        const bool ob = a.b1 <= v2;                                     // old best is the new runner-up
+        a.i2 = ob ? a.i1 : j2;
+        a.b2 = ob ? a.b1 : v2;
+        a.b1 = v1; a.i1 = j1;
+    } else {
+        const bool nv = v1 < a.b2;
+        a.i2 = nv ? j1 : a.i2;
+        a.b2 = nv ? v1 : a.b2;
+    }
+}
+
 // ---- CTA-pair (cta_group::2) helpers
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -701,29 +746,51 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 }
             }
             if (MODE != 1) {
-                // merge the trackers, then the column quarters (ties -> lower column index)
-                float b1 = B1[0], b2 = B2[0];
-                int i1 = BB[0] + (int)(__float_as_uint(B1[0]) & 31u);
+                // merge the trackers, then the column quarters (ties -> lower column index).
+                // KIND 1 also keeps the runner-up's index and a lower bound L on all other
+                // keys (a tracker's others are >= its B2), for the two-centroid fast path;
+                // a quarter hands (i2 >> 5) over in L's low 12 bits (L is only used
+                // with those bits cleared: a lower bound still).
+                Top2L t;
+                t.b1 = B1[0]; t.b2 = B2[0]; t.L = B2[0]; t.i2 = -1;
+                t.i1 = BB[0] + (int)(__float_as_uint(B1[0]) & 31u);
 #pragma unroll
                 for (int u = 1; u < NTRK; ++u) {
                     const int iu = BB[u] + (int)(__float_as_uint(B1[u]) & 31u);
-                    b2 = fminf(fminf(b2, B2[u]), fmaxf(b1, B1[u]));
-                    const bool tk = B1[u] < b1 || (B1[u] == b1 && iu < i1);
-                    i1 = tk ? iu : i1;
-                    b1 = fminf(b1, B1[u]);
+                    if (KIND) {
+                        top2l_merge(t, B1[u], iu, B2[u], -1, B2[u]);
+                    } else {
+                        t.b2 = fminf(fminf(t.b2, B2[u]), fmaxf(t.b1, B1[u]));
+                        const bool tk = B1[u] < t.b1 || (B1[u] == t.b1 && iu < t.i1);
+                        t.i1 = tk ? iu : t.i1;
+                        t.b1 = fminf(t.b1, B1[u]);
+                    }
                 }
-                if (cq > 0) mrg[(cq - 1) * TC_BM + r] = make_float4(b1, b2, __int_as_float(i1), 0.f);
+                if (cq > 0) {
+                    const unsigned hi = (KIND && t.i2 >= 0 && (t.i2 >> 5) < 0xFFF) ? (unsigned)(t.i2 >> 5) : 0xFFFu;
+                    const float Lp = __uint_as_float((__float_as_uint(t.L) & ~0xFFFu) | hi);
+                    mrg[(cq - 1) * TC_BM + r] = make_float4(t.b1, t.b2, __int_as_float(t.i1), Lp);
+                }
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");
                 if (cq == 0) {
+                    float b1, b2;
+                    int i1;
 #pragma unroll
                     for (int o = 0; o < NQ - 1; ++o) {
                         const float4 m = mrg[o * TC_BM + r];
                         const int oi1 = __float_as_int(m.z);
-                        b2 = fminf(fminf(b2, m.y), fmaxf(b1, m.x));
-                        const bool tk = m.x < b1 || (m.x == b1 && oi1 < i1);
-                        i1 = tk ? oi1 : i1;
-                        b1 = fminf(b1, m.x);
+                        if (KIND) {
+                            const unsigned hi = __float_as_uint(m.w) & 0xFFFu;
+                            const int oi2 = hi == 0xFFFu ? -1 : (int)(hi << 5) + (int)(__float_as_uint(m.y) & 31u);
+                            top2l_merge(t, m.x, oi1, m.y, oi2, __uint_as_float(__float_as_uint(m.w) & ~0xFFFu));
+                        } else {
+                            t.b2 = fminf(fminf(t.b2, m.y), fmaxf(t.b1, m.x));
+                            const bool tk = m.x < t.b1 || (m.x == t.b1 && oi1 < t.i1);
+                            t.i1 = tk ? oi1 : t.i1;
+                            t.b1 = fminf(t.b1, m.x);
+                        }
                     }
+                    b1 = t.b1; b2 = t.b2; i1 = t.i1;
                     const bool ok = frow < n_rows;
                     const long long row = (use_list && ok) ? (long long)d.act_rows[frow] : frow;
                     float tau;
@@ -738,6 +805,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         tau = Usc * (gam * (xn + 2.0f * cmax2) + tau_abs) + 7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
                     }
                     const bool flag = ok && (b2 - b1 <= tau);
+                    // two-centroid fast path: every key other than b1, b2 is >= L > b1 + tau,
+                    // so only i1 and i2 can be the exact argmin
+                    bool pair = false;
+                    if (KIND && flag && t.i2 >= 0 && K <= 131040)
+                        pair = wdecode(__uint_as_float(__float_as_uint(t.L) & ~0xFFFu)) > b1 + tau;
                     if (ok) lab_out[row] = i1;
                     if (KIND && ok && d.ub) {
                         // Hamerly bounds for the next assignment (distance units, rounded
@@ -751,7 +823,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         d.ub[row] = u;
                         d.lb[row] = l;
                     }
-                    push_flag_tc(d, g.branch, flag, row, b1, tau);
+                    push_flag_tc(d, g.branch, flag && !pair, row, b1, tau);
+                    if (KIND) push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
                 }
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
             } else if (frow < n_rows) {
@@ -1135,13 +1208,47 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
     }
 }
 
+// Exact fp64 decision between the two centroids of each two-centroid near-tie
+// row (the same arithmetic as k_refine_exact; lowest index on exact ties).
+__global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int D = d.d;
+    int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
+    long long np = d.pair_count[g.branch];
+    if (np > d.fcap) np = d.fcap;
+    for (long long f = (long long)blockIdx.x * 8 + warp; f < np; f += (long long)gridDim.x * 8) {
+        const long long row = d.pair_rows[f];
+        const int2 jj = d.pair_j[f];
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int k = lane + 32 * v;
+            if (k < D) {
+                const double x = (double)__ldg(d.X + row * D + k);
+                const double d0 = x - (double)__ldg(d.C + (long long)jj.x * D + k);
+                const double d1 = x - (double)__ldg(d.C + (long long)jj.y * D + k);
+                a0 = fma(d0, d0, a0);
+                a1 = fma(d1, d1, a1);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        if (lane == 0) lab_out[row] = (a1 < a0 || (a1 == a0 && jj.y < jj.x)) ? jj.y : jj.x;
+    }
+}
+
 int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
     // the 2xFP16 engine reads the flagged rows in place (DX splitter); 3xTF32 TMAs a gathered copy
     const int gather = d.tc_kind == 1 ? 0 : 1;
     if (gather) k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
     k_refine_exact<<<4 * g_num_sms, 256, 0, s>>>(d, g);
-    return 2 + gather;
+    if (d.tc_kind == 1) k_refine_pair<<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    return 2 + gather + (d.tc_kind == 1 ? 1 : 0);
 }
 
 }  // namespace aakm

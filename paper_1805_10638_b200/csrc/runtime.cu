@@ -139,7 +139,7 @@ static void dbg(const char* what, cudaStream_t s) {
 // ------------------------------------------------------------------ layout
 namespace {
 struct Layout {
-    size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt,
+    size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
         ub, lb, act_rows, C_ref, shift, total,
@@ -173,6 +173,8 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.Xf = take((size_t)fc * d * 4 + 16);
     L.cand = take((size_t)fc * AAKM_MAXC * 4 + 4);
     L.cand_cnt = take((size_t)fc * 16 + 16);
+    L.pair_rows = take((size_t)fc * 4 + 4);
+    L.pair_j = take((size_t)fc * 8 + 8);
     const size_t pk = (2 * KD + K + 4) * 8;     // [S_hi | S_lo | N | E_hi | E_lo | E | changed], int64 words (pk_words)
     L.scratch = o;
     size_t s0 = take(256);                 // flag counts
@@ -453,6 +455,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.fcap = fcap_of(n_local);
     D.flag_count = (long long*)(w + L.scratch);
     D.act_count = (long long*)(w + L.scratch + 32);                   // [2], zeroed per pass with the flags
+    D.pair_count = (long long*)(w + L.scratch + 64);                  // [2], likewise
+    D.pair_rows = (int*)(w + L.pair_rows); D.pair_j = (int2*)(w + L.pair_j);
     D.packed[0] = (long long*)(w + L.scratch + 256);
     D.packed[1] = (long long*)(w + L.packed1);
     D.upd_part = (double*)(w + L.upd_part);
@@ -1001,10 +1005,11 @@ kmeans_status kmeans_bounded_stats(kmeans_handle* h, int64_t* rows_scored, int64
 kmeans_status kmeans_last_flagged(kmeans_handle* h, int64_t* flagged) {
     LIVE(h);
     if (!flagged) return KMEANS_ERR_INVALID;
-    long long v[2];
+    long long v[2], pr[2];
     CK(h, cudaStreamSynchronize(h->stream));
     CK(h, cudaMemcpy(v, h->d.flag_count, 16, cudaMemcpyDeviceToHost));
-    *flagged = v[0];
+    CK(h, cudaMemcpy(pr, h->d.pair_count, 16, cudaMemcpyDeviceToHost));
+    *flagged = v[0] + pr[0];                            // candidate-pass rows + two-centroid rows
     return KMEANS_OK;
 }
 
