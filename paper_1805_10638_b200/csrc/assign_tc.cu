@@ -304,6 +304,11 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];"
                  ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1) : "memory");
 }
+// L2 prefetch of 4 gathered rows through the {d, 1}-box map of X (d.xg_map)
+__device__ __forceinline__ void tma_prefetch_gather4(const void* map, int r0, int r1, int r2, int r3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+}
 template <int KIND, int CG>
 __device__ __forceinline__ void mma_cg(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum, uint32_t idesc) {
     if (CG == 2) {
@@ -546,10 +551,23 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         // DX candidate pass (MODE 1): the flagged rows are read in place through the
         // flag list (no gathered copy), so there is nothing to prefetch by TMA
         const float* Xsrc = (MODE == 0 || DX) ? d.X : d.Xf;
+        // gathered rows (candidate pass, bounded list): the first splitter warp
+        // prefetches the next tile's rows into L2 with TMA gather4 (4 rows per lane)
+        auto prefetch_list = [&](long long itn) {
+            if (!(DX && (MODE == 1 || use_list) && d.xg_map && t < 32 && live(itn))) return;
+            const long long g0 = tile_of(itn) * TC_BM + 4 * t;
+            if (g0 >= n_rows) return;
+            const int4 rw = *reinterpret_cast<const int4*>(rows_of + g0);
+            const long long last = n_rows - 1 - g0;                      // rows past the list repeat the last one
+            tma_prefetch_gather4(d.xg_map, rw.x, last >= 1 ? rw.y : rw.x, last >= 2 ? rw.z : rw.x,
+                                 last >= 3 ? rw.w : rw.x);
+        };
+        prefetch_list(0);
         for (long long it = 0; live(it); ++it) {
             if (DX) {
                 if (MODE != 1 && !use_list && t == 0 && live(it + 1))   // next row tile -> L2
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(it + 1) * TC_BM));
+                prefetch_list(it + 1);
             } else {
                 mbar_wait_sleep(stfull, sph, 128);
                 sph ^= 1;
