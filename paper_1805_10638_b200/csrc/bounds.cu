@@ -72,31 +72,51 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
     // labels the bounds refer to: the previous pass's final labels (branch A), or
     // branch A's labels of this pass (branch B assigns the fallback after it)
     const int* lab_ref = g.branch == 0 ? d.lab[cur ^ 1] : lab_out;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long n = d.n;
-    for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
-        const long long i = i0 + threadIdx.x;
-        bool unsafe = false;
-        if (i < n) {
-            const int a = lab_ref[i];
-            const float u = __fadd_ru(d.ub[i], d.shift[a]);
-            const float l = __fsub_rd(d.lb[i], smax);
-            if (u < l) {
-                d.ub[i] = u;
-                d.lb[i] = l;
-                if (g.branch == 0) lab_out[i] = a;
-            } else {
-                unsafe = true;
+    // 1024 rows per block step (4 consecutive rows per thread); the unproven rows of
+    // a step are appended with ONE atomic per block step, in row order within it
+    __shared__ int wcnt[8];
+    __shared__ long long sbase;
+    constexpr int RPT = 4;
+    const long long step = (long long)blockDim.x * RPT;
+    for (long long i0 = (long long)blockIdx.x * step; i0 < n; i0 += (long long)gridDim.x * step) {
+        const long long ib = i0 + (long long)threadIdx.x * RPT;
+        unsigned um = 0;                                        // bit k: row ib + k unproven
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const long long i = ib + k;
+            if (i < n) {
+                const int a = lab_ref[i];
+                const float u = __fadd_ru(d.ub[i], d.shift[a]);
+                const float l = __fsub_rd(d.lb[i], smax);
+                if (u < l) {
+                    d.ub[i] = u;
+                    d.lb[i] = l;
+                    if (g.branch == 0) lab_out[i] = a;
+                } else {
+                    um |= 1u << k;
+                }
             }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, unsafe);
-        if (m) {
-            long long base = 0;
-            if (lane == 0) base = (long long)atomicAdd((unsigned long long*)&d.act_count[g.branch],
-                                                       (unsigned long long)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (unsafe) d.act_rows[base + __popc(m & ((1u << lane) - 1))] = (int)i;
+        int c = __popc(um), incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
+        if (lane == 31) wcnt[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int v = wcnt[w]; wcnt[w] = tot; tot += v; }
+            sbase = tot ? (long long)atomicAdd((unsigned long long*)&d.act_count[g.branch], (unsigned long long)tot) : 0;
+        }
+        __syncthreads();
+        long long pos = sbase + wcnt[warp] + incl - c;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+            if (um & (1u << k)) d.act_rows[pos++] = (int)(ib + k);
+        __syncthreads();                                        // wcnt / sbase reused next step
     }
 }
 
@@ -105,8 +125,8 @@ int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s) {
     if (kb > 1184) kb = 1184;
     if (kb < 1) kb = 1;
     k_shift<<<kb, 256, 0, s>>>(d, g);
-    long long rb = (d.n + 255) / 256;
-    if (rb > 4 * 1184) rb = 4 * 1184;
+    long long rb = (d.n + 1023) / 1024;                      // 1024 rows per block step
+    if (rb > 2 * 1184) rb = 2 * 1184;
     if (rb < 1) rb = 1;
     k_bounds<<<(int)rb, 256, 0, s>>>(d, g);
     return 2;
