@@ -1227,35 +1227,58 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
 }
 
 // Exact fp64 decision between the two centroids of each two-centroid near-tie
-// row (the same arithmetic as k_refine_exact; lowest index on exact ties).
+// row: direct differences (Eq. 3), LPR = d/4 lanes per row with a float4 each
+// and a fixed xor-tree sum; lowest index on exact ties. Two row groups per warp
+// step keep more loads in flight.
+template <int LPR>
 __global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
+    constexpr int RPW = 32 / LPR;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int D = d.d;
+    const int h = lane / LPR, c4i = lane % LPR;
     int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
     long long np = d.pair_count[g.branch];
     if (np > d.fcap) np = d.fcap;
-    for (long long f = (long long)blockIdx.x * 8 + warp; f < np; f += (long long)gridDim.x * 8) {
-        const long long row = d.pair_rows[f];
-        const int2 jj = d.pair_j[f];
-        double a0 = 0.0, a1 = 0.0;
+    const float4* X4 = reinterpret_cast<const float4*>(d.X);
+    const float4* C4 = reinterpret_cast<const float4*>(d.C);
+    const long long W = (long long)gridDim.x * 8;
+    for (long long f0 = ((long long)blockIdx.x * 8 + warp) * RPW * 2; f0 < np; f0 += W * RPW * 2) {
+        long long row[2];
+        int2 jj[2];
+        float4 x[2], c0[2], c1[2];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int k = lane + 32 * v;
-            if (k < D) {
-                const double x = (double)__ldg(d.X + row * D + k);
-                const double d0 = x - (double)__ldg(d.C + (long long)jj.x * D + k);
-                const double d1 = x - (double)__ldg(d.C + (long long)jj.y * D + k);
-                a0 = fma(d0, d0, a0);
-                a1 = fma(d1, d1, a1);
+        for (int u = 0; u < 2; ++u) {
+            const long long f = f0 + u * RPW + h;
+            const bool ok = f < np;
+            row[u] = ok ? d.pair_rows[f] : 0;
+            jj[u] = ok ? d.pair_j[f] : make_int2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            x[u] = X4[row[u] * LPR + c4i];
+            c0[u] = C4[(long long)jj[u].x * LPR + c4i];
+            c1[u] = C4[(long long)jj[u].y * LPR + c4i];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            double a0, a1, t;
+            t = (double)x[u].x - (double)c0[u].x; a0 = t * t;
+            t = (double)x[u].y - (double)c0[u].y; a0 = fma(t, t, a0);
+            t = (double)x[u].z - (double)c0[u].z; a0 = fma(t, t, a0);
+            t = (double)x[u].w - (double)c0[u].w; a0 = fma(t, t, a0);
+            t = (double)x[u].x - (double)c1[u].x; a1 = t * t;
+            t = (double)x[u].y - (double)c1[u].y; a1 = fma(t, t, a1);
+            t = (double)x[u].z - (double)c1[u].z; a1 = fma(t, t, a1);
+            t = (double)x[u].w - (double)c1[u].w; a1 = fma(t, t, a1);
+#pragma unroll
+            for (int o = 1; o < LPR; o <<= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
             }
+            const long long f = f0 + u * RPW + h;
+            if (c4i == 0 && f < np)
+                lab_out[row[u]] = (a1 < a0 || (a1 == a0 && jj[u].y < jj[u].x)) ? jj[u].y : jj[u].x;
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-        }
-        if (lane == 0) lab_out[row] = (a1 < a0 || (a1 == a0 && jj.y < jj.x)) ? jj.y : jj.x;
     }
 }
 
@@ -1265,7 +1288,10 @@ int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_
     if (gather) k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
     k_refine_exact<<<4 * g_num_sms, 256, 0, s>>>(d, g);
-    if (d.tc_kind == 1) k_refine_pair<<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    if (d.tc_kind == 1) {                                          // d in {64, 128}
+        if (d.d == 64) k_refine_pair<16><<<4 * g_num_sms, 256, 0, s>>>(d, g);
+        else k_refine_pair<32><<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    }
     return 2 + gather + (d.tc_kind == 1 ? 1 : 0);
 }
 
