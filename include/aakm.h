@@ -23,7 +23,8 @@
  *  - SPMD: with nranks > 1, assign/update/aa_step/run are COLLECTIVE (like
  *    NCCL calls): every rank calls them in the same order; X is the rank's
  *    contiguous row shard; C and config are identical on all ranks.  Ranks
- *    combine [S | N | E | changed] with one ncclAllReduce per G-evaluation;
+ *    combine [S | N | E | changed] (exact int64 fixed point) with one
+ *    ncclAllReduce per G-evaluation;
  *    the Anderson step is replicated (deterministic kernels, identical bytes).
  *  - Errors: KMEANS_ERR_INVALID is returned before any work is enqueued (null
  *    required pointer, d < 1, k < 1, k > n_global, m0 < 0, m0 > m_max,
