@@ -288,3 +288,29 @@ def test_streamed_host_pass_matches_resident(cfg, N, K, chunks, bounded):
     for x, y in zip(ref, got):
         assert x == y, (x, y)
     assert np.array_equal(sa["C"], sb["C"])
+
+
+@pytest.mark.parametrize("path", ["tc16", "tc"])
+def test_exact_two_and_four_way_ties(path):
+    """Rows at the exact midpoint of two centroids (two-centroid fast path on the
+    2xFP16 engine) and at the centre of four equidistant centroids (candidate
+    pass): the labels equal the oracle's lowest-index argmin bit for bit."""
+    rng = np.random.default_rng(11)
+    d, K = 64, 96
+    C = (2 * rng.integers(-8, 9, (K, d))).astype(np.float32)      # even integers: midpoints exact
+    n2 = 3000
+    a = rng.integers(0, K, n2)
+    b = (a + 1 + rng.integers(0, K - 1, n2)) % K
+    X2 = (C[a] + C[b]) / 2                                        # ||x - c_a|| == ||x - c_b|| exactly
+    # four centroids at +-2 e_p, +-2 e_q around a far-away centre: every one at distance 2
+    base = np.full(d, 40.0, np.float32)
+    C4 = np.stack([base + 2 * np.eye(d, dtype=np.float32)[0], base - 2 * np.eye(d, dtype=np.float32)[0],
+                   base + 2 * np.eye(d, dtype=np.float32)[1], base - 2 * np.eye(d, dtype=np.float32)[1]])
+    C = np.concatenate([C, C4]).astype(np.float32)
+    X = np.concatenate([X2, np.repeat(base[None], 200, 0)]).astype(np.float32)
+    km = aakm.KMeans(dev(X), C.shape[0], aakm.config(assign_path=path))
+    lab, E, _ = km.assign(dev(C))
+    km.close()
+    ref = oracle.assign(X, C.astype(np.float64))
+    np.testing.assert_array_equal(lab.cpu().numpy(), ref)
+    assert (ref[n2:] == K).all()                                  # lowest index of the four
