@@ -392,8 +392,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     constexpr bool DX = KIND == 1;
     const bool inplace = NXB == 0;
     const int nxb = inplace ? 1 : NXB;
-    uint8_t* xst = smem;                                           // fp32 X tile (TMA target, splitter-owned)
-    uint8_t* opb = (inplace || DX) ? smem : xst + A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
+    // KIND 0 stages X in two fp32 tiles (TMA two row tiles ahead, so the split never
+    // waits a TMA round trip); in place: one
+    const int nst = (DX || inplace) ? 1 : 2;
+    uint8_t* xst = smem;                                           // fp32 X tiles (TMA targets, splitter-owned)
+    uint8_t* opb = (inplace || DX) ? smem : xst + nst * A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
     uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // KIND 0: constant A side of the folded block
     float* xnorm = reinterpret_cast<float*>(ablk + (KIND ? 0 : AAKM_CNIMG_BYTES)); // [XRr][128] ||x||^2 ring (slot = iteration % XRr)
@@ -403,8 +406,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint64_t* empty = bars + S;                                    // [S]  stage consumed (multicast commit)
     uint64_t* accf = bars + 2 * S;                                 // [4]  accumulator ready (multicast commit)
     uint64_t* acce = accf + 4;                                     // [4]  accumulator drained (leader: all epilogues)
-    uint64_t* stfull = acce + 4;                                   // X staging landed
-    uint64_t* opready = stfull + 1;                                // [2] operand buffer split (leader: both CTAs)
+    uint64_t* stfull = acce + 4;                                   // [2] X staging tile landed
+    uint64_t* opready = stfull + 2;                                // [2] operand buffer split (leader: both CTAs)
     uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
     uint64_t* xready = opempty + 2;                                // [XRr] ||x||^2 slot written (epilogue side)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XRr);
@@ -429,6 +432,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         for (int b = 0; b < 4; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4 * CG); }
         for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2 * CG); mbar_init(opempty + b, 1); }
         mbar_init(stfull, 1);
+        mbar_init(stfull + 1, 1);
         for (int b = 0; b < XRr; ++b) mbar_init(xready + b, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -542,8 +546,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (MODE != 1 && !use_list)
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(0) * TC_BM));
             } else {
-                mbar_expect_tx(stfull, A * ATOM_BYTES_X);
-                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(0) * TC_BM));
+                for (int q = 0; q < nst && live(q); ++q) {
+                    mbar_expect_tx(stfull + q, A * ATOM_BYTES_X);
+                    for (int a = 0; a < A; ++a)
+                        tma_load_2d(xst + (q * A + a) * ATOM_BYTES_X, tmx, stfull + q, a * 32, (int)(tile_of(q) * TC_BM));
+                }
             }
         }
         const float inv_sx = KIND ? 1.0f / d.st->c_scale : 1.0f;     // exact (power of 2)
@@ -568,10 +575,13 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (MODE != 1 && !use_list && t == 0 && live(it + 1))   // next row tile -> L2
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(it + 1) * TC_BM));
                 prefetch_list(it + 1);
-            } else {
+            } else if (nst == 1) {
                 mbar_wait_sleep(stfull, sph, 128);
                 sph ^= 1;
+            } else {
+                mbar_wait_sleep(stfull + (it & 1), (uint32_t)(it >> 1) & 1u, 128);
             }
+            const uint8_t* xs = xst + (nst == 2 ? (int)(it & 1) * A * ATOM_BYTES_X : 0);   // this tile's staging
             if (!inplace) {
                 mbar_wait_sleep(opempty + xb, ((eph >> xb) & 1u) ^ 1u, 256);  // the MMAs of tile - NXB are done
                 eph ^= 1u << xb;
@@ -588,7 +598,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
                             const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
-                            const float4 v = *reinterpret_cast<const float4*>(xst + off);
+                            const float4 v = *reinterpret_cast<const float4*>(xs + off);
                             float4 h, l;
                             h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
                             h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
@@ -661,9 +671,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 mbar_wait(opempty, eph & 1u);
                 eph ^= 1u;
             }
-            if (t == 0 && live(it + 1)) {
+            if (nst == 1 && t == 0 && live(it + 1)) {
                 mbar_expect_tx(stfull, A * ATOM_BYTES_X);
                 for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(it + 1) * TC_BM));
+            }
+            if (nst == 2 && t == 0 && live(it + 2)) {                 // refill the tile just converted
+                const int q = (int)(it & 1);
+                mbar_expect_tx(stfull + q, A * ATOM_BYTES_X);
+                for (int a = 0; a < A; ++a)
+                    tma_load_2d(xst + (q * A + a) * ATOM_BYTES_X, tmx, stfull + q, a * 32, (int)(tile_of(it + 2) * TC_BM));
             }
             if (++xb == nxb) xb = 0;
         }
@@ -875,13 +891,13 @@ static int xr_of(int NT, int NXB, int cg) {
 
 static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2) {
     const int natom = kind ? A / 2 : A;
-    const int staging = (NXB == 0 || kind == 1) ? 0 : A;   // in place / direct X: no staging tile
+    const int staging = (NXB == 0 || kind == 1) ? 0 : 2 * A;   // in place / direct X: none; KIND 0: two tiles
     const int nb = NXB == 0 ? 1 : NXB;
     const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + (kind ? AAKM_CNIMG_BYTES : 0);
     const int xr = xr_of(NT, NXB, cg);
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
            (kind ? 0 : AAKM_CNIMG_BYTES) + (size_t)xr * TC_BM * 4 + (NQ - 1) * TC_BM * 16 +
-           (size_t)(2 * S + 13 + xr) * 8 + 16;
+           (size_t)(2 * S + 14 + xr) * 8 + 16;
 }
 
 // stages S and operand buffers NXB: prefer double-buffered X operands while
