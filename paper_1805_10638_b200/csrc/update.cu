@@ -19,15 +19,11 @@
 
 namespace aakm {
 
-__device__ __forceinline__ void red_add_f64(double* p, double v) {
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
 struct Pick {
     const int* lab;
     const int* prev;
     const float* C;
-    long long* out;       // packed [S_hi | S_lo | N | E | changed]
+    long long* out;       // packed [S_hi | S_lo | N | E_hi | E_lo | E | changed]
 };
 
 __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
