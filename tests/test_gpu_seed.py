@@ -94,3 +94,17 @@ def test_seeded_run_matches_oracle():
     assert rep["converged"] and ref["converged"]
     assert rep["iters"] == ref["iters"]
     assert abs(rep["energy"] - ref["energy"]) <= 1e-6 * ref["energy"]
+
+
+def test_seed_k1_and_k_equals_n():
+    """K = 1 is one uniform index; K = N over distinct rows draws every row once
+    (each round picks a remaining row with D^2 > 0), in the oracle's order."""
+    rng = np.random.default_rng(5)
+    X = rng.normal(0, 1, (300, 8)).astype(np.float32)
+    for K in (1, 300):
+        u = rng.random(K)
+        C, idx, ref = seed_both(X, K, u)
+        np.testing.assert_array_equal(idx, ref)
+        np.testing.assert_array_equal(C, X[ref])
+        if K == 300:
+            assert sorted(idx.tolist()) == list(range(300))
