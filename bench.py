@@ -183,6 +183,7 @@ def time_to_converge(cfgname, rank, world, barrier):
         scored, total = km.bounded_stats()
         km.close()
         out.update({pre + "seconds": float(t.item()), pre + "iters": rep["iters"], pre + "n_assign": rep["n_assign"],
+                    pre + "iterations_per_s": rep["iters"] / max(float(t.item()), 1e-9),
                     pre + "converged": bool(rep["converged"]), pre + "energy": rep["energy"],
                     pre + "rows_scored_frac": scored / max(total, 1)})
         if pre == "":
@@ -356,6 +357,7 @@ def main():
                    "K": cfg.K, "parallelism": f"dp{world}", "assign_path": path,
                    "l2": f"inputs larger than L2 (X shard {n_local * cfg.d * 4 / 1e9:.2f} GB > 126 MB)"},
         "passes": args.steps, "assign_passes": n_assign, "converged_in_window": passes_done is None,
+        "iterations_per_s": args.steps / (ms_max / 1e3),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n_local * cfg.d * 4,
                 "d2h_bytes_per_step": cfg.K * cfg.d * 4, "steps": e2e_steps, "wall_s": wall,
                 "h2d": f"pinned host -> device in {E2E_CHUNKS} row chunks overlapping the assignment"},
