@@ -276,6 +276,7 @@ def main():
         km.aa_step(None, info=False)
     st0 = km.state_export()
     km.assign_timing()                         # drop warm-up timings
+    km.update_timing()
     n_assign0 = st0["n_assign"]
     L0 = km.launch_count()
     barrier()
@@ -291,6 +292,7 @@ def main():
     st1 = km.state_export()
     n_assign = st1["n_assign"] - n_assign0
     a_ms, a_n = km.assign_timing()
+    u_ms, u_n = km.update_timing()
     t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -367,6 +369,14 @@ def main():
                      "kernel": f"assign_{path}", "avg_launch_ms": avg_ms, "launches": a_n},
         "clocks": clk.summary(),
     }
+    if u_n:
+        u_avg = u_ms / u_n
+        ubytes = n_local * cfg.d * 4.0 + n_local * 4.0        # X once + the labels
+        line["update_roofline"] = {"bound": "hbm", "achieved": ubytes / (u_avg / 1e3) / 1e9,
+                                   "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                   "frac": ubytes / (u_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                   "kernel": "update (label sort + segmented sums + fp64 energy)",
+                                   "avg_ms": u_avg, "launches": u_n}
     km.close()
     if args.ttc_config != "none":
         line["time_to_converge"] = time_to_converge(args.ttc_config, rank, world, barrier)

@@ -259,6 +259,12 @@ AAKM_API kmeans_status kmeans_aa_step_host(kmeans_handle *h, const float *X_host
 AAKM_API kmeans_status kmeans_assign_timing(kmeans_handle *h, double *ms_total /*host*/,
                                    int64_t *launches /*host*/);
 
+/* The same for the update partials of those G-evaluations (the label-sorted
+ * segmented sums with the energy, or the atomic engine), branch A only.
+ * Synchronises. */
+AAKM_API kmeans_status kmeans_update_timing(kmeans_handle *h, double *ms_total /*host*/,
+                                   int64_t *launches /*host*/);
+
 /* Number of library kernels launched on this handle so far (graph replays
  * count every kernel node). */
 AAKM_API int64_t kmeans_launch_count(const kmeans_handle *h);

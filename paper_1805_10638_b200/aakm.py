@@ -91,6 +91,7 @@ def lib():
                 "kmeans_bounded_stats": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
                 "kmeans_seed_pp": ([P, P, P, P], I32),
                 "kmeans_aa_step_host": ([P, P, I32, P, P], I32),
+                "kmeans_update_timing": ([P, ct.POINTER(D), ct.POINTER(I64)], I32),
                 "kmeans_assign_path_name": ([P], ct.c_char_p),
                 "kmeans_destroy": ([P], I32),
                 "kmeans_last_error": ([P], ct.c_char_p),
@@ -329,6 +330,12 @@ class KMeans:
     def assign_timing(self):
         ms, n = ct.c_double(), ct.c_int64()
         self._c(lib().kmeans_assign_timing(self.h, ct.byref(ms), ct.byref(n)))
+        return ms.value, n.value
+
+    def update_timing(self):
+        """(ms, launches) of the timed update partials since the last call (cfg.timing)."""
+        ms, n = ct.c_double(), ct.c_int64()
+        self._c(lib().kmeans_update_timing(self.h, ct.byref(ms), ct.byref(n)))
         return ms.value, n.value
 
     def bounded_stats(self):

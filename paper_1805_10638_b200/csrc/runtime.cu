@@ -43,6 +43,8 @@ struct kmeans_handle {
     long long kernels_per_pass = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // assignment timing (branch A)
     size_t ev_used = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> uev;  // update timing (branch A)
+    size_t uev_used = 0;
     DevState* st_host = nullptr;                             // pinned
     TraceRec* tr_host = nullptr;                             // pinned
     double* scal_host = nullptr;                             // pinned (E, changed)
@@ -314,7 +316,18 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     dbg("assign", s);
     refine_engine(h, d, g, s);
     dbg("refine", s);
+    std::pair<cudaEvent_t, cudaEvent_t>* uevp = nullptr;
+    if (timing && branch == 0) {
+        if (h->uev_used == h->uev.size()) {
+            cudaEvent_t a, b;
+            CK(h, cudaEventCreate(&a)); CK(h, cudaEventCreate(&b));
+            h->uev.push_back({a, b});
+        }
+        uevp = &h->uev[h->uev_used++];
+        CK(h, cudaEventRecord(uevp->first, s));
+    }
     h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
+    if (uevp) CK(h, cudaEventRecord(uevp->second, s));
     dbg("update", s);
     st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
@@ -932,6 +945,21 @@ kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* 
     return KMEANS_OK;
 }
 
+kmeans_status kmeans_update_timing(kmeans_handle* h, double* ms_total, int64_t* launches) {
+    LIVE(h);
+    CK(h, cudaStreamSynchronize(h->stream));
+    double tot = 0.0;
+    for (size_t i = 0; i < h->uev_used; ++i) {
+        float ms = 0.f;
+        CK(h, cudaEventElapsedTime(&ms, h->uev[i].first, h->uev[i].second));
+        tot += ms;
+    }
+    if (ms_total) *ms_total = tot;
+    if (launches) *launches = (int64_t)h->uev_used;
+    h->uev_used = 0;
+    return KMEANS_OK;
+}
+
 int64_t kmeans_launch_count(const kmeans_handle* h) { return h ? h->launches : 0; }
 
 // K-Means++ seeding (seed.cu, reading R-A27): K rounds, each one pass over X
@@ -1034,6 +1062,7 @@ kmeans_status kmeans_destroy(kmeans_handle* h) {
     if (h->tcm) tc_free_maps(h->tcm);
     if (h->tcm_api) tc_free_maps(h->tcm_api);
     for (auto& e : h->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (auto& e : h->uev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (h->run_ev[0]) cudaEventDestroy(h->run_ev[0]);
     if (h->run_ev[1]) cudaEventDestroy(h->run_ev[1]);
     if (h->st_host) cudaFreeHost(h->st_host);
