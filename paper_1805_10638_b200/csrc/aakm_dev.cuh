@@ -111,6 +111,8 @@ struct Dev {
     int* perm;            // rows bucketed by label (n)
     float* ub;            // bounded engine (nullptr = dense): per row, upper bound on ||x_i - c_{rho_i}||
     float* lb;            //   ... and lower bound on min_{j != rho_i} ||x_i - c_j||, w.r.t. C_ref
+    int* pj2;             //   two-centroid rows: the other candidate (-1: none); then ub bounds
+                          //   both candidates' distances and lb every other centroid's
     int* act_rows;        //   rows the bounds could not prove unchanged (capacity n)
     long long* act_count; //   [2] their counts, branch A / B (zeroed per pass with packed)
     float* C_ref;         //   centroids the bounds refer to (the last assigned set)

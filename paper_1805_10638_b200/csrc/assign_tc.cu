@@ -847,15 +847,25 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     if (ok) lab_out[row] = i1;
                     if (KIND && ok && d.ub) {
                         // Hamerly bounds for the next assignment (distance units, rounded
-                        // outward): each accumulator is within tau of its exact value;
-                        // near-tie rows are left for the exact refine and always recomputed
+                        // outward): each accumulator is within tau of its exact value.
+                        // Two-centroid rows bound both candidates (u from b2) and every
+                        // other centroid (l from L), so k_bounds can keep them off the
+                        // tensor engine while the pair stays apart from the rest; other
+                        // near-tie rows are always recomputed
                         float u = INFINITY, l = 0.f;
+                        int p2 = -1;
                         if (!flag) {
                             u = __fsqrt_ru(__fdiv_ru(fmaxf(b1 + tau - 6.0f, 0.0f), Usc)) * 1.000001f;
                             l = __fsqrt_rd(__fdiv_rd(fmaxf(b2 - tau - 6.0f, 0.0f), Usc)) * 0.999999f;
+                        } else if (pair) {
+                            const float Lk = wdecode(__uint_as_float(__float_as_uint(t.L) & ~0xFFFu));
+                            u = __fsqrt_ru(__fdiv_ru(fmaxf(b2 + tau - 6.0f, 0.0f), Usc)) * 1.000001f;
+                            l = __fsqrt_rd(__fdiv_rd(fmaxf(Lk - tau - 6.0f, 0.0f), Usc)) * 0.999999f;
+                            p2 = t.i2;
                         }
                         d.ub[row] = u;
                         d.lb[row] = l;
+                        d.pj2[row] = p2;
                     }
                     push_flag_tc(d, g.branch, flag && !pair, row, b1, tau);
                     if (KIND) push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
@@ -1238,7 +1248,10 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (acc < bd || (acc == bd && j < bj)) { bd = acc; bj = j; }
         }
-        if (lane == 0) lab_out[row] = bj;
+        if (lane == 0) {
+            lab_out[row] = bj;
+            if (d.pj2) { d.pj2[row] = -1; d.ub[row] = INFINITY; }   // bounded: re-score next time
+        }
     }
 }
 
@@ -1292,8 +1305,11 @@ __global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
                 a1 += __shfl_xor_sync(0xffffffffu, a1, o);
             }
             const long long f = f0 + u * RPW + h;
-            if (c4i == 0 && f < np)
-                lab_out[row[u]] = (a1 < a0 || (a1 == a0 && jj[u].y < jj[u].x)) ? jj[u].y : jj[u].x;
+            if (c4i == 0 && f < np) {
+                const bool w1 = a1 < a0 || (a1 == a0 && jj[u].y < jj[u].x);
+                lab_out[row[u]] = w1 ? jj[u].y : jj[u].x;
+                if (d.pj2) d.pj2[row[u]] = w1 ? jj[u].x : jj[u].y;  // bounded: the other candidate
+            }
         }
     }
 }

@@ -86,16 +86,41 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const long long i = ib + k;
+            bool pr = false;
+            int a = 0, p2 = -1;
             if (i < n) {
-                const int a = lab_ref[i];
-                const float u = __fadd_ru(d.ub[i], d.shift[a]);
+                a = lab_ref[i];
+                p2 = d.pj2[i];
+                // two-centroid rows: ub bounds both candidates, so it moves with the
+                // larger of their shifts; proven, the argmin is one of the two
+                const float sh = p2 >= 0 ? fmaxf(d.shift[a], d.shift[p2]) : d.shift[a];
+                const float u = __fadd_ru(d.ub[i], sh);
                 const float l = __fsub_rd(d.lb[i], smax);
                 if (u < l) {
                     d.ub[i] = u;
                     d.lb[i] = l;
                     if (g.branch == 0) lab_out[i] = a;
+                    pr = p2 >= 0;
                 } else {
                     um |= 1u << k;
+                }
+            }
+            // proven two-centroid rows go straight to the pair list (k_refine_pair)
+            const unsigned pm = __ballot_sync(0xffffffffu, pr);
+            if (pm) {
+                long long pb = 0;
+                if (lane == __ffs(pm) - 1)
+                    pb = (long long)atomicAdd((unsigned long long*)&d.pair_count[g.branch], (unsigned long long)__popc(pm));
+                pb = __shfl_sync(0xffffffffu, pb, __ffs(pm) - 1);
+                if (pr) {
+                    const long long f = pb + __popc(pm & ((1u << lane) - 1));
+                    if (f < d.fcap) {
+                        d.pair_rows[f] = (int)i;
+                        d.pair_j[f] = make_int2(a, p2);
+                    } else {                                    // list full: score the row instead
+                        d.ub[i] = INFINITY;
+                        um |= 1u << k;
+                    }
                 }
             }
         }

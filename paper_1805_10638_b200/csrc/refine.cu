@@ -89,7 +89,10 @@ __global__ void __launch_bounds__(256) k_refine(Dev d, GEval g, long long first)
             int oj = __shfl_xor_sync(0xffffffffu, bj, o);
             if (ov < bd || (ov == bd && oj < bj)) { bd = ov; bj = oj; }
         }
-        if (lane == 0) lab_out[row] = bj;
+        if (lane == 0) {
+            lab_out[row] = bj;
+            if (d.pj2) { d.pj2[row] = -1; d.ub[row] = INFINITY; }   // bounded: re-score next time
+        }
         __syncwarp();
     }
 }

@@ -144,7 +144,7 @@ struct Layout {
     size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, C_ref, shift, total,
+        ub, lb, act_rows, pj2, C_ref, shift, total,
         scratch_bytes;
 };
 
@@ -203,7 +203,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.trace = take((size_t)AAKM_TRACE_CAP * sizeof(TraceRec));
     // bounded engine (2xFP16, cfg.bounded): 12 B per row + 2 centroid-sized arrays
     const size_t nb = bounded ? (size_t)n : 0;
-    L.ub = take(nb * 4 + 4); L.lb = take(nb * 4 + 4); L.act_rows = take(nb * 4 + 4);
+    L.ub = take(nb * 4 + 4); L.lb = take(nb * 4 + 4); L.act_rows = take(nb * 4 + 4); L.pj2 = take(nb * 4 + 4);
     L.C_ref = take(bounded ? KD * 4 : 4); L.shift = take(bounded ? (size_t)K * 4 : 4);
     L.total = o;
     return L;
@@ -499,6 +499,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.key_mul = 32u;
     if (h->path == KMEANS_PATH_TC16 && cfg->bounded) {                 // bounded engine (Algorithm 1 passes)
         D.ub = (float*)(w + L.ub); D.lb = (float*)(w + L.lb); D.act_rows = (int*)(w + L.act_rows);
+        D.pj2 = (int*)(w + L.pj2);
         D.C_ref = (float*)(w + L.C_ref); D.shift = (float*)(w + L.shift);
     }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
@@ -508,6 +509,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
                 : h->path == KMEANS_PATH_TC16 ? tau_gamma_tc16(d) : tau_gamma_simt(d);
     h->da = D;
     h->da.ub = nullptr; h->da.lb = nullptr; h->da.act_rows = nullptr;    // the API calls stay dense
+    h->da.pj2 = nullptr;
     h->da.C_ref = nullptr; h->da.shift = nullptr;
     h->da.st = (DevState*)(w + L.st_api);
     h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
