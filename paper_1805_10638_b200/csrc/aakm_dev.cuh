@@ -51,6 +51,7 @@ struct alignas(16) DevState {
     unsigned int shift_max_bits, shift_tmp, shift_ctr, pad3;   // max_j ||c_j - c_ref_j|| (float bits)
     long long seed_max;          // K-Means++: max_i D2_i of the current round (fixed point)
     int seed_err, pad4;          // K-Means++: 2 = fewer distinct samples than K
+    int bnd_ready0, pad5;        // bounded engine: bnd_ready at the snapshot
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -117,6 +118,10 @@ struct Dev {
     long long* act_count; //   [2] their counts, branch A / B (zeroed per pass with packed)
     float* C_ref;         //   centroids the bounds refer to (the last assigned set)
     float* shift;         //   ||c_j - c_ref_j|| of the set being assigned (K)
+    float* ub0;           //   snapshot of (ub, lb, pj2, C_ref) taken before branch A, restored
+    float* lb0;           //   for the fallback B on a rejection (bounds w.r.t. the previous
+    int* pj20;            //   pass's set instead of the rejected jump)
+    float* C_ref0;
     float* Gring;         // H x K*d
     float* Fring;         // H x K*d
     double* gram_part;    // AAKM_GRAM_BLOCKS x (2*H)

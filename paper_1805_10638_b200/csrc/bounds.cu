@@ -11,9 +11,11 @@
 //   k_shift   s_j and max_j s_j for the set about to be assigned; C_ref <- it
 //   k_bounds  per row: the Hamerly test; proven rows keep (copy) their label and
 //             move their bounds, the rest are appended to act_rows
-// AA jumps are handled by construction: the shifts are measured between
-// whichever two sets are assigned consecutively (C^t, then C_AU^t on a
-// rejection, then C^{t+1}).  All bound arithmetic rounds outward.
+// AA jumps: branch A's shifts are measured from the previous pass's assigned
+// set; the state is snapshotted first (k_bnd_save), and a fallback B (after a
+// rejected jump) restores it (k_bnd_restore), so B's shifts are measured from
+// that same set, not from the rejected candidate.  All bound arithmetic rounds
+// outward.
 #include <math.h>
 
 #include "aakm_dev.cuh"
@@ -69,9 +71,9 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
     const float smax = __uint_as_float(st->shift_max_bits);
     const int cur = st->cur;
     int* lab_out = g.lab_out ? g.lab_out : d.lab[cur];
-    // labels the bounds refer to: the previous pass's final labels (branch A), or
-    // branch A's labels of this pass (branch B assigns the fallback after it)
-    const int* lab_ref = g.branch == 0 ? d.lab[cur ^ 1] : lab_out;
+    // labels the bounds refer to: the previous pass's final labels P^{t-1}, for both
+    // branches (B restored the snapshot taken before A)
+    const int* lab_ref = d.lab[cur ^ 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long n = d.n;
     // 1024 rows per block step (4 consecutive rows per thread); the unproven rows of
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
                 if (u < l) {
                     d.ub[i] = u;
                     d.lb[i] = l;
-                    if (g.branch == 0) lab_out[i] = a;
+                    lab_out[i] = a;
                     pr = p2 >= 0;
                 } else {
                     um |= 1u << k;
@@ -145,7 +147,35 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
     }
 }
 
+// branch A: snapshot the bounds state; branch B (rejection only): restore it
+__global__ void __launch_bounds__(256) k_bnd_save(Dev d, GEval g, int restore) {
+    if (!geval_active(d, g)) return;
+    if (!restore && d.st->lloyd) return;                       // a Lloyd candidate is never rejected (R-A9)
+    const long long n = d.n, KD = (long long)d.K * d.d;
+    const long long st = (long long)gridDim.x * blockDim.x;
+    float* ub = restore ? d.ub : d.ub0;
+    float* lb = restore ? d.lb : d.lb0;
+    int* p2 = restore ? d.pj2 : d.pj20;
+    float* cr = restore ? d.C_ref : d.C_ref0;
+    const float* ubs = restore ? d.ub0 : d.ub;
+    const float* lbs = restore ? d.lb0 : d.lb;
+    const int* p2s = restore ? d.pj20 : d.pj2;
+    const float* crs = restore ? d.C_ref0 : d.C_ref;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+        ub[i] = ubs[i]; lb[i] = lbs[i]; p2[i] = p2s[i];
+    }
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < KD; i += st) cr[i] = crs[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (restore) d.st->bnd_ready = d.st->bnd_ready0;
+        else d.st->bnd_ready0 = d.st->bnd_ready;
+    }
+}
+
 int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s) {
+    long long cb = (d.n + 255) / 256;
+    if (cb > 4 * 1184) cb = 4 * 1184;
+    if (cb < 1) cb = 1;
+    k_bnd_save<<<(int)cb, 256, 0, s>>>(d, g, g.branch == 1 ? 1 : 0);
     int kb = (int)((d.K + 7) / 8);
     if (kb > 1184) kb = 1184;
     if (kb < 1) kb = 1;
@@ -154,7 +184,7 @@ int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s) {
     if (rb > 2 * 1184) rb = 2 * 1184;
     if (rb < 1) rb = 1;
     k_bounds<<<(int)rb, 256, 0, s>>>(d, g);
-    return 2;
+    return 3;
 }
 
 }  // namespace aakm

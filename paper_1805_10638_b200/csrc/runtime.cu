@@ -144,7 +144,7 @@ struct Layout {
     size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, pj2, C_ref, shift, total,
+        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, total,
         scratch_bytes;
 };
 
@@ -205,6 +205,8 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     const size_t nb = bounded ? (size_t)n : 0;
     L.ub = take(nb * 4 + 4); L.lb = take(nb * 4 + 4); L.act_rows = take(nb * 4 + 4); L.pj2 = take(nb * 4 + 4);
     L.C_ref = take(bounded ? KD * 4 : 4); L.shift = take(bounded ? (size_t)K * 4 : 4);
+    L.ub0 = take(nb * 4 + 4); L.lb0 = take(nb * 4 + 4); L.pj20 = take(nb * 4 + 4);
+    L.C_ref0 = take(bounded ? KD * 4 : 4);
     L.total = o;
     return L;
 }
@@ -501,6 +503,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         D.ub = (float*)(w + L.ub); D.lb = (float*)(w + L.lb); D.act_rows = (int*)(w + L.act_rows);
         D.pj2 = (int*)(w + L.pj2);
         D.C_ref = (float*)(w + L.C_ref); D.shift = (float*)(w + L.shift);
+        D.ub0 = (float*)(w + L.ub0); D.lb0 = (float*)(w + L.lb0); D.pj20 = (int*)(w + L.pj20);
+        D.C_ref0 = (float*)(w + L.C_ref0);
     }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
@@ -511,6 +515,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     h->da.ub = nullptr; h->da.lb = nullptr; h->da.act_rows = nullptr;    // the API calls stay dense
     h->da.pj2 = nullptr;
     h->da.C_ref = nullptr; h->da.shift = nullptr;
+    h->da.ub0 = nullptr; h->da.lb0 = nullptr; h->da.pj20 = nullptr; h->da.C_ref0 = nullptr;
     h->da.st = (DevState*)(w + L.st_api);
     h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
     h->da.cn = (float*)(w + L.cna);
