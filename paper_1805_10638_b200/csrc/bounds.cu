@@ -82,51 +82,9 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
     __shared__ long long sbase;
     constexpr int RPT = 4;
     const long long step = (long long)blockDim.x * RPT;
-    for (long long i0 = (long long)blockIdx.x * step; i0 < n; i0 += (long long)gridDim.x * step) {
-        const long long ib = i0 + (long long)threadIdx.x * RPT;
-        unsigned um = 0;                                        // bit k: row ib + k unproven
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-            const long long i = ib + k;
-            bool pr = false;
-            int a = 0, p2 = -1;
-            if (i < n) {
-                a = lab_ref[i];
-                p2 = d.pj2[i];
-                // two-centroid rows: ub bounds both candidates, so it moves with the
-                // larger of their shifts; proven, the argmin is one of the two
-                const float sh = p2 >= 0 ? fmaxf(d.shift[a], d.shift[p2]) : d.shift[a];
-                const float u = __fadd_ru(d.ub[i], sh);
-                const float l = __fsub_rd(d.lb[i], smax);
-                if (u < l) {
-                    d.ub[i] = u;
-                    d.lb[i] = l;
-                    lab_out[i] = a;
-                    pr = p2 >= 0;
-                } else {
-                    um |= 1u << k;
-                }
-            }
-            // proven two-centroid rows go straight to the pair list (k_refine_pair)
-            const unsigned pm = __ballot_sync(0xffffffffu, pr);
-            if (pm) {
-                long long pb = 0;
-                if (lane == __ffs(pm) - 1)
-                    pb = (long long)atomicAdd((unsigned long long*)&d.pair_count[g.branch], (unsigned long long)__popc(pm));
-                pb = __shfl_sync(0xffffffffu, pb, __ffs(pm) - 1);
-                if (pr) {
-                    const long long f = pb + __popc(pm & ((1u << lane) - 1));
-                    if (f < d.fcap) {
-                        d.pair_rows[f] = (int)i;
-                        d.pair_j[f] = make_int2(a, p2);
-                    } else {                                    // list full: score the row instead
-                        d.ub[i] = INFINITY;
-                        um |= 1u << k;
-                    }
-                }
-            }
-        }
-        int c = __popc(um), incl = c;
+    // exclusive block prefix of per-thread counts, one atomic on *ctr per block step
+    auto block_append = [&](int c, unsigned long long* ctr) -> long long {
+        int incl = c;
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
@@ -136,14 +94,59 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
         if (threadIdx.x == 0) {
             int tot = 0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int v = wcnt[w]; wcnt[w] = tot; tot += v; }
-            sbase = tot ? (long long)atomicAdd((unsigned long long*)&d.act_count[g.branch], (unsigned long long)tot) : 0;
+            sbase = tot ? (long long)atomicAdd(ctr, (unsigned long long)tot) : 0;
         }
         __syncthreads();
-        long long pos = sbase + wcnt[warp] + incl - c;
+        const long long pos = sbase + wcnt[warp] + incl - c;
+        __syncthreads();                                        // wcnt / sbase reusable
+        return pos;
+    };
+    for (long long i0 = (long long)blockIdx.x * step; i0 < n; i0 += (long long)gridDim.x * step) {
+        const long long ib = i0 + (long long)threadIdx.x * RPT;
+        unsigned um = 0, pm = 0;                                // bit k: row ib + k unproven / proven pair
+        int pa[RPT], pb2[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const long long i = ib + k;
+            pa[k] = 0; pb2[k] = -1;
+            if (i < n) {
+                const int a = lab_ref[i];
+                const int p2 = d.pj2[i];
+                // two-centroid rows: ub bounds both candidates, so it moves with the
+                // larger of their shifts; proven, the argmin is one of the two
+                const float sh = p2 >= 0 ? fmaxf(d.shift[a], d.shift[p2]) : d.shift[a];
+                const float u = __fadd_ru(d.ub[i], sh);
+                const float l = __fsub_rd(d.lb[i], smax);
+                if (u < l) {
+                    d.ub[i] = u;
+                    d.lb[i] = l;
+                    lab_out[i] = a;
+                    if (p2 >= 0) { pm |= 1u << k; pa[k] = a; pb2[k] = p2; }
+                } else {
+                    um |= 1u << k;
+                }
+            }
+        }
+        // proven two-centroid rows go straight to the pair list (k_refine_pair)
+        if (__syncthreads_or(pm != 0)) {
+            long long f = block_append(__popc(pm), (unsigned long long*)&d.pair_count[g.branch]);
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                if (!(pm & (1u << k))) continue;
+                if (f < d.fcap) {
+                    d.pair_rows[f] = (int)(ib + k);
+                    d.pair_j[f] = make_int2(pa[k], pb2[k]);
+                } else {                                        // list full: score the row instead
+                    d.ub[ib + k] = INFINITY;
+                    um |= 1u << k;
+                }
+                ++f;
+            }
+        }
+        long long pos = block_append(__popc(um), (unsigned long long*)&d.act_count[g.branch]);
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
             if (um & (1u << k)) d.act_rows[pos++] = (int)(ib + k);
-        __syncthreads();                                        // wcnt / sbase reused next step
     }
 }
 
