@@ -193,7 +193,7 @@ def time_to_converge(cfgname, rank, world, barrier):
 
 
 # --------------------------------------------------------------------- K-Means++ seeding (f3)
-E2E_CHUNKS = 16
+E2E_CHUNKS = int(os.environ.get("AAKM_E2E_CHUNKS", "64"))   # 16: 8.60e11, 32: 8.59e11, 64: 8.66e11 (c5)
 
 
 def seed_pp_bench(cfgname, rank, world, barrier, peaks):
