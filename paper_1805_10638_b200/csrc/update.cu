@@ -111,16 +111,18 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 }
 
 // ------------------------------------------------------------------
-// Sorted engine for large shards (n >= AAKM_SORTED_MIN_ROWS): rows are
-// bucketed by label, then each warp sums a chunk of <= SEG_ROWS rows of one
-// cluster in fp64 registers (lanes over d) and issues d atomics per chunk
-// instead of d per row.  X is read exactly once, as contiguous row segments;
-// the energy uses the chunk's centroid kept in registers.
-//   k_hist     N_j (block histograms in smem) + #changed + label check
-//   k_scan_a   per cluster: N_j -> packed, per-(block, cluster) offsets within the cluster
-//   k_scan_b   exclusive scans over clusters, chunk counts, chunk -> cluster map
-//   k_scatter  perm[offset_j + rank] = row (warp-aggregated cursors)
-//   k_segsum   S_j += sum of the chunk's rows, E += sum (x - c_j)^2
+// Sorted engine (n_global >= AAKM_SORTED_MIN_ROWS): rows are bucketed by
+// label, then a warp sums a chunk of <= SEG_ROWS rows of one cluster in int32
+// fixed-point registers (exact, see fx_add) and issues one int64 atomic per
+// coordinate and part per chunk instead of per row.  X is read exactly once;
+// the energy parts use the chunk's centroid.
+//   k_hist         N_j (block histograms in smem) + #changed + label check
+//   k_scan_a       per cluster: N_j -> packed, per-(block, cluster) offsets
+//   k_scan_b       exclusive scans over clusters (row offsets, chunk counts)
+//   k_scatter      chunk table {j, first row, rows} + perm[offset_j + rank] = row
+//   k_segsum_bulk  d = 4 LPR: rows gathered by TMA tile::gather4 into per-warp
+//                  mbarrier rings; S_j += chunk rows, E += per-lane parts
+//   k_segsum       other d: lanes over coordinates, the same sums
 
 constexpr int SEG_ROWS = 256;
 
