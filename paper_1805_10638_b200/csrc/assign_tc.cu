@@ -14,8 +14,9 @@
 // ||x - c||^2 / (2 s^2) + 6, a "window" value whose bits order as integers).
 // The argmin is fused into the epilogue (TMEM -> registers): per row the best
 // score b1 (index i1, lowest index on ties) and the runner-up b2; rows with
-// b2 - b1 within the engine's rigorous error bound are flagged for the exact
-// fp64 re-decision (candidate pass MODE 1 + k_refine_exact).  MODE 2 runs the
+// b2 - b1 within the engine's rigorous error bound are re-decided exactly in
+// fp64: KIND 1 rows whose window provably holds two centroids by k_refine_pair,
+// the rest by the candidate pass (MODE 1) + k_refine_exact.  MODE 2 runs the
 // same over a gathered row list and writes Hamerly bounds (bounds.cu).
 //
 // Persistent, warp-specialised CTAs in 2-CTA clusters (CG = 2): each pair runs
@@ -27,15 +28,17 @@
 //   warp 16    TMA producer: ring of S stages, each one 128-B K-atom of C_hi
 //              and C_lo for this CTA's 128 centroids (+ the folded block)
 //   warp 17    MMA issuer (leader CTA, one thread); 2 x 256 fp32 TMEM columns
-//   warps 18-19 TMEM allocator (warp 18), then the X splitter: KIND 0 TMAs an
-//              fp32 staging tile, KIND 1 reads its rows straight from global
-//              (L2-prefetched one tile ahead); both write the double-buffered
-//              hi/lo operand tiles (+ KIND 1's per-row folded A block) + ||x||^2
+//   warps 18-19 TMEM allocator (warp 18), then the X splitter: KIND 0 TMAs two
+//              fp32 staging tiles (two row tiles ahead), KIND 1 reads its rows
+//              straight from global (L2-prefetched one tile ahead; gather4 for
+//              row lists); both write the double-buffered hi/lo operand tiles
+//              (+ KIND 1's per-row folded A block) + ||x||^2
 //   warps 0-15 epilogue, four per SMSP (TMEM lane quarter = warp % 4): each
 //              column quarter scores 64 of the 256 columns of every tile (two
 //              tcgen05.ld.x32 in flight, accumulator released right after) with
 //              4 independent top-2 trackers per thread; quarters merge per row
-//              through shared memory
+//              through shared memory (KIND 1 also keeps the runner-up's index
+//              and a lower bound on every other key: the two-centroid test)
 // X is read from HBM once per pass; C tiles stream from L2.
 #include <cuda.h>
 #include <cuda_fp16.h>

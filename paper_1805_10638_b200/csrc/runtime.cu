@@ -4,8 +4,9 @@
 // sequence whose data-dependent branches (converge / reject) are device
 // predicates (aa.cu), so the same sequence can be launched eagerly or
 // captured once into a CUDA graph and replayed until the device sets `done`.
-// Multi-rank: one ncclAllReduce(sum, fp64) of the packed [S'|N|E|changed]
-// vector per G-evaluation, issued in-stream (and captured in the graph).
+// Multi-rank: one ncclAllReduce(sum, int64) of the packed exact fixed-point
+// [S_hi|S_lo|N|E_hi|E_lo|E|changed] vector per G-evaluation, issued in-stream
+// (and captured in the graph).
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <math.h>
