@@ -613,16 +613,21 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         }
                     }
                 } else {
+                    // the row's source, resolved ONCE (through the row list for MODE 1/2): the
+                    // compiler cannot hoist a load of rows_of past the shared-memory stores below
+                    const long long grow = tile_of(it) * TC_BM + r;
+                    const bool live_row = grow < n_rows;
+                    const long long xrow = !live_row ? 0
+                                         : (MODE == 1 || use_list) ? (long long)__ldg(rows_of + grow) : grow;
+                    const float4* srow = reinterpret_cast<const float4*>(Xsrc + xrow * A * 32);
 #pragma unroll
                     for (int a16 = 0; a16 < NATOM; ++a16) {
 #pragma unroll
                         for (int c16 = 0; c16 < 8; ++c16) {
                             // columns 64 a16 + 8 c16 .. + 8 of row r (zeros past the last row)
-                            const long long grow = tile_of(it) * TC_BM + r;
                             float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-                            if (grow < n_rows) {
-                                const long long xrow = (MODE == 1 || use_list) ? (long long)rows_of[grow] : grow;
-                                const float4* src = reinterpret_cast<const float4*>(Xsrc + xrow * A * 32) + a16 * 16 + c16 * 2;
+                            if (live_row) {
+                                const float4* src = srow + a16 * 16 + c16 * 2;
                                 v0 = __ldg(src); v1 = __ldg(src + 1);
                             }
                             const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
