@@ -14,7 +14,8 @@
  *  - Row-major layouts: X is n_local x d float32, C/G are K x d float32
  *    (centroid-major), labels are int32 in [0, K).
  *  - Ownership: X and the workspace are BORROWED from the caller and must stay
- *    alive and unmodified until kmeans_destroy.  The library allocates no
+ *    alive and unmodified until kmeans_destroy (kmeans_aa_step_host is the
+ *    one call that rewrites X, from the caller's host copy).  The library allocates no
  *    device memory of its own except NCCL's internal buffers (nranks > 1).
  *    Outputs go to caller buffers.
  *  - Streams: all work is enqueued on the stream given to kmeans_create.
@@ -84,7 +85,7 @@ typedef struct {
     int32_t max_iters;   /* cap on passes t (not an error when reached)           */
     double ridge;        /* lambda on the unit-diagonal scaled Gram (R-A14)       */
     int32_t assign_path; /* KMEANS_PATH_*                                        */
-    int32_t timing;      /* 1 = record CUDA events around each assignment launch  */
+    int32_t timing;      /* 1 = CUDA events around each assignment and update   */
     int32_t bounded;     /* 1 = Hamerly-bounded assignment in the Algorithm 1
                             passes (aa_step / run; 2xFP16 engine only, otherwise
                             ignored): per row an upper bound on the distance to
