@@ -314,3 +314,19 @@ def test_exact_two_and_four_way_ties(path):
     ref = oracle.assign(X, C.astype(np.float64))
     np.testing.assert_array_equal(lab.cpu().numpy(), ref)
     assert (ref[n2:] == K).all()                                  # lowest index of the four
+
+
+def test_assign_and_update_timing_hooks():
+    """cfg.timing records one assignment and one update interval per main
+    G-evaluation (branch A); both read back positive and reset on read."""
+    X, C0, c = make("c5", N=70_000, K=256)
+    km = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, timing=True))
+    km.aa_step(dev(C0))
+    km.assign_timing(); km.update_timing()
+    for _ in range(4):
+        km.aa_step(info=False)
+    a_ms, a_n = km.assign_timing()
+    u_ms, u_n = km.update_timing()
+    assert a_n == 4 and u_n == 4 and a_ms > 0 and u_ms > 0
+    assert km.assign_timing() == (0.0, 0) and km.update_timing() == (0.0, 0)
+    km.close()
