@@ -217,8 +217,6 @@ int ora_adjust_m(int m, int m_max, double E_t, double E1, double E2,
     return m;
 }
 
-static double fl32(double v) { return (double)(float)v; }
-
 /* ------------------------------------------------------------------------ */
 /* Algorithm 1 as a state machine, one loop pass per call. */
 typedef struct {
@@ -227,7 +225,6 @@ typedef struct {
     /* config (PAPER.md:177 defaults; R-A18 m0) */
     int32_t m_max; double eps1; double eps2; int32_t dynamic_m;
     int64_t max_iters; double ridge;
-    int32_t parity;       /* 0 exact fp64 state; 1 fp32-rounded G, F, C (c.2) */
     /* state */
     double *C;            /* C^t, K*d                                         */
     double *fallback;     /* C_AU^t = G^{t-1} (R-A3), K*d                     */
@@ -277,10 +274,7 @@ void ora_init(ora_state *s, const double *C0, int32_t m0)
     double *F = (double *)malloc(sizeof(double) * KD);
     ora_assign(s->X, s->N, s->d, C0, s->K, s->labels_prev);
     ora_update(s->X, s->N, s->d, s->labels_prev, s->K, C0, G, NULL);
-    for (int64_t o = 0; o < KD; ++o) {
-        if (s->parity) G[o] = fl32(G[o]);
-        F[o] = s->parity ? fl32(G[o] - C0[o]) : G[o] - C0[o];
-    }
+    for (int64_t o = 0; o < KD; ++o) F[o] = G[o] - C0[o];
     s->hist_count = 0;
     push_hist(s, G, F);
     memcpy(s->C, G, sizeof(double) * KD);
@@ -337,10 +331,7 @@ int ora_pass(ora_state *s)
     double *G = (double *)malloc(sizeof(double) * KD);
     double *F = (double *)malloc(sizeof(double) * KD);
     ora_update(s->X, N, s->d, s->labels, s->K, s->C, G, NULL);
-    for (int64_t o = 0; o < KD; ++o) {
-        if (s->parity) G[o] = fl32(G[o]);
-        F[o] = s->parity ? fl32(G[o] - s->C[o]) : G[o] - s->C[o];
-    }
+    for (int64_t o = 0; o < KD; ++o) F[o] = G[o] - s->C[o];
     push_hist(s, G, F);   /* Ghist[j] = G^{t-j}, Fhist[j] = F^{t-j} */
 
     /* PAPER.md:154  m_t = min(m, t) */
@@ -366,7 +357,7 @@ int ora_pass(ora_state *s)
         for (int j = 1; j <= m_t; ++j)
             v -= s->theta[j - 1] *
                  (s->Ghist[(int64_t)(j - 1) * KD + o] - s->Ghist[(int64_t)j * KD + o]);
-        Cn[o] = s->parity ? fl32(v) : v;
+        Cn[o] = v;
     }
     s->lloyd = all_zero;
 

@@ -42,7 +42,6 @@ class _State(ct.Structure):
         ("X", ct.c_void_p), ("N", ct.c_int64), ("d", ct.c_int32), ("K", ct.c_int32),
         ("m_max", ct.c_int32), ("eps1", ct.c_double), ("eps2", ct.c_double),
         ("dynamic_m", ct.c_int32), ("max_iters", ct.c_int64), ("ridge", ct.c_double),
-        ("parity", ct.c_int32),
         ("C", ct.c_void_p), ("fallback", ct.c_void_p), ("Ghist", ct.c_void_p),
         ("Fhist", ct.c_void_p), ("hist_count", ct.c_int32),
         ("labels_prev", ct.c_void_p), ("labels", ct.c_void_p),
@@ -160,7 +159,6 @@ class OracleConfig:
     dynamic_m: bool = True
     max_iters: int = 10000
     ridge: float = 1e-10
-    parity: bool = False   # c.2 "parity" mode: fp32-rounded G, F, C
 
 
 class AAState:
@@ -184,7 +182,7 @@ class AAState:
         s.X = self.X.ctypes.data; s.N = self.N; s.d = self.d; s.K = K
         c = self.cfg
         s.m_max = c.m_max; s.eps1 = c.eps1; s.eps2 = c.eps2; s.dynamic_m = int(c.dynamic_m)
-        s.max_iters = c.max_iters; s.ridge = c.ridge; s.parity = int(c.parity)
+        s.max_iters = c.max_iters; s.ridge = c.ridge
         s.C = self.C.ctypes.data; s.fallback = self.fallback.ctypes.data
         s.Ghist = self.Ghist.ctypes.data; s.Fhist = self.Fhist.ctypes.data
         s.labels_prev = self.labels_prev.ctypes.data; s.labels = self.labels.ctypes.data
