@@ -239,7 +239,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "tc16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e timed steps (default: --steps)")
     ap.add_argument("--ttc-config", default="c4", help="config run to convergence for time_to_converge ('none' skips)")
     ap.add_argument("--seed-config", default="c5", help="config seeded by kmeans_seed_pp for seed_pp ('none' skips)")
     args = ap.parse_args()
@@ -261,7 +261,7 @@ def main():
     Xs = torch.from_numpy(X).cuda()
     X_host = torch.from_numpy(X).pin_memory()
     C0d = torch.from_numpy(C0).cuda()
-    km = aakm.KMeans(Xs, cfg.K, aakm.config(m0=cfg.m0, assign_path=args.path, timing=True),
+    km = aakm.KMeans(Xs, cfg.K, aakm.config(m0=cfg.m0, assign_path=args.path, timing=True, x_refresh=True),
                      n_global=cfg.N, rank=rank, nranks=world)
     stream = km.stream
 
@@ -301,8 +301,8 @@ def main():
     value = cfg.N * cfg.K * n_assign / (ms_max / 1e3)
 
     # e2e: host inputs, H2D of the shard + D2H of the result inside the timed region
-    C_host = torch.empty(cfg.K, cfg.d, dtype=torch.float32).pin_memory()
-    e2e_steps = max(1, args.e2e_steps)
+    C_host = torch.empty(cfg.K, cfg.d, dtype=torch.float64).pin_memory()
+    e2e_steps = args.e2e_steps if args.e2e_steps > 0 else args.steps
     with torch.cuda.stream(stream):                               # one untimed e2e step (copy stream, events)
         km.aa_step_host(X_host, chunks=E2E_CHUNKS, info=False)
     barrier()
@@ -310,7 +310,7 @@ def main():
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    tmpC = torch.empty(cfg.K, cfg.d, dtype=torch.float32, device="cuda")
+    tmpC = torch.empty(cfg.K, cfg.d, dtype=torch.float64, device="cuda")
     lib = aakm.lib()
     with torch.cuda.stream(stream):
         for _ in range(e2e_steps):
@@ -356,14 +356,16 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32-exact contraction (2xFP16 / 3xTF32 split + fp64 near-tie refine), f64 state",
+        "data": "synthetic",
         "config": {"workload": f"{args.config}: Algorithm 1 passes (m0={cfg.m0}, dynamic m)", "N": cfg.N, "d": cfg.d,
                    "K": cfg.K, "parallelism": f"dp{world}", "assign_path": path,
                    "l2": f"inputs larger than L2 (X shard {n_local * cfg.d * 4 / 1e9:.2f} GB > 126 MB)"},
         "passes": args.steps, "assign_passes": n_assign, "converged_in_window": passes_done is None,
         "iterations_per_s": args.steps / (ms_max / 1e3),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n_local * cfg.d * 4,
-                "d2h_bytes_per_step": cfg.K * cfg.d * 4, "steps": e2e_steps, "wall_s": wall,
+                "d2h_bytes_per_step": cfg.K * cfg.d * 8, "steps": e2e_steps, "wall_s": wall,
                 "h2d": f"pinned host -> device in {E2E_CHUNKS} row chunks overlapping the assignment"},
         "gpu_launches": launches,
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

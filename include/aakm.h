@@ -11,11 +11,14 @@
  *
  * Conventions for every entry point:
  *  - Array pointers are DEVICE pointers unless marked (host).
- *  - Row-major layouts: X is n_local x d float32, C/G are K x d float32
- *    (centroid-major), labels are int32 in [0, K).
+ *  - Row-major layouts: X is n_local x d float32 (the samples, BASELINE.json's
+ *    fp32 data); centroids C, G, C0 are K x d float64 (centroid-major): the
+ *    whole Algorithm 1 state -- C^t, the fallback, the G/F history -- is fp64
+ *    on the device (DESIGN.md R-A17); labels are int32 in [0, K).
  *  - Ownership: X and the workspace are BORROWED from the caller and must stay
- *    alive and unmodified until kmeans_destroy (kmeans_aa_step_host is the
- *    one call that rewrites X, from the caller's host copy).  The library allocates no
+ *    alive and unmodified until kmeans_destroy (the one exception is opt-in:
+ *    with cfg.x_refresh = 1, kmeans_aa_step_host rewrites X from the caller's
+ *    host copy).  The library allocates no
  *    device memory of its own except NCCL's internal buffers (nranks > 1).
  *    Outputs go to caller buffers.
  *  - Streams: all work is enqueued on the stream given to kmeans_create.
@@ -52,7 +55,7 @@ extern "C" {
 #endif
 
 #define KMEANS_M_MAX 30          /* m_bar of PAPER.md:177; ring = m_max + 1 slots */
-#define KMEANS_ABI_VERSION 3
+#define KMEANS_ABI_VERSION 4
 
 typedef struct kmeans_handle kmeans_handle;
 typedef struct CUstream_st *kmeans_stream_t;   /* == cudaStream_t */
@@ -96,6 +99,12 @@ typedef struct {
                             through the tensor engine as a gathered row list.
                             Labels stay exact.  Default 0 (dense: bench.py's
                             dist-evals/s metric counts N*K per pass).            */
+    int32_t x_refresh;   /* 1 = X is a staging buffer that kmeans_aa_step_host
+                            may overwrite from host memory (the e2e path); the
+                            new rows must stay inside the create-time ranges
+                            (max |x_ik|, max ||x_i||), which a device check
+                            enforces.  0 (default): X is never written, and
+                            kmeans_aa_step_host returns INVALID.                 */
 } kmeans_config;
 
 /* Result of kmeans_run (fields per DESIGN.md R-A19). */
@@ -126,15 +135,16 @@ typedef struct {
 } kmeans_step_info;
 
 /* Algorithm 1 state, for checkpoint/resume and lockstep parity tests.
- * All pointers are HOST buffers supplied by the caller:
+ * All pointers are HOST buffers supplied by the caller (fp64, the device
+ * state verbatim):
  *   C, fallback: K*d; Ghist, Fhist: (m_max+1)*K*d, entry 0 = newest
  *   (G^t, F^t), entry j = (G^{t-j}, F^{t-j}); labels_prev: n_local. */
 typedef struct {
-    float *C;            /* C^t, the iterate the next pass evaluates              */
-    float *fallback;     /* C_AU^t = G^{t-1} (R-A3)                               */
-    float *Ghist;
-    float *Fhist;
-    int32_t *labels_prev;/* P^{t-1}                                              */
+    double *C;           /* C^t, the iterate the next pass evaluates              */
+    double *fallback;    /* C_AU^t = G^{t-1} (R-A3)                               */
+    double *Ghist;
+    double *Fhist;
+    int32_t *labels_prev;/* P^{t-1}; for a finished state (done) the final P^t    */
     int32_t hist_count;  /* valid history entries                                 */
     int32_t m;
     int32_t lloyd;       /* C^t is a Lloyd iterate (theta == 0)                   */
@@ -175,7 +185,7 @@ AAKM_API kmeans_status kmeans_create(kmeans_handle **out /*host*/, const float *
  * C: K x d.  labels_out: n_local (exact nearest centroid, lowest index on
  * exact fp64 ties).  energy_out / changed_out are GLOBAL (allreduced) host
  * scalars, may be NULL; changed is 0 when labels_prev is NULL.  Synchronises. */
-AAKM_API kmeans_status kmeans_assign(kmeans_handle *h, const float *C, const int32_t *labels_prev,
+AAKM_API kmeans_status kmeans_assign(kmeans_handle *h, const double *C, const int32_t *labels_prev,
                             int32_t *labels_out, double *energy_out /*host*/,
                             int64_t *changed_out /*host*/);
 
@@ -183,26 +193,26 @@ AAKM_API kmeans_status kmeans_assign(kmeans_handle *h, const float *C, const int
  * all ranks; an empty cluster keeps C_prev's row (R-A15).  labels: n_local in
  * [0, K) (out-of-range -> INVALID after the sync).  counts_out: K int64
  * device, nullable.  Synchronises (to report label errors). */
-AAKM_API kmeans_status kmeans_update(kmeans_handle *h, const int32_t *labels, const float *C_prev,
-                            float *G_out, int64_t *counts_out);
+AAKM_API kmeans_status kmeans_update(kmeans_handle *h, const int32_t *labels, const double *C_prev,
+                            double *G_out, int64_t *counts_out);
 
 /* Algorithm 1, one step.  C0 != NULL: line 1 -- P^0 =
  * Assign(C^0), C^1 = G(C^0), F^0 = C^1 - C^0, E^0 = +inf, m = m0, t = 1.
  * C0 == NULL: one loop pass t under rule R3 (R-A10).
  * info/theta_out (host, nullable; theta_out >= m_max doubles): when either is
  * non-NULL the call synchronises; otherwise it is asynchronous. */
-AAKM_API kmeans_status kmeans_aa_step(kmeans_handle *h, const float *C0, kmeans_step_info *info /*host*/,
+AAKM_API kmeans_status kmeans_aa_step(kmeans_handle *h, const double *C0, kmeans_step_info *info /*host*/,
                              double *theta_out /*host*/);
 
 /* Algorithm 1 to convergence (rule R3) or max_iters, without a host sync per
  * pass (CUDA-graph replay, device-side control).  C_out: K x d (global,
  * identical on all ranks), labels_out: n_local; both nullable.  Synchronises. */
-AAKM_API kmeans_status kmeans_run(kmeans_handle *h, const float *C0, float *C_out, int32_t *labels_out,
+AAKM_API kmeans_status kmeans_run(kmeans_handle *h, const double *C0, double *C_out, int32_t *labels_out,
                          kmeans_report *rep /*host*/);
 
 /* Current iterate C^t and the labels of the last assignment (device copies).
  * Asynchronous. */
-AAKM_API kmeans_status kmeans_get_centroids(kmeans_handle *h, float *C_out, int32_t *labels_out);
+AAKM_API kmeans_status kmeans_get_centroids(kmeans_handle *h, double *C_out, int32_t *labels_out);
 
 /* Checkpoint / lockstep hooks (host buffers, see kmeans_state).  Synchronise.
  * export: the state between two passes (after kmeans_aa_step / kmeans_run).
@@ -221,7 +231,7 @@ AAKM_API kmeans_status kmeans_state_import(kmeans_handle *h, const kmeans_state 
  * values sum to the global E).  labels_prev nullable (changed = 0).
  * Synchronises. */
 AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *labels,
-                                     const int32_t *labels_prev, const float *C,
+                                     const int32_t *labels_prev, const double *C,
                                      double *packed_out);
 
 /* K-Means++ seeding (Arthur & Vassilvitskii 2007, which the paper uses among
@@ -248,10 +258,16 @@ AAKM_API kmeans_status kmeans_seed_pp(kmeans_handle *h, const double *u /*host*/
  * (clamped to [1, 64]) on a private copy stream, and the dense tensor-core
  * assignment starts on each block as soon as it has landed, so the transfer
  * overlaps the contraction. Other engines (SIMT, cfg.bounded) copy first,
- * then run the pass. Requires a started run (kmeans_aa_step with C0).
+ * then run the pass. Requires a started run (kmeans_aa_step with C0) and
+ * cfg.x_refresh = 1 at create.  X_host's rows must lie inside the create-time
+ * ranges of X (max |x_ik| and max ||x_i|| of the shard given to kmeans_create:
+ * every operand scale and fixed-point scale was derived from them); a device
+ * check after the copy enforces it, and a violation poisons the handle, reported
+ * as INVALID by the next synchronising call (step info, kmeans_run).  The
+ * bounded engine's per-row bounds are reset (new rows).
  * Asynchronous unless info/theta are requested; X_host must stay valid until
  * the stream has passed this call. Collective when nranks > 1. Errors: INVALID
- * for a NULL X_host with n_local > 0. */
+ * for a NULL X_host with n_local > 0 or cfg.x_refresh = 0. */
 AAKM_API kmeans_status kmeans_aa_step_host(kmeans_handle *h, const float *X_host /*host*/, int32_t chunks,
                                            kmeans_step_info *info /*host*/, double *theta_out /*host*/);
 

@@ -34,7 +34,8 @@ class AAKMError(RuntimeError):
 class Config(ct.Structure):
     _fields_ = [("m0", ct.c_int32), ("m_max", ct.c_int32), ("eps1", ct.c_double), ("eps2", ct.c_double),
                 ("dynamic_m", ct.c_int32), ("max_iters", ct.c_int32), ("ridge", ct.c_double),
-                ("assign_path", ct.c_int32), ("timing", ct.c_int32), ("bounded", ct.c_int32)]
+                ("assign_path", ct.c_int32), ("timing", ct.c_int32), ("bounded", ct.c_int32),
+                ("x_refresh", ct.c_int32)]
 
 
 class Report(ct.Structure):
@@ -112,7 +113,7 @@ def header_symbols():
 
 
 def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000, ridge=1e-10,
-           assign_path="auto", timing=False, bounded=False) -> Config:
+           assign_path="auto", timing=False, bounded=False, x_refresh=False) -> Config:
     """Algorithm 1 settings (m0 = 5 per BASELINE configs, reading R-A18)."""
     c = Config()
     c.m0, c.m_max, c.eps1, c.eps2 = m0, m_max, eps1, eps2
@@ -120,6 +121,7 @@ def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000,
     c.assign_path = PATHS[assign_path] if isinstance(assign_path, str) else int(assign_path)
     c.timing = int(timing)
     c.bounded = int(bounded)
+    c.x_refresh = int(x_refresh)
     return c
 
 
@@ -188,9 +190,10 @@ class KMeans:
     def _c(self, rc):
         self._check(rc, self.h)
 
-    def _f32(self, C):
+    def _f64(self, C):
+        """Centroids as a contiguous K x d float64 device tensor (the ABI's fp64 state)."""
         t = self.torch
-        C = t.as_tensor(C, dtype=t.float32, device=self.device).reshape(self.K, self.d).contiguous()
+        C = t.as_tensor(C, dtype=t.float64, device=self.device).reshape(self.K, self.d).contiguous()
         return C
 
     def _i32(self, L):
@@ -208,7 +211,7 @@ class KMeans:
     def assign(self, C, labels_prev=None):
         """Eq. 3 labels, global E(P, C) and #changed vs labels_prev."""
         t = self.torch
-        C = self._f32(C)
+        C = self._f64(C)
         lp = None if labels_prev is None else self._i32(labels_prev)
         out = t.empty(self.n, dtype=t.int32, device=self.device)
         E, ch = ct.c_double(), ct.c_int64()
@@ -219,7 +222,7 @@ class KMeans:
         """Eq. 4 means (global), empty clusters keep C_prev; returns (G, counts)."""
         t = self.torch
         labels = self._i32(labels)
-        C_prev = self._f32(C_prev)
+        C_prev = self._f64(C_prev)
         G = t.empty_like(C_prev)
         cnt = t.empty(self.K, dtype=t.int64, device=self.device)
         self._c(lib().kmeans_update(self.h, _ptr(labels), _ptr(C_prev), _ptr(G), _ptr(cnt)))
@@ -228,7 +231,7 @@ class KMeans:
     def update_partials(self, labels, C, labels_prev=None):
         t = self.torch
         labels = self._i32(labels)
-        C = self._f32(C)
+        C = self._f64(C)
         lp = None if labels_prev is None else self._i32(labels_prev)
         out = t.empty(self.K * self.d + self.K + 2, dtype=t.float64, device=self.device)
         self._c(lib().kmeans_update_partials(self.h, _ptr(labels), _ptr(lp), _ptr(C), _ptr(out)))
@@ -236,7 +239,7 @@ class KMeans:
 
     def aa_step(self, C0=None, info=True):
         """Algorithm 1 line 1 (C0 given) or one loop pass; returns the pass info dict (or None)."""
-        C0 = None if C0 is None else self._f32(C0)
+        C0 = None if C0 is None else self._f64(C0)
         if not info:
             self._c(lib().kmeans_aa_step(self.h, _ptr(C0), None, None))
             return None
@@ -270,7 +273,7 @@ class KMeans:
     def run(self, C0):
         """Algorithm 1 to convergence (rule R3); returns (C, labels, report dict)."""
         t = self.torch
-        C0 = self._f32(C0)
+        C0 = self._f64(C0)
         C = t.empty_like(C0)
         labels = t.empty(self.n, dtype=t.int32, device=self.device)
         rep = Report()
@@ -279,7 +282,7 @@ class KMeans:
 
     def centroids(self):
         t = self.torch
-        C = t.empty(self.K, self.d, dtype=t.float32, device=self.device)
+        C = t.empty(self.K, self.d, dtype=t.float64, device=self.device)
         lab = t.empty(self.n, dtype=t.int32, device=self.device)
         self._c(lib().kmeans_get_centroids(self.h, _ptr(C), _ptr(lab)))
         self.stream.synchronize()
@@ -288,8 +291,8 @@ class KMeans:
     def state_export(self):
         H = self.cfg.m_max + 1
         KD = self.K * self.d
-        C = np.zeros(KD, np.float32); fb = np.zeros(KD, np.float32)
-        Gh = np.zeros(H * KD, np.float32); Fh = np.zeros(H * KD, np.float32)
+        C = np.zeros(KD, np.float64); fb = np.zeros(KD, np.float64)
+        Gh = np.zeros(H * KD, np.float64); Fh = np.zeros(H * KD, np.float64)
         lp = np.zeros(max(self.n, 1), np.int32)
         gr = np.zeros(H * H, np.float64)
         s = State()
@@ -311,11 +314,11 @@ class KMeans:
         KD = self.K * self.d
         hc = int(st["hist_count"])
         H = self.cfg.m_max + 1
-        C = np.ascontiguousarray(st["C"], np.float32).reshape(KD)
-        fb = np.ascontiguousarray(st["fallback"], np.float32).reshape(KD)
-        Gh = np.zeros(H * KD, np.float32); Fh = np.zeros(H * KD, np.float32)
-        Gh[: hc * KD] = np.ascontiguousarray(st["Ghist"], np.float32).reshape(-1)[: hc * KD]
-        Fh[: hc * KD] = np.ascontiguousarray(st["Fhist"], np.float32).reshape(-1)[: hc * KD]
+        C = np.ascontiguousarray(st["C"], np.float64).reshape(KD)
+        fb = np.ascontiguousarray(st["fallback"], np.float64).reshape(KD)
+        Gh = np.zeros(H * KD, np.float64); Fh = np.zeros(H * KD, np.float64)
+        Gh[: hc * KD] = np.ascontiguousarray(st["Ghist"], np.float64).reshape(-1)[: hc * KD]
+        Fh[: hc * KD] = np.ascontiguousarray(st["Fhist"], np.float64).reshape(-1)[: hc * KD]
         lp = np.ascontiguousarray(st["labels_prev"], np.int32).reshape(-1)
         gr = np.ascontiguousarray(st["gram"], np.float64) if with_gram else None
         s = State()

@@ -27,7 +27,9 @@ namespace aakm {
 // mode 0: mix from (st->alpha, st->alpha_slot, st->n_alpha), active if !done
 // mode 1: C <- G[st->fb_slot] (fallback C_AU^t = G^{t-1}, R-A3), active if reject
 // mode 2: C <- src (caller centroids / C^0), always
-__global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const float* src) {
+// C^t is fp64 (the whole Anderson state is, R-A17); the engines' operands are
+// derived from it here: fl32(C) for SIMT, the tf32 hi/lo split of -C, ||c||^2.
+__global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const double* src) {
     DevState* st = d.st;
     if (mode == 0 && st->done) return;
     if (mode == 1 && (st->done || !st->reject)) return;
@@ -38,7 +40,7 @@ __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const float* s
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
     int na = 1;
     double al[AAKM_H_SLOTS];
-    const float* base[AAKM_H_SLOTS];
+    const double* base[AAKM_H_SLOTS];
     if (mode == 0) {
         na = st->n_alpha;
         for (int q = 0; q < na; ++q) { al[q] = st->alpha[q]; base[q] = d.Gring + (long long)st->alpha_slot[q] * KD; }
@@ -52,35 +54,35 @@ __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const float* s
         double nrm = 0.0;
         for (int k = lane; k < D; k += 32) {
             const long long e = j * D + k;
-            float c;
+            double c;
             if (na == 1 && al[0] == 1.0) {
                 c = base[0][e];
             } else {
-                double v = 0.0;
-                for (int q = 0; q < na; ++q) v = fma(al[q], (double)base[q][e], v);
-                c = (float)v;
+                c = 0.0;
+                for (int q = 0; q < na; ++q) c = fma(al[q], base[q][e], c);   // C^{t+1} = sum_j alpha_j G^{t-j}
             }
             d.C[e] = c;
+            if (d.C32) d.C32[e] = (float)c;
             // tensor operands hold -c (the engine accumulates ||c||^2/2 - x.c directly)
-            const float hi = __uint_as_float(__float_as_uint(-c) & 0xFFFFE000u);  // tf32 truncation
+            const float hi = __uint_as_float(__float_as_uint((float)-c) & 0xFFFFE000u);   // tf32 truncation
             d.Chi[e] = hi;
-            d.Clo[e] = -c - hi;                                              // exact in fp32
-            nrm = fma((double)c, (double)c, nrm);
+            d.Clo[e] = (float)(-c - (double)hi);
+            nrm = fma(c, c, nrm);
         }
         for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
         const float cnj = (float)nrm;
         if (lane == 0) d.cn[j] = cnj;
         if (d.cnimg && d.tc_kind == 0 && lane < 8) {
-            // 3xTF32 engine: ||c||^2/2 = h + m + l exactly (3 x 11 significand bits >= 24),
+            // 3xTF32 engine: ||c||^2/2 = h + m + l to ~33 bits (3 tf32 parts of the fp64 value),
             // row j of the folded K block; the A side holds (1, 1, 1, 0, ...)
-            const float v = 0.5f * cnj;
-            const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-            const float m = __uint_as_float(__float_as_uint(v - h) & 0xFFFFE000u);
-            const float l = v - h - m;
+            const double v = 0.5 * nrm;
+            const float h = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
+            const float m = __uint_as_float(__float_as_uint((float)(v - (double)h)) & 0xFFFFE000u);
+            const float l = (float)(v - (double)h - (double)m);
             const float val = lane == 0 ? h : lane == 1 ? m : lane == 2 ? l : 0.f;
             *reinterpret_cast<float*>(d.cnimg + (size_t)(j >> 7) * AAKM_CNIMG_BYTES + cnimg_off((int)(j & 127), lane * 4)) = val;
         }
-        bmax = fmaxf(bmax, cnj);
+        bmax = fmaxf(bmax, __double2float_ru(nrm));
     }
     // max ||c||^2: per-block max -> atomicMax into cmax2_tmp; last block publishes and resets
     for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const float* s
     }
 }
 
-void launch_combine(const Dev& d, int mode, const float* src, cudaStream_t s) {
+void launch_combine(const Dev& d, int mode, const double* src, cudaStream_t s) {
     long long warps = d.K;
     int blocks = (int)((warps + 7) / 8);
     if (blocks > 1184) blocks = 1184;
@@ -173,15 +175,15 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
     const long long KD = (long long)d.K * D;
     const long long* pk = st->reject ? d.packed[1] : d.packed[0];
     const long long slot = st->t % d.H;
-    float* G = d.Gring + slot * KD;
-    float* F = d.Fring + slot * KD;
+    double* G = d.Gring + slot * KD;
+    double* F = d.Fring + slot * KD;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
          e += (long long)gridDim.x * blockDim.x) {
         const long long nj = pk[pk_n(d) + e / D];
-        const float c = d.C[e];
-        const float g = nj > 0 ? (float)(fx_value(pk[e], pk[KD + e], d.fx_inv) / (double)nj) : c;   // G = S / N (Eq. 4)
+        const double c = d.C[e];
+        const double g = nj > 0 ? fx_value(pk[e], pk[KD + e], d.fx_inv) / (double)nj : c;   // G = S / N (Eq. 4)
         G[e] = g;
-        F[e] = g - c;                                            // F^t = G^t - C^t (fp32)
+        F[e] = g - c;                                            // F^t = G^t - C^t (fp64)
     }
 }
 
@@ -195,7 +197,7 @@ void launch_finalize(const Dev& d, cudaStream_t s) {
 // ---------------------------------------------------------------- gram
 // For the window tau = t, t-1, ..., t-W+1 (W = min(t, H-1)):
 //   q < W : <dF(t), dF(t-q)>,   q >= W : <dF(t-(q-W)), F^t>,
-// dF(tau) = F^tau - F^{tau-1} formed exactly in fp64 from the fp32 ring.
+// dF(tau) = F^tau - F^{tau-1} formed in fp64 from the fp64 ring.
 __global__ void __launch_bounds__(128) k_gram(Dev d) {
     DevState* st = d.st;
     if (st->done || st->init_mode) return;
@@ -206,18 +208,18 @@ __global__ void __launch_bounds__(128) k_gram(Dev d) {
     double acc_g[AAKM_H_SLOTS - 1], acc_b[AAKM_H_SLOTS - 1];
 #pragma unroll
     for (int q = 0; q < AAKM_H_SLOTS - 1; ++q) { acc_g[q] = 0.0; acc_b[q] = 0.0; }
-    const float* F[AAKM_H_SLOTS];
+    const double* F[AAKM_H_SLOTS];
     for (int q = 0; q <= W; ++q) F[q] = d.Fring + ((t - q) % H) * KD;   // F^{t-q}
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
          e += (long long)gridDim.x * blockDim.x) {
-        const double ft = (double)F[0][e];
+        const double ft = F[0][e];
         double prev = ft;
         double dft = 0.0;
 #pragma unroll
         for (int q = 0; q < AAKM_H_SLOTS - 1; ++q) {
             if (q < W) {
-                const double older = (double)F[q + 1][e];
-                const double df = prev - older;                  // dF(t-q), exact
+                const double older = F[q + 1][e];
+                const double df = prev - older;                  // dF(t-q)
                 if (q == 0) dft = df;
                 acc_g[q] = fma(dft, df, acc_g[q]);
                 acc_b[q] = fma(df, ft, acc_b[q]);
@@ -431,9 +433,14 @@ __global__ void k_advance(Dev d) {
     }
     st->E2 = st->E1; st->E1 = st->E_final;
     st->hist_count = st->hist_count + 1 < d.H ? st->hist_count + 1 : d.H;
-    st->cur ^= 1;
     st->t += 1;
-    if (st->t > d.max_iters) { st->done = 1; st->converged = 0; st->final_traced = 1; }
+    if (st->t > d.max_iters) {
+        // stop (not converged) with C = C^{t+1} and the labels P^t of the pass just
+        // run; cur is NOT flipped, so lab[cur] holds P^t as after a converged stop
+        st->done = 1; st->converged = 0; st->final_traced = 1;
+        return;
+    }
+    st->cur ^= 1;
 }
 
 void launch_advance(const Dev& d, cudaStream_t s) { k_advance<<<1, 1, 0, s>>>(d); }

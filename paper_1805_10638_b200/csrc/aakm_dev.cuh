@@ -67,9 +67,10 @@ struct Dev {
     long long max_iters;
     double eps1, eps2, ridge;
     DevState* st;
-    float* C;             // current iterate C^t (K x d)
-    float* Chi;           // tf32(C) (tensor path)
-    float* Clo;           // C - tf32(C)
+    double* C;            // current iterate C^t (K x d, fp64: the Anderson state is fp64, R-A17)
+    float* C32;           // fl32(C^t): the SIMT engine's operand (its bound adds |c - fl32(c)|)
+    float* Chi;           // tf32(-C) (tensor path)
+    float* Clo;           // -C - tf32(-C) rounded to fp32
     float* cn;            // ||c_j||^2 (fp32, from fp64)
     uint8_t* cnimg;       // tensor engines: ||c||^2/2 column block per 128-centroid tile, UMMA
                           // no-swizzle K-major image (AAKM_CNIMG_BYTES per tile); nullptr on SIMT
@@ -116,14 +117,14 @@ struct Dev {
                           //   both candidates' distances and lb every other centroid's
     int* act_rows;        //   rows the bounds could not prove unchanged (capacity n)
     long long* act_count; //   [2] their counts, branch A / B (zeroed per pass with packed)
-    float* C_ref;         //   centroids the bounds refer to (the last assigned set)
+    double* C_ref;        //   centroids the bounds refer to (the last assigned set)
     float* shift;         //   ||c_j - c_ref_j|| of the set being assigned (K)
     float* ub0;           //   snapshot of (ub, lb, pj2, C_ref) taken before branch A, restored
     float* lb0;           //   for the fallback B on a rejection (bounds w.r.t. the previous
     int* pj20;            //   pass's set instead of the rejected jump)
-    float* C_ref0;
-    float* Gring;         // H x K*d
-    float* Fring;         // H x K*d
+    double* C_ref0;
+    double* Gring;        // H x K*d (fp64)
+    double* Fring;        // H x K*d (fp64)
     double* gram_part;    // AAKM_GRAM_BLOCKS x (2*H)
     TraceRec* trace;
     int nranks;
@@ -132,7 +133,10 @@ struct Dev {
     int gram_blocks;
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
+    int dev;              // CUDA device ordinal of the handle
+    int num_sms;          // its SM count (persistent grids)
 };
+#define AAKM_MAX_DEVICES 64
 
 // Which labels/centroids a G-evaluation kernel works on.
 struct GEval {
@@ -153,7 +157,7 @@ __device__ __forceinline__ bool geval_active(const Dev& d, const GEval& g) {
 }
 
 // ---- launchers (host side, defined in the .cu files) ----
-void launch_combine(const Dev& d, int mode, const float* src, cudaStream_t s);
+void launch_combine(const Dev& d, int mode, const double* src, cudaStream_t s);
 void launch_assign_simt(const Dev& d, const GEval& g, cudaStream_t s);
 void launch_assign_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 void* tc_make_maps(const Dev& d);   // TMA tensor maps of (X, C_hi, C_lo); nullptr if unsupported
@@ -189,11 +193,13 @@ void launch_gram(const Dev& d, cudaStream_t s);
 void launch_solve(const Dev& d, cudaStream_t s);
 void launch_advance(const Dev& d, cudaStream_t s);
 void launch_reset(const Dev& d, cudaStream_t s);
-void launch_update_G(const Dev& d, const long long* packed, const float* Cprev, float* G,
+void launch_update_G(const Dev& d, const long long* packed, const double* Cprev, double* G,
                      long long* counts, cudaStream_t s);
 void launch_energy(const Dev& d, const GEval& g, cudaStream_t s);       // E after the allreduce
-void launch_partials_out(const Dev& d, const long long* packed, const float* C, double* out, cudaStream_t s);
+void launch_partials_out(const Dev& d, const long long* packed, double* out, cudaStream_t s);
 void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
+// st->label_error |= 2 if the stats in out (launch_xstats_max) exceed (amax, nmax2) (float bits)
+void launch_xcheck(const Dev& d, const unsigned int* out, unsigned int amax, unsigned int nmax2, cudaStream_t s);
 
 // fixed-point sums (update.cu) -> fp64: (hi + lo 2^-22) 2^(e-22), exact conversions
 __host__ __device__ inline double fx_value(long long hi, long long lo, double fx_inv) {

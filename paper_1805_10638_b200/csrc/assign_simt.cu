@@ -11,17 +11,19 @@
 // refine.cu, so the labels equal the exact fp64 argmin.
 //
 // Layout: X row-major (n x d) fp32; each thread owns R rows held in
-// registers; C (pre-scaled by -2) and ||c||^2 are staged in shared memory in
+// registers; fl32(C) (pre-scaled by -2) and ||c||^2 are staged in shared memory in
 // K-tiles and read as warp-broadcast vector loads.
 #include "aakm_dev.cuh"
 
 namespace aakm {
 
 // Rigorous bound for the FFMA chain: each score has error
-// <= (d+2) u (||x||^2 + 2 max||c||^2); the gap of two scores twice that.
-// Flag when gap <= 2 * 2 (d+2) u (||x||^2 + cmax2) (factor 2 covers the
-// 2 max||c||^2 term and ||x||^2 evaluated in fp32).
-float tau_gamma_simt(int d) { return 8.0f * (float)(d + 2) * 5.9604645e-8f; }
+// <= (d+2) u (||x||^2 + 2 max||c||^2) for the chain, plus u (||x||^2 + ||c||^2)
+// because the operand is fl32(c) of the fp64 centroid (2 |x.(c - fl32 c)| <=
+// 2u ||x|| ||c||): (d+3) u (||x||^2 + 2 max||c||^2) per score, the gap of two
+// scores twice that.  Flag when gap <= 2 * 2 (d+3) u (||x||^2 + cmax2) (factor
+// 2 covers the 2 max||c||^2 term and ||x||^2 evaluated in fp32).
+float tau_gamma_simt(int d) { return 8.0f * (float)(d + 3) * 5.9604645e-8f; }
 
 template <int D>
 struct RowsPerThread { static constexpr int value = D <= 4 ? 8 : (D <= 16 ? 4 : 2); };
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(256) k_assign_simt(Dev d, GEval g, int KT) {
         const int kc = min(KT, d.K - kt);
         __syncthreads();
         for (int e = threadIdx.x; e < kc * D; e += blockDim.x)
-            cs[e] = -2.0f * d.C[(long long)kt * D + e];
+            cs[e] = -2.0f * d.C32[(long long)kt * D + e];
         for (int e = threadIdx.x; e < kc; e += blockDim.x) cns[e] = d.cn[kt + e];
         __syncthreads();
         for (int j = 0; j < kc; ++j) {
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(128) k_assign_simt_generic(Dev d, GEval g, int
     for (int kt = 0; kt < d.K; kt += KT) {
         const int kc = min(KT, d.K - kt);
         __syncthreads();
-        for (int e = threadIdx.x; e < kc * D; e += RB) cs[e] = -2.0f * d.C[(long long)kt * D + e];
+        for (int e = threadIdx.x; e < kc * D; e += RB) cs[e] = -2.0f * d.C32[(long long)kt * D + e];
         for (int e = threadIdx.x; e < kc; e += RB) cns[e] = d.cn[kt + e];
         __syncthreads();
         for (int j = 0; j < kc; ++j) {

@@ -860,15 +860,19 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         // other centroid (l from L), so k_bounds can keep them off the
                         // tensor engine while the pair stays apart from the rest; other
                         // near-tie rows are always recomputed
+                        // The per-row folded constant (splitter: fl32(xn U + 6) in 22 bits, xn an fp32
+                        // FMA chain) is off from ||x||^2 U + 6 by at most ec; it cancels in every
+                        // comparison of the row but not in these absolute bounds.
+                        const float ec = Usc * xn * (float)(A * 32 + 2) * 5.9604645e-8f + (Usc * xn + 6.0f) * 4.7683716e-7f;
                         float u = INFINITY, l = 0.f;
                         int p2 = -1;
                         if (!flag) {
-                            u = __fsqrt_ru(__fdiv_ru(fmaxf(b1 + tau - 6.0f, 0.0f), Usc)) * 1.000001f;
-                            l = __fsqrt_rd(__fdiv_rd(fmaxf(b2 - tau - 6.0f, 0.0f), Usc)) * 0.999999f;
+                            u = __fsqrt_ru(__fdiv_ru(fmaxf(b1 + tau + ec - 6.0f, 0.0f), Usc)) * 1.000001f;
+                            l = __fsqrt_rd(__fdiv_rd(fmaxf(b2 - tau - ec - 6.0f, 0.0f), Usc)) * 0.999999f;
                         } else if (pair) {
                             const float Lk = wdecode(__uint_as_float(__float_as_uint(t.L) & ~0xFFFu));
-                            u = __fsqrt_ru(__fdiv_ru(fmaxf(b2 + tau - 6.0f, 0.0f), Usc)) * 1.000001f;
-                            l = __fsqrt_rd(__fdiv_rd(fmaxf(Lk - tau - 6.0f, 0.0f), Usc)) * 0.999999f;
+                            u = __fsqrt_ru(__fdiv_ru(fmaxf(b2 + tau + ec - 6.0f, 0.0f), Usc)) * 1.000001f;
+                            l = __fsqrt_rd(__fdiv_rd(fmaxf(Lk - tau - ec - 6.0f, 0.0f), Usc)) * 0.999999f;
                             p2 = t.i2;
                         }
                         d.ub[row] = u;
@@ -895,7 +899,6 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 }
 
 // ------------------------------------------------------------------ host side
-static int g_num_sms = 0;
 
 // ||x||^2 ring depth: the splitter runs at most NXB + ceil(NACC/NT) row tiles ahead
 // of the epilogue, so the ring needs one slot more than that (power of two)
@@ -962,11 +965,7 @@ float tau_gamma_tc16(int d) { return 4.0f * (3.0f * 2.3841858e-7f + (3.0f * d / 
     X(4, 1, 0, CG) X(2, 0, 1, CG) X(4, 0, 1, CG) X(2, 1, 1, CG) X(4, 1, 1, CG) X(2, 2, 1, CG) X(4, 2, 1, CG)
 
 cudaError_t setup_tc() {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
 #define AAKM_FN(A_, M_, K_, C_) (const void*)k_assign_tc<A_, M_, K_, C_>,
     const void* fns[] = {AAKM_TC_INSTANCES(AAKM_FN, 1) AAKM_TC_INSTANCES(AAKM_FN, 2)};
 #undef AAKM_FN
@@ -1068,18 +1067,19 @@ static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, con
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
-    int grid = g_num_sms;
+    int grid = d.num_sms;
     if (CG == 2) {
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
         cfg.attrs = at; cfg.numAttrs = 1;
         // pairs that can be co-resident (a persistent grid must not wait on itself)
-        static int max_clusters[2] = {0, 0};
-        int& mc = max_clusters[smem > 200 * 1024 ? 1 : 0];
+        // per device and shared-memory class (written once per value: a benign race)
+        static int max_clusters[AAKM_MAX_DEVICES][2] = {};
+        int& mc = max_clusters[d.dev & (AAKM_MAX_DEVICES - 1)][smem > 200 * 1024 ? 1 : 0];
         if (mc == 0) {
-            cfg.gridDim = dim3(g_num_sms & ~1);
+            cfg.gridDim = dim3(d.num_sms & ~1);
             if (cudaOccupancyMaxActiveClusters(&mc, (const void*)k_assign_tc<A, MODE, KIND, CG>, &cfg) != cudaSuccess || mc < 1)
-                mc = g_num_sms / 2;
+                mc = d.num_sms / 2;
             cudaGetLastError();
         }
         grid = 2 * mc;
@@ -1166,10 +1166,10 @@ __global__ void __launch_bounds__(256) k_csplit16(Dev d, int mode) {
     __half* hi = reinterpret_cast<__half*>(d.Chi16);
     __half* lo = reinterpret_cast<__half*>(d.Clo16);
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
-        const float v = -d.C[e] * inv;                   // operands hold -c (scores accumulate directly)
-        const __half h = __float2half_rn(v);
+        const double v = -d.C[e] * (double)inv;          // operands hold -c (scores accumulate directly)
+        const __half h = __double2half(v);               // from the fp64 C^t: h + l carries 22 bits of it
         hi[e] = h;
-        lo[e] = __float2half_rn(v - __half2float(h));
+        lo[e] = __double2half(v - (double)__half2float(h));
     }
     if (d.cnimg) {
         // B side of the folded block: (h, l) of ||c_j||^2 / (2 s^2) <= 32, then (1, 1) which
@@ -1248,7 +1248,7 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
             for (int v = 0; v < 4; ++v) {
                 const int k = lane + 32 * v;
                 if (k < D) {
-                    const double df = xv[v] - (double)__ldg(d.C + (long long)j * D + k);
+                    const double df = xv[v] - __ldg(d.C + (long long)j * D + k);
                     acc = fma(df, df, acc);
                 }
             }
@@ -1264,7 +1264,7 @@ __global__ void __launch_bounds__(256) k_refine_exact(Dev d, GEval g) {
 }
 
 // Exact fp64 decision between the two centroids of each two-centroid near-tie
-// row: direct differences (Eq. 3), LPR = d/4 lanes per row with a float4 each
+// row: direct differences (Eq. 3), LPR = d/4 lanes per row with 4 coordinates each
 // and a fixed xor-tree sum; lowest index on exact ties. Two row groups per warp
 // step keep more loads in flight.
 template <int LPR>
@@ -1277,12 +1277,13 @@ __global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
     long long np = d.pair_count[g.branch];
     if (np > d.fcap) np = d.fcap;
     const float4* X4 = reinterpret_cast<const float4*>(d.X);
-    const float4* C4 = reinterpret_cast<const float4*>(d.C);
+    const double2* C2 = reinterpret_cast<const double2*>(d.C);
     const long long W = (long long)gridDim.x * 8;
     for (long long f0 = ((long long)blockIdx.x * 8 + warp) * RPW * 2; f0 < np; f0 += W * RPW * 2) {
         long long row[2];
         int2 jj[2];
-        float4 x[2], c0[2], c1[2];
+        float4 x[2];
+        double2 c0[2][2], c1[2][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const long long f = f0 + u * RPW + h;
@@ -1293,20 +1294,20 @@ __global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             x[u] = X4[row[u] * LPR + c4i];
-            c0[u] = C4[(long long)jj[u].x * LPR + c4i];
-            c1[u] = C4[(long long)jj[u].y * LPR + c4i];
+            c0[u][0] = C2[((long long)jj[u].x * LPR + c4i) * 2]; c0[u][1] = C2[((long long)jj[u].x * LPR + c4i) * 2 + 1];
+            c1[u][0] = C2[((long long)jj[u].y * LPR + c4i) * 2]; c1[u][1] = C2[((long long)jj[u].y * LPR + c4i) * 2 + 1];
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             double a0, a1, t;
-            t = (double)x[u].x - (double)c0[u].x; a0 = t * t;
-            t = (double)x[u].y - (double)c0[u].y; a0 = fma(t, t, a0);
-            t = (double)x[u].z - (double)c0[u].z; a0 = fma(t, t, a0);
-            t = (double)x[u].w - (double)c0[u].w; a0 = fma(t, t, a0);
-            t = (double)x[u].x - (double)c1[u].x; a1 = t * t;
-            t = (double)x[u].y - (double)c1[u].y; a1 = fma(t, t, a1);
-            t = (double)x[u].z - (double)c1[u].z; a1 = fma(t, t, a1);
-            t = (double)x[u].w - (double)c1[u].w; a1 = fma(t, t, a1);
+            t = (double)x[u].x - c0[u][0].x; a0 = t * t;
+            t = (double)x[u].y - c0[u][0].y; a0 = fma(t, t, a0);
+            t = (double)x[u].z - c0[u][1].x; a0 = fma(t, t, a0);
+            t = (double)x[u].w - c0[u][1].y; a0 = fma(t, t, a0);
+            t = (double)x[u].x - c1[u][0].x; a1 = t * t;
+            t = (double)x[u].y - c1[u][0].y; a1 = fma(t, t, a1);
+            t = (double)x[u].z - c1[u][1].x; a1 = fma(t, t, a1);
+            t = (double)x[u].w - c1[u][1].y; a1 = fma(t, t, a1);
 #pragma unroll
             for (int o = 1; o < LPR; o <<= 1) {
                 a0 += __shfl_xor_sync(0xffffffffu, a0, o);
@@ -1325,12 +1326,12 @@ __global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
 int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s) {
     // the 2xFP16 engine reads the flagged rows in place (DX splitter); 3xTF32 TMAs a gathered copy
     const int gather = d.tc_kind == 1 ? 0 : 1;
-    if (gather) k_gather_flagged<<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    if (gather) k_gather_flagged<<<4 * d.num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
-    k_refine_exact<<<4 * g_num_sms, 256, 0, s>>>(d, g);
+    k_refine_exact<<<4 * d.num_sms, 256, 0, s>>>(d, g);
     if (d.tc_kind == 1) {                                          // d in {64, 128}
-        if (d.d == 64) k_refine_pair<16><<<4 * g_num_sms, 256, 0, s>>>(d, g);
-        else k_refine_pair<32><<<4 * g_num_sms, 256, 0, s>>>(d, g);
+        if (d.d == 64) k_refine_pair<16><<<4 * d.num_sms, 256, 0, s>>>(d, g);
+        else k_refine_pair<32><<<4 * d.num_sms, 256, 0, s>>>(d, g);
     }
     return 2 + gather + (d.tc_kind == 1 ? 1 : 0);
 }

@@ -25,7 +25,7 @@ namespace aakm {
 __global__ void __launch_bounds__(256) k_shift(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     DevState* st = d.st;
-    const float* C = d.C;
+    const double* C = d.C;
     const int D = d.d;
     const int lane = threadIdx.x & 31;
     float bmax = 0.f;
@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(256) k_shift(Dev d, GEval g) {
          j += (long long)gridDim.x * (blockDim.x >> 5)) {
         double s = 0.0;
         for (int k = lane; k < D; k += 32) {
-            const float c = C[j * D + k];
-            const double df = (double)c - (double)d.C_ref[j * D + k];
+            const double c = C[j * D + k];
+            const double df = c - d.C_ref[j * D + k];
             s = fma(df, df, s);
             d.C_ref[j * D + k] = c;
         }
@@ -159,11 +159,11 @@ __global__ void __launch_bounds__(256) k_bnd_save(Dev d, GEval g, int restore) {
     float* ub = restore ? d.ub : d.ub0;
     float* lb = restore ? d.lb : d.lb0;
     int* p2 = restore ? d.pj2 : d.pj20;
-    float* cr = restore ? d.C_ref : d.C_ref0;
+    double* cr = restore ? d.C_ref : d.C_ref0;
     const float* ubs = restore ? d.ub0 : d.ub;
     const float* lbs = restore ? d.lb0 : d.lb;
     const int* p2s = restore ? d.pj20 : d.pj2;
-    const float* crs = restore ? d.C_ref0 : d.C_ref;
+    const double* crs = restore ? d.C_ref0 : d.C_ref;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
         ub[i] = ubs[i]; lb[i] = lbs[i]; p2[i] = p2s[i];
     }

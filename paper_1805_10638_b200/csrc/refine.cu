@@ -8,18 +8,18 @@
 // __d*_rn intrinsics so no FMA contraction changes the result.
 //
 // Two phases per flagged row (one warp per row):
-//  1. fp32 candidate filter: the same FFMA-chain score as assign_simt.cu for
+//  1. fp32 candidate filter: the same FFMA-chain score on fl32(C) as assign_simt.cu for
 //     every centroid; with the rigorous fp32 bound e, only centroids with
 //     score <= min score + 2e can be the exact argmin;
-//  2. fp64 exact distances for those candidates only.
+//  2. fp64 distances to the fp64 centroids for those candidates only.
 #include "aakm_dev.cuh"
 
 namespace aakm {
 
-__device__ __forceinline__ double exact_sqdist(const float* __restrict__ x, const float* __restrict__ c, int D) {
+__device__ __forceinline__ double exact_sqdist(const float* __restrict__ x, const double* __restrict__ c, int D) {
     double acc = 0.0;
     for (int k = 0; k < D; ++k) {
-        double diff = __dsub_rn((double)x[k], (double)c[k]);
+        double diff = __dsub_rn((double)x[k], c[k]);
         acc = __dadd_rn(acc, __dmul_rn(diff, diff));
     }
     return acc;
@@ -48,15 +48,15 @@ __global__ void __launch_bounds__(256) k_refine(Dev d, GEval g, long long first)
         // phase 1: fp32 scores and their minimum
         float best = INFINITY;
         for (int j = lane; j < d.K; j += 32) {
-            const float* c = d.C + (long long)j * D;
+            const float* c = d.C32 + (long long)j * D;
             float s = d.cn[j];
             for (int k = 0; k < D; ++k) s = fmaf(xw[k], -2.0f * c[k], s);
             best = fminf(best, s);
         }
         for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
-        // 2e with e the per-score bound of the fp32 chain (same gamma as the SIMT engine)
-        const float lim = best + 8.0f * (float)(D + 2) * 5.9604645e-8f * (xn + cmax2);
+        // 2e with e the per-score bound of the fp32 chain on fl32(C) (the SIMT engine's gamma)
+        const float lim = best + 8.0f * (float)(D + 3) * 5.9604645e-8f * (xn + cmax2);
         // phase 2: exact fp64 on candidates (recompute s; collect in smem, overflow -> all)
         int ncand = 0;
         bool overflow = false;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_refine(Dev d, GEval g, long long first)
             int j = j0 + lane;
             bool isc = false;
             if (j < d.K) {
-                const float* c = d.C + (long long)j * D;
+                const float* c = d.C32 + (long long)j * D;
                 float s = d.cn[j];
                 for (int k = 0; k < D; ++k) s = fmaf(xw[k], -2.0f * c[k], s);
                 isc = s <= lim;

@@ -16,6 +16,7 @@
 
 #include <string>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "../../include/aakm.h"
@@ -58,6 +59,8 @@ struct kmeans_handle {
     long long feed_tiles = 0;                                // row tiles per chunk (even)
     cudaEvent_t run_ev[2] = {nullptr, nullptr};
     int* done_host = nullptr;                                // pinned
+    unsigned int* xchk = nullptr;                            // device, 2 words: stats of a refreshed X
+    unsigned int x_stat[2] = {0u, 0u};                       // this rank's create-time max |x|, max ||x||^2 (float bits)
 };
 
 static thread_local std::string g_create_err;
@@ -142,10 +145,10 @@ static void dbg(const char* what, cudaStream_t s) {
 // ------------------------------------------------------------------ layout
 namespace {
 struct Layout {
-    size_t st, st_api, C, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
+    size_t st, st_api, C, C32, Ca32, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, total,
+        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, total,
         scratch_bytes;
 };
 
@@ -162,10 +165,10 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     auto take = [&](size_t bytes) { size_t r = o; o = al(o + bytes); return r; };
     L.st = take(sizeof(DevState));
     L.st_api = take(sizeof(DevState));
-    L.C = take(KD * 4); L.Chi = take(KD * 4); L.Clo = take(KD * 4); L.cn = take((size_t)K * 4);
+    L.C = take(KD * 8); L.C32 = take(KD * 4); L.Chi = take(KD * 4); L.Clo = take(KD * 4); L.cn = take((size_t)K * 4);
     const size_t cnimg = (size_t)((K + 127) / 128) * AAKM_CNIMG_BYTES;
     L.cnimg = take(cnimg);
-    L.Ca = take(KD * 4); L.Cahi = take(KD * 4); L.Calo = take(KD * 4); L.cna = take((size_t)K * 4);
+    L.Ca = take(KD * 8); L.Ca32 = take(KD * 4); L.Cahi = take(KD * 4); L.Calo = take(KD * 4); L.cna = take((size_t)K * 4);
     L.cnimga = take(cnimg);
     L.C16h = take(KD * 2); L.C16l = take(KD * 2); L.Ca16h = take(KD * 2); L.Ca16l = take(KD * 2);
     L.lab0 = take((size_t)n * 4); L.lab1 = take((size_t)n * 4);
@@ -198,16 +201,17 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.seed_x = take((size_t)(d + 2) * 4);
     L.seed_idx = take((size_t)K * 8);
     L.seed_u = take((size_t)K * 8);
-    L.Gring = take((size_t)H * KD * 4);
-    L.Fring = take((size_t)H * KD * 4);
+    L.Gring = take((size_t)H * KD * 8);             // fp64 Anderson history (R-A17)
+    L.Fring = take((size_t)H * KD * 8);
     L.gram_part = take((size_t)AAKM_GRAM_BLOCKS * 2 * AAKM_H_SLOTS * 8);
     L.trace = take((size_t)AAKM_TRACE_CAP * sizeof(TraceRec));
     // bounded engine (2xFP16, cfg.bounded): 12 B per row + 2 centroid-sized arrays
     const size_t nb = bounded ? (size_t)n : 0;
     L.ub = take(nb * 4 + 4); L.lb = take(nb * 4 + 4); L.act_rows = take(nb * 4 + 4); L.pj2 = take(nb * 4 + 4);
-    L.C_ref = take(bounded ? KD * 4 : 4); L.shift = take(bounded ? (size_t)K * 4 : 4);
+    L.C_ref = take(bounded ? KD * 8 : 8); L.shift = take(bounded ? (size_t)K * 4 : 4);
     L.ub0 = take(nb * 4 + 4); L.lb0 = take(nb * 4 + 4); L.pj20 = take(nb * 4 + 4);
-    L.C_ref0 = take(bounded ? KD * 4 : 4);
+    L.C_ref0 = take(bounded ? KD * 8 : 8);
+    L.xchk = take(16);
     L.total = o;
     return L;
 }
@@ -249,7 +253,7 @@ static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
 
 // Centroid prep after every change of C (a1 / a13): ||c||^2, tf32 split, and
 // for the 2xFP16 engine the scaled fp16 hi/lo operands.
-static void combine(kmeans_handle* h, const Dev& d, int mode, const float* src, cudaStream_t s) {
+static void combine(kmeans_handle* h, const Dev& d, int mode, const double* src, cudaStream_t s) {
     launch_combine(d, mode, src, s);
     h->launches++;
     if (d.tc_kind == 1) { launch_csplit16(d, mode, s); h->launches++; }
@@ -385,13 +389,66 @@ static kmeans_status ensure_graph(kmeans_handle* h) {
     return KMEANS_OK;
 }
 
-static kmeans_status start(kmeans_handle* h, const float* C0) {
+static kmeans_status start(kmeans_handle* h, const double* C0) {
     launch_reset(h->d, h->stream);
     dbg("reset", h->stream);
     combine(h, h->d, 2, C0, h->stream);
     dbg("combine_c0", h->stream);
     h->launches += 2;
     return enqueue_pass(h, h->stream, h->cfg.timing != 0);   // Algorithm 1 line 1
+}
+
+// Every resource a handle may hold, released in one place (kmeans_destroy and
+// every failure exit of kmeans_create).  sync: drain the streams first.
+static void release(kmeans_handle* h, bool sync) {
+    if (!h) return;
+    if (sync && h->stream) cudaStreamSynchronize(h->stream);
+    if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    if (h->copy_stream) {
+        if (sync) cudaStreamSynchronize(h->copy_stream);
+        cudaStreamDestroy(h->copy_stream);
+        for (auto e : h->feed_ev) if (e) cudaEventDestroy(e);
+        if (h->feed_gate) cudaEventDestroy(h->feed_gate);
+        if (h->feed_all) cudaEventDestroy(h->feed_all);
+    }
+    if (h->tcm) tc_free_maps(h->tcm);
+    if (h->tcm_api) tc_free_maps(h->tcm_api);
+    for (auto& e : h->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (auto& e : h->uev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    if (h->run_ev[0]) cudaEventDestroy(h->run_ev[0]);
+    if (h->run_ev[1]) cudaEventDestroy(h->run_ev[1]);
+    if (h->st_host) cudaFreeHost(h->st_host);
+    if (h->tr_host) cudaFreeHost(h->tr_host);
+    if (h->scal_host) cudaFreeHost(h->scal_host);
+    if (h->done_host) cudaFreeHost(h->done_host);
+    if (h->comm) {
+        if (sync) ncclCommDestroy(h->comm);
+        else ncclCommAbort(h->comm);             // a failed / poisoned communicator may never complete
+    }
+    delete h;
+}
+
+// kmeans_aa_step_host refreshed X with rows outside the create-time ranges: the
+// pass that used them is meaningless, so the handle is poisoned.
+static void x_range_error(kmeans_handle* h) {
+    h->err = "X_host rows exceed the create-time range of X (max |x_ik| or max ||x_i||): "
+             "every operand and fixed-point scale was derived from it";
+    h->poisoned = true;
+}
+
+// One-time kernel attribute setup (max dynamic shared memory) PER DEVICE: the
+// attributes are device state, so a handle on a second GPU repeats it.
+static cudaError_t setup_device(int dev) {
+    static std::mutex mu;
+    static bool done[AAKM_MAX_DEVICES] = {};
+    if (dev < 0 || dev >= AAKM_MAX_DEVICES) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev]) return cudaSuccess;
+    for (cudaError_t e : {setup_simt(), setup_refine(), setup_update(), setup_tc(), setup_seed()})
+        if (e != cudaSuccess) return e;
+    done[dev] = true;
+    return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ ABI
@@ -460,7 +517,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.dynamic_m = cfg->dynamic_m; D.max_iters = cfg->max_iters; D.eps1 = cfg->eps1; D.eps2 = cfg->eps2;
     D.ridge = cfg->ridge;
     D.st = (DevState*)(w + L.st);
-    D.C = (float*)(w + L.C); D.Chi = (float*)(w + L.Chi); D.Clo = (float*)(w + L.Clo); D.cn = (float*)(w + L.cn);
+    D.C = (double*)(w + L.C); D.C32 = (float*)(w + L.C32); D.Chi = (float*)(w + L.Chi); D.Clo = (float*)(w + L.Clo); D.cn = (float*)(w + L.cn);
     D.lab[0] = (int*)(w + L.lab0); D.lab[1] = (int*)(w + L.lab1);
     D.flag_rows = (int*)(w + L.flags);
     D.flag_b1 = (float*)(w + L.fb1);
@@ -484,7 +541,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.seed_T = (long long*)(w + L.seed_T); D.seed_x = (int*)(w + L.seed_x);
     D.seed_idx = (long long*)(w + L.seed_idx); D.seed_u = (double*)(w + L.seed_u);
     D.perm = (int*)(w + L.perm);
-    D.Gring = (float*)(w + L.Gring); D.Fring = (float*)(w + L.Fring);
+    D.Gring = (double*)(w + L.Gring); D.Fring = (double*)(w + L.Fring);
     D.gram_part = (double*)(w + L.gram_part);
     D.trace = (TraceRec*)(w + L.trace);
     D.nranks = nranks;
@@ -503,9 +560,9 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     if (h->path == KMEANS_PATH_TC16 && cfg->bounded) {                 // bounded engine (Algorithm 1 passes)
         D.ub = (float*)(w + L.ub); D.lb = (float*)(w + L.lb); D.act_rows = (int*)(w + L.act_rows);
         D.pj2 = (int*)(w + L.pj2);
-        D.C_ref = (float*)(w + L.C_ref); D.shift = (float*)(w + L.shift);
+        D.C_ref = (double*)(w + L.C_ref); D.shift = (float*)(w + L.shift);
         D.ub0 = (float*)(w + L.ub0); D.lb0 = (float*)(w + L.lb0); D.pj20 = (int*)(w + L.pj20);
-        D.C_ref0 = (float*)(w + L.C_ref0);
+        D.C_ref0 = (double*)(w + L.C_ref0);
     }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
@@ -518,29 +575,27 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     h->da.C_ref = nullptr; h->da.shift = nullptr;
     h->da.ub0 = nullptr; h->da.lb0 = nullptr; h->da.pj20 = nullptr; h->da.C_ref0 = nullptr;
     h->da.st = (DevState*)(w + L.st_api);
-    h->da.C = (float*)(w + L.Ca); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
+    h->da.C = (double*)(w + L.Ca); h->da.C32 = (float*)(w + L.Ca32); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
     h->da.cn = (float*)(w + L.cna);
     h->da.cnimg = tcpath ? (uint8_t*)(w + L.cnimga) : nullptr;
     h->da.Chi16 = w + L.Ca16h; h->da.Clo16 = w + L.Ca16l;
     h->scratch = w + L.scratch;
     h->scratch_bytes = L.scratch_bytes;
+    h->xchk = (unsigned int*)(w + L.xchk);
 
 #define CKC(call)                                                                         \
     do {                                                                                  \
         cudaError_t e_ = (call);                                                          \
         if (e_ != cudaSuccess) {                                                          \
             g_create_err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
-            delete h;                                                                     \
+            release(h, false);                                                            \
             return KMEANS_ERR_CUDA;                                                       \
         }                                                                                 \
     } while (0)
-    {
-        static bool once = false;
-        if (!once) {
-            CKC(setup_simt()); CKC(setup_refine()); CKC(setup_update()); CKC(setup_tc()); CKC(setup_seed());
-            once = true;
-        }
-    }
+    CKC(cudaGetDevice(&D.dev));
+    CKC(cudaDeviceGetAttribute(&D.num_sms, cudaDevAttrMultiProcessorCount, D.dev));
+    h->da.dev = D.dev; h->da.num_sms = D.num_sms;
+    CKC(setup_device(D.dev));
     CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     // this rank's max |x_ik| and max ||x_i||^2 (one pass; float bits of non-negative
     // values order as uints): the 2xFP16 operand scale (rank-local) and, reduced
@@ -552,6 +607,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         launch_xstats_max(X, n_local, d, mx, h->stream);
         CKC(cudaMemcpyAsync(mloc, mx, 8, cudaMemcpyDeviceToHost, h->stream));
         CKC(cudaStreamSynchronize(h->stream));
+        memcpy(h->x_stat, mloc, 8);
     }
     if (h->path == KMEANS_PATH_TC16) {
         const float m = mloc[0];
@@ -566,7 +622,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         h->tcm_api = tc_make_maps(h->da);
         if (!h->tcm || !h->tcm_api) {
             g_create_err = "cuTensorMapEncodeTiled failed for the tensor-core engine";
-            delete h;
+            release(h, false);
             return KMEANS_ERR_CUDA;
         }
     }
@@ -593,8 +649,9 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         memcpy(&id, uid128, 128);
         ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
         if (r != ncclSuccess) {
+            h->comm = nullptr;
             g_create_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
-            delete h;
+            release(h, false);
             return KMEANS_ERR_NCCL;
         }
     }
@@ -605,7 +662,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         CKC(cudaMemcpyAsync(mx, mloc, 8, cudaMemcpyHostToDevice, h->stream));
         if (nranks > 1) {
             ncclResult_t r = ncclAllReduce(mx, mx, 2, ncclFloat32, ncclMax, h->comm, h->stream);
-            if (r != ncclSuccess) { g_create_err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); delete h; return KMEANS_ERR_NCCL; }
+            if (r != ncclSuccess) { g_create_err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); release(h, false); return KMEANS_ERR_NCCL; }
         }
         unsigned int mb[2];
         CKC(cudaMemcpyAsync(mb, mx, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -630,7 +687,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     return KMEANS_OK;
 }
 
-kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* labels_prev, int32_t* labels_out,
+kmeans_status kmeans_assign(kmeans_handle* h, const double* C, const int32_t* labels_prev, int32_t* labels_out,
                             double* energy_out, int64_t* changed_out) {
     LIVE(h);
     if (!C || (!labels_out && h->d.n > 0)) FAIL(h, KMEANS_ERR_INVALID, "C or labels_out is NULL");
@@ -660,7 +717,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const float* C, const int32_t* lab
     return KMEANS_OK;
 }
 
-kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const float* C_prev, float* G_out,
+kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const double* C_prev, double* G_out,
                             int64_t* counts_out) {
     LIVE(h);
     if ((!labels && h->d.n > 0) || !C_prev || !G_out) FAIL(h, KMEANS_ERR_INVALID, "NULL labels/C_prev/G_out");
@@ -684,7 +741,7 @@ kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const float
 }
 
 kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, const int32_t* labels_prev,
-                                     const float* C, double* packed_out) {
+                                     const double* C, double* packed_out) {
     LIVE(h);
     if ((!labels && h->d.n > 0) || !C || !packed_out) FAIL(h, KMEANS_ERR_INVALID, "NULL argument");
     cudaStream_t s = h->stream;
@@ -695,7 +752,7 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
     combine(h, d, 2, C, s);                               // max ||c||^2 of C (the energy scale)
     h->launches += launch_update(d, g, s);
-    launch_partials_out(d, d.packed[0], C, packed_out, s);            // unreduced, as doubles
+    launch_partials_out(d, d.packed[0], packed_out, s);               // unreduced, as doubles
     h->launches += 1;
     CK(h, cudaStreamSynchronize(s));
     CK(h, cudaGetLastError());
@@ -726,6 +783,8 @@ static kmeans_status step_info(kmeans_handle* h, kmeans_step_info* info, double*
         cudaStream_t s = h->stream;
         CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
         CK(h, cudaStreamSynchronize(s));
+        if (h->st_host->label_error & 2) x_range_error(h);
+        if (h->poisoned) return KMEANS_ERR_INVALID;
         const long long n = h->st_host->trace_len;
         if (n > 0)
             CK(h, cudaMemcpy(h->tr_host, h->d.trace + (n - 1), sizeof(TraceRec), cudaMemcpyDeviceToHost));
@@ -734,7 +793,7 @@ static kmeans_status step_info(kmeans_handle* h, kmeans_step_info* info, double*
     return KMEANS_OK;
 }
 
-kmeans_status kmeans_aa_step(kmeans_handle* h, const float* C0, kmeans_step_info* info, double* theta_out) {
+kmeans_status kmeans_aa_step(kmeans_handle* h, const double* C0, kmeans_step_info* info, double* theta_out) {
     LIVE(h);
     kmeans_status st;
     if (C0) st = start(h, C0);
@@ -750,6 +809,7 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
                                   double* theta_out) {
     LIVE(h);
     const Dev& d = h->d;
+    if (!h->cfg.x_refresh) FAIL(h, KMEANS_ERR_INVALID, "kmeans_aa_step_host needs cfg.x_refresh = 1 at create");
     if (!X_host && d.n > 0) FAIL(h, KMEANS_ERR_INVALID, "X_host is NULL");
     if (chunks < 1) chunks = 1;
     if (chunks > 64) chunks = 64;
@@ -773,7 +833,16 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
                               h->copy_stream));
         CK(h, cudaEventRecord(h->feed_ev[c], h->copy_stream));
     }
+    // the new rows must stay inside the create-time ranges every scale was derived
+    // from (2xFP16 operand scale and tau_abs, fixed-point update and energy scales):
+    // one stats pass on the copy stream, checked on the device (label_error bit 2,
+    // reported by the next synchronising call)
+    CK(h, cudaMemsetAsync(h->xchk, 0, 8, h->copy_stream));
+    launch_xstats_max(d.X, d.n, d.d, h->xchk, h->copy_stream);
+    launch_xcheck(d, h->xchk, h->x_stat[0], h->x_stat[1], h->copy_stream);
+    h->launches += 2;
     CK(h, cudaEventRecord(h->feed_all, h->copy_stream));
+    if (d.ub) CK(h, cudaMemsetAsync(&d.st->bnd_ready, 0, sizeof(int), s));   // new rows: no valid bounds
     const bool streamed = nc > 0 && !d.ub && (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16);
     if (!streamed) {
         CK(h, cudaStreamWaitEvent(s, h->feed_all, 0));
@@ -790,7 +859,7 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
     return step_info(h, info, theta_out);
 }
 
-kmeans_status kmeans_run(kmeans_handle* h, const float* C0, float* C_out, int32_t* labels_out, kmeans_report* rep) {
+kmeans_status kmeans_run(kmeans_handle* h, const double* C0, double* C_out, int32_t* labels_out, kmeans_report* rep) {
     LIVE(h);
     if (!C0 || !rep) FAIL(h, KMEANS_ERR_INVALID, "C0 or rep is NULL");
     cudaStream_t s = h->stream;
@@ -814,10 +883,11 @@ kmeans_status kmeans_run(kmeans_handle* h, const float* C0, float* C_out, int32_
         if (batch < 16) batch *= 2;
     }
     CK(h, cudaEventRecord(h->run_ev[1], s));
-    if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 4, cudaMemcpyDeviceToDevice, s));
+    if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 8, cudaMemcpyDeviceToDevice, s));
     CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
     CK(h, cudaStreamSynchronize(s));
     const DevState& S = *h->st_host;
+    if (S.label_error & 2) { x_range_error(h); return KMEANS_ERR_INVALID; }
     if (labels_out && h->d.n > 0)
         CK(h, cudaMemcpyAsync(labels_out, h->d.lab[S.cur], (size_t)h->d.n * 4, cudaMemcpyDeviceToDevice, s));
     float ms = 0.f;
@@ -836,10 +906,10 @@ kmeans_status kmeans_run(kmeans_handle* h, const float* C0, float* C_out, int32_
     return KMEANS_OK;
 }
 
-kmeans_status kmeans_get_centroids(kmeans_handle* h, float* C_out, int32_t* labels_out) {
+kmeans_status kmeans_get_centroids(kmeans_handle* h, double* C_out, int32_t* labels_out) {
     LIVE(h);
     cudaStream_t s = h->stream;
-    if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 4, cudaMemcpyDeviceToDevice, s));
+    if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 8, cudaMemcpyDeviceToDevice, s));
     if (labels_out) {
         CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
         CK(h, cudaStreamSynchronize(s));
@@ -863,19 +933,21 @@ kmeans_status kmeans_state_export(kmeans_handle* h, kmeans_state* out) {
     out->hist_count = S.hist_count; out->m = S.m; out->lloyd = S.lloyd; out->done = S.done; out->t = S.t;
     out->E1 = S.E1; out->E2 = S.E2;
     out->n_accepted = S.n_accepted; out->n_rejected = S.n_rejected; out->n_assign = S.n_assign;
-    if (out->C) CK(h, cudaMemcpy(out->C, d.C, KD * 4, cudaMemcpyDeviceToHost));
+    if (out->C) CK(h, cudaMemcpy(out->C, d.C, KD * 8, cudaMemcpyDeviceToHost));
     // between passes the newest history entry is (G^{t-1}, F^{t-1})
     for (int j = 0; j < S.hist_count; ++j) {
         const long long slot = ((S.t - 1 - j) % d.H + d.H) % d.H;
-        if (out->Ghist) CK(h, cudaMemcpy(out->Ghist + j * KD, d.Gring + slot * KD, KD * 4, cudaMemcpyDeviceToHost));
-        if (out->Fhist) CK(h, cudaMemcpy(out->Fhist + j * KD, d.Fring + slot * KD, KD * 4, cudaMemcpyDeviceToHost));
+        if (out->Ghist) CK(h, cudaMemcpy(out->Ghist + j * KD, d.Gring + slot * KD, KD * 8, cudaMemcpyDeviceToHost));
+        if (out->Fhist) CK(h, cudaMemcpy(out->Fhist + j * KD, d.Fring + slot * KD, KD * 8, cudaMemcpyDeviceToHost));
     }
     if (out->fallback && S.hist_count > 0) {
         const long long slot = ((S.t - 1) % d.H + d.H) % d.H;
-        CK(h, cudaMemcpy(out->fallback, d.Gring + slot * KD, KD * 4, cudaMemcpyDeviceToHost));
+        CK(h, cudaMemcpy(out->fallback, d.Gring + slot * KD, KD * 8, cudaMemcpyDeviceToHost));
     }
     if (out->labels_prev && d.n > 0) {
-        const int which = S.done ? (S.cur ^ 1) : (S.cur ^ 1);
+        // between passes P^{t-1} = lab[cur ^ 1]; a finished run (converged or max_iters)
+        // did not flip cur, so its final P^t is lab[cur] (kmeans_get_centroids agrees)
+        const int which = S.done ? S.cur : (S.cur ^ 1);
         CK(h, cudaMemcpy(out->labels_prev, d.lab[which], (size_t)d.n * 4, cudaMemcpyDeviceToHost));
     }
     if (out->gram)
@@ -898,11 +970,13 @@ kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
     // history into the ring slots it came from: entry j = (G^{t-1-j}, F^{t-1-j})
     for (int j = 0; j < st->hist_count; ++j) {
         const long long slot = ((st->t - 1 - j) % d.H + d.H) % d.H;
-        CK(h, cudaMemcpy(d.Gring + slot * KD, st->Ghist + j * KD, KD * 4, cudaMemcpyHostToDevice));
-        CK(h, cudaMemcpy(d.Fring + slot * KD, st->Fhist + j * KD, KD * 4, cudaMemcpyHostToDevice));
+        CK(h, cudaMemcpy(d.Gring + slot * KD, st->Ghist + j * KD, KD * 8, cudaMemcpyHostToDevice));
+        CK(h, cudaMemcpy(d.Fring + slot * KD, st->Fhist + j * KD, KD * 8, cudaMemcpyHostToDevice));
     }
-    CK(h, cudaMemcpy(d.C, st->C, KD * 4, cudaMemcpyHostToDevice));
-    if (d.n > 0) CK(h, cudaMemcpy(d.lab[1], st->labels_prev, (size_t)d.n * 4, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(d.C, st->C, KD * 8, cudaMemcpyHostToDevice));
+    // cur = 0 below: a live state's P^{t-1} goes to lab[cur ^ 1]; a finished one's
+    // final labels to lab[cur] (the buffers export and get_centroids read)
+    if (d.n > 0) CK(h, cudaMemcpy(d.lab[st->done ? 0 : 1], st->labels_prev, (size_t)d.n * 4, cudaMemcpyHostToDevice));
     // the control state, on top of the current device state (keeps engine-side fields)
     CK(h, cudaMemcpy(h->st_host, d.st, sizeof(DevState), cudaMemcpyDeviceToHost));
     DevState S = *h->st_host;
@@ -922,8 +996,8 @@ kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
             for (int b = 0; b <= a; ++b) {
                 double v = 0.0;
                 for (size_t e = 0; e < KD; ++e) {
-                    const double da = (double)st->Fhist[a * KD + e] - (double)st->Fhist[(a + 1) * KD + e];
-                    const double db = (double)st->Fhist[b * KD + e] - (double)st->Fhist[(b + 1) * KD + e];
+                    const double da = st->Fhist[a * KD + e] - st->Fhist[(a + 1) * KD + e];
+                    const double db = st->Fhist[b * KD + e] - st->Fhist[(b + 1) * KD + e];
                     v += da * db;
                 }
                 const long long sa = ((st->t - 1 - a) % d.H + d.H) % d.H, sb = ((st->t - 1 - b) % d.H + d.H) % d.H;
@@ -1057,28 +1131,7 @@ const char* kmeans_assign_path_name(const kmeans_handle* h) {
 kmeans_status kmeans_destroy(kmeans_handle* h) {
     if (!h) return KMEANS_ERR_INVALID;
     if (g_prof) prof_dump();
-    if (!h->poisoned) cudaStreamSynchronize(h->stream);
-    if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
-    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
-    if (h->copy_stream) {
-        if (!h->poisoned) cudaStreamSynchronize(h->copy_stream);
-        cudaStreamDestroy(h->copy_stream);
-        for (auto e : h->feed_ev) cudaEventDestroy(e);
-        cudaEventDestroy(h->feed_gate);
-        cudaEventDestroy(h->feed_all);
-    }
-    if (h->tcm) tc_free_maps(h->tcm);
-    if (h->tcm_api) tc_free_maps(h->tcm_api);
-    for (auto& e : h->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-    for (auto& e : h->uev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-    if (h->run_ev[0]) cudaEventDestroy(h->run_ev[0]);
-    if (h->run_ev[1]) cudaEventDestroy(h->run_ev[1]);
-    if (h->st_host) cudaFreeHost(h->st_host);
-    if (h->tr_host) cudaFreeHost(h->tr_host);
-    if (h->scal_host) cudaFreeHost(h->scal_host);
-    if (h->done_host) cudaFreeHost(h->done_host);
-    if (h->comm) ncclCommDestroy(h->comm);
-    delete h;
+    release(h, !h->poisoned);
     return KMEANS_OK;
 }
 

@@ -22,7 +22,7 @@ namespace aakm {
 struct Pick {
     const int* lab;
     const int* prev;
-    const float* C;
+    const double* C;      // C^t (fp64)
     long long* out;       // packed [S_hi | S_lo | N | E_hi | E_lo | E | changed]
 };
 
@@ -87,14 +87,14 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
                 red_add_s64(p.out + pk_n(d) + j, 1);
             }
             const float* x = d.X + row * D;
-            const float* c = p.C + (long long)j * D;
+            const double* c = p.C + (long long)j * D;
             for (int k = gl; k < D; k += GS) {
                 const float xv = __ldcs(x + k);
                 int hi = 0, lo = 0;
                 fx_add(xv, sc, hi, lo);
                 red_add_s64(p.out + (long long)j * D + k, hi);
                 red_add_s64(p.out + KD + (long long)j * D + k, lo);
-                const double df = (double)xv - (double)__ldg(c + k);
+                const double df = (double)xv - __ldg(c + k);
                 e = fma(df, df, e);
             }
         }
@@ -342,12 +342,12 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             rid[u] = qi < cnt ? d.perm[r0 + qi] : -1;
         }
         int hi[V], lo[V];                         // <= 256 rows per chunk: int32 cannot overflow
-        float cj[V];
+        double cj[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             hi[v] = 0; lo[v] = 0;
             const int k = lane + 32 * v;
-            cj[v] = k < D ? __ldg(p.C + (long long)j * D + k) : 0.f;
+            cj[v] = k < D ? __ldg(p.C + (long long)j * D + k) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < SEG_ROWS / 32; ++u) {
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
                     for (int v = 0; v < V; ++v) {
                         fx_add(xv[t][v], sc, hi[v], lo[v]);   // zeros add nothing
                         const int k = lane + 32 * v;
-                        if (k < D) { const double df = (double)xv[t][v] - (double)cj[v]; e = fma(df, df, e); }
+                        if (k < D) { const double df = (double)xv[t][v] - cj[v]; e = fma(df, df, e); }
                     }
                     if (ok[t]) ea += energy_fx(e * q);   // this lane's part of e_row
                 }
@@ -419,7 +419,7 @@ template <int LPR> struct SegBulk {
     static constexpr int SR = 16;                                      // rows per item
     static constexpr int GP = 4 * RB > 128 ? 4 * RB : 128;            // gather4 group pitch (TMA dst: 128 B aligned)
     static constexpr int CO = SR / 4 * GP;                         // c_j row offset
-    static constexpr int SLOT = (CO + RB + 127) / 128 * 128;           // rows + c_j
+    static constexpr int SLOT = (CO + 2 * RB + 127) / 128 * 128;       // rows + c_j (fp64: 2 RB bytes)
     static constexpr int WARP = (SEG_NS * SLOT + SEG_NS * 16 + SEG_NS * 8 + 127) / 128 * 128;
     static constexpr int WPB = SEG_SMEM / WARP > 16 ? 16 : SEG_SMEM / WARP;
     static constexpr int SMEM = WPB * WARP;
@@ -515,10 +515,10 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         uint64_t* b = bar + ps;
         unsigned char* slot = ring + ps * SB::SLOT;
         const int ng = (qa.nr + 3) >> 2;                               // gather4 instructions
-        if (lane == 0) { rec[ps] = make_int4(qa.j, qa.nr, qa.last, 0); sb_expect(b, (unsigned)((4 * ng + 1) * RB)); }
+        if (lane == 0) { rec[ps] = make_int4(qa.j, qa.nr, qa.last, 0); sb_expect(b, (unsigned)((4 * ng + 2) * RB)); }
         __syncwarp();
         if (lane < ng) sb_gather4(slot + lane * SB::GP, d.xg_map, qa.i0, qa.i1, qa.i2, qa.i3, b);
-        if (lane == 31) sb_copy(slot + SB::CO, Cb + (long long)qa.j * RB, RB, b);
+        if (lane == 31) sb_copy(slot + SB::CO, Cb + (long long)qa.j * 2 * RB, 2 * RB, b);
         ps = ps + 1 == SEG_NS ? 0 : ps + 1;
         ++inflight;
         qa = qb;
@@ -538,8 +538,9 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         phase ^= 1u << cs;
         const int4 r = rec[cs];                                        // {j, rows, last}
         const unsigned char* slot = ring + cs * SB::SLOT;
-        const float4 c = *reinterpret_cast<const float4*>(slot + SB::CO + 16 * c4i);
-        const double cx = c.x, cy = c.y, cz = c.z, cw = c.w;
+        const double2 c01 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i);
+        const double2 c23 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i + 16);
+        const double cx = c01.x, cy = c01.y, cz = c23.x, cw = c23.y;
 #pragma unroll
         for (int i = 0; i < IT; ++i) {                                 // branch-free: rows past r.y read as 0
             const int rr = i * RPW + h;
@@ -643,17 +644,17 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
 }
 
 // kmeans_update API: G = S / N (empty -> C_prev row, R-A15), counts.
-__global__ void k_update_G(Dev d, const long long* packed, const float* Cprev, float* G, long long* counts) {
+__global__ void k_update_G(Dev d, const long long* packed, const double* Cprev, double* G, long long* counts) {
     const long long KD = (long long)d.K * d.d;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
         const long long j = e / d.d;
         const long long nj = packed[pk_n(d) + j];
-        G[e] = nj > 0 ? (float)(fx_value(packed[e], packed[KD + e], d.fx_inv) / (double)nj) : Cprev[e];
+        G[e] = nj > 0 ? fx_value(packed[e], packed[KD + e], d.fx_inv) / (double)nj : Cprev[e];
         if (counts && e % d.d == 0) counts[j] = nj;
     }
 }
 
-void launch_update_G(const Dev& d, const long long* packed, const float* Cprev, float* G,
+void launch_update_G(const Dev& d, const long long* packed, const double* Cprev, double* G,
                      long long* counts, cudaStream_t s) {
     long long KD = (long long)d.K * d.d;
     int blocks = (int)((KD + 255) / 256);
@@ -692,8 +693,7 @@ __global__ void k_partials_out(Dev d, const long long* pk, double* out) {
     }
 }
 
-void launch_partials_out(const Dev& d, const long long* packed, const float* C, double* out, cudaStream_t s) {
-    (void)C;
+void launch_partials_out(const Dev& d, const long long* packed, double* out, cudaStream_t s) {
     k_partials_out<<<64, 256, 0, s>>>(d, packed, out);
 }
 
@@ -719,6 +719,14 @@ __global__ void k_xstats_max(const float* X, long long n, int D, unsigned int* o
 
 void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s) {
     if (n > 0) k_xstats_max<<<592, 256, 0, s>>>(X, n, d, out);
+}
+
+__global__ void k_xcheck(Dev d, const unsigned int* out, unsigned int amax, unsigned int nmax2) {
+    if (out[0] > amax || out[1] > nmax2) atomicOr(&d.st->label_error, 2);   // non-negative float bits order as uints
+}
+
+void launch_xcheck(const Dev& d, const unsigned int* out, unsigned int amax, unsigned int nmax2, cudaStream_t s) {
+    k_xcheck<<<1, 1, 0, s>>>(d, out, amax, nmax2);
 }
 
 }  // namespace aakm

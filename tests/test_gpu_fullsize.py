@@ -1,8 +1,9 @@
 """-m gpu: BASELINE.json's full-size configs in the launch configuration bench.py
 times (auto engine, CTA pairs, graph-free aa_step), checked against the CPU
 oracle where it can afford it:
-  * assignment: a seeded 20 000-row sample decided by the oracle one row at a
-    time (north-star tie rule), plus label range / counts properties for all rows;
+  * assignment: a seeded 1 % row sample (at least 20 000 rows)
+    decided by the oracle one row at a time (north-star tie rule), plus label
+    range / counts properties for all rows;
   * energy and update: the oracle's full O(N d) sums over every row (exact fp64);
   * one Algorithm 1 pass after line 1: the exported C^{t+1} is finite and the
     accepted / rejected energies obey the guard.
@@ -37,7 +38,7 @@ def test_full_size_sampled(cfg, path):
     lab = lab.cpu().numpy()
     assert lab.min() >= 0 and lab.max() < c.K
     rng = np.random.default_rng(2024)
-    rows = np.sort(rng.choice(c.N, 20_000, replace=False))
+    rows = np.sort(rng.choice(c.N, max(20_000, c.N // 100), replace=False))
     check_assign(X[rows], C, lab[rows], msg=f"{cfg}/{path} sampled rows")
     E_ora = oracle.energy(X, C.astype(np.float64), lab)   # every row, fp64
     assert abs(E - E_ora) <= 1e-6 * E_ora, (E, E_ora)

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 def test_partials_sum_over_shards(cfg, N, world):
     require_gpu()
     X, C0, c = make(cfg, N=N)
-    C = C0 + np.float32(0.01)
+    C = C0.astype(np.float64) + 0.01
     prev = oracle.assign(X, C0.astype(np.float64))
     lab = oracle.assign(X, C.astype(np.float64))
     K, d = C.shape

@@ -42,7 +42,8 @@ def test_assign_parity(cfg, N, K, path):
     km = handle(X, c.K, path)
     rng = np.random.default_rng(1)
     prev = rng.integers(0, c.K, size=c.N).astype(np.int32)
-    for C in (C0, C0 + rng.normal(0, 0.05, C0.shape).astype(np.float32)):
+    # C^0 (samples: fp32 values) and a perturbed fp64 C (the Algorithm 1 state is fp64)
+    for C in (C0.astype(np.float64), C0 + rng.normal(0, 0.05, C0.shape)):
         lab, E, ch = km.assign(dev(C), dev(prev))
         lab = lab.cpu().numpy()
         lab_ora, ndiff = check_assign(X, C, lab, msg=f"{cfg}/{path}")
@@ -129,11 +130,11 @@ def test_ragged_small_n(n):
     km.close()
 
 
-def _lockstep(cfg, N=None, K=None, seed=0, m0=5, max_passes=400, path="auto"):
+def _lockstep(cfg, N=None, K=None, seed=0, m0=5, max_passes=400, path="auto", dynamic_m=True):
     X, C0, c = make(cfg, seed=seed, N=N, K=K)
-    km = handle(X, c.K, path, m0=m0)
+    km = handle(X, c.K, path, m0=m0, dynamic_m=dynamic_m)
     info0 = km.aa_step(dev(C0))
-    ora = oracle.AAState(X, oracle.OracleConfig(m0=m0, parity=True))
+    ora = oracle.AAState(X, oracle.OracleConfig(m0=m0, dynamic_m=dynamic_m))
     ora.init(C0.astype(np.float64))
     s = km.state_export()
     err, ok = g_close(s["C"], ora.C)
@@ -185,16 +186,38 @@ def test_end_to_end_parity(cfg, N, K, seed, path):
     X, C0, c = make(cfg, seed=seed, N=N, K=K)
     km = handle(X, c.K, path, m0=5)
     C, lab, rep = km.run(dev(C0))
-    ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=5, parity=True))
+    ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=5))
     assert rep["converged"] and ref["converged"]
     assert rep["iters"] == ref["iters"], (rep, {k: v for k, v in ref.items() if k not in ("C", "labels", "trace")})
     assert abs(rep["energy"] - ref["energy"]) <= 1e-4 * ref["energy"]
     assert rep["n_assign"] == rep["iters"] + rep["n_rejected"]
     # the returned C is a fixed point: it is the mean of its own partition
     G, _ = km.update(lab, C)
-    err, ok = g_close(G.cpu().numpy(), C.cpu().numpy().astype(np.float64))
+    err, ok = g_close(G.cpu().numpy(), C.cpu().numpy())
     assert ok.all(), err
+    err, ok = g_close(C.cpu().numpy(), ref["C"])
+    assert ok.all(), f"final C vs oracle: {err}"
     km.close()
+
+
+@pytest.mark.parametrize("cfg,N,K,m0", [("c1", None, None, 2), ("c1", None, None, 5), ("c2", None, None, 2),
+                                        ("c2", None, None, 5), ("c4", 8_000, 256, 2)])
+def test_fixed_m_end_to_end(cfg, N, K, m0):
+    # Table 2's "Fixed m" columns: dynamic_m = 0, m = m0 throughout
+    X, C0, c = make(cfg, N=N, K=K)
+    km = handle(X, c.K, m0=m0, dynamic_m=False)
+    C, lab, rep = km.run(dev(C0))
+    ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=m0, dynamic_m=False))
+    assert rep["converged"] and ref["converged"]
+    assert rep["m_final"] == m0 == ref["m_final"]
+    assert rep["iters"] == ref["iters"] and rep["n_rejected"] == ref["rejected"]
+    assert abs(rep["energy"] - ref["energy"]) <= 1e-4 * ref["energy"]
+    km.close()
+
+
+@pytest.mark.parametrize("cfg,N,K,m0", [("c2", None, None, 2), ("c4", 6_000, 128, 5)])
+def test_fixed_m_lockstep(cfg, N, K, m0):
+    assert _lockstep(cfg, N, K, 0, m0=m0, dynamic_m=False) >= 2
 
 
 @pytest.mark.parametrize("cfg,N,K", [("c1", None, None), ("c2", None, None), ("c4", 6_000, 128)])
@@ -209,11 +232,24 @@ def test_m0_is_lloyd_on_gpu(cfg, N, K):
     km.close()
 
 
-def test_max_iters_reported_not_error():
+@pytest.mark.parametrize("max_iters", [1, 3, 8])
+def test_max_iters_reported_not_error(max_iters):
+    # stopping at the cap returns C^{t+1} and the labels P^t of the last pass, as the oracle does
     X, C0, c = make("c2")
-    km = handle(X, c.K, max_iters=3)
+    km = handle(X, c.K, max_iters=max_iters)
     C, lab, rep = km.run(dev(C0))
-    assert rep["converged"] == 0 and rep["iters"] == 4
+    ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=5, max_iters=max_iters))
+    assert rep["converged"] == 0 and not ref["converged"]
+    assert rep["iters"] == ref["iters"] == max_iters + 1
+    np.testing.assert_array_equal(lab.cpu().numpy(), ref["labels"])
+    err, ok = g_close(C.cpu().numpy(), ref["C"])
+    assert ok.all(), err
+    C2, lab2 = km.centroids()                         # the same buffers through get_centroids
+    np.testing.assert_array_equal(lab2.cpu().numpy(), lab.cpu().numpy())
+    np.testing.assert_array_equal(C2.cpu().numpy(), C.cpu().numpy())
+    st = km.state_export()                            # a finished state exports its final labels
+    assert st["done"] == 1
+    np.testing.assert_array_equal(st["labels_prev"], ref["labels"])
     km.close()
 
 

@@ -90,7 +90,7 @@ def test_seeded_run_matches_oracle():
     km.close()
     ref_idx = oracle.seed_pp(X, 32, u)
     np.testing.assert_array_equal(idx, ref_idx)
-    ref = oracle.run(X, X[ref_idx].astype(np.float64), oracle.OracleConfig(m0=5, parity=True))
+    ref = oracle.run(X, X[ref_idx].astype(np.float64), oracle.OracleConfig(m0=5))
     assert rep["converged"] and ref["converged"]
     assert rep["iters"] == ref["iters"]
     assert abs(rep["energy"] - ref["energy"]) <= 1e-6 * ref["energy"]
