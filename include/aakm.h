@@ -105,6 +105,14 @@ typedef struct {
                             (max |x_ik|, max ||x_i||), which a device check
                             enforces.  0 (default): X is never written, and
                             kmeans_aa_step_host returns INVALID.                 */
+    int32_t comm_always; /* 1 = build an NCCL communicator even when nranks == 1
+                            (a real 1-rank communicator: every allreduce of the
+                            data plane, graph-captured ones included, runs
+                            through NCCL; results are bitwise those of the
+                            communicator-free path).  With a communicator, every
+                            synchronising call polls ncclCommGetAsyncError and
+                            aborts after AAKM_COMM_TIMEOUT_S seconds (default
+                            600) instead of blocking on a failed peer.           */
 } kmeans_config;
 
 /* Result of kmeans_run (fields per DESIGN.md R-A19). */
@@ -294,6 +302,37 @@ AAKM_API kmeans_status kmeans_last_flagged(kmeans_handle *h, int64_t *flagged /*
  * (local to this rank).  Equal unless cfg.bounded proved rows unchanged. */
 AAKM_API kmeans_status kmeans_bounded_stats(kmeans_handle *h, int64_t *rows_scored /*host*/,
                                             int64_t *rows_total /*host*/);
+
+/* Exactness-margin probe (test hook): runs the handle's dense assignment
+ * engine on C (K x d fp64) and writes, per local row, the engine's raw top-2
+ * values and its near-tie threshold: rows_out (device, n_local x 4 float) =
+ * (b1, b2, tau, bits of the chosen index i1), before any near-tie refine.
+ * kind_out (host): 0 = 3xTF32, values are scores ||c||^2/2 - x.c (key-packed,
+ * DESIGN.md §5.3); 1 = 2xFP16, values are window accumulators
+ * U ||x - c||^2 + 6 with U = *unit_out (host); 2 = SIMT FP32, values are
+ * scores ||c||^2 - 2 x.c.  Every computed value must lie within tau / 2 of
+ * its exact counterpart for the near-tie flagging (row a3) to be rigorous.
+ * Synchronises; clobbers the API label buffer only. */
+AAKM_API kmeans_status kmeans_debug_scores(kmeans_handle *h, const double *C, float *rows_out,
+                                           int32_t *kind_out /*host*/, double *unit_out /*host*/);
+
+/* Bounded engine (cfg.bounded) test hooks.
+ * export: the Hamerly state between passes -- per local row ub (upper bound on
+ * ||x_i - c_ref,rho_i||, and on the second candidate's distance when p2 >= 0),
+ * lb (lower bound on every other ||x_i - c_ref,j||), p2 (the two-centroid row's
+ * other candidate, -1 if none) -- and C_ref (K x d fp64, the centroid set the
+ * bounds refer to); rho_i are the labels of the last assignment (state export's
+ * labels_prev).  Device outputs, each nullable.  Synchronises.
+ * repeat: runs the bounded assignment of the current iterate twice back to back
+ * (the second call sees zero drift), writes the bounds after the first call
+ * (device, nullable), the rows each call re-scored on the tensor engine
+ * (scored_out, host 2) and whether the labels agree (same_out, host).
+ * DESTRUCTIVE (overwrites P^{t-1}); restart with kmeans_aa_step(C0).
+ * Errors: INVALID without a bounded engine; STATE outside a live run. */
+AAKM_API kmeans_status kmeans_bounds_export(kmeans_handle *h, float *ub_out, float *lb_out, int32_t *p2_out,
+                                            double *Cref_out);
+AAKM_API kmeans_status kmeans_bounds_repeat(kmeans_handle *h, float *ub1_out, float *lb1_out,
+                                            int64_t *scored_out /*host*/, int32_t *same_out /*host*/);
 
 /* Name of the assignment engine the handle selected ("simt"/"tc"/"tc16"). */
 AAKM_API const char *kmeans_assign_path_name(const kmeans_handle *h);

@@ -35,7 +35,7 @@ class Config(ct.Structure):
     _fields_ = [("m0", ct.c_int32), ("m_max", ct.c_int32), ("eps1", ct.c_double), ("eps2", ct.c_double),
                 ("dynamic_m", ct.c_int32), ("max_iters", ct.c_int32), ("ridge", ct.c_double),
                 ("assign_path", ct.c_int32), ("timing", ct.c_int32), ("bounded", ct.c_int32),
-                ("x_refresh", ct.c_int32)]
+                ("x_refresh", ct.c_int32), ("comm_always", ct.c_int32)]
 
 
 class Report(ct.Structure):
@@ -94,6 +94,9 @@ def lib():
                 "kmeans_aa_step_host": ([P, P, I32, P, P], I32),
                 "kmeans_update_timing": ([P, ct.POINTER(D), ct.POINTER(I64)], I32),
                 "kmeans_assign_path_name": ([P], ct.c_char_p),
+                "kmeans_debug_scores": ([P, P, P, ct.POINTER(I32), ct.POINTER(D)], I32),
+                "kmeans_bounds_export": ([P, P, P, P, P], I32),
+                "kmeans_bounds_repeat": ([P, P, P, P, ct.POINTER(I32)], I32),
                 "kmeans_destroy": ([P], I32),
                 "kmeans_last_error": ([P], ct.c_char_p),
             }
@@ -113,7 +116,7 @@ def header_symbols():
 
 
 def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000, ridge=1e-10,
-           assign_path="auto", timing=False, bounded=False, x_refresh=False) -> Config:
+           assign_path="auto", timing=False, bounded=False, x_refresh=False, comm_always=False) -> Config:
     """Algorithm 1 settings (m0 = 5 per BASELINE configs, reading R-A18)."""
     c = Config()
     c.m0, c.m_max, c.eps1, c.eps2 = m0, m_max, eps1, eps2
@@ -122,6 +125,7 @@ def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000,
     c.timing = int(timing)
     c.bounded = int(bounded)
     c.x_refresh = int(x_refresh)
+    c.comm_always = int(comm_always)
     return c
 
 
@@ -360,6 +364,38 @@ class KMeans:
         self._c(lib().kmeans_seed_pp(self.h, u.ctypes.data_as(ct.c_void_p), _ptr(C),
                                      idx.ctypes.data_as(ct.c_void_p)))
         return C, idx
+
+    def debug_scores(self, C):
+        """kmeans_debug_scores: per row (b1, b2, tau, i1) of the dense engine on C,
+        before the near-tie refine; returns (rows as an n x 4 float32 tensor with the
+        index reinterpreted, kind, unit)."""
+        t = self.torch
+        C = self._f64(C)
+        out = t.empty((self.n, 4), dtype=t.float32, device=self.device)
+        kind, unit = ct.c_int32(), ct.c_double()
+        self._c(lib().kmeans_debug_scores(self.h, _ptr(C), _ptr(out), ct.byref(kind), ct.byref(unit)))
+        return out, kind.value, unit.value
+
+    def bounds_export(self):
+        """(ub, lb, p2, C_ref) of the bounded engine between passes (kmeans_bounds_export)."""
+        t = self.torch
+        ub = t.empty(self.n, dtype=t.float32, device=self.device)
+        lb = t.empty_like(ub)
+        p2 = t.empty(self.n, dtype=t.int32, device=self.device)
+        Cr = t.empty((self.K, self.d), dtype=t.float64, device=self.device)
+        self._c(lib().kmeans_bounds_export(self.h, _ptr(ub), _ptr(lb), _ptr(p2), _ptr(Cr)))
+        return ub, lb, p2, Cr
+
+    def bounds_repeat(self):
+        """kmeans_bounds_repeat (destructive): (ub, lb after call 1, rows scored by the two
+        calls, labels identical)."""
+        t = self.torch
+        ub = t.empty(self.n, dtype=t.float32, device=self.device)
+        lb = t.empty_like(ub)
+        sc = (ct.c_int64 * 2)()
+        same = ct.c_int32()
+        self._c(lib().kmeans_bounds_repeat(self.h, _ptr(ub), _ptr(lb), sc, ct.byref(same)))
+        return ub, lb, (sc[0], sc[1]), bool(same.value)
 
     def last_flagged(self) -> int:
         v = ct.c_int64()

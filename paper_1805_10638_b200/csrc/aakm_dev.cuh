@@ -133,6 +133,7 @@ struct Dev {
     int gram_blocks;
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
+    float4* dbg_rows;     // kmeans_debug_scores only: per row (b1, b2, tau, i1 bits) of the dense engine
     int dev;              // CUDA device ordinal of the handle
     int num_sms;          // its SM count (persistent grids)
 };

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(256) k_assign_simt(Dev d, GEval g, int KT) {
         const float tau = gam * (xn[r] + cmax2);
         bool flag = ok && (b2[r] - b1[r] <= tau);
         if (ok) lab_out[row] = i1[r];
+        if (d.dbg_rows && ok) d.dbg_rows[row] = make_float4(b1[r], b2[r], tau, __int_as_float(i1[r]));
         push_flag(d, g.branch, flag, row, b1[r], tau);
     }
 }
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(128) k_assign_simt_generic(Dev d, GEval g, int
     const float tau = d.tau_gamma * (xn + cmax2);
     bool flag = ok && (b2 - b1 <= tau);
     if (ok) lab_out[row] = i1;
+    if (d.dbg_rows && ok) d.dbg_rows[row] = make_float4(b1, b2, tau, __int_as_float(i1));
     push_flag(d, g.branch, flag, row, b1, tau);
 }
 

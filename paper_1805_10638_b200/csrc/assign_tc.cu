@@ -853,6 +853,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     if (KIND && flag && t.i2 >= 0 && K <= 131040)
                         pair = wdecode(__uint_as_float(__float_as_uint(t.L) & ~0xFFFu)) > b1 + tau;
                     if (ok) lab_out[row] = i1;
+                    if (d.dbg_rows && ok && MODE == 0)               // kmeans_debug_scores (margin probes)
+                        d.dbg_rows[row] = make_float4(b1, b2, tau, __int_as_float(i1));
                     if (KIND && ok && d.ub) {
                         // Hamerly bounds for the next assignment (distance units, rounded
                         // outward): each accumulator is within tau of its exact value.

@@ -16,7 +16,9 @@
 
 #include <string>
 #include <algorithm>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/aakm.h"
@@ -61,6 +63,7 @@ struct kmeans_handle {
     int* done_host = nullptr;                                // pinned
     unsigned int* xchk = nullptr;                            // device, 2 words: stats of a refreshed X
     unsigned int x_stat[2] = {0u, 0u};                       // this rank's create-time max |x|, max ||x||^2 (float bits)
+    cudaEvent_t sync_ev = nullptr;                           // polled by sync_stream when a communicator exists
 };
 
 static thread_local std::string g_create_err;
@@ -134,6 +137,17 @@ static void dbg(const char* what, cudaStream_t s) {
             (h)->poisoned = true;                                                          \
             return KMEANS_ERR_NCCL;                                                        \
         }                                                                                  \
+    } while (0)
+
+// Wait for the stream.  With a communicator, poll instead of blocking: a peer
+// that failed (ncclCommGetAsyncError) or a collective that does not complete
+// within AAKM_COMM_TIMEOUT_S seconds (default 600) aborts the communicator and
+// poisons the handle, so kmeans_run cannot hang forever on a dead rank.
+static kmeans_status sync_stream(kmeans_handle* h, cudaStream_t s);
+#define SYNC(h, s)                                                                         \
+    do {                                                                                   \
+        kmeans_status r_ = sync_stream((h), (s));                                          \
+        if (r_ != KMEANS_OK) return r_;                                                    \
     } while (0)
 
 #define LIVE(h)                                                                            \
@@ -275,7 +289,7 @@ static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
 // rank (and every rank count) sees the same bytes.  The E slot is still zero
 // here; k_energy fills it from the reduced sums afterwards.
 static kmeans_status allreduce(kmeans_handle* h, long long* buf, cudaStream_t s) {
-    if (h->nranks <= 1) return KMEANS_OK;
+    if (!h->comm) return KMEANS_OK;                 // nranks == 1 (unless cfg.comm_always)
     const size_t cnt = (size_t)pk_words(h->d);     // the E slot is still 0 here (k_energy runs after)
     NK(h, ncclAllReduce(buf, buf, cnt, ncclInt64, ncclSum, h->comm, s));
     return KMEANS_OK;
@@ -338,7 +352,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     dbg("update", s);
     st = allreduce(h, d.packed[branch], s);
     if (st != KMEANS_OK) return st;
-    if (h->nranks > 1) dbg("allreduce", s);
+    if (h->comm) dbg("allreduce", s);
     launch_energy(d, g, s);
     dbg("energy", s);
     launch_control(d, branch, s);
@@ -418,6 +432,7 @@ static void release(kmeans_handle* h, bool sync) {
     for (auto& e : h->uev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (h->run_ev[0]) cudaEventDestroy(h->run_ev[0]);
     if (h->run_ev[1]) cudaEventDestroy(h->run_ev[1]);
+    if (h->sync_ev) cudaEventDestroy(h->sync_ev);
     if (h->st_host) cudaFreeHost(h->st_host);
     if (h->tr_host) cudaFreeHost(h->tr_host);
     if (h->scal_host) cudaFreeHost(h->scal_host);
@@ -427,6 +442,44 @@ static void release(kmeans_handle* h, bool sync) {
         else ncclCommAbort(h->comm);             // a failed / poisoned communicator may never complete
     }
     delete h;
+}
+
+static double comm_timeout_s() {
+    static const double t = getenv("AAKM_COMM_TIMEOUT_S") ? atof(getenv("AAKM_COMM_TIMEOUT_S")) : 600.0;
+    return t > 0.0 ? t : 600.0;
+}
+
+static kmeans_status sync_stream(kmeans_handle* h, cudaStream_t s) {
+    if (!h->comm) {
+        CK(h, cudaStreamSynchronize(s));
+        return KMEANS_OK;
+    }
+    if (!h->sync_ev) CK(h, cudaEventCreateWithFlags(&h->sync_ev, cudaEventDisableTiming));
+    CK(h, cudaEventRecord(h->sync_ev, s));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 0;; ++spin) {
+        const cudaError_t q = cudaEventQuery(h->sync_ev);
+        if (q == cudaSuccess) return KMEANS_OK;
+        if (q != cudaErrorNotReady) CK(h, q);
+        ncclResult_t ar = ncclSuccess;
+        ncclResult_t r = ncclCommGetAsyncError(h->comm, &ar);
+        if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+            h->err = std::string("NCCL asynchronous error: ") + ncclGetErrorString(r != ncclSuccess ? r : ar);
+            ncclCommAbort(h->comm);
+            h->comm = nullptr;
+            h->poisoned = true;
+            return KMEANS_ERR_NCCL;
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > comm_timeout_s()) {
+            h->err = "collective did not complete within AAKM_COMM_TIMEOUT_S seconds (peer failure?): communicator aborted";
+            ncclCommAbort(h->comm);
+            h->comm = nullptr;
+            h->poisoned = true;
+            return KMEANS_ERR_NCCL;
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
 }
 
 // kmeans_aa_step_host refreshed X with rows outside the create-time ranges: the
@@ -644,9 +697,12 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     CKC(cudaMemsetAsync(w + L.st, 0, sizeof(DevState), h->stream));
     CKC(cudaMemsetAsync(w + L.st_api, 0, sizeof(DevState), h->stream));
     CKC(cudaMemsetAsync(w + L.upd_part, 0, (size_t)AAKM_UPD_MAX_BLOCKS * 16, h->stream));
-    if (nranks > 1) {
+    if (nranks > 1 || cfg->comm_always) {
+        // nranks == 1 with cfg.comm_always: a real 1-rank communicator, so every
+        // allreduce of the data plane runs through NCCL (tests of that path on one GPU)
         ncclUniqueId id;
-        memcpy(&id, uid128, 128);
+        if (nranks > 1) memcpy(&id, uid128, 128);
+        else if (ncclGetUniqueId(&id) != ncclSuccess) { g_create_err = "ncclGetUniqueId failed"; release(h, false); return KMEANS_ERR_NCCL; }
         ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
         if (r != ncclSuccess) {
             h->comm = nullptr;
@@ -660,13 +716,17 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     {
         unsigned int* mx = (unsigned int*)(w + L.scratch);            // scratch is free until the first pass
         CKC(cudaMemcpyAsync(mx, mloc, 8, cudaMemcpyHostToDevice, h->stream));
-        if (nranks > 1) {
+        if (h->comm) {
             ncclResult_t r = ncclAllReduce(mx, mx, 2, ncclFloat32, ncclMax, h->comm, h->stream);
             if (r != ncclSuccess) { g_create_err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); release(h, false); return KMEANS_ERR_NCCL; }
         }
         unsigned int mb[2];
         CKC(cudaMemcpyAsync(mb, mx, 8, cudaMemcpyDeviceToHost, h->stream));
-        CKC(cudaStreamSynchronize(h->stream));
+        if (sync_stream(h, h->stream) != KMEANS_OK) {           // polls NCCL errors / timeout
+            g_create_err = h->err;
+            release(h, false);
+            return KMEANS_ERR_NCCL;
+        }
         float mf[2];
         memcpy(mf, mb, 8);
         int ex = 0;
@@ -708,12 +768,91 @@ kmeans_status kmeans_assign(kmeans_handle* h, const double* C, const int32_t* la
     h->launches += 1;
     CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + pk_e(d), 16, cudaMemcpyDeviceToHost, s));   // E, changed
     CK(h, cudaMemcpyAsync(h->scal_host + 2, d.flag_count, 8, cudaMemcpyDeviceToHost, s));
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     CK(h, cudaGetLastError());
     long long raw[2];
     memcpy(raw, h->scal_host, 16);
     if (energy_out) memcpy(energy_out, &raw[0], 8);                  // fp64 bits (k_energy)
     if (changed_out) *changed_out = labels_prev ? (int64_t)raw[1] : 0;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_debug_scores(kmeans_handle* h, const double* C, float* rows_out, int32_t* kind_out,
+                                  double* unit_out) {
+    LIVE(h);
+    if (!C || (!rows_out && h->d.n > 0) || !kind_out || !unit_out) FAIL(h, KMEANS_ERR_INVALID, "NULL argument");
+    cudaStream_t s = h->stream;
+    Dev d = h->da;
+    d.dbg_rows = reinterpret_cast<float4*>(rows_out);
+    CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+    combine(h, d, 2, C, s);
+    GEval g{};
+    g.branch = 0; g.force = 1; g.lab_out = d.lab[0]; g.prev_mode = 1;
+    assign_engine(h, d, g, s);
+    h->launches += 1;
+    float sc = 1.f;
+    CK(h, cudaMemcpyAsync(h->scal_host, &d.st->c_scale, 4, cudaMemcpyDeviceToHost, s));
+    SYNC(h, s);
+    CK(h, cudaGetLastError());
+    memcpy(&sc, h->scal_host, 4);
+    if (h->path == KMEANS_PATH_TC16) { *kind_out = 1; *unit_out = 0.5 / ((double)sc * (double)sc); }
+    else if (h->path == KMEANS_PATH_TC) { *kind_out = 0; *unit_out = 1.0; }
+    else { *kind_out = 2; *unit_out = 1.0; }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_bounds_export(kmeans_handle* h, float* ub_out, float* lb_out, int32_t* p2_out, double* Cref_out) {
+    LIVE(h);
+    const Dev& d = h->d;
+    if (!d.ub) FAIL(h, KMEANS_ERR_INVALID, "handle has no bounded engine (cfg.bounded = 1, 2xFP16 engine)");
+    cudaStream_t s = h->stream;
+    const size_t n = (size_t)d.n;
+    if (ub_out && n) CK(h, cudaMemcpyAsync(ub_out, d.ub, n * 4, cudaMemcpyDeviceToDevice, s));
+    if (lb_out && n) CK(h, cudaMemcpyAsync(lb_out, d.lb, n * 4, cudaMemcpyDeviceToDevice, s));
+    if (p2_out && n) CK(h, cudaMemcpyAsync(p2_out, d.pj2, n * 4, cudaMemcpyDeviceToDevice, s));
+    if (Cref_out) CK(h, cudaMemcpyAsync(Cref_out, d.C_ref, (size_t)d.K * d.d * 8, cudaMemcpyDeviceToDevice, s));
+    SYNC(h, s);
+    return KMEANS_OK;
+}
+
+// Two bounded assignments of the current C^t back to back (SPEC.md:126 idempotence):
+// the second sees zero drift.  Destructive test hook (overwrites P^{t-1}).
+kmeans_status kmeans_bounds_repeat(kmeans_handle* h, float* ub1_out, float* lb1_out, int64_t* scored_out,
+                                   int32_t* same_out) {
+    LIVE(h);
+    const Dev& d = h->d;
+    if (!d.ub) FAIL(h, KMEANS_ERR_INVALID, "handle has no bounded engine (cfg.bounded = 1, 2xFP16 engine)");
+    if (!scored_out || !same_out) FAIL(h, KMEANS_ERR_INVALID, "NULL output");
+    cudaStream_t s = h->stream;
+    CK(h, cudaMemcpyAsync(h->st_host, d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    SYNC(h, s);
+    if (h->st_host->done || h->st_host->init_mode) FAIL(h, KMEANS_ERR_STATE, "needs a live Algorithm 1 state");
+    const int cur = h->st_host->cur;
+    long long sc[2];
+    for (int k = 0; k < 2; ++k) {
+        CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+        GEval g{};
+        g.branch = 0; g.force = 1; g.prev_mode = 1;
+        assign_engine(h, d, g, s);                      // labels -> lab[st->cur], lab_ref = lab[cur ^ 1]
+        refine_engine(h, d, g, s);
+        CK(h, cudaMemcpyAsync(&sc[k], d.act_count, 8, cudaMemcpyDeviceToHost, s));
+        if (k == 0) {
+            if (ub1_out && d.n) CK(h, cudaMemcpyAsync(ub1_out, d.ub, (size_t)d.n * 4, cudaMemcpyDeviceToDevice, s));
+            if (lb1_out && d.n) CK(h, cudaMemcpyAsync(lb1_out, d.lb, (size_t)d.n * 4, cudaMemcpyDeviceToDevice, s));
+            const int nc = cur ^ 1;                     // the bounds now refer to the labels just written
+            CK(h, cudaMemcpyAsync(&d.st->cur, &nc, 4, cudaMemcpyHostToDevice, s));
+        }
+        SYNC(h, s);
+    }
+    std::vector<int> a(d.n), b(d.n);
+    if (d.n) {
+        CK(h, cudaMemcpy(a.data(), d.lab[cur], (size_t)d.n * 4, cudaMemcpyDeviceToHost));
+        CK(h, cudaMemcpy(b.data(), d.lab[cur ^ 1], (size_t)d.n * 4, cudaMemcpyDeviceToHost));
+    }
+    const int c0 = cur;
+    CK(h, cudaMemcpy(&d.st->cur, &c0, 4, cudaMemcpyHostToDevice));
+    scored_out[0] = sc[0]; scored_out[1] = sc[1];
+    *same_out = a == b ? 1 : 0;
     return KMEANS_OK;
 }
 
@@ -734,7 +873,7 @@ kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const doubl
     launch_update_G(d, d.packed[0], C_prev, G_out, (long long*)counts_out, s);
     h->launches += 1;
     CK(h, cudaMemcpyAsync(h->done_host, &d.st->label_error, 4, cudaMemcpyDeviceToHost, s));
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     CK(h, cudaGetLastError());
     if (*h->done_host) FAIL(h, KMEANS_ERR_INVALID, "labels outside [0, K)");
     return KMEANS_OK;
@@ -754,7 +893,7 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     h->launches += launch_update(d, g, s);
     launch_partials_out(d, d.packed[0], packed_out, s);               // unreduced, as doubles
     h->launches += 1;
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     CK(h, cudaGetLastError());
     return KMEANS_OK;
 }
@@ -782,7 +921,7 @@ static kmeans_status step_info(kmeans_handle* h, kmeans_step_info* info, double*
     if (info || theta_out) {
         cudaStream_t s = h->stream;
         CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-        CK(h, cudaStreamSynchronize(s));
+        SYNC(h, s);
         if (h->st_host->label_error & 2) x_range_error(h);
         if (h->poisoned) return KMEANS_ERR_INVALID;
         const long long n = h->st_host->trace_len;
@@ -877,7 +1016,7 @@ kmeans_status kmeans_run(kmeans_handle* h, const double* C0, double* C_out, int3
         }
         passes += batch;
         CK(h, cudaMemcpyAsync(h->done_host, &h->d.st->done, 4, cudaMemcpyDeviceToHost, s));
-        CK(h, cudaStreamSynchronize(s));
+        SYNC(h, s);
         if (*h->done_host) break;
         if (passes > (long long)h->cfg.max_iters + 8) FAIL(h, KMEANS_ERR_STATE, "run did not terminate");
         if (batch < 16) batch *= 2;
@@ -885,14 +1024,14 @@ kmeans_status kmeans_run(kmeans_handle* h, const double* C0, double* C_out, int3
     CK(h, cudaEventRecord(h->run_ev[1], s));
     if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 8, cudaMemcpyDeviceToDevice, s));
     CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     const DevState& S = *h->st_host;
     if (S.label_error & 2) { x_range_error(h); return KMEANS_ERR_INVALID; }
     if (labels_out && h->d.n > 0)
         CK(h, cudaMemcpyAsync(labels_out, h->d.lab[S.cur], (size_t)h->d.n * 4, cudaMemcpyDeviceToDevice, s));
     float ms = 0.f;
     CK(h, cudaEventElapsedTime(&ms, h->run_ev[0], h->run_ev[1]));
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     memset(rep, 0, sizeof(*rep));
     rep->converged = S.converged;
     rep->iters = S.converged ? S.t + 1 : S.t;
@@ -912,7 +1051,7 @@ kmeans_status kmeans_get_centroids(kmeans_handle* h, double* C_out, int32_t* lab
     if (C_out) CK(h, cudaMemcpyAsync(C_out, h->d.C, (size_t)h->d.K * h->d.d * 8, cudaMemcpyDeviceToDevice, s));
     if (labels_out) {
         CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-        CK(h, cudaStreamSynchronize(s));
+        SYNC(h, s);
         // after a pass the last assignment is P^t = lab[cur ^ 1] unless the run stopped (done)
         const DevState& S = *h->st_host;
         int which = S.done ? S.cur : (S.cur ^ 1);
@@ -926,7 +1065,7 @@ kmeans_status kmeans_state_export(kmeans_handle* h, kmeans_state* out) {
     if (!out) FAIL(h, KMEANS_ERR_INVALID, "NULL state");
     cudaStream_t s = h->stream;
     CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     const DevState& S = *h->st_host;
     const Dev& d = h->d;
     const size_t KD = (size_t)d.K * d.d;
@@ -966,7 +1105,7 @@ kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
     if (st->t < 1) FAIL(h, KMEANS_ERR_INVALID, "t < 1 (export after Algorithm 1 line 1)");
     cudaStream_t s = h->stream;
     const size_t KD = (size_t)d.K * d.d;
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     // history into the ring slots it came from: entry j = (G^{t-1-j}, F^{t-1-j})
     for (int j = 0; j < st->hist_count; ++j) {
         const long long slot = ((st->t - 1 - j) % d.H + d.H) % d.H;
@@ -1007,14 +1146,14 @@ kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
     }
     CK(h, cudaMemcpy(d.st, &S, sizeof(DevState), cudaMemcpyHostToDevice));
     combine(h, d, 2, d.C, s);                                     // operand prep of C^t
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     CK(h, cudaGetLastError());
     return KMEANS_OK;
 }
 
 kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* launches) {
     LIVE(h);
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h, h->stream);
     double tot = 0.0;
     for (size_t i = 0; i < h->ev_used; ++i) {
         float ms = 0.f;
@@ -1029,7 +1168,7 @@ kmeans_status kmeans_assign_timing(kmeans_handle* h, double* ms_total, int64_t* 
 
 kmeans_status kmeans_update_timing(kmeans_handle* h, double* ms_total, int64_t* launches) {
     LIVE(h);
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h, h->stream);
     double tot = 0.0;
     for (size_t i = 0; i < h->uev_used; ++i) {
         float ms = 0.f;
@@ -1057,13 +1196,13 @@ kmeans_status kmeans_seed_pp(kmeans_handle* h, const double* u, float* C_out, in
     cudaStream_t s = h->stream;
     const long long N = h->n_global;
     long long offset = 0;                               // this rank's first global row
-    if (h->nranks > 1) {
+    if (h->comm) {
         std::vector<long long> nl(h->nranks, 0);
         nl[h->rank] = d.n;
         CK(h, cudaMemcpyAsync(d.seed_T, nl.data(), 8 * h->nranks, cudaMemcpyHostToDevice, s));
         NK(h, ncclAllReduce(d.seed_T, d.seed_T, h->nranks, ncclInt64, ncclSum, h->comm, s));
         CK(h, cudaMemcpyAsync(nl.data(), d.seed_T, 8 * h->nranks, cudaMemcpyDeviceToHost, s));
-        CK(h, cudaStreamSynchronize(s));
+        SYNC(h, s);
         for (int q = 0; q < h->rank; ++q) offset += nl[q];
     }
     CK(h, cudaMemcpyAsync(d.seed_u, u, 8 * (size_t)K, cudaMemcpyHostToDevice, s));
@@ -1078,17 +1217,17 @@ kmeans_status kmeans_seed_pp(kmeans_handle* h, const double* u, float* C_out, in
     if (i0 > N - 1) i0 = N - 1;
     const long long loc = (i0 >= offset && i0 < offset + d.n) ? i0 - offset : -1;
     launch_seed_first(d, loc, i0, s);
-    if (h->nranks > 1) NK(h, ncclAllReduce(d.seed_x, d.seed_x, d.d + 2, ncclInt32, ncclSum, h->comm, s));
+    if (h->comm) NK(h, ncclAllReduce(d.seed_x, d.seed_x, d.d + 2, ncclInt32, ncclSum, h->comm, s));
     launch_seed_commit(d, C_out, 0, s);
     h->launches += 2;
     for (int r = 1; r < K; ++r) {
         launch_seed_dist(d, C_out + (long long)(r - 1) * d.d, r == 1, scale, s);
-        if (h->nranks > 1)
+        if (h->comm)
             NK(h, ncclAllReduce(&d.st->seed_max, &d.st->seed_max, 1, ncclInt64, ncclMax, h->comm, s));
         launch_seed_weights(d, log2n, h->rank, h->nranks, s);
-        if (h->nranks > 1) NK(h, ncclAllReduce(d.seed_T, d.seed_T, h->nranks, ncclInt64, ncclSum, h->comm, s));
+        if (h->comm) NK(h, ncclAllReduce(d.seed_T, d.seed_T, h->nranks, ncclInt64, ncclSum, h->comm, s));
         launch_seed_select(d, r, log2n, h->rank, h->nranks, offset, s);
-        if (h->nranks > 1) NK(h, ncclAllReduce(d.seed_x, d.seed_x, d.d + 2, ncclInt32, ncclSum, h->comm, s));
+        if (h->comm) NK(h, ncclAllReduce(d.seed_x, d.seed_x, d.d + 2, ncclInt32, ncclSum, h->comm, s));
         launch_seed_commit(d, C_out, r, s);
         h->launches += 5;
         if ((r & 255) == 0) CK(h, cudaGetLastError());
@@ -1096,7 +1235,7 @@ kmeans_status kmeans_seed_pp(kmeans_handle* h, const double* u, float* C_out, in
     int err = 0;
     CK(h, cudaMemcpyAsync(&err, &d.st->seed_err, 4, cudaMemcpyDeviceToHost, s));
     if (idx_out) CK(h, cudaMemcpyAsync(idx_out, d.seed_idx, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
-    CK(h, cudaStreamSynchronize(s));
+    SYNC(h, s);
     CK(h, cudaGetLastError());
     if (err) FAIL(h, KMEANS_ERR_INVALID, "fewer distinct samples than K (every remaining D^2 is 0)");
     return KMEANS_OK;
@@ -1106,7 +1245,7 @@ kmeans_status kmeans_bounded_stats(kmeans_handle* h, int64_t* rows_scored, int64
     LIVE(h);
     if (!rows_scored || !rows_total) FAIL(h, KMEANS_ERR_INVALID, "NULL output");
     CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h, h->stream);
     *rows_scored = h->st_host->rows_scored;
     *rows_total = h->st_host->rows_total;
     return KMEANS_OK;
@@ -1116,7 +1255,7 @@ kmeans_status kmeans_last_flagged(kmeans_handle* h, int64_t* flagged) {
     LIVE(h);
     if (!flagged) return KMEANS_ERR_INVALID;
     long long v[2], pr[2];
-    CK(h, cudaStreamSynchronize(h->stream));
+    SYNC(h, h->stream);
     CK(h, cudaMemcpy(v, h->d.flag_count, 16, cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(pr, h->d.pair_count, 16, cudaMemcpyDeviceToHost));
     *flagged = v[0] + pr[0];                            // candidate-pass rows + two-centroid rows
