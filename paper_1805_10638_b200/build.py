@@ -25,14 +25,18 @@ def nccl_dir():
     raise RuntimeError("torch-wheel NCCL (nvidia/nccl) not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    global OUT, BUILD
+    if out:                                  # A/B variant builds (tools/): another .so and build dir
+        OUT, BUILD = out, out + ".build"
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "aakm.h")]
     nd = nccl_dir()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     flags = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
              "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include"),
-             "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+             "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
+             *os.environ.get("AAKM_NVCC_EXTRA", "").split()]     # perf experiments only (A/B variants)
     # content stamp (sources + flags): mtimes alone missed edits made while a build ran
     h = hashlib.sha256(" ".join(flags).encode())
     for p in srcs + hdrs:

@@ -11,7 +11,7 @@
 #define AAKM_MAXC 32               // candidates kept per flagged row
 #define AAKM_SORTED_MIN_ROWS 65536  // label-sorted update engine from this many rows
 #define AAKM_SORTED_MAX_K 16384     // ... and up to this many clusters (smem histograms)
-#define AAKM_SEG_BLOCKS 148         // row blocks of the histogram / scatter
+#define AAKM_SEG_BLOCKS_MAX 512     // row blocks of the histogram / scatter (Dev::seg_blocks)
 #define AAKM_MAX_RANKS 1024         // NCCL ranks per communicator this build sizes for
 #define AAKM_SEED_BLOCKS 1184      // row blocks of the K-Means++ passes (8 x 148)
 #define AAKM_CNIMG_BYTES 4096       // folded ||c||^2 block of one 128-centroid tile (128 rows x 32 B)
@@ -130,6 +130,7 @@ struct Dev {
     int nranks;
     int upd_blocks;
     int upd_sorted;       // label-sorted update engine (chosen from n_global, d, K: the same on every rank)
+    int seg_blocks;       // its row blocks (histogram / scatter partition; 2 per SM for K <= 4096)
     int gram_blocks;
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
@@ -230,6 +231,10 @@ __device__ inline double energy_q(const Dev& d) {
 __device__ inline long long energy_fx(double v) {
     return __double_as_longlong(v + 6291456.0) - 0x4158000000000000LL;
 }
+// the same before the constant is removed (the caller subtracts count * ENERGY_FX_BIAS
+// once per flush): energy_bits(e, q) - ENERGY_FX_BIAS == energy_fx(e * q) (q is a power of 2)
+#define ENERGY_FX_BIAS 0x4158000000000000LL
+__device__ inline long long energy_bits(double e, double q) { return __double_as_longlong(fma(e, q, 6291456.0)); }
 __device__ inline void energy_flush(long long& acc, long long& hi, long long& lo) {
     hi += acc >> 30;
     lo += acc & 0x3fffffffLL;

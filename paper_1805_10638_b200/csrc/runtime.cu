@@ -203,7 +203,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.packed1 = take(pk);                  // packed[1]
     L.scratch_bytes = o - L.scratch;
     L.upd_part = take((size_t)AAKM_UPD_MAX_BLOCKS * 16);
-    L.seg_bh = take((size_t)AAKM_SEG_BLOCKS * K * 4);
+    L.seg_bh = take((size_t)AAKM_SEG_BLOCKS_MAX * K * 4);
     L.seg_off = take((size_t)K * 4 + 4);
     L.seg_chunk = take((size_t)K * 4 + 4);
     L.seg_cmap = take(((size_t)n / 256 + K + 1) * 16);
@@ -647,7 +647,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     } while (0)
     CKC(cudaGetDevice(&D.dev));
     CKC(cudaDeviceGetAttribute(&D.num_sms, cudaDevAttrMultiProcessorCount, D.dev));
-    h->da.dev = D.dev; h->da.num_sms = D.num_sms;
+    D.seg_blocks = std::min(AAKM_SEG_BLOCKS_MAX, D.num_sms);      // (2 per SM measured slower: c5 scatter 157 vs 129 us)
+    h->da.dev = D.dev; h->da.num_sms = D.num_sms; h->da.seg_blocks = D.seg_blocks;
     CKC(setup_device(D.dev));
     CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     // this rank's max |x_ik| and max ||x_i||^2 (one pass; float bits of non-negative

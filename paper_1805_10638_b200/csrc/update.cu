@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 //   k_hist         N_j (block histograms in smem) + #changed + label check
 //   k_scan_a       per cluster: N_j -> packed, per-(block, cluster) offsets
 //   k_scan_b       exclusive scans over clusters (row offsets, chunk counts)
-//   k_scatter      chunk table {j, first row, rows} + perm[offset_j + rank] = row
+//   k_scatter      chunk table {j, first row, rows} + perm[offset_j + rank] = row, written
+//                  from per-block counting-sorted sub-tiles (coalesced runs)
 //   k_segsum_bulk  d = 4 LPR: rows gathered by TMA tile::gather4 into per-warp
 //                  mbarrier rings; S_j += chunk rows, E += per-lane parts
 //   k_segsum       other d: lanes over coordinates, the same sums
@@ -164,7 +165,7 @@ __device__ void finish_changed(const Dev& d, long long* out, long long ch) {
 // base + local rank (shared-memory counters): no global atomics on the
 // contended per-cluster cursors.
 __device__ __forceinline__ void block_rows(const Dev& d, long long& r0, long long& r1) {
-    const long long per = (d.n + gridDim.x - 1) / gridDim.x;
+    const long long per = ((d.n + gridDim.x - 1) / gridDim.x + 7) & ~7LL;    // 32-B aligned row ranges
     r0 = (long long)blockIdx.x * per;
     r1 = min(d.n, r0 + per);
 }
@@ -180,22 +181,26 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     block_rows(d, r0, r1);
     long long ch = 0;
     int bad = 0;
-    // 4 labels per thread per step (more loads in flight: the pass is latency-bound)
-    const long long nv = (r1 - r0) / 4;
+    // 8 labels per thread per step as two 16-B loads (more bytes in flight: the pass is
+    // latency-bound); row ranges start 32-B aligned, a caller's unaligned labels go scalar
+    const bool vec = ((reinterpret_cast<uintptr_t>(p.lab) | reinterpret_cast<uintptr_t>(p.prev)) & 15) == 0;
+    const long long nv = vec ? (r1 - r0) / 8 : 0;
     for (long long v = threadIdx.x; v < nv; v += blockDim.x) {
-        const long long i = r0 + 4 * v;
-        int l4[4], p4[4];
+        const long long i = r0 + 8 * v;
+        const int4 la = *reinterpret_cast<const int4*>(p.lab + i), lb = *reinterpret_cast<const int4*>(p.lab + i + 4);
+        int4 pa = la, pb = lb;
+        if (p.prev) { pa = *reinterpret_cast<const int4*>(p.prev + i); pb = *reinterpret_cast<const int4*>(p.prev + i + 4); }
+        const int l8[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+        const int p8[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { l4[u] = p.lab[i + u]; p4[u] = p.prev ? p.prev[i + u] : l4[u]; }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = l4[u];
+        for (int u = 0; u < 8; ++u) {
+            const int j = l8[u];
             if (j < 0 || j >= K) { bad = 1; continue; }
-            ch += (p4[u] != j);
+            ch += (p8[u] != j);
             atomicAdd(&hs[j], 1);
         }
     }
-    for (long long i = r0 + 4 * nv + threadIdx.x; i < r1; i += blockDim.x) {
+    for (long long i = r0 + 8 * nv + threadIdx.x; i < r1; i += blockDim.x) {
         const int j = p.lab[i];
         if (j < 0 || j >= K) { bad = 1; continue; }
         if (p.prev) ch += (p.prev[i] != j);
@@ -208,30 +213,38 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     finish_changed(d, p.out, ch);
 }
 
-// Phase A (one thread per cluster, many blocks): N_j = sum over row blocks, and
-// the per-(block, cluster) offsets within cluster j (exclusive scan over blocks).
+// Phase A (one warp per cluster): N_j = sum over the row blocks, and the
+// per-(block, cluster) offsets within cluster j (exclusive scan over blocks:
+// lane l owns a contiguous run of blocks, then a warp scan of the run sums).
 __global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     const int K = d.K;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (j >= K) return;
-    long long o = 0;
-    int b = 0;
-    for (; b + 8 <= nblk; b += 8) {
-        int t[8];
+    const int per = (nblk + 31) / 32;                    // <= 16 for the <= 512 row blocks this build uses
+    const int b0 = min(nblk, lane * per), b1 = min(nblk, b0 + per);
+    int t[16];
+    int sum = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = d.seg_bh[(long long)(b + u) * K + j];
+    for (int u = 0; u < 16; ++u) {
+        t[u] = (u < per && b0 + u < b1) ? d.seg_bh[(long long)(b0 + u) * K + j] : 0;
+        sum += t[u];
+    }
+    int inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    int o = inc - sum;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) { d.seg_bh[(long long)(b + u) * K + j] = (int)o; o += t[u]; }
+    for (int u = 0; u < 16; ++u)
+        if (u < per && b0 + u < b1) { d.seg_bh[(long long)(b0 + u) * K + j] = o; o += t[u]; }
+    if (lane == 31) {
+        d.seg_off[j] = inc;                               // count for now; phase B makes it an offset
+        p.out[pk_n(d) + j] = inc;                         // N_j
     }
-    for (; b < nblk; ++b) {
-        const int t = d.seg_bh[(long long)b * K + j];
-        d.seg_bh[(long long)b * K + j] = (int)o;
-        o += t;
-    }
-    d.seg_off[j] = (int)o;                               // count for now; phase B makes it an offset
-    p.out[pk_n(d) + j] = o;                              // N_j
 }
 
 // Phase B (one block): exclusive scans over clusters of the counts and of the
@@ -278,11 +291,53 @@ __global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
     if (threadIdx.x == 0) { d.seg_off[K] = (int)carry[0]; d.seg_chunk[K] = (int)carry[1]; }
 }
 
-__global__ void __launch_bounds__(1024) k_scatter(Dev d, GEval g) {
+// Exclusive scan of v[0..n) in place by one 1024-thread block (n <= 16 * 1024);
+// returns the total to every thread.
+__device__ int block_exscan(int* v, int n) {
+    __shared__ int ws[32];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int a = threadIdx.x * per, b = min(n, a + per);
+    int s = 0;
+    for (int i = a; i < b; ++i) s += v[i];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int x = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        ws[lane] = x;
+    }
+    __syncthreads();
+    int run = inc - s + (w ? ws[w - 1] : 0);
+    const int tot = ws[(blockDim.x >> 5) - 1];
+    for (int i = a; i < b; ++i) { const int t = v[i]; v[i] = run; run += t; }
+    __syncthreads();
+    return tot;
+}
+
+// Rows bucketed by label: block b re-walks its row range (the same ranges as
+// k_hist) in sub-tiles of T rows.  A sub-tile is counting-sorted by label in
+// shared memory first, then written out in sorted order, so consecutive threads
+// store consecutive perm entries of one cluster's run (whole sectors) instead
+// of one scattered 4-byte store per row.  Within a cluster the order of rows
+// is arbitrary (smem atomics); every sum downstream is order-free.
+constexpr int SCAT_RPT = 16;          // rows per thread per sub-tile (T <= 16 * blockDim)
+__global__ void __launch_bounds__(1024, 1) k_scatter(Dev d, GEval g, int T) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
-    extern __shared__ int cur[];
+    extern __shared__ __align__(16) unsigned char scat_sm[];
     const int K = d.K;
+    int* gcur = reinterpret_cast<int*>(scat_sm);   // K: next global perm slot of each cluster for this block
+    int* loff = gcur + K;           // K + 1: sub-tile counts -> exclusive offsets -> output bases
+    int2* stage = reinterpret_cast<int2*>(loff + K + 1 + 1);   // T: {row, label} sorted by label (8-B aligned)
     // chunk table {j, first sorted row, rows}: chunk w belongs to the last cluster
     // whose first chunk is <= w (binary search; empty clusters share starts)
     const long long nch = d.seg_chunk[K];
@@ -296,25 +351,76 @@ __global__ void __launch_bounds__(1024) k_scatter(Dev d, GEval g) {
         d.seg_cmap[w] = make_int4(lo, (int)r0, (int)min((long long)SEG_ROWS, (long long)d.seg_off[lo + 1] - r0), 0);
     }
     const int* bh = d.seg_bh + (long long)blockIdx.x * K;
-    for (int j = threadIdx.x; j < K; j += blockDim.x) cur[j] = bh[j] + d.seg_off[j];
-    __syncthreads();
+    for (int j = threadIdx.x; j < K; j += blockDim.x) gcur[j] = bh[j] + d.seg_off[j];
     long long r0, r1;
     block_rows(d, r0, r1);
-    const long long nv = (r1 - r0) / 4;
-    for (long long v = threadIdx.x; v < nv; v += blockDim.x) {
-        const long long i = r0 + 4 * v;
-        int l4[4];
+    for (long long t0 = r0; t0 < r1; t0 += T) {
+        const int nt = (int)min((long long)T, r1 - t0);
+        for (int j = threadIdx.x; j <= K; j += blockDim.x) loff[j] = 0;
+        __syncthreads();
+        int jr[SCAT_RPT], rk[SCAT_RPT];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) l4[u] = p.lab[i + u];
+        for (int u = 0; u < SCAT_RPT; ++u) {
+            const int q = u * (int)blockDim.x + threadIdx.x;
+            jr[u] = q < nt ? p.lab[t0 + q] : -1;
+        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (l4[u] >= 0 && l4[u] < K) d.perm[atomicAdd(&cur[l4[u]], 1)] = (int)(i + u);
+        for (int u = 0; u < SCAT_RPT; ++u) {
+            if (jr[u] >= 0 && jr[u] < K) rk[u] = atomicAdd(&loff[jr[u]], 1);
+            else jr[u] = -1;
+        }
+        __syncthreads();
+        const int nv = block_exscan(loff, K);
+#pragma unroll
+        for (int u = 0; u < SCAT_RPT; ++u)
+            if (jr[u] >= 0) stage[loff[jr[u]] + rk[u]] = make_int2((int)(t0 + u * (int)blockDim.x + threadIdx.x), jr[u]);
+        __syncthreads();
+        // loff[j] -> output base gcur[j] - loff[j] (consecutive sorted entries of a cluster
+        // map to consecutive perm slots); gcur advances by the sub-tile's counts
+        {
+            int cb[AAKM_SORTED_MAX_K / 1024], bb[AAKM_SORTED_MAX_K / 1024];   // K <= 16 per thread (1024 threads)
+#pragma unroll
+            for (int u = 0; u < AAKM_SORTED_MAX_K / 1024; ++u) {
+                const int j = threadIdx.x + u * (int)blockDim.x;
+                if (j < K) {
+                    const int o = loff[j];
+                    cb[u] = (j + 1 < K ? loff[j + 1] : nv) - o;
+                    bb[u] = gcur[j] - o;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < AAKM_SORTED_MAX_K / 1024; ++u) {
+                const int j = threadIdx.x + u * (int)blockDim.x;
+                if (j < K) { loff[j] = bb[u]; gcur[j] += cb[u]; }
+            }
+        }
+        __syncthreads();
+        int q = threadIdx.x;
+        for (; q + 3 * (int)blockDim.x < nv; q += 4 * blockDim.x) {
+            int2 e[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) e[u] = stage[q + u * blockDim.x];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d.perm[loff[e[u].y] + q + u * (int)blockDim.x] = e[u].x;
+        }
+        for (; q < nv; q += blockDim.x) {
+            const int2 e = stage[q];
+            d.perm[loff[e.y] + q] = e.x;
+        }
+        __syncthreads();
     }
-    for (long long i = r0 + 4 * nv + threadIdx.x; i < r1; i += blockDim.x) {
-        const int j = p.lab[i];
-        if (j < 0 || j >= K) continue;
-        d.perm[atomicAdd(&cur[j], 1)] = (int)i;
-    }
+}
+
+static_assert(sizeof(int2) == 8, "stage entry");
+constexpr int SCAT_SMEM = 220 * 1024;   // dynamic shared memory of k_scatter (+ its static scan buffer)
+// sub-tile rows: a multiple of the block size, <= SCAT_RPT rows per thread, inside
+// this block's share of the SM's shared memory
+static int scatter_tile(int K, int bt, int per_sm) {
+    const int budget = (per_sm == 2 ? 110 * 1024 : SCAT_SMEM) - 8 * (K + 1);
+    int T = budget / 8;
+    T = T / bt * bt;
+    return T > SCAT_RPT * bt ? SCAT_RPT * bt : T;
 }
 
 template <int V>   // floats per lane: d <= 32 * V
@@ -403,7 +509,7 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
 // Each warp walks its chunks (<= SEG_ROWS rows of one cluster j) as items of
 // <= SR rows (32, or 16 for d = 128). Producer side: lanes 0..SR/4-1 each start one TMA tile::gather4
 // (4 rows by index from the X map) and lane 31 a cp.async.bulk of the centroid
-// row c_j into a slot of the warp's SEG_NS-deep shared-memory ring, all
+// row c_j into a slot of the warp's NS-deep shared-memory ring, all
 // completing on the slot's mbarrier; the item's {j, rows, last} go to the
 // slot's record. Row ids
 // are loaded two items ahead and chunk records one chunk ahead, so no global
@@ -411,17 +517,22 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
 // each), RPW = 32 / LPR rows per shared-memory instruction. The sums are the
 // same exact fixed point as the other engines; the energy parts are this
 // lane's 4 coordinates by direct fp64 differences (energy_fx).
-constexpr int SEG_NS = 3;          // ring depth (items per warp)
+#ifndef AAKM_SEG_WMAX
+#define AAKM_SEG_WMAX 16
+#endif
 constexpr int SEG_SMEM = 215040;   // shared memory budget per block
 
 template <int LPR> struct SegBulk {
+    // ring depth (items per warp): 3, but 2 for d = 128 (LPR 32), whose 8-KB items
+    // otherwise leave too few warps per SM (c4: 2 slots x 11 warps 353 us, 3 x 7 458 us)
+    static constexpr int NS = LPR >= 32 ? 2 : 3;
     static constexpr int RB = 16 * LPR;                               // row bytes
     static constexpr int SR = 16;                                      // rows per item
     static constexpr int GP = 4 * RB > 128 ? 4 * RB : 128;            // gather4 group pitch (TMA dst: 128 B aligned)
     static constexpr int CO = SR / 4 * GP;                         // c_j row offset
     static constexpr int SLOT = (CO + 2 * RB + 127) / 128 * 128;       // rows + c_j (fp64: 2 RB bytes)
-    static constexpr int WARP = (SEG_NS * SLOT + SEG_NS * 16 + SEG_NS * 8 + 127) / 128 * 128;
-    static constexpr int WPB = SEG_SMEM / WARP > 16 ? 16 : SEG_SMEM / WARP;
+    static constexpr int WARP = (NS * SLOT + NS * 16 + NS * 8 + 127) / 128 * 128;
+    static constexpr int WPB = SEG_SMEM / WARP > AAKM_SEG_WMAX ? AAKM_SEG_WMAX : SEG_SMEM / WARP;
     static constexpr int SMEM = WPB * WARP;
 };
 
@@ -473,6 +584,7 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = lane / LPR, c4i = lane % LPR;
     unsigned char* ring = sm + warp * SB::WARP;
+    constexpr int SEG_NS = SB::NS;
     int4* rec = reinterpret_cast<int4*>(ring + SEG_NS * SB::SLOT);
     uint64_t* bar = reinterpret_cast<uint64_t*>(rec + SEG_NS);
     if (lane < SEG_NS) sb_init(bar + lane);
@@ -530,6 +642,8 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
     const float sc = d.fx_scale;
     const double q = energy_q(d);
     long long ehi = 0, elo = 0, ea = 0;
+    long long eb = 0;                                                  // full items: biased energy bits
+    int ne = 0;                                                        //   ... and how many
     unsigned phase = 0;                                                // bit b: parity of slot b
     int cs = 0;                                                        // consumer slot
     int h0 = 0, h1 = 0, h2 = 0, h3 = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
@@ -541,23 +655,42 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         const double2 c01 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i);
         const double2 c23 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i + 16);
         const double cx = c01.x, cy = c01.y, cz = c23.x, cw = c23.y;
+        if (d.dbg & 8) {                                               // AAKM_TC_DBG=8 probe: data movement only
+        } else if (RPW <= SR && r.y == SR) {                           // full item (warp-uniform): no masks
 #pragma unroll
-        for (int i = 0; i < IT; ++i) {                                 // branch-free: rows past r.y read as 0
-            const int rr = i * RPW + h;
-            const int ra = RPW > SR ? min(rr, SR - 1) : rr;                // stay inside the slot
-            const unsigned char* a = SB::GP == 4 * RB ? slot + ra * RB + 16 * c4i
-                                                      : slot + (ra >> 2) * SB::GP + (ra & 3) * RB + 16 * c4i;
-            float4 xv = *reinterpret_cast<const float4*>(a);
-            const bool ok = rr < r.y;
-            if (!ok) xv = make_float4(0.f, 0.f, 0.f, 0.f);              // adds nothing to the sums
-            fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
-            fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
-            double df = (double)xv.x - cx, e = df * df;                    // this lane's part of e_row
-            df = (double)xv.y - cy; e = fma(df, df, e);
-            df = (double)xv.z - cz; e = fma(df, df, e);
-            df = (double)xv.w - cw; e = fma(df, df, e);
-            const long long v = energy_fx(e * q);
-            ea += ok ? v : 0;
+            for (int i = 0; i < IT; ++i) {
+                const int rr = i * RPW + h;
+                const unsigned char* a = SB::GP == 4 * RB ? slot + rr * RB + 16 * c4i
+                                                          : slot + (rr >> 2) * SB::GP + (rr & 3) * RB + 16 * c4i;
+                const float4 xv = *reinterpret_cast<const float4*>(a);
+                fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
+                fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
+                double df = (double)xv.x - cx, e = df * df;                // this lane's part of e_row
+                df = (double)xv.y - cy; e = fma(df, df, e);
+                df = (double)xv.z - cz; e = fma(df, df, e);
+                df = (double)xv.w - cw; e = fma(df, df, e);
+                eb += energy_bits(e, q);                                   // bias removed at the flush
+            }
+            ne += IT;
+        } else {
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {                             // branch-free: rows past r.y read as 0
+                const int rr = i * RPW + h;
+                const int ra = RPW > SR ? min(rr, SR - 1) : rr;            // stay inside the slot
+                const unsigned char* a = SB::GP == 4 * RB ? slot + ra * RB + 16 * c4i
+                                                          : slot + (ra >> 2) * SB::GP + (ra & 3) * RB + 16 * c4i;
+                float4 xv = *reinterpret_cast<const float4*>(a);
+                const bool ok = rr < r.y;
+                if (!ok) xv = make_float4(0.f, 0.f, 0.f, 0.f);          // adds nothing to the sums
+                fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
+                fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
+                double df = (double)xv.x - cx, e = df * df;                // this lane's part of e_row
+                df = (double)xv.y - cy; e = fma(df, df, e);
+                df = (double)xv.z - cz; e = fma(df, df, e);
+                df = (double)xv.w - cw; e = fma(df, df, e);
+                const long long v = energy_fx(e * q);
+                ea += ok ? v : 0;
+            }
         }
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads done before the slot refills
@@ -566,6 +699,8 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         produce();
         if (!r.z) continue;
         // chunk done: combine the RPW row slots (lanes with equal c4i), exact int64 sums
+        ea += eb - (long long)ne * ENERGY_FX_BIAS;                     // (mod 2^64: exact)
+        eb = 0; ne = 0;
         energy_flush(ea, ehi, elo);                                    // <= SEG_ROWS rows
         long long s8[8] = {h0, h1, h2, h3, l0, l1, l2, l3};
 #pragma unroll
@@ -594,13 +729,13 @@ template <int LPR> static cudaError_t seg_attr() {
 template <int LPR> static void seg_launch(const Dev& d, const GEval& g, cudaStream_t s) {
     using SB = SegBulk<LPR>;
     const int per_sm = SB::SMEM <= 113 * 1024 ? 2 : 1;
-    k_segsum_bulk<LPR><<<AAKM_SEG_BLOCKS * per_sm, 32 * SB::WPB, SB::SMEM, s>>>(d, g);
+    k_segsum_bulk<LPR><<<d.num_sms * per_sm, 32 * SB::WPB, SB::SMEM, s>>>(d, g);
 }
 
 cudaError_t setup_update() {
     cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
+    e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAT_SMEM);
     if (e != cudaSuccess) return e;
     for (cudaError_t f : {seg_attr<1>(), seg_attr<2>(), seg_attr<4>(), seg_attr<8>(), seg_attr<16>(), seg_attr<32>()})
         if (f != cudaSuccess) return f;
@@ -619,10 +754,15 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
         return 1;
     }
     const size_t hs = (size_t)d.K * 4;
-    k_hist<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
-    k_scan_a<<<(d.K + 255) / 256, 256, 0, s>>>(d, g, AAKM_SEG_BLOCKS);
+    const int bt = 1024;                                       // k_scatter assumes 1024 threads (K <= 16 per thread)
+    k_hist<<<d.seg_blocks, bt, hs, s>>>(d, g);
+    static_assert(AAKM_SEG_BLOCKS_MAX <= 512, "k_scan_a: <= 16 row blocks per lane");
+    k_scan_a<<<(d.K + 7) / 8, 256, 0, s>>>(d, g, d.seg_blocks);
     k_scan_b<<<1, 1024, 0, s>>>(d, g);
-    k_scatter<<<AAKM_SEG_BLOCKS, 1024, hs, s>>>(d, g);
+    {
+        const int T = scatter_tile(d.K, bt, d.seg_blocks > d.num_sms ? 2 : 1);
+        k_scatter<<<d.seg_blocks, bt, (size_t)(2 * d.K + 2) * 4 + (size_t)T * 8, s>>>(d, g, T);
+    }
     if (d.xg_map) {
         switch (d.d / 4) {
             case 1: seg_launch<1>(d, g, s); return 5;
