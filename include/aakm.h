@@ -279,6 +279,25 @@ AAKM_API kmeans_status kmeans_seed_pp(kmeans_handle *h, const double *u /*host*/
 AAKM_API kmeans_status kmeans_aa_step_host(kmeans_handle *h, const float *X_host /*host*/, int32_t chunks,
                                            kmeans_step_info *info /*host*/, double *theta_out /*host*/);
 
+/* Per-pass trace of the Algorithm 1 run since its line 1 (kmeans_aa_step(C0) or
+ * kmeans_run): one record per loop pass t = 1, 2, ... (the fields of
+ * kmeans_step_info; the converged pass included), at most AAKM's device ring
+ * of 8192 passes.  out: host, cap records (nullable when cap == 0); n_out:
+ * host, the number of records the run holds (may exceed cap: the first cap are
+ * copied).  Synchronises. */
+AAKM_API kmeans_status kmeans_trace_export(kmeans_handle *h, kmeans_step_info *out /*host*/, int64_t cap,
+                                           int64_t *n_out /*host*/);
+
+/* Checked-workspace mode (test hook; compute-sanitizer is unavailable on the
+ * GPU pool): with the environment variable AAKM_WS_CANARY=1 set before
+ * kmeans_workspace_size / kmeans_create, every region of the workspace carve is
+ * followed by a 256-byte canary (0xA5) written at create.  This call counts the
+ * canary bytes that changed (a kernel wrote past the end of its region):
+ * bad_bytes (host) must stay 0; n_guards (host, nullable) = canaries checked
+ * (0 when the mode is off).  Synchronises. */
+AAKM_API kmeans_status kmeans_debug_check_canaries(kmeans_handle *h, int64_t *bad_bytes /*host*/,
+                                                   int64_t *n_guards /*host*/);
+
 /* Sum of CUDA-event durations (ms) of the assignment launches recorded since
  * the last call (config.timing = 1), and their count.  Synchronises. */
 AAKM_API kmeans_status kmeans_assign_timing(kmeans_handle *h, double *ms_total /*host*/,

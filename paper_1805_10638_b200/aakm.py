@@ -96,6 +96,8 @@ def lib():
                 "kmeans_assign_path_name": ([P], ct.c_char_p),
                 "kmeans_debug_scores": ([P, P, P, ct.POINTER(I32), ct.POINTER(D)], I32),
                 "kmeans_bounds_export": ([P, P, P, P, P], I32),
+                "kmeans_trace_export": ([P, P, I64, ct.POINTER(I64)], I32),
+                "kmeans_debug_check_canaries": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
                 "kmeans_bounds_repeat": ([P, P, P, P, ct.POINTER(I32)], I32),
                 "kmeans_destroy": ([P], I32),
                 "kmeans_last_error": ([P], ct.c_char_p),
@@ -333,6 +335,20 @@ class KMeans:
         s.E1, s.E2 = float(st["E1"]), float(st["E2"])
         s.n_accepted, s.n_rejected, s.n_assign = int(st["n_accepted"]), int(st["n_rejected"]), int(st["n_assign"])
         self._c(lib().kmeans_state_import(self.h, ct.byref(s)))
+
+    def trace(self, cap=8192):
+        """The per-pass trace of the current run (kmeans_trace_export): a list of
+        step-info dicts, one per loop pass."""
+        n = ct.c_int64()
+        buf = (StepInfo * max(cap, 1))()
+        self._c(lib().kmeans_trace_export(self.h, buf, cap, ct.byref(n)))
+        return [_struct(buf[i]) for i in range(min(n.value, cap))]
+
+    def check_canaries(self):
+        """(changed canary bytes, canaries) of the checked-workspace mode (AAKM_WS_CANARY=1)."""
+        bad, n = ct.c_int64(), ct.c_int64()
+        self._c(lib().kmeans_debug_check_canaries(self.h, ct.byref(bad), ct.byref(n)))
+        return bad.value, n.value
 
     def assign_timing(self):
         ms, n = ct.c_double(), ct.c_int64()

@@ -64,6 +64,8 @@ struct kmeans_handle {
     unsigned int* xchk = nullptr;                            // device, 2 words: stats of a refreshed X
     unsigned int x_stat[2] = {0u, 0u};                       // this rank's create-time max |x|, max ||x||^2 (float bits)
     cudaEvent_t sync_ev = nullptr;                           // polled by sync_stream when a communicator exists
+    std::vector<size_t> guards;                              // AAKM_WS_CANARY: canary offsets in the workspace
+    char* ws_base = nullptr;
 };
 
 static thread_local std::string g_create_err;
@@ -164,7 +166,17 @@ struct Layout {
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
         ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, total,
         scratch_bytes;
+    std::vector<size_t> guards;   // AAKM_WS_CANARY=1: a 256-B canary after every region
 };
+
+// Checked-workspace mode (compute-sanitizer is not available on the GPU pool): every
+// workspace region is followed by a 256-byte canary filled at create; a kernel that
+// writes past the end of its region changes it (kmeans_debug_check_canaries).
+static bool ws_canary() {
+    static const bool on = getenv("AAKM_WS_CANARY") && atoi(getenv("AAKM_WS_CANARY")) != 0;
+    return on;
+}
+constexpr unsigned char CANARY = 0xA5;
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -176,7 +188,13 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     size_t o = 0;
     const size_t KD = (size_t)K * d;
     const int H = m_max + 1;
-    auto take = [&](size_t bytes) { size_t r = o; o = al(o + bytes); return r; };
+    const bool canary = ws_canary();
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o = al(o + bytes);
+        if (canary) { L.guards.push_back(o); o += 256; }
+        return r;
+    };
     L.st = take(sizeof(DevState));
     L.st_api = take(sizeof(DevState));
     L.C = take(KD * 8); L.C32 = take(KD * 4); L.Chi = take(KD * 4); L.Clo = take(KD * 4); L.cn = take((size_t)K * 4);
@@ -196,12 +214,13 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.pair_rows = take((size_t)fc * 4 + 4);
     L.pair_j = take((size_t)fc * 8 + 8);
     const size_t pk = (2 * KD + K + 4) * 8;     // [S_hi | S_lo | N | E_hi | E_lo | E | changed], int64 words (pk_words)
-    L.scratch = o;
-    size_t s0 = take(256);                 // flag counts
-    (void)s0;
-    take(pk);                              // packed[0]
-    L.packed1 = take(pk);                  // packed[1]
+    L.scratch = o;                         // one block, zeroed every pass: no canaries inside
+    o = al(o + 256);                       // flag counts
+    o = al(o + pk);                        // packed[0]
+    L.packed1 = o;
+    o = al(o + pk);                        // packed[1]
     L.scratch_bytes = o - L.scratch;
+    if (canary) { L.guards.push_back(o); o += 256; }
     L.upd_part = take((size_t)AAKM_UPD_MAX_BLOCKS * 16);
     L.seg_bh = take((size_t)AAKM_SEG_BLOCKS_MAX * K * 4);
     L.seg_off = take((size_t)K * 4 + 4);
@@ -635,6 +654,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     h->scratch = w + L.scratch;
     h->scratch_bytes = L.scratch_bytes;
     h->xchk = (unsigned int*)(w + L.xchk);
+    h->guards = L.guards;
+    h->ws_base = w;
 
 #define CKC(call)                                                                         \
     do {                                                                                  \
@@ -695,6 +716,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     CKC(cudaMallocHost(&h->done_host, 64));
     CKC(cudaEventCreate(&h->run_ev[0]));
     CKC(cudaEventCreate(&h->run_ev[1]));
+    for (size_t g : L.guards) CKC(cudaMemsetAsync(w + g, CANARY, 256, h->stream));
     CKC(cudaMemsetAsync(w + L.st, 0, sizeof(DevState), h->stream));
     CKC(cudaMemsetAsync(w + L.st_api, 0, sizeof(DevState), h->stream));
     CKC(cudaMemsetAsync(w + L.upd_part, 0, (size_t)AAKM_UPD_MAX_BLOCKS * 16, h->stream));
@@ -1149,6 +1171,44 @@ kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
     combine(h, d, 2, d.C, s);                                     // operand prep of C^t
     SYNC(h, s);
     CK(h, cudaGetLastError());
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_debug_check_canaries(kmeans_handle* h, int64_t* bad_bytes, int64_t* n_guards) {
+    LIVE(h);
+    if (!bad_bytes) FAIL(h, KMEANS_ERR_INVALID, "NULL output");
+    SYNC(h, h->stream);
+    std::vector<unsigned char> buf(256);
+    long long bad = 0;
+    for (size_t g : h->guards) {
+        CK(h, cudaMemcpy(buf.data(), h->ws_base + g, 256, cudaMemcpyDeviceToHost));
+        for (unsigned char c : buf) bad += c != CANARY;
+    }
+    *bad_bytes = bad;
+    if (n_guards) *n_guards = (int64_t)h->guards.size();
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_trace_export(kmeans_handle* h, kmeans_step_info* out, int64_t cap, int64_t* n_out) {
+    LIVE(h);
+    if (!n_out || (cap > 0 && !out)) FAIL(h, KMEANS_ERR_INVALID, "NULL output");
+    cudaStream_t s = h->stream;
+    CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    SYNC(h, s);
+    const long long n = h->st_host->trace_len;
+    *n_out = n;
+    const long long m = std::min<long long>(n, cap);
+    if (m <= 0) return KMEANS_OK;
+    std::vector<TraceRec> tr((size_t)m);
+    CK(h, cudaMemcpy(tr.data(), h->d.trace, (size_t)m * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < m; ++i) {
+        const TraceRec& r = tr[(size_t)i];
+        kmeans_step_info& o = out[i];
+        memset(&o, 0, sizeof(o));
+        o.t = r.t; o.m = r.m; o.m_t = r.m_t; o.accepted = r.accepted; o.rejected = r.rejected;
+        o.converged = r.converged; o.lloyd = r.lloyd; o.energy_cand = r.E_cand; o.energy = r.E_final;
+        o.changed = r.changed;
+    }
     return KMEANS_OK;
 }
 

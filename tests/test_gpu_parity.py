@@ -265,3 +265,22 @@ def test_accepted_energies_monotone_on_gpu():
             break
     assert all(b <= a * (1 + 1e-12) for a, b in zip(Es, Es[1:]))
     km.close()
+
+
+@pytest.mark.parametrize("cfg,N,K,m0", [("c1", None, None, 5), ("c2", None, None, 2)])
+def test_trace_export_matches_oracle_trace(cfg, N, K, m0):
+    # kmeans_trace_export: one record per loop pass of a kmeans_run, against the oracle's own trace
+    X, C0, c = make(cfg, N=N, K=K)
+    km = handle(X, c.K, m0=m0)
+    _, _, rep = km.run(dev(C0))
+    tr = km.trace()
+    ref = oracle.run(X, C0.astype(np.float64), oracle.OracleConfig(m0=m0), trace=True)
+    assert len(tr) == len(ref["trace"]) == rep["iters"] - 1
+    for g, o in zip(tr, ref["trace"]):
+        tag = f"{cfg} t={o['t']}"
+        assert g["t"] == o["t"] and g["m"] == o["m"] and g["changed"] == o["changed"], (tag, g, o)
+        assert g["accepted"] == o["accepted"] and g["rejected"] == o["rejected"], (tag, g, o)
+        assert abs(g["energy"] - o["E"]) <= 1e-6 * o["E"], (tag, g, o)
+        assert abs(g["energy_cand"] - o["E_cand"]) <= 1e-6 * o["E_cand"], (tag, g, o)
+    assert tr[-1]["converged"] == 1
+    km.close()
