@@ -113,6 +113,16 @@ typedef struct {
                             synchronising call polls ncclCommGetAsyncError and
                             aborts after AAKM_COMM_TIMEOUT_S seconds (default
                             600) instead of blocking on a failed peer.           */
+    int32_t fused_comm;  /* 1 = f4: the per-G-evaluation combine fused into the
+                            update's flushes (NCCL 2.28 device API): the packed
+                            [S|N|E|changed] vectors live in an NCCL symmetric
+                            window and every flush adds into ALL ranks' replicas
+                            (multimem.red through the NVLS multicast address, or
+                            system-scope reds to each LSA peer), fenced by two
+                            device barriers per G-evaluation -- no allreduce
+                            launch.  Needs a communicator (nranks > 1 or
+                            comm_always) whose ranks share one NVLink domain.
+                            Same bytes as the allreduce path.                    */
 } kmeans_config;
 
 /* Result of kmeans_run (fields per DESIGN.md R-A19). */
@@ -352,6 +362,11 @@ AAKM_API kmeans_status kmeans_bounds_export(kmeans_handle *h, float *ub_out, flo
                                             double *Cref_out);
 AAKM_API kmeans_status kmeans_bounds_repeat(kmeans_handle *h, float *ub1_out, float *lb1_out,
                                             int64_t *scored_out /*host*/, int32_t *same_out /*host*/);
+
+/* How the ranks combine: mode (host) = -1 no communicator, 0 ncclAllReduce,
+ * 1 fused multimem (NVLS), 2 fused LSA unicast; lsa_size (host, nullable) =
+ * ranks in the NVLink team of the fused path (0 otherwise). */
+AAKM_API kmeans_status kmeans_comm_info(kmeans_handle *h, int32_t *mode /*host*/, int32_t *lsa_size /*host*/);
 
 /* Name of the assignment engine the handle selected ("simt"/"tc"/"tc16"). */
 AAKM_API const char *kmeans_assign_path_name(const kmeans_handle *h);

@@ -35,7 +35,7 @@ class Config(ct.Structure):
     _fields_ = [("m0", ct.c_int32), ("m_max", ct.c_int32), ("eps1", ct.c_double), ("eps2", ct.c_double),
                 ("dynamic_m", ct.c_int32), ("max_iters", ct.c_int32), ("ridge", ct.c_double),
                 ("assign_path", ct.c_int32), ("timing", ct.c_int32), ("bounded", ct.c_int32),
-                ("x_refresh", ct.c_int32), ("comm_always", ct.c_int32)]
+                ("x_refresh", ct.c_int32), ("comm_always", ct.c_int32), ("fused_comm", ct.c_int32)]
 
 
 class Report(ct.Structure):
@@ -97,6 +97,7 @@ def lib():
                 "kmeans_debug_scores": ([P, P, P, ct.POINTER(I32), ct.POINTER(D)], I32),
                 "kmeans_bounds_export": ([P, P, P, P, P], I32),
                 "kmeans_trace_export": ([P, P, I64, ct.POINTER(I64)], I32),
+                "kmeans_comm_info": ([P, ct.POINTER(I32), ct.POINTER(I32)], I32),
                 "kmeans_debug_check_canaries": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
                 "kmeans_bounds_repeat": ([P, P, P, P, ct.POINTER(I32)], I32),
                 "kmeans_destroy": ([P], I32),
@@ -118,7 +119,8 @@ def header_symbols():
 
 
 def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000, ridge=1e-10,
-           assign_path="auto", timing=False, bounded=False, x_refresh=False, comm_always=False) -> Config:
+           assign_path="auto", timing=False, bounded=False, x_refresh=False, comm_always=False,
+           fused_comm=False) -> Config:
     """Algorithm 1 settings (m0 = 5 per BASELINE configs, reading R-A18)."""
     c = Config()
     c.m0, c.m_max, c.eps1, c.eps2 = m0, m_max, eps1, eps2
@@ -128,6 +130,7 @@ def config(m0=5, m_max=30, eps1=0.02, eps2=0.5, dynamic_m=True, max_iters=10000,
     c.bounded = int(bounded)
     c.x_refresh = int(x_refresh)
     c.comm_always = int(comm_always)
+    c.fused_comm = int(fused_comm)
     return c
 
 
@@ -343,6 +346,12 @@ class KMeans:
         buf = (StepInfo * max(cap, 1))()
         self._c(lib().kmeans_trace_export(self.h, buf, cap, ct.byref(n)))
         return [_struct(buf[i]) for i in range(min(n.value, cap))]
+
+    def comm_info(self):
+        """(mode, lsa_size): -1 no communicator, 0 ncclAllReduce, 1 fused multimem, 2 fused LSA unicast."""
+        m, l = ct.c_int32(), ct.c_int32()
+        self._c(lib().kmeans_comm_info(self.h, ct.byref(m), ct.byref(l)))
+        return m.value, l.value
 
     def check_canaries(self):
         """(changed canary bytes, canaries) of the checked-workspace mode (AAKM_WS_CANARY=1)."""

@@ -14,6 +14,7 @@
 #define AAKM_SEG_BLOCKS_MAX 512     // row blocks of the histogram / scatter (Dev::seg_blocks)
 #define AAKM_MAX_RANKS 1024         // NCCL ranks per communicator this build sizes for
 #define AAKM_SEED_BLOCKS 1184      // row blocks of the K-Means++ passes (8 x 148)
+#define AAKM_MAX_LSA 8              // f4 unicast fallback: LSA peers (one NVLink domain of 8 GPUs)
 #define AAKM_CNIMG_BYTES 4096       // folded ||c||^2 block of one 128-centroid tile (128 rows x 32 B)
 
 namespace aakm {
@@ -52,6 +53,7 @@ struct alignas(16) DevState {
     long long seed_max;          // K-Means++: max_i D2_i of the current round (fixed point)
     int seed_err, pad4;          // K-Means++: 2 = fewer distinct samples than K
     int bnd_ready0, pad5;        // bounded engine: bnd_ready at the snapshot
+    unsigned int fc_ctr, pad6;   // f4 fused combine: blocks done zeroing (comm.cu)
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -135,6 +137,13 @@ struct Dev {
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
     float4* dbg_rows;     // kmeans_debug_scores only: per row (b1, b2, tau, i1 bits) of the dense engine
+    // f4 fused combine (cfg.fused_comm, comm.cu): packed[0] / packed[1] are this rank's
+    // replica of an NCCL symmetric window; every flush adds into all replicas
+    int fused;            // 0 off, 1 multimem (NVLS multicast address mc0), 2 LSA peer pointers
+    int lsa_n;            // LSA peers (fused == 2), this rank included
+    long long pk_off1;    // words from packed[0] to packed[1] inside the window
+    long long* mc0;       // multicast address of packed[0]
+    long long* lsa0[AAKM_MAX_LSA];   // every LSA peer's replica of packed[0]
     int dev;              // CUDA device ordinal of the handle
     int num_sms;          // its SM count (persistent grids)
 };
@@ -200,6 +209,13 @@ void launch_update_G(const Dev& d, const long long* packed, const double* Cprev,
 void launch_energy(const Dev& d, const GEval& g, cudaStream_t s);       // E after the allreduce
 void launch_partials_out(const Dev& d, const long long* packed, double* out, cudaStream_t s);
 void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
+// f4 fused combine (comm.cu); comm is an ncclComm_t; setup returns an error message or nullptr
+const char* fused_setup(void** handle, void* comm, Dev& d, void* scratch, cudaStream_t s);
+void fused_free(void* handle, void* comm);
+int fused_mode(const void* handle);
+int fused_lsa_size(const void* handle);
+int launch_fused_zero(const Dev& d, const GEval& g, const void* handle, cudaStream_t s);
+int launch_fused_flushed(const Dev& d, const GEval& g, const void* handle, cudaStream_t s);
 // st->label_error |= 2 if the stats in out (launch_xstats_max) exceed (amax, nmax2) (float bits)
 void launch_xcheck(const Dev& d, const unsigned int* out, unsigned int amax, unsigned int nmax2, cudaStream_t s);
 

@@ -66,6 +66,7 @@ struct kmeans_handle {
     cudaEvent_t sync_ev = nullptr;                           // polled by sync_stream when a communicator exists
     std::vector<size_t> guards;                              // AAKM_WS_CANARY: canary offsets in the workspace
     char* ws_base = nullptr;
+    void* fused = nullptr;                                   // f4 fused combine resources (comm.cu)
 };
 
 static thread_local std::string g_create_err;
@@ -366,12 +367,17 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         uevp = &h->uev[h->uev_used++];
         CK(h, cudaEventRecord(uevp->first, s));
     }
+    if (d.fused) h->launches += launch_fused_zero(d, g, h->fused, s);      // f4: zero + "zeroed" barrier
     h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
     if (uevp) CK(h, cudaEventRecord(uevp->second, s));
     dbg("update", s);
-    st = allreduce(h, d.packed[branch], s);
-    if (st != KMEANS_OK) return st;
-    if (h->comm) dbg("allreduce", s);
+    if (d.fused) {
+        h->launches += launch_fused_flushed(d, g, h->fused, s);           // f4: "flushed" barrier
+    } else {
+        st = allreduce(h, d.packed[branch], s);
+        if (st != KMEANS_OK) return st;
+    }
+    if (h->comm) dbg("combine", s);
     launch_energy(d, g, s);
     dbg("energy", s);
     launch_control(d, branch, s);
@@ -456,6 +462,7 @@ static void release(kmeans_handle* h, bool sync) {
     if (h->tr_host) cudaFreeHost(h->tr_host);
     if (h->scal_host) cudaFreeHost(h->scal_host);
     if (h->done_host) cudaFreeHost(h->done_host);
+    if (h->fused) fused_free(h->fused, h->comm);
     if (h->comm) {
         if (sync) ncclCommDestroy(h->comm);
         else ncclCommAbort(h->comm);             // a failed / poisoned communicator may never complete
@@ -762,6 +769,15 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             dv->upd_sorted = srt ? 1 : 0;
         }
         h->x_gamax = mf[0];
+        if (cfg->fused_comm) {                                         // f4: packed vectors in a symmetric window
+            const char* m = h->comm ? fused_setup(&h->fused, h->comm, h->d, w + L.scratch, h->stream)
+                                    : "fused_comm needs a communicator (nranks > 1 or comm_always)";
+            if (m) {
+                g_create_err = m;
+                release(h, false);
+                return h->comm ? KMEANS_ERR_NCCL : KMEANS_ERR_INVALID;
+            }
+        }
         CKC(cudaMemsetAsync(w + L.scratch, 0, 128, h->stream));
     }
     CKC(cudaStreamSynchronize(h->stream));
@@ -1320,6 +1336,14 @@ kmeans_status kmeans_last_flagged(kmeans_handle* h, int64_t* flagged) {
     CK(h, cudaMemcpy(v, h->d.flag_count, 16, cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(pr, h->d.pair_count, 16, cudaMemcpyDeviceToHost));
     *flagged = v[0] + pr[0];                            // candidate-pass rows + two-centroid rows
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_comm_info(kmeans_handle* h, int32_t* mode, int32_t* lsa_size) {
+    LIVE(h);
+    if (!mode) FAIL(h, KMEANS_ERR_INVALID, "NULL mode");
+    *mode = h->fused ? fused_mode(h->fused) : (h->comm ? 0 : -1);
+    if (lsa_size) *lsa_size = h->fused ? fused_lsa_size(h->fused) : 0;
     return KMEANS_OK;
 }
 

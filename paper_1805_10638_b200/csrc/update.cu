@@ -23,7 +23,9 @@ struct Pick {
     const int* lab;
     const int* prev;
     const double* C;      // C^t (fp64)
-    long long* out;       // packed [S_hi | S_lo | N | E_hi | E_lo | E | changed]
+    long long* out;       // packed [S_hi | S_lo | N | E_hi | E_lo | E | changed] (local replica)
+    int fz;               // f4 fused combine: 0 = local adds (+ ncclAllReduce), 1 = multimem, 2 = LSA peers
+    long long wo;         // word offset of this branch's buffer in the symmetric window
 };
 
 __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
@@ -33,7 +35,25 @@ __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
     p.prev = g.prev_mode == 0 ? d.lab[cur ^ 1] : (g.prev_mode == 2 ? g.lab_prev : nullptr);
     p.C = d.C;
     p.out = g.packed_out ? g.packed_out : d.packed[g.branch];
+    p.fz = g.packed_out ? 0 : d.fused;
+    p.wo = g.branch ? d.pk_off1 : 0;
     return p;
+}
+
+// Every contribution to the packed vector.  Plain mode: a red.add into this rank's
+// buffer (the ranks then combine with ncclAllReduce).  Fused mode (f4, comm.cu): the
+// add goes to EVERY rank's replica of the symmetric window at once -- one
+// multimem.red through the NVLS multicast address, or one system-scope red per LSA
+// peer -- so after the "flushed" device barrier each replica holds the global sum.
+__device__ __forceinline__ void pk_add(const Dev& d, const Pick& p, long long idx, long long v) {
+    if (p.fz == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.out + idx), (unsigned long long)v);
+    } else if (p.fz == 1) {
+        asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(d.mc0 + p.wo + idx), "l"(v) : "memory");
+    } else {
+        for (int r = 0; r < d.lsa_n; ++r)
+            asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(d.lsa0[r] + p.wo + idx), "l"(v) : "memory");
+    }
 }
 
 // x -> (hi, lo) with x 2^(22-e) = hi + lo 2^-22 (+ |residual| <= 2^-23), both
@@ -51,7 +71,7 @@ __device__ __forceinline__ void red_add_s64(long long* p, long long v) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
-__device__ void finish_changed(const Dev& d, long long* out, long long ch);
+__device__ void finish_changed(const Dev& d, const Pick& p, long long ch);
 
 // Lanes are grouped per row (group = next pow2 >= d, <= 32) so a row's d
 // coordinates are read and reduced as one coalesced segment; S_j and N_j go
@@ -84,7 +104,7 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
         if (okj) {
             if (gl == 0) {
                 if (p.prev) ch += (p.prev[row] != j);
-                red_add_s64(p.out + pk_n(d) + j, 1);
+                pk_add(d, p, pk_n(d) + j, 1);
             }
             const float* x = d.X + row * D;
             const double* c = p.C + (long long)j * D;
@@ -92,8 +112,8 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
                 const float xv = __ldcs(x + k);
                 int hi = 0, lo = 0;
                 fx_add(xv, sc, hi, lo);
-                red_add_s64(p.out + (long long)j * D + k, hi);
-                red_add_s64(p.out + KD + (long long)j * D + k, lo);
+                pk_add(d, p, (long long)j * D + k, hi);
+                pk_add(d, p, KD + (long long)j * D + k, lo);
                 const double df = (double)xv - __ldg(c + k);
                 e = fma(df, df, e);
             }
@@ -106,8 +126,8 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
         ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
         elo += __shfl_xor_sync(0xffffffffu, elo, o);
     }
-    if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
-    finish_changed(d, p.out, ch);
+    if (lane == 0 && (ehi | elo)) { pk_add(d, p, pk_ehi(d), ehi); pk_add(d, p, pk_ehi(d) + 1, elo); }
+    finish_changed(d, p, ch);
 }
 
 // ------------------------------------------------------------------
@@ -127,7 +147,7 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 
 constexpr int SEG_ROWS = 256;
 
-__device__ void finish_changed(const Dev& d, long long* out, long long ch) {
+__device__ void finish_changed(const Dev& d, const Pick& p, long long ch) {
     __shared__ long long sc[32];
     __shared__ bool last;
     for (int o = 16; o; o >>= 1) ch += __shfl_xor_sync(0xffffffffu, ch, o);
@@ -154,7 +174,7 @@ __device__ void finish_changed(const Dev& d, long long* out, long long ch) {
     if (threadIdx.x == 0) {
         long long bc = 0;
         for (int i = 0; i < nw; ++i) bc += sc[i];
-        out[pk_ch(d)] += bc;                              // changed (packed was zeroed)
+        pk_add(d, p, pk_ch(d), bc);                       // changed (packed was zeroed)
         d.st->hist_ctr = 0;
     }
 }
@@ -210,7 +230,7 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     __syncthreads();
     int* bh = d.seg_bh + (long long)blockIdx.x * K;
     for (int j = threadIdx.x; j < K; j += blockDim.x) bh[j] = hs[j];
-    finish_changed(d, p.out, ch);
+    finish_changed(d, p, ch);
 }
 
 // Phase A (one warp per cluster): N_j = sum over the row blocks, and the
@@ -243,7 +263,7 @@ __global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
         if (u < per && b0 + u < b1) { d.seg_bh[(long long)(b0 + u) * K + j] = o; o += t[u]; }
     if (lane == 31) {
         d.seg_off[j] = inc;                               // count for now; phase B makes it an offset
-        p.out[pk_n(d) + j] = inc;                         // N_j
+        pk_add(d, p, pk_n(d) + j, inc);                   // N_j (the buffer was zeroed)
     }
 }
 
@@ -491,8 +511,8 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
         for (int v = 0; v < V; ++v) {
             const int k = lane + 32 * v;
             if (k < D) {
-                red_add_s64(p.out + (long long)j * D + k, hi[v]);
-                red_add_s64(p.out + KD + (long long)j * D + k, lo[v]);
+                pk_add(d, p, (long long)j * D + k, hi[v]);
+                pk_add(d, p, KD + (long long)j * D + k, lo[v]);
             }
         }
     }
@@ -500,7 +520,7 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
         ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
         elo += __shfl_xor_sync(0xffffffffu, elo, o);
     }
-    if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
+    if (lane == 0 && (ehi | elo)) { pk_add(d, p, pk_ehi(d), ehi); pk_add(d, p, pk_ehi(d) + 1, elo); }
 }
 
 // ------------------------------------------------------------------
@@ -709,10 +729,9 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
             for (int t = 0; t < 8; ++t) s8[t] += __shfl_xor_sync(0xffffffffu, s8[t], o);
         }
         if (h == 0) {
-            long long* oh = p.out + (long long)r.x * D + 4 * c4i;
-            long long* ol = oh + KD;
+            const long long oh = (long long)r.x * D + 4 * c4i;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) { red_add_s64(oh + t, s8[t]); red_add_s64(ol + t, s8[4 + t]); }
+            for (int t = 0; t < 4; ++t) { pk_add(d, p, oh + t, s8[t]); pk_add(d, p, KD + oh + t, s8[4 + t]); }
         }
         h0 = h1 = h2 = h3 = l0 = l1 = l2 = l3 = 0;
     }
@@ -720,7 +739,7 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
         elo += __shfl_xor_sync(0xffffffffu, elo, o);
     }
-    if (lane == 0 && (ehi | elo)) { red_add_s64(p.out + pk_ehi(d), ehi); red_add_s64(p.out + pk_ehi(d) + 1, elo); }
+    if (lane == 0 && (ehi | elo)) { pk_add(d, p, pk_ehi(d), ehi); pk_add(d, p, pk_ehi(d) + 1, elo); }
 }
 
 template <int LPR> static cudaError_t seg_attr() {
