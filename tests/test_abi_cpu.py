@@ -54,7 +54,7 @@ def test_abi_version_and_defaults(L):
     # PAPER.md:177 defaults; dense assignment unless asked for the bounded engine
     assert (c.m0, c.m_max, c.eps1, c.eps2, c.dynamic_m) == (2, 30, 0.02, 0.5, 1)
     assert c.bounded == 0 and c.x_refresh == 0 and c.comm_always == 0 and c.fused_comm == 0
-    assert ct.sizeof(aakm.Config) == 72
+    assert ct.sizeof(aakm.Config) == 64
     assert L.kmeans_config_default(None) == 1
 
 
