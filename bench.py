@@ -102,6 +102,19 @@ class ClockSampler:
                 "reasons": [v for k, v in REASONS.items() if mask & k and k != 0x1], "samples": len(load)}
 
 
+# --------------------------------------------------------------------- multi-rank timing
+def max_over_ranks(value, world, device="cuda"):
+    """The bench's time of a multi-rank step: the max over ranks of each rank's
+    device-timed duration (the contract's "max over ranks"); world == 1: value."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # --------------------------------------------------------------------- oracle arm
 def cpu_baseline(X, C0, cfgname, budget_rows=None):
     """The oracle's Assignment-Step (its dominant step) on a bounded row sample."""
@@ -177,13 +190,11 @@ def time_to_converge(cfgname, rank, world, barrier):
         _, _, rep = km.run(C0d)
         e1.record(km.stream)
         barrier()
-        t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = max_over_ranks(e0.elapsed_time(e1) / 1e3, world)
         scored, total = km.bounded_stats()
         km.close()
-        out.update({pre + "seconds": float(t.item()), pre + "iters": rep["iters"], pre + "n_assign": rep["n_assign"],
-                    pre + "iterations_per_s": rep["iters"] / max(float(t.item()), 1e-9),
+        out.update({pre + "seconds": sec, pre + "iters": rep["iters"], pre + "n_assign": rep["n_assign"],
+                    pre + "iterations_per_s": rep["iters"] / max(sec, 1e-9),
                     pre + "converged": bool(rep["converged"]), pre + "energy": rep["energy"],
                     pre + "rows_scored_frac": scored / max(total, 1)})
         if pre == "":
@@ -215,10 +226,7 @@ def seed_pp_bench(cfgname, rank, world, barrier, peaks):
     _, idx = km.seed_pp(u)
     e1.record(km.stream)
     barrier()
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    sec = float(t.item())
+    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3, world)
     launches = km.launch_count() - L0
     km.close()
     n = X.shape[0]
@@ -293,10 +301,7 @@ def main():
     n_assign = st1["n_assign"] - n_assign0
     a_ms, a_n = km.assign_timing()
     u_ms, u_n = km.update_timing()
-    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ms_max = max_over_ranks(ms, world)
     passes_done = args.steps if not st1["done"] else None
     value = cfg.N * cfg.K * n_assign / (ms_max / 1e3)
 
@@ -324,10 +329,7 @@ def main():
     e_ms = e0.elapsed_time(e1)
     wall = time.perf_counter() - t0
     e_na = km.state_export()["n_assign"] - st_e0
-    te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = cfg.N * cfg.K * e_na / (float(te.item()) / 1e3)
+    e2e_val = cfg.N * cfg.K * e_na / (max_over_ranks(e_ms, world) / 1e3)
 
     peaks, peak_kind = load_peaks()
     path = km.path

@@ -94,3 +94,34 @@ def test_make_shard_matches_make():
                 assert np.array_equal(C0s, C0)
                 parts.append(Xs)
             assert np.array_equal(np.concatenate(parts), X)
+
+
+def _bench_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        # each rank's own duration; the job's time is the slowest rank's
+        t = bench.max_over_ranks(1.5 + rank, world, device="cpu")
+        # every rank draws only its rows; the shards tile the config
+        X, C0, c = synthetic.make_shard("c1", rank, world)
+        lo, hi = synthetic.shard_bounds(c.N, rank, world)
+        sizes = torch.tensor([hi - lo, X.shape[0]], dtype=torch.int64)
+        dist.all_reduce(sizes)
+        if rank == 0:
+            np.save(out + ".npy", np.array([t, sizes[0].item(), sizes[1].item(), c.N]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_rank_plumbing(tmp_path, world):
+    """bench.py's N>1 host logic under gloo: max-over-ranks timing and the row
+    shards each rank draws (they tile N exactly)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = str(tmp_path / "bench")
+    mp.spawn(_bench_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    t, n1, n2, N = np.load(out + ".npy")
+    assert t == 1.5 + (world - 1)
+    assert n1 == n2 == N
