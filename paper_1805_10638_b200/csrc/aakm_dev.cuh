@@ -137,6 +137,7 @@ struct Dev {
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
     float4* dbg_rows;     // kmeans_debug_scores only: per row (b1, b2, tau, i1 bits) of the dense engine
+    unsigned long long* dbg_ts;   // AAKM_TC_TRACE probe: pipeline event stamps (nullptr in normal runs)
     // f4 fused combine (cfg.fused_comm, comm.cu): packed[0] / packed[1] are this rank's
     // replica of an NCCL symmetric window; every flush adds into all replicas
     int fused;            // 0 off, 1 multimem (NVLS multicast address mc0), 2 LSA peer pointers

@@ -104,6 +104,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     while (!mbar_try(b, parity))
         if (clock64() - t0 > (1ll << 32)) __trap();
 }
+// try_wait with a suspend-time hint: the waiting warp is parked (woken when the
+// phase completes or after ns) instead of re-issuing the poll, so the epilogue
+// warps that wait do not take issue slots from the ones that work
+__device__ __forceinline__ bool mbar_try_hint(uint64_t* b, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(su32(b)), "r"(parity), "r"(ns) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_epi(uint64_t* b, uint32_t parity, bool hint) {
+    if (mbar_try(b, parity)) return;
+    const long long t0 = clock64();
+    uint32_t n = 0;
+    while (!(hint ? mbar_try_hint(b, parity, 1000u) : mbar_try(b, parity)))
+        if ((++n & 63u) == 0 && clock64() - t0 > (1ll << 32)) __trap();
+}
 // Same with a sleep between polls: for warps off the critical path (producer,
 // splitter), whose spinning would otherwise take issue slots from the epilogue.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, uint32_t ns) {
@@ -119,6 +138,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// AAKM_TC_TRACE probe: %globaltimer stamps of pipeline events of CTAs 0 and 1 (perf only)
+__device__ __forceinline__ void tc_stamp(const Dev& d, int ev, long long it) {
+    if (!d.dbg_ts || blockIdx.x > 1 || it >= 256) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    d.dbg_ts[(blockIdx.x * 8 + ev) * 256 + it] = t;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -287,6 +313,12 @@ __device__ __forceinline__ void mbar_arrive_cl(uint32_t caddr) {
 __device__ __forceinline__ void mbar_arrive_cl_relaxed(uint32_t caddr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
+// Remote arrive with the default semantics (.release, .cta scope), as CUTLASS's
+// ClusterBarrier::arrive(cta_id): no MEMBAR.GPU (the writer's generic smem stores
+// are handed to the tensor core by fence.proxy.async before it).
+__device__ __forceinline__ void mbar_arrive_cl_default(uint32_t caddr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -359,7 +391,7 @@ template <int A, int MODE, int KIND, int CG>   // d = 32 * A (KIND 1: A even); C
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
             const __grid_constant__ CUtensorMap tm_clo, const __grid_constant__ CUtensorMap tm_cn, Dev d, GEval g,
-            int S, int NT, int NXB, int XRr) {
+            int S, int NT, int NXB, int XRr, int NST, int RES) {
     // Every CTA of a pair must run the same pipeline (barriers are shared), so the
     // early exits depend only on grid-uniform device state.
     if (!geval_active(d, g)) return;
@@ -397,7 +429,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     const int nxb = inplace ? 1 : NXB;
     // KIND 0 stages X in two fp32 tiles (TMA two row tiles ahead, so the split never
     // waits a TMA round trip); in place: one
-    const int nst = (DX || inplace) ? 1 : 2;
+    const int nst = (DX || inplace) ? 1 : NST;
     uint8_t* xst = smem;                                           // fp32 X tiles (TMA targets, splitter-owned)
     uint8_t* opb = (inplace || DX) ? smem : xst + nst * A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
@@ -409,8 +441,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint64_t* empty = bars + S;                                    // [S]  stage consumed (multicast commit)
     uint64_t* accf = bars + 2 * S;                                 // [4]  accumulator ready (multicast commit)
     uint64_t* acce = accf + 4;                                     // [4]  accumulator drained (leader: all epilogues)
-    uint64_t* stfull = acce + 4;                                   // [2] X staging tile landed
-    uint64_t* opready = stfull + 2;                                // [2] operand buffer split (leader: both CTAs)
+    uint64_t* stfull = acce + 4;                                   // [8] X staging tile landed (ring of nst)
+    uint64_t* opready = stfull + 8;                                // [2] operand buffer split (leader: both CTAs)
     uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
     uint64_t* xready = opempty + 2;                                // [XRr] ||x||^2 slot written (epilogue side)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XRr);
@@ -434,8 +466,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
         for (int b = 0; b < 4; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4 * CG); }
         for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2 * CG); mbar_init(opempty + b, 1); }
-        mbar_init(stfull, 1);
-        mbar_init(stfull + 1, 1);
+        for (int b = 0; b < 8; ++b) mbar_init(stfull + b, 1);
         for (int b = 0; b < XRr; ++b) mbar_init(xready + b, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -466,7 +497,17 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     const CUtensorMap* tmx = &tm_x;
 
     if (warp == W_PROD) {
-        if (lane == 0) {                                           // ---- TMA producer (C operands, this CTA's half)
+        if (lane == 0 && RES) {                                    // ---- resident C (NT == 1): loaded once
+            for (int a = 0; a < NATOM && live(0); ++a) {
+                if (leader) mbar_expect_tx(full + a, CG * (a == NATOM - 1 ? STAGE_BYTES : STAGE_MAIN));
+                uint8_t* st = stg + (size_t)a * STAGE_BYTES;
+                const uint32_t fb = lead(full + a);
+                const int crow = (int)rank * TC_BN;
+                tma_load_2d_cg<CG>(st, &tm_chi, fb, a * AELEM, crow);
+                tma_load_2d_cg<CG>(st + TC_BN * 128, &tm_clo, fb, a * AELEM, crow);
+                if (a == NATOM - 1) tma_load_2d_cg<CG>(st + STAGE_MAIN, &tm_cn, fb, 0, (int)rank * 4);
+            }
+        } else if (lane == 0) {                                    // ---- TMA producer (C operands, this CTA's half)
             int s = 0; uint32_t ph = 0;
             for (long long it = 0; live(it); ++it) {
                 for (int nt = 0; nt < NT; ++nt) {
@@ -497,18 +538,25 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             int xb = 0;
             for (long long it = 0; live(it); ++it) {
                 mbar_wait(opready + xb, (oph >> xb) & 1u);
+                tc_stamp(d, 1, it);                                // operands ready seen by the MMA thread
                 oph ^= 1u << xb;
                 tc_fence_after();
                 const uint32_t xhi_a = opb_a + (uint32_t)(xb * OPB);
                 const uint32_t xlo_a = xhi_a + (uint32_t)(NATOM * ATOM_BYTES_X);
                 for (int nt = 0; nt < NT; ++nt) {
                     mbar_wait(acce + acc, aph ^ 1);
+                    if (NT == 1) tc_stamp(d, 2, it);               // accumulator free seen by the MMA thread
                     tc_fence_after();
                     const uint32_t dt = tmem + (uint32_t)(acc * AW);
                     for (int a = 0; a < NATOM; ++a) {
-                        mbar_wait(full + s, ph);
-                        tc_fence_after();
-                        const uint32_t sb = stg_a + (uint32_t)(s * STAGE_BYTES);
+                        if (!RES) {
+                            mbar_wait(full + s, ph);
+                            tc_fence_after();
+                        } else if (it == 0) {                      // resident C: landed once
+                            mbar_wait(full + a, 0);
+                            tc_fence_after();
+                        }
+                        const uint32_t sb = stg_a + (uint32_t)((RES ? a : s) * STAGE_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if (d.dbg & 4) break;                   // debug: no MMAs (feed/epilogue probe)
@@ -527,10 +575,13 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             const uint32_t fa = KIND ? xhi_a + (uint32_t)(2 * NATOM * ATOM_BYTES_X) : ablk_a;
                             mma_cg<KIND, CG>(dt, sdesc_ns(fa), sdesc_ns(sb + STAGE_MAIN), 1u, IDESC_CG);
                         }
-                        commit_cg<CG>(empty + s);                  // frees the stage (both halves) when done
-                        if (++s == S) { s = 0; ph ^= 1; }
+                        if (!RES) {
+                            commit_cg<CG>(empty + s);              // frees the stage (both halves) when done
+                            if (++s == S) { s = 0; ph ^= 1; }
+                        }
                     }
                     commit_cg<CG>(accf + acc);                     // accumulator ready in both CTAs
+                    if (NT == 1) tc_stamp(d, 3, it);
                     if (++acc == NACC_) { acc = 0; aph ^= 1; }
                 }
                 commit_cg<CG>(opempty + xb);                       // operand buffers no longer read
@@ -541,7 +592,6 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         // Owns the fp32 staging tile: TMA-prefetches the next row tile as soon as
         // the current one is converted, so the MMA never waits on X.
         const int t = threadIdx.x - W_SPLIT * 32;                  // 0..63: rows t and t + 64
-        uint32_t sph = 0;
         uint32_t eph = 0;                                          // phase bit per operand buffer
         int xb = 0;
         if (t == 0 && live(0)) {
@@ -578,24 +628,24 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (MODE != 1 && !use_list && t == 0 && live(it + 1))   // next row tile -> L2
                     for (int a = 0; a < A; ++a) tma_prefetch_2d(tmx, a * 32, (int)(tile_of(it + 1) * TC_BM));
                 prefetch_list(it + 1);
-            } else if (nst == 1) {
-                mbar_wait_sleep(stfull, sph, 128);
-                sph ^= 1;
             } else {
-                mbar_wait_sleep(stfull + (it & 1), (uint32_t)(it >> 1) & 1u, 128);
+                mbar_wait_sleep(stfull + (int)(it % nst), (uint32_t)(it / nst) & 1u, 128);
             }
-            const uint8_t* xs = xst + (nst == 2 ? (int)(it & 1) * A * ATOM_BYTES_X : 0);   // this tile's staging
+            const uint8_t* xs = xst + (int)(it % nst) * A * ATOM_BYTES_X;   // this tile's staging (ring of nst)
             if (!inplace) {
                 mbar_wait_sleep(opempty + xb, ((eph >> xb) & 1u) ^ 1u, 256);  // the MMAs of tile - NXB are done
                 eph ^= 1u << xb;
             }
             uint8_t* xhi = opb + xb * OPB;
             uint8_t* xlo = xhi + NATOM * ATOM_BYTES_X;
-#pragma unroll 1
-            for (int rr = 0; rr < 2; ++rr) {
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {                       // both rows interleaved (ILP)
                 const int r = t + 64 * rr;
                 float xn = 0.f;
                 if (KIND == 0) {
+                    // four independent ||x||^2 chains (one per float4 lane): the splitter is on
+                    // the critical path at small K, and a single 4d-long FMA chain was its latency
+                    float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
 #pragma unroll
                     for (int a = 0; a < A; ++a) {
 #pragma unroll
@@ -607,11 +657,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                             h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
                             h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
                             h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
-                            xn = fmaf(v.x, v.x, xn); xn = fmaf(v.y, v.y, xn); xn = fmaf(v.z, v.z, xn); xn = fmaf(v.w, v.w, xn);
+                            q0 = fmaf(v.x, v.x, q0); q1 = fmaf(v.y, v.y, q1); q2 = fmaf(v.z, v.z, q2); q3 = fmaf(v.w, v.w, q3);
                             *reinterpret_cast<float4*>(xhi + off) = h;
                             *reinterpret_cast<float4*>(xlo + off) = l;
                         }
                     }
+                    xn = (q0 + q1) + (q2 + q3);
                 } else {
                     // the row's source, resolved ONCE (through the row list for MODE 1/2): the
                     // compiler cannot hoist a load of rows_of past the shared-memory stores below
@@ -664,9 +715,13 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-                if (CG == 2) mbar_arrive_cl(lead(opready + xb));   // once per row tile: release.cluster is affordable
+                if (CG == 2) {
+                    if (d.dbg & 32) mbar_arrive_cl_default(lead(opready + xb));   // probe: CUTLASS-style arrive
+                    else mbar_arrive_cl(lead(opready + xb));
+                }
                 else mbar_arrive(opready + xb);
                 mbar_arrive(xready + (it & (XRr - 1)));
+                if (warp == W_SPLIT) tc_stamp(d, 0, it);           // splitter done with the tile
             }
             if (DX) {
                 if (++xb == nxb) xb = 0;
@@ -679,15 +734,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 mbar_wait(opempty, eph & 1u);
                 eph ^= 1u;
             }
-            if (nst == 1 && t == 0 && live(it + 1)) {
-                mbar_expect_tx(stfull, A * ATOM_BYTES_X);
-                for (int a = 0; a < A; ++a) tma_load_2d(xst + a * ATOM_BYTES_X, tmx, stfull, a * 32, (int)(tile_of(it + 1) * TC_BM));
-            }
-            if (nst == 2 && t == 0 && live(it + 2)) {                 // refill the tile just converted
-                const int q = (int)(it & 1);
+            if (t == 0 && live(it + nst)) {                            // refill the tile just converted
+                const int q = (int)(it % nst);
                 mbar_expect_tx(stfull + q, A * ATOM_BYTES_X);
                 for (int a = 0; a < A; ++a)
-                    tma_load_2d(xst + (q * A + a) * ATOM_BYTES_X, tmx, stfull + q, a * 32, (int)(tile_of(it + 2) * TC_BM));
+                    tma_load_2d(xst + (q * A + a) * ATOM_BYTES_X, tmx, stfull + q, a * 32, (int)(tile_of(it + nst) * TC_BM));
             }
             if (++xb == nxb) xb = 0;
         }
@@ -713,7 +764,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             // NXB + ceil(NACC / NT) row tiles ahead of the epilogue (operand buffers +
             // accumulators); the ring has one slot more (xr_of), so it neither
             // aliases a phase nor overwrites an unread slot.
-            mbar_wait(xready + (it & (XRr - 1)), (uint32_t)(it / XRr) & 1u);
+            mbar_wait_epi(xready + (it & (XRr - 1)), (uint32_t)(it / XRr) & 1u, (d.dbg & 64) != 0);
             const float xn = cq == 0 ? xnorm[(it & (XRr - 1)) * TC_BM + r] : 0.f;
             // NTRK independent top-2 trackers.  MODE 0 keys pack the column's position
             // inside its 32-column batch into the 5 low mantissa bits of the score (a
@@ -728,7 +779,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             int cnt = 0;
             if (MODE == 1 && frow < n_rows) lim = d.flag_b1[frow] + d.flag_tau[frow];
             for (int nt = 0; nt < NT; ++nt) {
-                mbar_wait(accf + acc, aph);
+                mbar_wait_epi(accf + acc, aph, (d.dbg & 64) != 0);
+                if (warp == 0 && lane == 0 && NT == 1) tc_stamp(d, 4, it);   // epilogue sees the accumulator
                 tc_fence_after();
                 // all CG 32-column batches of this warp in flight at once, one wait, then
                 // the accumulator goes back to the MMA warp before any math
@@ -885,6 +937,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     if (KIND) push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
                 }
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
+                if (warp == 0 && lane == 0) tc_stamp(d, 5, it);    // epilogue done with the tile
             } else if (frow < n_rows) {
                 d.cand_cnt[frow * NQ + cq] = cnt;
             }
@@ -912,24 +965,38 @@ static int xr_of(int NT, int NXB, int cg) {
     return xr;
 }
 
-static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2) {
+static int env_cap(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2, int nst = 2) {
     const int natom = kind ? A / 2 : A;
-    const int staging = (NXB == 0 || kind == 1) ? 0 : 2 * A;   // in place / direct X: none; KIND 0: two tiles
+    const int staging = (NXB == 0 || kind == 1) ? 0 : nst * A;   // in place / direct X: none; KIND 0: nst tiles
     const int nb = NXB == 0 ? 1 : NXB;
     const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + (kind ? AAKM_CNIMG_BYTES : 0);
     const int xr = xr_of(NT, NXB, cg);
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
            (kind ? 0 : AAKM_CNIMG_BYTES) + (size_t)xr * TC_BM * 4 + (NQ - 1) * TC_BM * 16 +
-           (size_t)(2 * S + 14 + xr) * 8 + 16;
+           (size_t)(2 * S + 20 + xr) * 8 + 16;
+}
+
+// NT == 1 (K <= 256 with CTA pairs), KIND 0: the C operand tile never changes, so it
+// stays resident (S = NATOM stages, loaded once) and the shared memory the C ring
+// would take goes to X staging tiles instead: nst (<= 8) fp32 X tiles in flight per
+// CTA, so the X stream keeps up with the tensor pipe (c3: 2 tiles -> ~2.4 TB/s of X).
+static bool pick_resident(int kind, int A, int NT, int& NXB, int& NST, int cg = 2) {
+    if (kind != 0 || NT != 1 || env_cap("AAKM_TC_NORES", 0)) return false;
+    static const int maxst = env_cap("AAKM_TC_MAXST", 8);
+    for (NXB = 2; NXB >= 1; --NXB)
+        for (NST = maxst; NST >= 3; --NST)
+            if (smem_need(kind, A, A, NT, NXB, cg, NST) <= (size_t)SMEM_LIMIT) return true;
+    return false;
 }
 
 // stages S and operand buffers NXB: prefer double-buffered X operands while
 // keeping >= 3 C stages, else single-buffer (>= 2 stages)
 // AAKM_TC_MAXS / AAKM_TC_MAXNXB: perf-experiment caps (unset in normal runs)
-static int env_cap(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 static void pick_pipe(int kind, int A, int NT, int& S, int& NXB, int cg = 2) {
     static const int maxs = env_cap("AAKM_TC_MAXS", 6), maxnxb = env_cap("AAKM_TC_MAXNXB", 2);
     for (NXB = maxnxb; NXB >= (kind == 0 ? 0 : 1); --NXB)
@@ -1063,7 +1130,7 @@ static int tc_cg() {
 
 template <int A, int MODE, int KIND, int CG>
 static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, const GEval& g, int S, int NT, int NXB,
-                       int XRr, long long n_tiles, size_t smem, cudaStream_t s) {
+                       int XRr, long long n_tiles, size_t smem, cudaStream_t s, int NST, int RES) {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(TC_THREADS);
     cfg.dynamicSmemBytes = smem;
@@ -1090,30 +1157,32 @@ static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, con
     if (CG == 2) grid = (grid + 1) & ~1;
     if (grid < CG) grid = CG;
     cfg.gridDim = dim3(grid);
-    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB, XRr);
+    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB, XRr, NST, RES);
 }
 
 template <int MODE, int KIND, int CG>
 static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStream_t s) {
     const int A = d.d / 32;
     const int NT = (d.K + TC_BN * CG - 1) / (TC_BN * CG);
-    int S, NXB;
-    pick_pipe(KIND, A, NT, S, NXB, CG);
-    const size_t smem = smem_need(KIND, A, S, NT, NXB, CG);
+    int S, NXB, NST = 2;
+    const int RES = pick_resident(KIND, A, NT, NXB, NST, CG) ? 1 : 0;
+    if (RES) S = A;                                               // resident C: NATOM stages, loaded once
+    else pick_pipe(KIND, A, NT, S, NXB, CG);
+    const size_t smem = smem_need(KIND, A, S, NT, NXB, CG, NST);
     const int xr = xr_of(NT, NXB, CG);
     const CUtensorMap& xm = MODE == 1 ? m->xf : m->x;
     long long n_tiles = MODE == 0 ? (d.n + TC_BM - 1) / TC_BM : 1ll << 40;
     if (MODE == 0 && g.tile1 > 0) n_tiles = min(n_tiles, g.tile1) - g.tile0;
     if constexpr (KIND == 0) {
         switch (A) {
-            case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
-            case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
-            case 3: launch_one<3, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
-            default: launch_one<4, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s); break;
+            case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            case 3: launch_one<3, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            default: launch_one<4, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
         }
     } else {
-        if (A == 2) launch_one<2, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s);
-        else launch_one<4, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s);
+        if (A == 2) launch_one<2, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
+        else launch_one<4, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
     }
 }
 

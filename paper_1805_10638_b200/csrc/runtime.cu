@@ -644,6 +644,10 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         D.C_ref0 = (double*)(w + L.C_ref0);
     }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
+    if (getenv("AAKM_TC_TRACE")) {                                     // perf probe only: a 32 KB stamp buffer
+        if (cudaMalloc(&D.dbg_ts, 2 * 8 * 256 * 8) != cudaSuccess) D.dbg_ts = nullptr;
+        else cudaMemset(D.dbg_ts, 0, 2 * 8 * 256 * 8);
+    }
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
     D.x_scale = 1.f; D.x_inv_scale = 1.f; D.x_absmax = 0.f;
     D.tau_gamma = h->path == KMEANS_PATH_TC ? tau_gamma_tc(d)
@@ -1355,6 +1359,21 @@ const char* kmeans_assign_path_name(const kmeans_handle* h) {
 kmeans_status kmeans_destroy(kmeans_handle* h) {
     if (!h) return KMEANS_ERR_INVALID;
     if (g_prof) prof_dump();
+    if (h->d.dbg_ts) {                                                 // AAKM_TC_TRACE: dump the stamps
+        std::vector<unsigned long long> ts(2 * 8 * 256);
+        cudaDeviceSynchronize();
+        cudaMemcpy(ts.data(), h->d.dbg_ts, ts.size() * 8, cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(getenv("AAKM_TC_TRACE"), "w")) {
+            for (int b = 0; b < 2; ++b)
+                for (int it = 0; it < 256; ++it) {
+                    fprintf(f, "%d %d", b, it);
+                    for (int e = 0; e < 6; ++e) fprintf(f, " %llu", ts[(b * 8 + e) * 256 + it]);
+                    fprintf(f, "\n");
+                }
+            fclose(f);
+        }
+        cudaFree(h->d.dbg_ts);
+    }
     release(h, !h->poisoned);
     return KMEANS_OK;
 }

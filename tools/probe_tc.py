@@ -16,3 +16,4 @@ for _ in range(5):
 ms, n = km.assign_timing()
 print(f"{cfg} {km.path} dbg={os.environ.get('AAKM_TC_DBG', '0')} N={N} assign avg {ms / n:.3f} ms -> "
       f"{2 * N * c.K * c.d / (ms / n * 1e-3) / 1e12:.1f} TF/s fp32-equiv, flagged {km.last_flagged()}")
+km.close()
