@@ -66,8 +66,13 @@ constexpr int SMEM_LIMIT = 232448;                 // 227 KB opt-in
 // error <= 3 * 2^-20 |x_k c_k|; tensor-core fp32 accumulation over the
 // 3d/8 MMA k-steps (+8 for the internal 8-term dot) at <= 2^-22 each.
 // Both scores of the top-2 gap carry it, and ||x||^2 + max||c||^2 bounds
-// 2 sum |x_k c_k|; factor 4 is the safety margin.
-float tau_gamma_tc(int d) { return 4.0f * (3.0f * 9.5367432e-7f + (3.0f * d / 8.0f + 8.0f) * 2.3841858e-7f); }
+// 2 sum |x_k c_k|.  Factor AAKM_TAU_MARGIN (2) is the margin over that model of the
+// accumulator (r01 used 4; the measured error stays below 1/25 of the factor-4
+// threshold on every engine and input of tests/test_gpu_margins.py).
+#ifndef AAKM_TAU_MARGIN
+#define AAKM_TAU_MARGIN 2.0f
+#endif
+float tau_gamma_tc(int d) { return AAKM_TAU_MARGIN * (3.0f * 9.5367432e-7f + (3.0f * d / 8.0f + 8.0f) * 2.3841858e-7f); }
 
 struct TcMaps {
     CUtensorMap x, chi, clo, xf;     // chi/clo: tf32-split fp32 (kind 0) or fp16 (kind 1) operand maps
@@ -1027,7 +1032,7 @@ bool tc16_supported(int d, int K) {
 // 2xFP16 error bound: split error <= 3 * 2^-22 |x_k c_k|
 // (+ absolute subnormal term, tau_abs), accumulation over 3d/16 f16 MMA
 // k-steps (+16 for the internal 16-term dot) at <= 2^-22 each.
-float tau_gamma_tc16(int d) { return 4.0f * (3.0f * 2.3841858e-7f + (3.0f * d / 16.0f + 16.0f) * 2.3841858e-7f); }
+float tau_gamma_tc16(int d) { return AAKM_TAU_MARGIN * (3.0f * 2.3841858e-7f + (3.0f * d / 16.0f + 16.0f) * 2.3841858e-7f); }
 
 #define AAKM_TC_INSTANCES(X, CG)                                                                     \
     X(1, 0, 0, CG) X(2, 0, 0, CG) X(3, 0, 0, CG) X(4, 0, 0, CG) X(1, 1, 0, CG) X(2, 1, 0, CG) X(3, 1, 0, CG) \
