@@ -126,6 +126,15 @@ __device__ int adjust_m(int m, int m_max, double Et, double E1, double E2, doubl
 __global__ void k_control(Dev d, int stage) {
     DevState* st = d.st;
     if (st->done) return;
+    if (stage == 1 && !st->reject) return;
+    {
+        // E = (E_hi + 2^-30 E_lo) / q from the reduced fixed-point parts (what k_energy
+        // does for the API calls), fused here: one single-thread launch per G-evaluation
+        long long* pk = d.packed[stage];
+        const double q = energy_q(d);
+        const long long* e = pk + pk_ehi(d);
+        pk[pk_e(d)] = __double_as_longlong(((double)e[0] + (double)e[1] * 9.313225746154785e-10) / q);
+    }
     if (stage == 0) {
         const long long* pk = d.packed[0];
         const double E = __longlong_as_double(pk[pk_e(d)]);   // k_energy, after the allreduce
@@ -254,9 +263,8 @@ void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0,
 #define FULL 0xffffffffu
 // Fixed-order reduction of this pass's Gram partials: one warp per entry, lanes
 // stride over the blocks, then a fixed xor tree (same bytes on every rank).
-__global__ void __launch_bounds__(1024) k_gram_reduce(Dev d) {
+__device__ __forceinline__ void gram_reduce(const Dev& d) {
     DevState* st = d.st;
-    if (st->done) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int H = d.H;
     const long long t = st->t;
@@ -279,9 +287,13 @@ __global__ void __launch_bounds__(1024) k_gram_reduce(Dev d) {
     }
 }
 
-__global__ void __launch_bounds__(32) k_solve(Dev d) {
+// one block: all 32 warps reduce the Gram partials (fixed order), then warp 0 solves
+__global__ void __launch_bounds__(1024) k_solve(Dev d) {
     DevState* st = d.st;
     if (st->done) return;
+    gram_reduce(d);
+    __syncthreads();                                 // st->gram / st->bvec written by the block
+    if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     const int H = d.H;
     const long long t = st->t;
@@ -397,10 +409,7 @@ __global__ void __launch_bounds__(32) k_solve(Dev d) {
 }
 #undef FULL
 
-void launch_solve(const Dev& d, cudaStream_t s) {
-    k_gram_reduce<<<1, 1024, 0, s>>>(d);
-    k_solve<<<1, 32, 0, s>>>(d);
-}
+void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 1024, 0, s>>>(d); }
 
 // ---------------------------------------------------------------- advance
 __global__ void k_advance(Dev d) {

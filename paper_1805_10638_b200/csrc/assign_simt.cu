@@ -26,7 +26,7 @@ namespace aakm {
 float tau_gamma_simt(int d) { return 8.0f * (float)(d + 3) * 5.9604645e-8f; }
 
 template <int D>
-struct RowsPerThread { static constexpr int value = D <= 4 ? 8 : (D <= 16 ? 4 : 2); };
+struct RowsPerThread { static constexpr int value = D <= 4 ? 8 : (D <= 16 ? 4 : 2); };   // the most rows a thread keeps
 
 __device__ __forceinline__ void push_flag(const Dev& d, int branch, bool flag, long long row, float b1, float tau) {
     unsigned mask = __ballot_sync(0xffffffffu, flag);
@@ -45,10 +45,9 @@ __device__ __forceinline__ void push_flag(const Dev& d, int branch, bool flag, l
     }
 }
 
-template <int D>
+template <int D, int R>
 __global__ void __launch_bounds__(256) k_assign_simt(Dev d, GEval g, int KT) {
     if (!geval_active(d, g)) return;
-    constexpr int R = RowsPerThread<D>::value;
     extern __shared__ float4 smem4[];
     float* cs = reinterpret_cast<float*>(smem4);   // KT x D, holds -2 c
     float* cns = cs + KT * D;                      // KT
@@ -167,16 +166,28 @@ __global__ void __launch_bounds__(128) k_assign_simt_generic(Dev d, GEval g, int
     push_flag(d, g.branch, flag, row, b1, tau);
 }
 
-template <int D>
-static void launch_t(const Dev& d, const GEval& g, cudaStream_t s) {
-    constexpr int R = RowsPerThread<D>::value;
+template <int D, int R>
+static void launch_r(const Dev& d, const GEval& g, cudaStream_t s) {
     int KT = d.K;
     const int max_smem = 96 * 1024;
     if ((size_t)KT * (D + 1) * 4 > (size_t)max_smem) KT = max_smem / ((D + 1) * 4);
     size_t smem = (size_t)KT * (D + 1) * 4;
     long long blocks = (d.n + 256LL * R - 1) / (256LL * R);
     if (blocks < 1) blocks = 1;
-    k_assign_simt<D><<<(unsigned)blocks, 256, smem, s>>>(d, g, KT);
+    k_assign_simt<D, R><<<(unsigned)blocks, 256, smem, s>>>(d, g, KT);
+}
+
+// Rows per thread: as many as RowsPerThread allows (register reuse of each C
+// element) while the grid still covers every SM twice; small shards (c1: 10 000
+// rows, c2: 100 000) drop to fewer rows per thread instead of leaving SMs idle.
+template <int D>
+static void launch_t(const Dev& d, const GEval& g, cudaStream_t s) {
+    constexpr int RM = RowsPerThread<D>::value;
+    const long long want = 2LL * d.num_sms * 256;                 // threads for two blocks per SM
+    if (RM >= 8 && d.n >= want * 8) { launch_r<D, (RM >= 8 ? 8 : 1)>(d, g, s); return; }
+    if (RM >= 4 && d.n >= want * 4) { launch_r<D, (RM >= 4 ? 4 : 1)>(d, g, s); return; }
+    if (RM >= 2 && d.n >= want * 2) { launch_r<D, (RM >= 2 ? 2 : 1)>(d, g, s); return; }
+    launch_r<D, 1>(d, g, s);
 }
 
 cudaError_t setup_simt() {
@@ -185,13 +196,14 @@ cudaError_t setup_simt() {
         cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (r != cudaSuccess) e = r;
     };
-    set((const void*)k_assign_simt<1>, 96 * 1024);
-    set((const void*)k_assign_simt<2>, 96 * 1024);
-    set((const void*)k_assign_simt<3>, 96 * 1024);
-    set((const void*)k_assign_simt<4>, 96 * 1024);
-    set((const void*)k_assign_simt<8>, 96 * 1024);
-    set((const void*)k_assign_simt<16>, 96 * 1024);
-    set((const void*)k_assign_simt<32>, 96 * 1024);
+#define AAKM_SIMT_ATTR(D_)                                                  \
+    set((const void*)k_assign_simt<D_, 1>, 96 * 1024);                      \
+    set((const void*)k_assign_simt<D_, (RowsPerThread<D_>::value >= 2 ? 2 : 1)>, 96 * 1024); \
+    set((const void*)k_assign_simt<D_, (RowsPerThread<D_>::value >= 4 ? 4 : 1)>, 96 * 1024); \
+    set((const void*)k_assign_simt<D_, (RowsPerThread<D_>::value >= 8 ? 8 : 1)>, 96 * 1024);
+    AAKM_SIMT_ATTR(1) AAKM_SIMT_ATTR(2) AAKM_SIMT_ATTR(3) AAKM_SIMT_ATTR(4) AAKM_SIMT_ATTR(8)
+    AAKM_SIMT_ATTR(16) AAKM_SIMT_ATTR(32)
+#undef AAKM_SIMT_ATTR
     set((const void*)k_assign_simt_generic, 200 * 1024);
     return e;
 }

@@ -378,11 +378,9 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         if (st != KMEANS_OK) return st;
     }
     if (h->comm) dbg("combine", s);
-    launch_energy(d, g, s);
-    dbg("energy", s);
-    launch_control(d, branch, s);
+    launch_control(d, branch, s);                   // E from the reduced parts + Algorithm 1 control
     dbg("control", s);
-    h->launches += 2;
+    h->launches += 1;
     return KMEANS_OK;
 }
 
@@ -405,7 +403,7 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
     dbg("combine_mix", s);
     launch_advance(d, s);
     dbg("advance", s);
-    h->launches += 5;                               // finalize, gram, gram_reduce + solve, advance
+    h->launches += 4;                               // finalize, gram, gram_reduce + solve (one launch), advance
     CK(h, cudaGetLastError());
     return KMEANS_OK;
 }
