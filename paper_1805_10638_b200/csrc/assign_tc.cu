@@ -109,25 +109,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     while (!mbar_try(b, parity))
         if (clock64() - t0 > (1ll << 32)) __trap();
 }
-// try_wait with a suspend-time hint: the waiting warp is parked (woken when the
-// phase completes or after ns) instead of re-issuing the poll, so the epilogue
-// warps that wait do not take issue slots from the ones that work
-__device__ __forceinline__ bool mbar_try_hint(uint64_t* b, uint32_t parity, uint32_t ns) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok) : "r"(su32(b)), "r"(parity), "r"(ns) : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_epi(uint64_t* b, uint32_t parity, bool hint) {
-    if (mbar_try(b, parity)) return;
-    const long long t0 = clock64();
-    uint32_t n = 0;
-    while (!(hint ? mbar_try_hint(b, parity, 1000u) : mbar_try(b, parity)))
-        if ((++n & 63u) == 0 && clock64() - t0 > (1ll << 32)) __trap();
-}
 // Same with a sleep between polls: for warps off the critical path (producer,
 // splitter), whose spinning would otherwise take issue slots from the epilogue.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, uint32_t ns) {
@@ -146,6 +127,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 }
 // AAKM_TC_TRACE probe: %globaltimer stamps of pipeline events of CTAs 0 and 1 (perf only)
 __device__ __forceinline__ void tc_stamp(const Dev& d, int ev, long long it) {
+#ifndef AAKM_TC_TRACE_BUILD
+    return;                                  // compiled out unless built with -DAAKM_TC_TRACE_BUILD
+#endif
     if (!d.dbg_ts || blockIdx.x > 1 || it >= 256) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -643,8 +627,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             }
             uint8_t* xhi = opb + xb * OPB;
             uint8_t* xlo = xhi + NATOM * ATOM_BYTES_X;
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {                       // both rows interleaved (ILP)
+#pragma unroll (KIND == 0 ? 2 : 1)
+            for (int rr = 0; rr < 2; ++rr) {                       // KIND 0: both rows interleaved (ILP)
                 const int r = t + 64 * rr;
                 float xn = 0.f;
                 if (KIND == 0) {
@@ -769,7 +753,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             // NXB + ceil(NACC / NT) row tiles ahead of the epilogue (operand buffers +
             // accumulators); the ring has one slot more (xr_of), so it neither
             // aliases a phase nor overwrites an unread slot.
-            mbar_wait_epi(xready + (it & (XRr - 1)), (uint32_t)(it / XRr) & 1u, (d.dbg & 64) != 0);
+            mbar_wait(xready + (it & (XRr - 1)), (uint32_t)(it / XRr) & 1u);
             const float xn = cq == 0 ? xnorm[(it & (XRr - 1)) * TC_BM + r] : 0.f;
             // NTRK independent top-2 trackers.  MODE 0 keys pack the column's position
             // inside its 32-column batch into the 5 low mantissa bits of the score (a
@@ -784,7 +768,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             int cnt = 0;
             if (MODE == 1 && frow < n_rows) lim = d.flag_b1[frow] + d.flag_tau[frow];
             for (int nt = 0; nt < NT; ++nt) {
-                mbar_wait_epi(accf + acc, aph, (d.dbg & 64) != 0);
+                mbar_wait(accf + acc, aph);
                 if (warp == 0 && lane == 0 && NT == 1) tc_stamp(d, 4, it);   // epilogue sees the accumulator
                 tc_fence_after();
                 // all CG 32-column batches of this warp in flight at once, one wait, then
