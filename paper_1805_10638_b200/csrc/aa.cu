@@ -155,6 +155,7 @@ __global__ void k_control(Dev d, int stage) {
             if (E >= st->E1 || ch == 0) {                       // PAPER.md:142 (>=, R-A8); R-A10
                 st->reject = 1; st->rejected_now = 1; st->n_rejected += 1;
                 st->fb_slot = (int)((st->t - 1) % d.H);         // C_AU^t = G^{t-1} (R-A3)
+                if (d.condB) cudaGraphSetConditional(d.condB, 1u);   // graph replay: run branch B
             } else {
                 st->accepted_now = 1; st->n_accepted += 1;
             }

@@ -138,6 +138,8 @@ struct Dev {
     int dbg;              // AAKM_TC_DBG probe bits (perf experiments only; 0 in normal runs)
     float4* dbg_rows;     // kmeans_debug_scores only: per row (b1, b2, tau, i1 bits) of the dense engine
     unsigned long long* dbg_ts;   // AAKM_TC_TRACE probe: pipeline event stamps (nullptr in normal runs)
+    unsigned long long condB;     // kmeans_run's CUDA graph: conditional handle of the fallback branch B
+                                  // (k_control sets it on a rejection; 0 = eager launches, no conditional)
     // f4 fused combine (cfg.fused_comm, comm.cu): packed[0] / packed[1] are this rank's
     // replica of an NCCL symmetric window; every flush adds into all replicas
     int fused;            // 0 off, 1 multimem (NVLS multicast address mc0), 2 LSA peer pointers

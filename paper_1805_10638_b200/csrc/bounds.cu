@@ -164,7 +164,14 @@ __global__ void __launch_bounds__(256) k_bnd_save(Dev d, GEval g, int restore) {
     const float* lbs = restore ? d.lb0 : d.lb;
     const int* p2s = restore ? d.pj20 : d.pj2;
     const double* crs = restore ? d.C_ref0 : d.C_ref;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    // 16-B copies (the arrays are 256-B aligned carve regions), scalar tail
+    const long long n4 = n >> 2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += st) {
+        reinterpret_cast<float4*>(ub)[i] = reinterpret_cast<const float4*>(ubs)[i];
+        reinterpret_cast<float4*>(lb)[i] = reinterpret_cast<const float4*>(lbs)[i];
+        reinterpret_cast<int4*>(p2)[i] = reinterpret_cast<const int4*>(p2s)[i];
+    }
+    for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
         ub[i] = ubs[i]; lb[i] = lbs[i]; p2[i] = p2s[i];
     }
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < KD; i += st) cr[i] = crs[i];
@@ -175,8 +182,8 @@ __global__ void __launch_bounds__(256) k_bnd_save(Dev d, GEval g, int restore) {
 }
 
 int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s) {
-    long long cb = (d.n + 255) / 256;
-    if (cb > 4 * 1184) cb = 4 * 1184;
+    long long cb = (d.n / 4 + 255) / 256;                 // grid-stride, 16-B copies: 4 blocks per SM suffice
+    if (cb > 4 * d.num_sms) cb = 4 * d.num_sms;
     if (cb < 1) cb = 1;
     k_bnd_save<<<(int)cb, 256, 0, s>>>(d, g, g.branch == 1 ? 1 : 0);
     int kb = (int)((d.K + 7) / 8);
@@ -184,7 +191,7 @@ int launch_bounds_prep(const Dev& d, const GEval& g, cudaStream_t s) {
     if (kb < 1) kb = 1;
     k_shift<<<kb, 256, 0, s>>>(d, g);
     long long rb = (d.n + 1023) / 1024;                      // 1024 rows per block step
-    if (rb > 2 * 1184) rb = 2 * 1184;
+    if (rb > 4 * d.num_sms) rb = 4 * d.num_sms;
     if (rb < 1) rb = 1;
     k_bounds<<<(int)rb, 256, 0, s>>>(d, g);
     return 3;

@@ -64,6 +64,8 @@ struct kmeans_handle {
     unsigned int* xchk = nullptr;                            // device, 2 words: stats of a refreshed X
     unsigned int x_stat[2] = {0u, 0u};                       // this rank's create-time max |x|, max ||x||^2 (float bits)
     cudaEvent_t sync_ev = nullptr;                           // polled by sync_stream when a communicator exists
+    cudaStream_t body_stream = nullptr;                      // capture of the conditional branch-B body
+    long long kernels_b = 0;                                 // kernels inside it (launched only on rejections)
     std::vector<size_t> guards;                              // AAKM_WS_CANARY: canary offsets in the workspace
     char* ws_base = nullptr;
     void* fused = nullptr;                                   // f4 fused combine resources (comm.cu)
@@ -391,8 +393,38 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
     dbg("memset", s);
     kmeans_status st = geval(h, 0, s, timing);
     if (st != KMEANS_OK) return st;
-    st = geval(h, 1, s, false);
-    if (st != KMEANS_OK) return st;
+    if (d.condB) {
+        // graph capture: the fallback G-evaluation (branch B) goes into the body of a
+        // conditional IF node that k_control switches on only for a rejected iterate,
+        // so a pass without a rejection launches none of its ~10 kernels
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t g;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        CK(h, cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &nd));
+        alignas(cudaGraphNodeParams) unsigned char praw[sizeof(cudaGraphNodeParams)] = {};   // (a union: no default ctor)
+        cudaGraphNodeParams& p = *reinterpret_cast<cudaGraphNodeParams*>(praw);
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = d.condB;
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(h, cudaGraphAddNode(&node, g, deps, nd, &p));
+        if (!h->body_stream) CK(h, cudaStreamCreateWithFlags(&h->body_stream, cudaStreamNonBlocking));
+        CK(h, cudaStreamBeginCaptureToGraph(h->body_stream, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal));
+        const long long b0 = h->launches;
+        st = geval(h, 1, h->body_stream, false);
+        cudaGraph_t body;
+        const cudaError_t e = cudaStreamEndCapture(h->body_stream, &body);
+        if (st != KMEANS_OK) return st;
+        CK(h, e);
+        h->kernels_b = h->launches - b0;
+        CK(h, cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    } else {
+        st = geval(h, 1, s, false);
+        if (st != KMEANS_OK) return st;
+    }
     launch_finalize(d, s);
     dbg("finalize", s);
     launch_gram(d, s);
@@ -415,7 +447,21 @@ static kmeans_status ensure_graph(kmeans_handle* h) {
     cudaGraph_t g;
     long long before = h->launches;
     CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    // branch B as a conditional node (not with a plain NCCL communicator: its captured
+    // collectives stay outside conditional bodies; the predicated kernels run instead)
+    h->kernels_b = 0;
+    // (tiny shards keep the predicated kernels: c1's 50-us passes ran 10 % slower with
+    // the conditional node, c2's Lloyd passes 9 % faster, c3 1-4 %)
+    if ((!h->comm || h->d.fused) && h->n_global >= 50000) {
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t cg;
+        CK(h, cudaStreamGetCaptureInfo(h->cap_stream, &cst, nullptr, &cg, nullptr, nullptr));
+        cudaGraphConditionalHandle hb;
+        CK(h, cudaGraphConditionalHandleCreate(&hb, cg, 0, cudaGraphCondAssignDefault));
+        h->d.condB = hb;
+    }
     kmeans_status st = enqueue_pass(h, h->cap_stream, false);
+    h->d.condB = 0;                                 // eager launches never touch the handle
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (st != KMEANS_OK) return st;
     CK(h, e);
@@ -442,6 +488,7 @@ static void release(kmeans_handle* h, bool sync) {
     if (sync && h->stream) cudaStreamSynchronize(h->stream);
     if (h->pass_exec) cudaGraphExecDestroy(h->pass_exec);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    if (h->body_stream) cudaStreamDestroy(h->body_stream);
     if (h->copy_stream) {
         if (sync) cudaStreamSynchronize(h->copy_stream);
         cudaStreamDestroy(h->copy_stream);
@@ -1067,6 +1114,8 @@ kmeans_status kmeans_run(kmeans_handle* h, const double* C0, double* C_out, int3
     CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
     SYNC(h, s);
     const DevState& S = *h->st_host;
+    // the conditional branch-B body ran only on the passes that rejected an iterate
+    h->launches -= (passes - std::min<long long>(passes, S.n_rejected)) * h->kernels_b;
     if (S.label_error & 2) { x_range_error(h); return KMEANS_ERR_INVALID; }
     if (labels_out && h->d.n > 0)
         CK(h, cudaMemcpyAsync(labels_out, h->d.lab[S.cur], (size_t)h->d.n * 4, cudaMemcpyDeviceToDevice, s));
