@@ -336,10 +336,10 @@ AAKM_API kmeans_status kmeans_bounded_stats(kmeans_handle *h, int64_t *rows_scor
  * engine on C (K x d fp64) and writes, per local row, the engine's raw top-2
  * values and its near-tie threshold: rows_out (device, n_local x 4 float) =
  * (b1, b2, tau, bits of the chosen index i1), before any near-tie refine.
- * kind_out (host): 0 = 3xTF32, values are scores ||c||^2/2 - x.c (key-packed,
- * DESIGN.md §5.3); 1 = 2xFP16, values are window accumulators
- * U ||x - c||^2 + 6 with U = *unit_out (host); 2 = SIMT FP32, values are
- * scores ||c||^2 - 2 x.c.  Every computed value must lie within tau / 2 of
+ * kind_out (host): 1 = a tensor-core engine (3xTF32 or 2xFP16), values are
+ * window accumulators U ||x - c||^2 + 6 with U = *unit_out (host, 1/(2 s^2));
+ * 2 = SIMT FP32, values are scores ||c||^2 - 2 x.c (unit 1).  (0 is no longer
+ * produced: r01's 3xTF32 key-packed scores.)  Every computed value must lie within tau / 2 of
  * its exact counterpart for the near-tie flagging (row a3) to be rigorous.
  * Synchronises; clobbers the API label buffer only. */
 AAKM_API kmeans_status kmeans_debug_scores(kmeans_handle *h, const double *C, float *rows_out,

@@ -13,8 +13,8 @@
 //               Cholesky with drop-oldest (R-A14) -> theta -> mixing weights.
 //   k_combine   C^{t+1} = G^t - sum_j theta_j (G^{t-j+1} - G^{t-j})
 //               (minus sign R-A1) = sum_j alpha_j G^{t-j},
-//               fused with the centroid prep of the next assignment
-//               (||c||^2, tf32 hi/lo split, max ||c||^2).
+//               fused with the centroid prep of the next assignment (fl32(C),
+//               ||c||^2, max ||c||^2; the tensor operands follow in k_csplit16/32).
 //   k_advance   E^{t-2} <- E^{t-1} <- E^t, P^{t-1} <- P^t, t <- t+1, trace.
 // All reductions are fixed-order, so every rank computes identical bytes.
 #include <math.h>
@@ -27,8 +27,8 @@ namespace aakm {
 // mode 0: mix from (st->alpha, st->alpha_slot, st->n_alpha), active if !done
 // mode 1: C <- G[st->fb_slot] (fallback C_AU^t = G^{t-1}, R-A3), active if reject
 // mode 2: C <- src (caller centroids / C^0), always
-// C^t is fp64 (the whole Anderson state is, R-A17); the engines' operands are
-// derived from it here: fl32(C) for SIMT, the tf32 hi/lo split of -C, ||c||^2.
+// C^t is fp64 (the whole Anderson state is, R-A17); fl32(C) for SIMT and ||c||^2
+// are derived from it here, the tensor engines' operands by k_csplit16 / k_csplit32.
 __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const double* src) {
     DevState* st = d.st;
     if (mode == 0 && st->done) return;
@@ -63,25 +63,11 @@ __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const double* 
             }
             d.C[e] = c;
             if (d.C32) d.C32[e] = (float)c;
-            // tensor operands hold -c (the engine accumulates ||c||^2/2 - x.c directly)
-            const float hi = __uint_as_float(__float_as_uint((float)-c) & 0xFFFFE000u);   // tf32 truncation
-            d.Chi[e] = hi;
-            d.Clo[e] = (float)(-c - (double)hi);
             nrm = fma(c, c, nrm);
         }
         for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
         const float cnj = (float)nrm;
         if (lane == 0) d.cn[j] = cnj;
-        if (d.cnimg && d.tc_kind == 0 && lane < 8) {
-            // 3xTF32 engine: ||c||^2/2 = h + m + l to ~33 bits (3 tf32 parts of the fp64 value),
-            // row j of the folded K block; the A side holds (1, 1, 1, 0, ...)
-            const double v = 0.5 * nrm;
-            const float h = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
-            const float m = __uint_as_float(__float_as_uint((float)(v - (double)h)) & 0xFFFFE000u);
-            const float l = (float)(v - (double)h - (double)m);
-            const float val = lane == 0 ? h : lane == 1 ? m : lane == 2 ? l : 0.f;
-            *reinterpret_cast<float*>(d.cnimg + (size_t)(j >> 7) * AAKM_CNIMG_BYTES + cnimg_off((int)(j & 127), lane * 4)) = val;
-        }
         bmax = fmaxf(bmax, __double2float_ru(nrm));
     }
     // max ||c||^2: per-block max -> atomicMax into cmax2_tmp; last block publishes and resets

@@ -80,6 +80,7 @@ struct Dev {
     void* Chi16;          // 2xFP16 engine: fp16 hi of C / s_c
     void* Clo16;          // 2xFP16 engine: fp16 lo
     int tc_kind;          // 0 = 3xTF32, 1 = 2xFP16
+    int pair_ok;          // two-centroid near-tie fast path (k_refine_pair: d/4 a power of two <= 32)
     float x_scale;        // 2xFP16: create-time scale from max |x| (informational)
     float x_inv_scale;
     float x_absmax;       // 2xFP16: max |x_ik| over the shard (subnormal part of the error bound)

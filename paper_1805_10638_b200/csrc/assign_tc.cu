@@ -195,18 +195,7 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
     asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
-// key = score with its 5 low mantissa bits replaced by the column's position in
-// its 32-column batch; computed on the FMA pipe (IMAD.HI = >> 5, IMAD = *k32 + j).
-// k32 == 32 comes from a kernel parameter: with a literal 32 ptxas emits an ALU-pipe
-// LEA, and the ALU pipe (FMNMX) is the epilogue's bottleneck.
-__device__ __forceinline__ float pack_key(uint32_t sc_bits, uint32_t j, uint32_t k32) {
-    uint32_t hi, k;
-    asm("mul.hi.u32 %0, %1, 134217728;" : "=r"(hi) : "r"(sc_bits));
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(hi), "r"(k32), "n"(0));
-    return __uint_as_float(k + j);
-}
-
-// Window key (2xFP16 engine): the accumulator a = ||x - c||^2 / (2 s^2) + 6 lies in
+// Window key (both engines): the accumulator a = ||x - c||^2 / (2 s^2) + 6 lies in
 // [4, 134], so its float bits are 0 1000 0eee m..m (biased exponent 129..134) and
 // bits << 5 keeps the order: the dropped top 5 bits are constant, the new sign
 // bit (exponent bit 3) is 0, the new exponent field is never all-ones.  The low 5
@@ -400,8 +389,9 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     }
     constexpr int NATOM = KIND ? A / 2 : A;        // 128-B operand K-atoms per row
     constexpr int AELEM = KIND ? 64 : 32;          // elements per operand atom
-    // one operand buffer: hi + lo (+ KIND 1: this row tile's A side of the folded block)
-    constexpr int OPB = 2 * NATOM * ATOM_BYTES_X + (KIND ? AAKM_CNIMG_BYTES : 0);
+    // one operand buffer: hi + lo + this row tile's A side of the folded block (both kinds
+    // produce window keys: the accumulator is ||x - c||^2 / (2 s^2) + 6, see below)
+    constexpr int OPB = 2 * NATOM * ATOM_BYTES_X + AAKM_CNIMG_BYTES;
     constexpr int AW = TC_BN * CG;                 // accumulator columns = centroids per pair tile
     constexpr int NACC_ = 4 / CG;                  // accumulator buffers (512 TMEM columns)
     constexpr uint32_t IDESC_ = (KIND ? IDESC16 : IDESC) & ~((0x3Fu << 17) | (0x1Fu << 24));
@@ -422,8 +412,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint8_t* xst = smem;                                           // fp32 X tiles (TMA targets, splitter-owned)
     uint8_t* opb = (inplace || DX) ? smem : xst + nst * A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
-    uint8_t* ablk = stg + (size_t)S * STAGE_BYTES;                 // KIND 0: constant A side of the folded block
-    float* xnorm = reinterpret_cast<float*>(ablk + (KIND ? 0 : AAKM_CNIMG_BYTES)); // [XRr][128] ||x||^2 ring (slot = iteration % XRr)
+    float* xnorm = reinterpret_cast<float*>(stg + (size_t)S * STAGE_BYTES);   // [XRr][128] ||x||^2 ring (slot = iteration % XRr)
     float4* mrg = reinterpret_cast<float4*>(xnorm + XRr * TC_BM);     // [NQ-1][128] partial results of quarters 1..3
     uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + (NQ - 1) * TC_BM);
     uint64_t* full = bars;                                         // [S]  stage landed (leader: both halves)
@@ -440,17 +429,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     const int K = d.K;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;          // position in the CTA pair
     const bool leader = rank == 0;
-    // KIND 0: the accumulator is the score ||c||^2/2 - x.c; the constant A side of the folded
-    // block is (1, 1, 1, 0, ...) in every row.  KIND 1 ("window keys"): with the common scale
-    // s the accumulator is ||x - c||^2 / (2 s^2) + 6 in [4, 134]; its A side is per row tile
-    // (1, 1, h_i, l_i, 0, ...) with h_i + l_i = ||x_i||^2 / (2 s^2) + 6, written by the splitter.
-    if (KIND == 0) {
-        for (int i = threadIdx.x; i < TC_BM * 8; i += TC_THREADS) {
-            const int r = i >> 3, w = i & 7;
-            *reinterpret_cast<uint32_t*>(ablk + cnimg_off(r, w * 4)) = w < 3 ? 0x3F800000u : 0u;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-    }
+    // Window keys (both kinds): with the common power-of-two scale s the accumulator is
+    // ||x - c||^2 / (2 s^2) + 6 in [4, 134].  The folded block pairs, per row tile, the
+    // A side written by the splitter -- KIND 1 (fp16 pairs): (1, 1 | h_i, l_i | 0 ...),
+    // KIND 0 (tf32): (1, 1, 1, h_i, m_i, l_i, 0, 0), with the parts summing to
+    // ||x_i||^2 / (2 s^2) + 6 -- with the B side of each centroid (k_csplit16 / k_csplit32):
+    // (hc, lc | 1, 1 | 0 ...) / (hc, mc, lc, 1, 1, 1, 0, 0), parts of ||c_j||^2 / (2 s^2).
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
         for (int b = 0; b < 4; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4 * CG); }
@@ -523,7 +507,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         if (lane == 0 && leader) {                                 // ---- MMA issuer (the pair's leader)
             int s = 0, acc = 0; uint32_t ph = 0, aph = 0;
             uint32_t oph = 0;                                      // phase bit per operand buffer
-            const uint32_t opb_a = su32(opb), stg_a = su32(stg), ablk_a = su32(ablk);
+            const uint32_t opb_a = su32(opb), stg_a = su32(stg);
             int xb = 0;
             for (long long it = 0; live(it); ++it) {
                 mbar_wait(opready + xb, (oph >> xb) & 1u);
@@ -561,7 +545,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         // the folded block closes the sum: during the 3d/16 (3d/8) product steps
                         // the running sum stays within 2U sum|x_k c_k| <= U(||x||^2 + ||c||^2)
                         if (a == NATOM - 1 && !(d.dbg & 4)) {
-                            const uint32_t fa = KIND ? xhi_a + (uint32_t)(2 * NATOM * ATOM_BYTES_X) : ablk_a;
+                            const uint32_t fa = xhi_a + (uint32_t)(2 * NATOM * ATOM_BYTES_X);
                             mma_cg<KIND, CG>(dt, sdesc_ns(fa), sdesc_ns(sb + STAGE_MAIN), 1u, IDESC_CG);
                         }
                         if (!RES) {
@@ -595,7 +579,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 }
             }
         }
-        const float inv_sx = KIND ? 1.0f / d.st->c_scale : 1.0f;     // exact (power of 2)
+        const float inv_sx = 1.0f / d.st->c_scale;                 // exact (power of 2)
         const float hxs = 0.5f * inv_sx * inv_sx;
         // DX candidate pass (MODE 1): the flagged rows are read in place through the
         // flag list (no gathered copy), so there is nothing to prefetch by TMA
@@ -641,11 +625,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         for (int c = 0; c < 8; ++c) {
                             const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
                             const float4 v = *reinterpret_cast<const float4*>(xs + off);
+                            const float4 w = make_float4(v.x * inv_sx, v.y * inv_sx, v.z * inv_sx, v.w * inv_sx);   // exact
                             float4 h, l;
-                            h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
-                            h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
-                            h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
-                            h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
+                            h.x = __uint_as_float(__float_as_uint(w.x) & 0xFFFFE000u); l.x = w.x - h.x;
+                            h.y = __uint_as_float(__float_as_uint(w.y) & 0xFFFFE000u); l.y = w.y - h.y;
+                            h.z = __uint_as_float(__float_as_uint(w.z) & 0xFFFFE000u); l.z = w.z - h.z;
+                            h.w = __uint_as_float(__float_as_uint(w.w) & 0xFFFFE000u); l.w = w.w - h.w;
                             q0 = fmaf(v.x, v.x, q0); q1 = fmaf(v.y, v.y, q1); q2 = fmaf(v.z, v.z, q2); q3 = fmaf(v.w, v.w, q3);
                             *reinterpret_cast<float4*>(xhi + off) = h;
                             *reinterpret_cast<float4*>(xlo + off) = l;
@@ -689,7 +674,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     }
                 }
                 xnorm[(it & (XRr - 1)) * TC_BM + r] = xn;
-                if (KIND) {                                        // A side of the folded block, row r
+                if (KIND == 0) {                                   // A side of the folded block, row r (tf32)
+                    uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
+                    const float v = fmaf(xn, hxs, 6.0f);
+                    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                    const float m = __uint_as_float(__float_as_uint(v - h) & 0xFFFFE000u);
+                    const float l = (v - h) - m;                   // exact: v = h + m + l
+                    *reinterpret_cast<float4*>(fa + cnimg_off(r, 0)) = make_float4(1.f, 1.f, 1.f, h);
+                    *reinterpret_cast<float4*>(fa + cnimg_off(r, 16)) = make_float4(m, l, 0.f, 0.f);
+                } else {                                           // A side of the folded block, row r (fp16)
                     uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
                     const float v = fmaf(xn, hxs, 6.0f);
                     const __half h = __float2half_rn(v);
@@ -744,8 +737,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         int* lab_out = g.lab_out ? g.lab_out : d.lab[d.st->cur];
         const float cmax2 = __uint_as_float(d.st->cmax2_bits);
         const float gam = d.tau_gamma;
-        const float Usc = KIND ? 0.5f / (d.st->c_scale * d.st->c_scale) : 0.5f;  // accumulator units per distance unit
-        const float tau_abs = KIND ? d.st->tau_abs : 0.0f;
+        const float Usc = 0.5f / (d.st->c_scale * d.st->c_scale);  // accumulator units per distance unit
+        const float tau_abs = d.st->tau_abs;
         const uint32_t k32 = d.key_mul;
         int acc = 0; uint32_t aph = 0;
         for (long long it = 0; live(it); ++it) {
@@ -792,7 +785,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     const int j0 = nt * AW + (cq * CG + b) * 32;
                     if (j0 + 32 > K) {                              // ragged last tile: padded columns lose
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : (KIND ? 0x437A0000u : 0x7F7FFFFFu);
+                        for (int j = 0; j < 32; ++j) v[j] = j0 + j < K ? v[j] : 0x437A0000u;   // 250: above every window value
                     }
                     float O1[NTRK];
 #pragma unroll
@@ -804,10 +797,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 #pragma unroll
                             for (int pp = 0; pp < 2; ++pp) {
                                 const int u = ((j >> 1) + pp) & (NTRK - 1);
-                                const float ka = KIND ? wkey(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32)
-                                                      : pack_key(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
-                                const float kb = KIND ? wkey(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32)
-                                                      : pack_key(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
+                                const float ka = wkey(v[j + 2 * pp], (uint32_t)(j + 2 * pp), k32);
+                                const float kb = wkey(v[j + 2 * pp + 1], (uint32_t)(j + 2 * pp + 1), k32);
                                 const float m = fminf(ka, kb), M = fmaxf(ka, kb);
                                 B2[u] = fmin3(B2[u], M, fmaxf(B1[u], m));
                                 B1[u] = fminf(B1[u], m);
@@ -840,17 +831,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 #pragma unroll
                 for (int u = 1; u < NTRK; ++u) {
                     const int iu = BB[u] + (int)(__float_as_uint(B1[u]) & 31u);
-                    if (KIND) {
-                        top2l_merge(t, B1[u], iu, B2[u], -1, B2[u]);
-                    } else {
-                        t.b2 = fminf(fminf(t.b2, B2[u]), fmaxf(t.b1, B1[u]));
-                        const bool tk = B1[u] < t.b1 || (B1[u] == t.b1 && iu < t.i1);
-                        t.i1 = tk ? iu : t.i1;
-                        t.b1 = fminf(t.b1, B1[u]);
-                    }
+                    top2l_merge(t, B1[u], iu, B2[u], -1, B2[u]);
                 }
                 if (cq > 0) {
-                    const unsigned hi = (KIND && t.i2 >= 0 && (t.i2 >> 5) < 0xFFF) ? (unsigned)(t.i2 >> 5) : 0xFFFu;
+                    const unsigned hi = (t.i2 >= 0 && (t.i2 >> 5) < 0xFFF) ? (unsigned)(t.i2 >> 5) : 0xFFFu;
                     const float Lp = __uint_as_float((__float_as_uint(t.L) & ~0xFFFu) | hi);
                     mrg[(cq - 1) * TC_BM + r] = make_float4(t.b1, t.b2, __int_as_float(t.i1), Lp);
                 }
@@ -862,36 +846,22 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     for (int o = 0; o < NQ - 1; ++o) {
                         const float4 m = mrg[o * TC_BM + r];
                         const int oi1 = __float_as_int(m.z);
-                        if (KIND) {
-                            const unsigned hi = __float_as_uint(m.w) & 0xFFFu;
-                            const int oi2 = hi == 0xFFFu ? -1 : (int)(hi << 5) + (int)(__float_as_uint(m.y) & 31u);
-                            top2l_merge(t, m.x, oi1, m.y, oi2, __uint_as_float(__float_as_uint(m.w) & ~0xFFFu));
-                        } else {
-                            t.b2 = fminf(fminf(t.b2, m.y), fmaxf(t.b1, m.x));
-                            const bool tk = m.x < t.b1 || (m.x == t.b1 && oi1 < t.i1);
-                            t.i1 = tk ? oi1 : t.i1;
-                            t.b1 = fminf(t.b1, m.x);
-                        }
+                        const unsigned hi = __float_as_uint(m.w) & 0xFFFu;
+                        const int oi2 = hi == 0xFFFu ? -1 : (int)(hi << 5) + (int)(__float_as_uint(m.y) & 31u);
+                        top2l_merge(t, m.x, oi1, m.y, oi2, __uint_as_float(__float_as_uint(m.w) & ~0xFFFu));
                     }
                     b1 = t.b1; b2 = t.b2; i1 = t.i1;
                     const bool ok = frow < n_rows;
                     const long long row = (use_list && ok) ? (long long)d.act_rows[frow] : frow;
-                    float tau;
-                    if (KIND) {
-                        // window keys are exact accumulator values: decode.  The folded terms
-                        // enter last, so every partial sum is <= U (||x||^2 + ||c||^2) + 6
-                        b1 = wdecode(b1); b2 = wdecode(b2);
-                        tau = Usc * (gam * (xn + cmax2) + tau_abs) + gam * 8.0f;
-                    } else {
-                        // score units (the folded ||c||^2 term adds cmax2 to the accumulated
-                        // magnitude), + 2 key quanta (32 ulps each) of the larger-magnitude key
-                        tau = Usc * (gam * (xn + 2.0f * cmax2) + tau_abs) + 7.62939453e-6f * fmaxf(fabsf(b1), fabsf(b2));
-                    }
+                    // window keys are exact accumulator values: decode.  The folded terms
+                    // enter last, so every partial sum is <= U (||x||^2 + ||c||^2) + 6
+                    b1 = wdecode(b1); b2 = wdecode(b2);
+                    const float tau = Usc * (gam * (xn + cmax2) + tau_abs) + gam * 8.0f;
                     const bool flag = ok && (b2 - b1 <= tau);
                     // two-centroid fast path: every key other than b1, b2 is >= L > b1 + tau,
                     // so only i1 and i2 can be the exact argmin
                     bool pair = false;
-                    if (KIND && flag && t.i2 >= 0 && K <= 131040)
+                    if (d.pair_ok && flag && t.i2 >= 0 && K <= 131040)
                         pair = wdecode(__uint_as_float(__float_as_uint(t.L) & ~0xFFFu)) > b1 + tau;
                     if (ok) lab_out[row] = i1;
                     if (d.dbg_rows && ok && MODE == 0)               // kmeans_debug_scores (margin probes)
@@ -923,7 +893,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                         d.pj2[row] = p2;
                     }
                     push_flag_tc(d, g.branch, flag && !pair, row, b1, tau);
-                    if (KIND) push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
+                    push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
                 }
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
                 if (warp == 0 && lane == 0) tc_stamp(d, 5, it);    // epilogue done with the tile
@@ -963,10 +933,10 @@ static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2, int
     const int natom = kind ? A / 2 : A;
     const int staging = (NXB == 0 || kind == 1) ? 0 : nst * A;   // in place / direct X: none; KIND 0: nst tiles
     const int nb = NXB == 0 ? 1 : NXB;
-    const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + (kind ? AAKM_CNIMG_BYTES : 0);
+    const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + AAKM_CNIMG_BYTES;
     const int xr = xr_of(NT, NXB, cg);
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
-           (kind ? 0 : AAKM_CNIMG_BYTES) + (size_t)xr * TC_BM * 4 + (NQ - 1) * TC_BM * 16 +
+           (size_t)xr * TC_BM * 4 + (NQ - 1) * TC_BM * 16 +
            (size_t)(2 * S + 20 + xr) * 8 + 16;
 }
 
@@ -1248,11 +1218,55 @@ __global__ void __launch_bounds__(256) k_csplit16(Dev d, int mode) {
     }
 }
 
+// ---- 3xTF32 operand prep (KIND 0, window keys): the same common scale s as
+// k_csplit16; -c/s = hi + lo with hi = tf32(-c/s) (truncated) and lo the fp32 rest,
+// both from the fp64 C^t; the B side of the folded block is (hc, mc, lc, 1, 1, 1, 0, 0)
+// with hc + mc + lc = ||c_j||^2 / (2 s^2) (three tf32 parts of the fp64 value).
+__global__ void __launch_bounds__(256) k_csplit32(Dev d, int mode) {
+    DevState* st = d.st;
+    if (mode == 0 && st->done) return;
+    if (mode == 1 && (st->done || !st->reject)) return;
+    const float cmax2 = __uint_as_float(st->cmax2_bits);
+    const float cmax = sqrtf(cmax2);
+    const float M = fmaxf(cmax, d.x_nmax);
+    const float sc = M > 0.f ? exp2f(ceilf(log2f(M)) - 3.0f) : 1.0f;
+    const double inv = 1.0 / (double)sc;                                     // exact (power of 2)
+    const double U = 0.5 * inv * inv;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->c_scale = sc;
+        st->cn_amul = 1.0f;
+        // tf32 carries fp32's exponent range; only flushed subnormal operands (< 2^-126
+        // in operand units) can go missing: 8 d 2^-126 in accumulator units at most
+        st->tau_abs = 8.0f * (float)d.d * 1.17549435e-38f / (float)U;
+    }
+    const long long KD = (long long)d.K * d.d;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
+        const double v = -d.C[e] * inv;                  // operands hold -c / s
+        const float hi = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
+        d.Chi[e] = hi;
+        d.Clo[e] = (float)(v - (double)hi);
+    }
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x) {
+        const double* c = d.C + j * d.d;
+        double nrm = 0.0;
+        for (int k = 0; k < d.d; ++k) nrm = fma(c[k], c[k], nrm);
+        const double v = nrm * U;
+        const float h = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
+        const float m = __uint_as_float(__float_as_uint((float)(v - (double)h)) & 0xFFFFE000u);
+        const float l = (float)(v - (double)h - (double)m);
+        uint8_t* row = d.cnimg + (size_t)(j >> 7) * AAKM_CNIMG_BYTES;
+        const int r = (int)(j & 127);
+        *reinterpret_cast<float4*>(row + cnimg_off(r, 0)) = make_float4(h, m, l, 1.f);
+        *reinterpret_cast<float4*>(row + cnimg_off(r, 16)) = make_float4(1.f, 1.f, 0.f, 0.f);
+    }
+}
+
 void launch_csplit16(const Dev& d, int mode, cudaStream_t s) {
     long long KD = (long long)d.K * d.d;
     int blocks = (int)((KD + 255) / 256);
     if (blocks > 1184) blocks = 1184;
-    k_csplit16<<<blocks, 256, 0, s>>>(d, mode);
+    if (d.tc_kind == 1) k_csplit16<<<blocks, 256, 0, s>>>(d, mode);
+    else k_csplit32<<<blocks, 256, 0, s>>>(d, mode);
 }
 
 // ---- refine for the tensor-core engine: gather -> candidate pass -> exact fp64
@@ -1389,11 +1403,12 @@ int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_
     if (gather) k_gather_flagged<<<4 * d.num_sms, 256, 0, s>>>(d, g);
     launch_tc_mode<1>(d, g, static_cast<const TcMaps*>(maps), s);
     k_refine_exact<<<4 * d.num_sms, 256, 0, s>>>(d, g);
-    if (d.tc_kind == 1) {                                          // d in {64, 128}
-        if (d.d == 64) k_refine_pair<16><<<4 * d.num_sms, 256, 0, s>>>(d, g);
+    if (d.pair_ok) {                                               // d in {32, 64, 128}
+        if (d.d == 32) k_refine_pair<8><<<4 * d.num_sms, 256, 0, s>>>(d, g);
+        else if (d.d == 64) k_refine_pair<16><<<4 * d.num_sms, 256, 0, s>>>(d, g);
         else k_refine_pair<32><<<4 * d.num_sms, 256, 0, s>>>(d, g);
     }
-    return 2 + gather + (d.tc_kind == 1 ? 1 : 0);
+    return 2 + gather + (d.pair_ok ? 1 : 0);
 }
 
 }  // namespace aakm

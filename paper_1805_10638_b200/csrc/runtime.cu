@@ -292,7 +292,7 @@ static void assign_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
 static void combine(kmeans_handle* h, const Dev& d, int mode, const double* src, cudaStream_t s) {
     launch_combine(d, mode, src, s);
     h->launches++;
-    if (d.tc_kind == 1) { launch_csplit16(d, mode, s); h->launches++; }
+    if (d.cnimg) { launch_csplit16(d, mode, s); h->launches++; }   // tensor operands (both kinds)
 }
 
 // Exact re-decision of the near-tie rows: the tensor-core engine re-runs the
@@ -678,6 +678,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         D.gram_blocks = (int)(gb > AAKM_GRAM_BLOCKS ? AAKM_GRAM_BLOCKS : (gb < 1 ? 1 : gb));
     }
     D.tc_kind = h->path == KMEANS_PATH_TC16 ? 1 : 0;
+    D.pair_ok = (h->path == KMEANS_PATH_TC16 || h->path == KMEANS_PATH_TC) && (d == 32 || d == 64 || d == 128);
     const bool tcpath = h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16;
     D.cnimg = tcpath ? (uint8_t*)(w + L.cnimg) : nullptr;
     D.key_mul = 32u;
@@ -740,7 +741,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         CKC(cudaStreamSynchronize(h->stream));
         memcpy(h->x_stat, mloc, 8);
     }
-    if (h->path == KMEANS_PATH_TC16) {
+    if (h->path == KMEANS_PATH_TC16 || h->path == KMEANS_PATH_TC) {   // common operand scale s (window keys)
         const float m = mloc[0];
         const float sx = m > 0.f ? exp2f(ceilf(log2f(m)) - 13.0f) : 1.0f;
         const float xnm = sqrtf(mloc[1]) * (1.0f + 1e-6f);   // (already rounded up in fp32) margin
@@ -883,8 +884,7 @@ kmeans_status kmeans_debug_scores(kmeans_handle* h, const double* C, float* rows
     SYNC(h, s);
     CK(h, cudaGetLastError());
     memcpy(&sc, h->scal_host, 4);
-    if (h->path == KMEANS_PATH_TC16) { *kind_out = 1; *unit_out = 0.5 / ((double)sc * (double)sc); }
-    else if (h->path == KMEANS_PATH_TC) { *kind_out = 0; *unit_out = 1.0; }
+    if (h->path == KMEANS_PATH_TC16 || h->path == KMEANS_PATH_TC) { *kind_out = 1; *unit_out = 0.5 / ((double)sc * (double)sc); }
     else { *kind_out = 2; *unit_out = 1.0; }
     return KMEANS_OK;
 }
