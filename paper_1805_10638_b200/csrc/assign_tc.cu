@@ -52,7 +52,8 @@ constexpr int TC_BM = 128;
 constexpr int TC_BN = 128;
 constexpr int NTRK = 4;                            // independent top-2 trackers per thread (ILP)
 constexpr int NQ = 4;                              // epilogue column quarters (warps per SMSP)
-constexpr int TC_THREADS = 128 + NQ * 128;         // 4 control warps + 16 epilogue warps
+// 16 epilogue warps + producer + MMA issuer + NSW X-splitter warps (2, or 4: one per SMSP)
+constexpr int tc_threads(int nsw) { return 32 * (NQ * 4 + 2 + nsw); }
 constexpr int MAXCH = AAKM_MAXC / NQ;              // candidate slots per row per column quarter
 constexpr int W_PROD = NQ * 4;                     // warp roles: epilogue warps 0..15 first, so the
 constexpr int W_MMA = W_PROD + 1;                  // SMSP arbiter (highest warp id first) never starves
@@ -365,8 +366,10 @@ __device__ __forceinline__ void commit_cg(uint64_t* bar) {
 // KIND 1: 2xFP16 split with power-of-two scales s_x, s_c: v/s = h + l, h and l
 //         fp16 (11-bit significands each, 22 bits together); the same three
 //         products at the f16 tensor rate (twice tf32), K = 16 per MMA.
-template <int A, int MODE, int KIND, int CG>   // d = 32 * A (KIND 1: A even); CG = CTAs per MMA (1 or 2)
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// NSW: X-splitter warps (2: SMSPs 2-3; 4: one per SMSP, for small K where the
+// split of each row tile is on the critical path)
+template <int A, int MODE, int KIND, int CG, int NSW>   // d = 32 * A (KIND 1: A even); CG = CTAs per MMA (1 or 2)
+__global__ void __launch_bounds__(tc_threads(NSW), 1)
 k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_chi,
             const __grid_constant__ CUtensorMap tm_clo, const __grid_constant__ CUtensorMap tm_cn, Dev d, GEval g,
             int S, int NT, int NXB, int XRr, int NST, int RES) {
@@ -397,7 +400,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     constexpr uint32_t IDESC_ = (KIND ? IDESC16 : IDESC) & ~((0x3Fu << 17) | (0x1Fu << 24));
     constexpr uint32_t IDESC_CG = IDESC_ | ((uint32_t)(AW >> 3) << 17) | ((uint32_t)((TC_BM * CG) >> 4) << 24);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-B aligned by an offset from the __shared__ array (not an integer round
+    // trip), so every pointer derived from it stays in the shared address space:
+    // LDS/STS instead of generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     // NXB == 0: in-place mode (KIND 0, no room for a staging tile): the TMA
     // target is operand buffer 0's hi half and the split runs in place.
     // DX (KIND 1): no staging tile; the splitter reads its rows straight from
@@ -413,16 +419,19 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint8_t* opb = (inplace || DX) ? smem : xst + nst * A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
     float* xnorm = reinterpret_cast<float*>(stg + (size_t)S * STAGE_BYTES);   // [XRr][128] ||x||^2 ring (slot = iteration % XRr)
-    float4* mrg = reinterpret_cast<float4*>(xnorm + XRr * TC_BM);     // [NQ-1][128] partial results of quarters 1..3
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + (NQ - 1) * TC_BM);
+    // [NMRG][NQ-1][128] partial results of quarters 1..3: double-buffered when every row
+    // tile is one accumulator tile (NT == 1), where the merge is a large share of a tile
+    const int nmrg = NT == 1 ? 2 : 1;
+    float4* mrg = reinterpret_cast<float4*>(xnorm + XRr * TC_BM);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + nmrg * (NQ - 1) * TC_BM);
     uint64_t* full = bars;                                         // [S]  stage landed (leader: both halves)
     uint64_t* empty = bars + S;                                    // [S]  stage consumed (multicast commit)
     uint64_t* accf = bars + 2 * S;                                 // [4]  accumulator ready (multicast commit)
     uint64_t* acce = accf + 4;                                     // [4]  accumulator drained (leader: all epilogues)
     uint64_t* stfull = acce + 4;                                   // [8] X staging tile landed (ring of nst)
-    uint64_t* opready = stfull + 8;                                // [2] operand buffer split (leader: both CTAs)
-    uint64_t* opempty = opready + 2;                               // [2] operand buffer consumed by the MMAs
-    uint64_t* xready = opempty + 2;                                // [XRr] ||x||^2 slot written (epilogue side)
+    uint64_t* opready = stfull + 8;                                // [4] operand buffer split (leader: both CTAs)
+    uint64_t* opempty = opready + 4;                               // [4] operand buffer consumed by the MMAs
+    uint64_t* xready = opempty + 4;                                // [XRr] ||x||^2 slot written (epilogue side)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XRr);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -438,9 +447,9 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
         for (int b = 0; b < 4; ++b) { mbar_init(accf + b, 1); mbar_init(acce + b, NQ * 4 * CG); }
-        for (int b = 0; b < 2; ++b) { mbar_init(opready + b, 2 * CG); mbar_init(opempty + b, 1); }
+        for (int b = 0; b < 4; ++b) { mbar_init(opready + b, NSW * CG); mbar_init(opempty + b, 1); }
         for (int b = 0; b < 8; ++b) mbar_init(stfull + b, 1);
-        for (int b = 0; b < XRr; ++b) mbar_init(xready + b, 2);
+        for (int b = 0; b < XRr; ++b) mbar_init(xready + b, NSW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_SPLIT) {
@@ -561,10 +570,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (++xb == nxb) xb = 0;
             }
         }
-    } else if (warp >= W_SPLIT) {                                  // ---- X splitter (warps 18, 19)
+    } else if (warp >= W_SPLIT) {                                  // ---- X splitter (warps 18 .. 18 + NSW - 1)
         // Owns the fp32 staging tile: TMA-prefetches the next row tile as soon as
         // the current one is converted, so the MMA never waits on X.
-        const int t = threadIdx.x - W_SPLIT * 32;                  // 0..63: rows t and t + 64
+        constexpr int SPT = 32 * NSW;                              // splitter threads
+        constexpr int RPT = TC_BM / SPT;                           // rows per thread: t, t + SPT, ...
+        const int t = threadIdx.x - W_SPLIT * 32;
         uint32_t eph = 0;                                          // phase bit per operand buffer
         int xb = 0;
         if (t == 0 && live(0)) {
@@ -604,39 +615,70 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             } else {
                 mbar_wait_sleep(stfull + (int)(it % nst), (uint32_t)(it / nst) & 1u, 128);
             }
+            if (warp == W_SPLIT && lane == 0) tc_stamp(d, 6, it);       // splitter: X tile landed
             const uint8_t* xs = xst + (int)(it % nst) * A * ATOM_BYTES_X;   // this tile's staging (ring of nst)
             if (!inplace) {
                 mbar_wait_sleep(opempty + xb, ((eph >> xb) & 1u) ^ 1u, 256);  // the MMAs of tile - NXB are done
                 eph ^= 1u << xb;
             }
+            if (warp == W_SPLIT && lane == 0) tc_stamp(d, 7, it);       // splitter: operand buffer free
             uint8_t* xhi = opb + xb * OPB;
             uint8_t* xlo = xhi + NATOM * ATOM_BYTES_X;
-#pragma unroll (KIND == 0 ? 2 : 1)
-            for (int rr = 0; rr < 2; ++rr) {                       // KIND 0: both rows interleaved (ILP)
-                const int r = t + 64 * rr;
-                float xn = 0.f;
-                if (KIND == 0) {
-                    // four independent ||x||^2 chains (one per float4 lane): the splitter is on
-                    // the critical path at small K, and a single 4d-long FMA chain was its latency
-                    float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+            // KIND 0: all RPT rows of this thread at once.  Per atom every load of the
+            // staging tile is issued before the first store to the operand tiles: the
+            // compiler cannot move a load past a store it cannot prove disjoint, so
+            // interleaving them would serialise the shared-memory round trips.
+            // Four independent ||x||^2 chains per row (one per float4 lane).
+            float xnk[KIND == 0 ? RPT : 1];
+            if (KIND == 0 && (d.dbg & 128)) {                          // probe: no split work (timing only)
 #pragma unroll
-                    for (int a = 0; a < A; ++a) {
+                for (int rr = 0; rr < RPT; ++rr) xnk[rr] = 0.f;
+            } else if (KIND == 0) {
+                float q[RPT][4];
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) {
+                for (int rr = 0; rr < RPT; ++rr) q[rr][0] = q[rr][1] = q[rr][2] = q[rr][3] = 0.f;
+                constexpr int CPB = 8 / RPT;                           // chunks per load batch (8 float4 in flight)
+#pragma unroll
+                for (int ab = 0; ab < A * 8; ab += CPB) {
+                    const int a = ab / 8, c0 = ab % 8;
+                    float4 v[RPT][CPB];
+#pragma unroll
+                    for (int rr = 0; rr < RPT; ++rr) {
+                        const int r = t + SPT * rr;
+#pragma unroll
+                        for (int c = 0; c < CPB; ++c)
+                            v[rr][c] = *reinterpret_cast<const float4*>(xs + a * ATOM_BYTES_X + r * 128 + (((c0 + c) ^ (r & 7)) << 4));
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < RPT; ++rr) {
+                        const int r = t + SPT * rr;
+#pragma unroll
+                        for (int cc = 0; cc < CPB; ++cc) {
+                            const int c = c0 + cc;
+                            const float4 x4 = v[rr][cc];
                             const int off = a * ATOM_BYTES_X + r * 128 + ((c ^ (r & 7)) << 4);
-                            const float4 v = *reinterpret_cast<const float4*>(xs + off);
-                            const float4 w = make_float4(v.x * inv_sx, v.y * inv_sx, v.z * inv_sx, v.w * inv_sx);   // exact
+                            const float4 w = make_float4(x4.x * inv_sx, x4.y * inv_sx, x4.z * inv_sx, x4.w * inv_sx);   // exact
                             float4 h, l;
                             h.x = __uint_as_float(__float_as_uint(w.x) & 0xFFFFE000u); l.x = w.x - h.x;
                             h.y = __uint_as_float(__float_as_uint(w.y) & 0xFFFFE000u); l.y = w.y - h.y;
                             h.z = __uint_as_float(__float_as_uint(w.z) & 0xFFFFE000u); l.z = w.z - h.z;
                             h.w = __uint_as_float(__float_as_uint(w.w) & 0xFFFFE000u); l.w = w.w - h.w;
-                            q0 = fmaf(v.x, v.x, q0); q1 = fmaf(v.y, v.y, q1); q2 = fmaf(v.z, v.z, q2); q3 = fmaf(v.w, v.w, q3);
+                            q[rr][0] = fmaf(x4.x, x4.x, q[rr][0]); q[rr][1] = fmaf(x4.y, x4.y, q[rr][1]);
+                            q[rr][2] = fmaf(x4.z, x4.z, q[rr][2]); q[rr][3] = fmaf(x4.w, x4.w, q[rr][3]);
                             *reinterpret_cast<float4*>(xhi + off) = h;
                             *reinterpret_cast<float4*>(xlo + off) = l;
                         }
                     }
-                    xn = (q0 + q1) + (q2 + q3);
+                }
+#pragma unroll
+                for (int rr = 0; rr < RPT; ++rr) xnk[rr] = (q[rr][0] + q[rr][1]) + (q[rr][2] + q[rr][3]);
+            }
+#pragma unroll (KIND == 0 ? RPT : 1)
+            for (int rr = 0; rr < RPT; ++rr) {
+                const int r = t + SPT * rr;
+                float xn = 0.f;
+                if (KIND == 0) {
+                    xn = xnk[rr];
                 } else {
                     // the row's source, resolved ONCE (through the row list for MODE 1/2): the
                     // compiler cannot hoist a load of rows_of past the shared-memory stores below
@@ -711,7 +753,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             }
             // both splitter warps are done with the staging tile: prefetch the next one
             // (in place: only once the MMAs have consumed the tile)
-            asm volatile("bar.sync 5, 64;" ::: "memory");
+            asm volatile("bar.sync 5, %0;" ::"n"(SPT) : "memory");
             if (inplace && live(it + 1)) {
                 mbar_wait(opempty, eph & 1u);
                 eph ^= 1u;
@@ -836,7 +878,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 if (cq > 0) {
                     const unsigned hi = (t.i2 >= 0 && (t.i2 >> 5) < 0xFFF) ? (unsigned)(t.i2 >> 5) : 0xFFFu;
                     const float Lp = __uint_as_float((__float_as_uint(t.L) & ~0xFFFu) | hi);
-                    mrg[(cq - 1) * TC_BM + r] = make_float4(t.b1, t.b2, __int_as_float(t.i1), Lp);
+                    mrg[((nmrg == 2 ? (int)(it & 1) : 0) * (NQ - 1) + cq - 1) * TC_BM + r] = make_float4(t.b1, t.b2, __int_as_float(t.i1), Lp);
                 }
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");
                 if (cq == 0) {
@@ -844,7 +886,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     int i1;
 #pragma unroll
                     for (int o = 0; o < NQ - 1; ++o) {
-                        const float4 m = mrg[o * TC_BM + r];
+                        const float4 m = mrg[((nmrg == 2 ? (int)(it & 1) : 0) * (NQ - 1) + o) * TC_BM + r];
                         const int oi1 = __float_as_int(m.z);
                         const unsigned hi = __float_as_uint(m.w) & 0xFFFu;
                         const int oi2 = hi == 0xFFFu ? -1 : (int)(hi << 5) + (int)(__float_as_uint(m.y) & 31u);
@@ -895,7 +937,11 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     push_flag_tc(d, g.branch, flag && !pair, row, b1, tau);
                     push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
                 }
-                asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
+                // double-buffered (NT == 1): no second barrier.  Quarters 1..3 write this
+                // slot again (tile it + 2) only after the next tile's barrier, which quarter 0
+                // reaches once it has read it here, so they start the next tile while
+                // quarter 0 merges this one
+                if (nmrg == 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
                 if (warp == 0 && lane == 0) tc_stamp(d, 5, it);    // epilogue done with the tile
             } else if (frow < n_rows) {
                 d.cand_cnt[frow * NQ + cq] = cnt;
@@ -936,8 +982,8 @@ static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2, int
     const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + AAKM_CNIMG_BYTES;
     const int xr = xr_of(NT, NXB, cg);
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
-           (size_t)xr * TC_BM * 4 + (NQ - 1) * TC_BM * 16 +
-           (size_t)(2 * S + 20 + xr) * 8 + 16;
+           (size_t)xr * TC_BM * 4 + (NT == 1 ? 2 : 1) * (NQ - 1) * TC_BM * 16 +
+           (size_t)(2 * S + 24 + xr) * 8 + 16;
 }
 
 // NT == 1 (K <= 256 with CTA pairs), KIND 0: the C operand tile never changes, so it
@@ -946,8 +992,8 @@ static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2, int
 // CTA, so the X stream keeps up with the tensor pipe (c3: 2 tiles -> ~2.4 TB/s of X).
 static bool pick_resident(int kind, int A, int NT, int& NXB, int& NST, int cg = 2) {
     if (kind != 0 || NT != 1 || env_cap("AAKM_TC_NORES", 0)) return false;
-    static const int maxst = env_cap("AAKM_TC_MAXST", 8);
-    for (NXB = 2; NXB >= 1; --NXB)
+    static const int maxst = env_cap("AAKM_TC_MAXST", 8), maxnxb = env_cap("AAKM_TC_RESNXB", 3);
+    for (NXB = maxnxb; NXB >= 1; --NXB)
         for (NST = maxst; NST >= 3; --NST)
             if (smem_need(kind, A, A, NT, NXB, cg, NST) <= (size_t)SMEM_LIMIT) return true;
     return false;
@@ -988,13 +1034,15 @@ bool tc16_supported(int d, int K) {
 // k-steps (+16 for the internal 16-term dot) at <= 2^-22 each.
 float tau_gamma_tc16(int d) { return AAKM_TAU_MARGIN * (3.0f * 2.3841858e-7f + (3.0f * d / 16.0f + 16.0f) * 2.3841858e-7f); }
 
-#define AAKM_TC_INSTANCES(X, CG)                                                                     \
-    X(1, 0, 0, CG) X(2, 0, 0, CG) X(3, 0, 0, CG) X(4, 0, 0, CG) X(1, 1, 0, CG) X(2, 1, 0, CG) X(3, 1, 0, CG) \
-    X(4, 1, 0, CG) X(2, 0, 1, CG) X(4, 0, 1, CG) X(2, 1, 1, CG) X(4, 1, 1, CG) X(2, 2, 1, CG) X(4, 2, 1, CG)
+#define AAKM_TC_INSTANCES(X, CG)                                                                      \
+    X(1, 0, 0, CG, 2) X(2, 0, 0, CG, 2) X(3, 0, 0, CG, 2) X(4, 0, 0, CG, 2) X(1, 0, 0, CG, 4)             \
+    X(2, 0, 0, CG, 4) X(3, 0, 0, CG, 4) X(4, 0, 0, CG, 4) X(1, 1, 0, CG, 2) X(2, 1, 0, CG, 2)             \
+    X(3, 1, 0, CG, 2) X(4, 1, 0, CG, 2) X(2, 0, 1, CG, 2) X(4, 0, 1, CG, 2) X(2, 1, 1, CG, 2)             \
+    X(4, 1, 1, CG, 2) X(2, 2, 1, CG, 2) X(4, 2, 1, CG, 2)
 
 cudaError_t setup_tc() {
     cudaError_t e = cudaSuccess;
-#define AAKM_FN(A_, M_, K_, C_) (const void*)k_assign_tc<A_, M_, K_, C_>,
+#define AAKM_FN(A_, M_, K_, C_, W_) (const void*)k_assign_tc<A_, M_, K_, C_, W_>,
     const void* fns[] = {AAKM_TC_INSTANCES(AAKM_FN, 1) AAKM_TC_INSTANCES(AAKM_FN, 2)};
 #undef AAKM_FN
     for (auto f : fns) {
@@ -1087,11 +1135,11 @@ static int tc_cg() {
     return cg;
 }
 
-template <int A, int MODE, int KIND, int CG>
+template <int A, int MODE, int KIND, int CG, int NSW>
 static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, const GEval& g, int S, int NT, int NXB,
                        int XRr, long long n_tiles, size_t smem, cudaStream_t s, int NST, int RES) {
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(TC_THREADS);
+    cfg.blockDim = dim3(tc_threads(NSW));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -1102,11 +1150,11 @@ static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, con
         cfg.attrs = at; cfg.numAttrs = 1;
         // pairs that can be co-resident (a persistent grid must not wait on itself)
         // per device and shared-memory class (written once per value: a benign race)
-        static int max_clusters[AAKM_MAX_DEVICES][2] = {};
-        int& mc = max_clusters[d.dev & (AAKM_MAX_DEVICES - 1)][smem > 200 * 1024 ? 1 : 0];
+        static int max_clusters[AAKM_MAX_DEVICES][4] = {};
+        int& mc = max_clusters[d.dev & (AAKM_MAX_DEVICES - 1)][(smem > 200 * 1024 ? 1 : 0) + (NSW == 4 ? 2 : 0)];
         if (mc == 0) {
             cfg.gridDim = dim3(d.num_sms & ~1);
-            if (cudaOccupancyMaxActiveClusters(&mc, (const void*)k_assign_tc<A, MODE, KIND, CG>, &cfg) != cudaSuccess || mc < 1)
+            if (cudaOccupancyMaxActiveClusters(&mc, (const void*)k_assign_tc<A, MODE, KIND, CG, NSW>, &cfg) != cudaSuccess || mc < 1)
                 mc = d.num_sms / 2;
             cudaGetLastError();
         }
@@ -1116,7 +1164,27 @@ static void launch_one(const TcMaps* m, const CUtensorMap& xm, const Dev& d, con
     if (CG == 2) grid = (grid + 1) & ~1;
     if (grid < CG) grid = CG;
     cfg.gridDim = dim3(grid);
-    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB, XRr, NST, RES);
+    cudaLaunchKernelEx(&cfg, k_assign_tc<A, MODE, KIND, CG, NSW>, xm, m->chi, m->clo, m->cn, d, g, S, NT, NXB, XRr, NST, RES);
+}
+
+// 3xTF32 dense pass with one centroid tile per row tile (NT == 1, K <= 256):
+// AAKM_TC_NSW=4 runs four splitter warps (one per SMSP) instead of two.  An
+// experiment: at 704 threads the kernel gets 80 registers and the CTA-pair
+// epilogue spills (c3 0.145 -> 0.174 ms), so two stay the default.
+static int tc_nsw() {
+    static const int v = getenv("AAKM_TC_NSW") ? atoi(getenv("AAKM_TC_NSW")) : 2;
+    return v == 4 ? 4 : 2;
+}
+template <int A, int MODE, int CG>
+static void launch_k0(const TcMaps* m, const CUtensorMap& xm, const Dev& d, const GEval& g, int S, int NT, int NXB,
+                      int XRr, long long n_tiles, size_t smem, cudaStream_t s, int NST, int RES) {
+    if constexpr (MODE == 0) {
+        if (NT == 1 && tc_nsw() == 4) {
+            launch_one<A, MODE, 0, CG, 4>(m, xm, d, g, S, NT, NXB, XRr, n_tiles, smem, s, NST, RES);
+            return;
+        }
+    }
+    launch_one<A, MODE, 0, CG, 2>(m, xm, d, g, S, NT, NXB, XRr, n_tiles, smem, s, NST, RES);
 }
 
 template <int MODE, int KIND, int CG>
@@ -1134,14 +1202,14 @@ static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStre
     if (MODE == 0 && g.tile1 > 0) n_tiles = min(n_tiles, g.tile1) - g.tile0;
     if constexpr (KIND == 0) {
         switch (A) {
-            case 1: launch_one<1, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
-            case 2: launch_one<2, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
-            case 3: launch_one<3, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
-            default: launch_one<4, MODE, 0, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            case 1: launch_k0<1, MODE, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            case 2: launch_k0<2, MODE, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            case 3: launch_k0<3, MODE, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
+            default: launch_k0<4, MODE, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
         }
     } else {
-        if (A == 2) launch_one<2, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
-        else launch_one<4, MODE, 1, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
+        if (A == 2) launch_one<2, MODE, 1, CG, 2>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
+        else launch_one<4, MODE, 1, CG, 2>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
     }
 }
 

@@ -1414,7 +1414,7 @@ kmeans_status kmeans_destroy(kmeans_handle* h) {
             for (int b = 0; b < 2; ++b)
                 for (int it = 0; it < 256; ++it) {
                     fprintf(f, "%d %d", b, it);
-                    for (int e = 0; e < 6; ++e) fprintf(f, " %llu", ts[(b * 8 + e) * 256 + it]);
+                    for (int e = 0; e < 8; ++e) fprintf(f, " %llu", ts[(b * 8 + e) * 256 + it]);
                     fprintf(f, "\n");
                 }
             fclose(f);

@@ -311,16 +311,32 @@ __global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
     if (threadIdx.x == 0) { d.seg_off[K] = (int)carry[0]; d.seg_chunk[K] = (int)carry[1]; }
 }
 
-// Exclusive scan of v[0..n) in place by one 1024-thread block (n <= 16 * 1024);
-// returns the total to every thread.
-__device__ int block_exscan(int* v, int n) {
-    __shared__ int ws[32];
-    const int per = (n + blockDim.x - 1) / blockDim.x;
-    const int a = threadIdx.x * per, b = min(n, a + per);
-    int s = 0;
-    for (int i = a; i < b; ++i) s += v[i];
+// Rows bucketed by label: block b re-walks its row range (the same ranges as
+// k_hist) in sub-tiles of T rows.  A sub-tile is counting-sorted by label in
+// shared memory first, then written out in sorted order, so consecutive threads
+// store consecutive perm entries of one cluster's run (whole sectors) instead
+// of one scattered 4-byte store per row.  Within a cluster the order of rows
+// is arbitrary (smem atomics); every sum downstream is order-free.
+// Per sub-tile: [ranks: smem atomics] sync [bin scan] sync [stage] sync
+// [output + zero the counters + the next sub-tile's label loads] sync.  A row
+// travels as one packed word (label << 14 | rank or local row), T <= 2^14.
+constexpr int SCAT_BT = 1024;         // threads per block
+constexpr int SCAT_RPT = 16;          // rows per thread per sub-tile (T <= SCAT_RPT * SCAT_BT)
+constexpr int SCAT_LB = 14;           // local row / rank bits
+static_assert(SCAT_RPT * SCAT_BT <= (1 << SCAT_LB) && AAKM_SORTED_MAX_K <= (1 << (31 - SCAT_LB)), "packed rows");
+
+// cnt[i] (counts) -> exclusive offsets over i < K; base[i] = gcur[i] - offset
+// (perm slot of sorted entry q of cluster i is base[i] + q); gcur[i] += count.
+// Thread t owns the contiguous bins [t per, (t + 1) per).  Returns the total.
+__device__ __forceinline__ int scat_scan(int* cnt, int* gcur, int* base, int K) {
+    __shared__ int ws[SCAT_BT / 32];
+    const int per = (K + SCAT_BT - 1) / SCAT_BT;            // <= 16
+    const int a = threadIdx.x * per, b = min(K, a + per);
+    int sum = 0;
+    for (int i = a; i < b; ++i) sum += cnt[i];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int inc = s;
+    int inc = sum;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += t;
@@ -328,7 +344,8 @@ __device__ int block_exscan(int* v, int n) {
     if (lane == 31) ws[w] = inc;
     __syncthreads();
     if (w == 0) {
-        int x = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+        int x = ws[lane];
+#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += t;
@@ -336,32 +353,31 @@ __device__ int block_exscan(int* v, int n) {
         ws[lane] = x;
     }
     __syncthreads();
-    int run = inc - s + (w ? ws[w - 1] : 0);
-    const int tot = ws[(blockDim.x >> 5) - 1];
-    for (int i = a; i < b; ++i) { const int t = v[i]; v[i] = run; run += t; }
-    __syncthreads();
+    int run = inc - sum + (w ? ws[w - 1] : 0);
+    const int tot = ws[SCAT_BT / 32 - 1];
+    for (int i = a; i < b; ++i) {
+        const int c = cnt[i], gc = gcur[i];
+        cnt[i] = run;
+        base[i] = gc - run;
+        gcur[i] = gc + c;
+        run += c;
+    }
     return tot;
 }
 
-// Rows bucketed by label: block b re-walks its row range (the same ranges as
-// k_hist) in sub-tiles of T rows.  A sub-tile is counting-sorted by label in
-// shared memory first, then written out in sorted order, so consecutive threads
-// store consecutive perm entries of one cluster's run (whole sectors) instead
-// of one scattered 4-byte store per row.  Within a cluster the order of rows
-// is arbitrary (smem atomics); every sum downstream is order-free.
-constexpr int SCAT_RPT = 16;          // rows per thread per sub-tile (T <= 16 * blockDim)
-__global__ void __launch_bounds__(1024, 1) k_scatter(Dev d, GEval g, int T) {
+__global__ void __launch_bounds__(SCAT_BT, 1) k_scatter(Dev d, GEval g, int T) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
-    extern __shared__ __align__(16) unsigned char scat_sm[];
+    extern __shared__ __align__(16) int scat_sm[];
     const int K = d.K;
-    int* gcur = reinterpret_cast<int*>(scat_sm);   // K: next global perm slot of each cluster for this block
-    int* loff = gcur + K;           // K + 1: sub-tile counts -> exclusive offsets -> output bases
-    int2* stage = reinterpret_cast<int2*>(loff + K + 1 + 1);   // T: {row, label} sorted by label (8-B aligned)
+    int* cnt = scat_sm;             // K: sub-tile counts -> exclusive offsets
+    int* gcur = cnt + K;            // K: next global perm slot of each cluster for this block
+    int* base = gcur + K;           // K: output base of the sub-tile's sorted entries
+    int* stage = base + K;          // T: packed {label, local row}, sorted by label
     // chunk table {j, first sorted row, rows}: chunk w belongs to the last cluster
     // whose first chunk is <= w (binary search; empty clusters share starts)
     const long long nch = d.seg_chunk[K];
-    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < nch; w += (long long)gridDim.x * blockDim.x) {
+    for (long long w = (long long)blockIdx.x * SCAT_BT + threadIdx.x; w < nch; w += (long long)gridDim.x * SCAT_BT) {
         int lo = 0, hi = K - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -371,76 +387,63 @@ __global__ void __launch_bounds__(1024, 1) k_scatter(Dev d, GEval g, int T) {
         d.seg_cmap[w] = make_int4(lo, (int)r0, (int)min((long long)SEG_ROWS, (long long)d.seg_off[lo + 1] - r0), 0);
     }
     const int* bh = d.seg_bh + (long long)blockIdx.x * K;
-    for (int j = threadIdx.x; j < K; j += blockDim.x) gcur[j] = bh[j] + d.seg_off[j];
+    for (int j = threadIdx.x; j < K; j += SCAT_BT) { gcur[j] = bh[j] + d.seg_off[j]; cnt[j] = 0; }
     long long r0, r1;
     block_rows(d, r0, r1);
-    for (long long t0 = r0; t0 < r1; t0 += T) {
+    int pk[SCAT_RPT];
+    auto load = [&](long long t0) {
         const int nt = (int)min((long long)T, r1 - t0);
-        for (int j = threadIdx.x; j <= K; j += blockDim.x) loff[j] = 0;
-        __syncthreads();
-        int jr[SCAT_RPT], rk[SCAT_RPT];
 #pragma unroll
         for (int u = 0; u < SCAT_RPT; ++u) {
-            const int q = u * (int)blockDim.x + threadIdx.x;
-            jr[u] = q < nt ? p.lab[t0 + q] : -1;
+            const int q = u * SCAT_BT + threadIdx.x;
+            pk[u] = q < nt ? __ldcs(p.lab + t0 + q) : -1;
         }
+    };
+    if (r0 < r1) load(r0);
+    __syncthreads();
+    for (long long t0 = r0; t0 < r1; t0 += T) {
 #pragma unroll
         for (int u = 0; u < SCAT_RPT; ++u) {
-            if (jr[u] >= 0 && jr[u] < K) rk[u] = atomicAdd(&loff[jr[u]], 1);
-            else jr[u] = -1;
+            const int j = pk[u];
+            pk[u] = (unsigned)j < (unsigned)K ? (j << SCAT_LB) | atomicAdd(&cnt[j], 1) : -1;
         }
         __syncthreads();
-        const int nv = block_exscan(loff, K);
-#pragma unroll
-        for (int u = 0; u < SCAT_RPT; ++u)
-            if (jr[u] >= 0) stage[loff[jr[u]] + rk[u]] = make_int2((int)(t0 + u * (int)blockDim.x + threadIdx.x), jr[u]);
+        const int nv = scat_scan(cnt, gcur, base, K);
         __syncthreads();
-        // loff[j] -> output base gcur[j] - loff[j] (consecutive sorted entries of a cluster
-        // map to consecutive perm slots); gcur advances by the sub-tile's counts
-        {
-            int cb[AAKM_SORTED_MAX_K / 1024], bb[AAKM_SORTED_MAX_K / 1024];   // K <= 16 per thread (1024 threads)
 #pragma unroll
-            for (int u = 0; u < AAKM_SORTED_MAX_K / 1024; ++u) {
-                const int j = threadIdx.x + u * (int)blockDim.x;
-                if (j < K) {
-                    const int o = loff[j];
-                    cb[u] = (j + 1 < K ? loff[j + 1] : nv) - o;
-                    bb[u] = gcur[j] - o;
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int u = 0; u < AAKM_SORTED_MAX_K / 1024; ++u) {
-                const int j = threadIdx.x + u * (int)blockDim.x;
-                if (j < K) { loff[j] = bb[u]; gcur[j] += cb[u]; }
+        for (int u = 0; u < SCAT_RPT; ++u) {
+            if (pk[u] >= 0) {
+                const int j = pk[u] >> SCAT_LB;
+                stage[cnt[j] + (pk[u] & ((1 << SCAT_LB) - 1))] = (j << SCAT_LB) | (u * SCAT_BT + (int)threadIdx.x);
             }
         }
         __syncthreads();
+        if (t0 + T < r1) load(t0 + T);                       // next sub-tile's labels in flight under the output
+        for (int j = threadIdx.x; j < K; j += SCAT_BT) cnt[j] = 0;
         int q = threadIdx.x;
-        for (; q + 3 * (int)blockDim.x < nv; q += 4 * blockDim.x) {
-            int2 e[4];
+        for (; q + 3 * SCAT_BT < nv; q += 4 * SCAT_BT) {
+            int e[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) e[u] = stage[q + u * blockDim.x];
+            for (int u = 0; u < 4; ++u) e[u] = stage[q + u * SCAT_BT];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) d.perm[loff[e[u].y] + q + u * (int)blockDim.x] = e[u].x;
+            for (int u = 0; u < 4; ++u)
+                d.perm[base[e[u] >> SCAT_LB] + q + u * SCAT_BT] = (int)t0 + (e[u] & ((1 << SCAT_LB) - 1));
         }
-        for (; q < nv; q += blockDim.x) {
-            const int2 e = stage[q];
-            d.perm[loff[e.y] + q] = e.x;
+        for (; q < nv; q += SCAT_BT) {
+            const int e = stage[q];
+            d.perm[base[e >> SCAT_LB] + q] = (int)t0 + (e & ((1 << SCAT_LB) - 1));
         }
         __syncthreads();
     }
 }
 
-static_assert(sizeof(int2) == 8, "stage entry");
 constexpr int SCAT_SMEM = 220 * 1024;   // dynamic shared memory of k_scatter (+ its static scan buffer)
 // sub-tile rows: a multiple of the block size, <= SCAT_RPT rows per thread, inside
-// this block's share of the SM's shared memory
-static int scatter_tile(int K, int bt, int per_sm) {
-    const int budget = (per_sm == 2 ? 110 * 1024 : SCAT_SMEM) - 8 * (K + 1);
-    int T = budget / 8;
-    T = T / bt * bt;
-    return T > SCAT_RPT * bt ? SCAT_RPT * bt : T;
+// the shared memory left after the three K-sized arrays
+static int scatter_tile(int K) {
+    int T = (SCAT_SMEM - 12 * K) / 4;
+    T = T / SCAT_BT * SCAT_BT;
+    return T > SCAT_RPT * SCAT_BT ? SCAT_RPT * SCAT_BT : T;
 }
 
 template <int V>   // floats per lane: d <= 32 * V
@@ -676,6 +679,16 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         const double2 c23 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i + 16);
         const double cx = c01.x, cy = c01.y, cz = c23.x, cw = c23.y;
         if (d.dbg & 8) {                                               // AAKM_TC_DBG=8 probe: data movement only
+        } else if (d.dbg & 64) {                                       // AAKM_TC_DBG=64 probe: sums only, no energy
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+                const int rr = i * RPW + h;
+                const unsigned char* a = SB::GP == 4 * RB ? slot + rr * RB + 16 * c4i
+                                                          : slot + (rr >> 2) * SB::GP + (rr & 3) * RB + 16 * c4i;
+                const float4 xv = *reinterpret_cast<const float4*>(a);
+                fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
+                fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
+            }
         } else if (RPW <= SR && r.y == SR) {                           // full item (warp-uniform): no masks
 #pragma unroll
             for (int i = 0; i < IT; ++i) {
@@ -773,14 +786,14 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
         return 1;
     }
     const size_t hs = (size_t)d.K * 4;
-    const int bt = 1024;                                       // k_scatter assumes 1024 threads (K <= 16 per thread)
+    const int bt = 1024;
     k_hist<<<d.seg_blocks, bt, hs, s>>>(d, g);
     static_assert(AAKM_SEG_BLOCKS_MAX <= 512, "k_scan_a: <= 16 row blocks per lane");
     k_scan_a<<<(d.K + 7) / 8, 256, 0, s>>>(d, g, d.seg_blocks);
     k_scan_b<<<1, 1024, 0, s>>>(d, g);
     {
-        const int T = scatter_tile(d.K, bt, d.seg_blocks > d.num_sms ? 2 : 1);
-        k_scatter<<<d.seg_blocks, bt, (size_t)(2 * d.K + 2) * 4 + (size_t)T * 8, s>>>(d, g, T);
+        const int T = scatter_tile(d.K);
+        k_scatter<<<d.seg_blocks, SCAT_BT, (size_t)(3 * d.K + T) * 4, s>>>(d, g, T);
     }
     if (d.xg_map) {
         switch (d.d / 4) {
