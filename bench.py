@@ -381,7 +381,7 @@ def main():
         line["update_roofline"] = {"bound": "hbm", "achieved": ubytes / (u_avg / 1e3) / 1e9,
                                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                    "frac": ubytes / (u_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
-                                   "kernel": "update (label sort + segmented sums + fp64 energy)",
+                                   "kernel": "update (label sort + segmented sums; E from the sums by k_energy_x)",
                                    "avg_ms": u_avg, "launches": u_n}
     km.close()
     if args.ttc_config != "none":

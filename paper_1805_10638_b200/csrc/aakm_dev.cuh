@@ -97,10 +97,12 @@ struct Dev {
     int* pair_rows;       // near-tie rows whose window holds exactly two centroids (capacity fcap)
     int2* pair_j;         //   their two centroids (best key, runner-up)
     long long* pair_count;//   [2] counts, branch A / B (zeroed per pass with the flags)
-    long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E_hi | E_lo | E (fp64 bits) | changed]
+    long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E_hi | E_lo | E (fp64 bits) | changed | X2_hi | X2_lo]
     float fx_scale;       // 2^(22-e), |x| <= 2^e over all ranks: S in exact fixed point (update.cu)
     double fx_inv;        // 2^(e-22)
     double xn_gmax;       // max_i ||x_i|| over all ranks (rounded up): bounds every ||x_i - c||
+    long long* x2;        // sorted engine: this rank's sum_i ||x_i||^2 in units of 2^x2_e (two parts, as
+    int x2_e;             //   energy_flush), refreshed with X; x2_e = frexp exponent of 2 xn_gmax^2 - 51
     double* upd_part;     // per-block (E, changed) partials
     int* seg_bh;          // sorted update engine: per-block histograms -> scatter bases (SEG_BLOCKS x K)
     int* seg_off;         // row offsets of cluster j in perm (K+1)
@@ -211,8 +213,12 @@ void launch_reset(const Dev& d, cudaStream_t s);
 void launch_update_G(const Dev& d, const long long* packed, const double* Cprev, double* G,
                      long long* counts, cudaStream_t s);
 void launch_energy(const Dev& d, const GEval& g, cudaStream_t s);       // E after the allreduce
+// sorted engine: E's parts from the (reduced or local) packed S, N, X2 and C (update.cu)
+int launch_energy_x(const Dev& d, const GEval& g, cudaStream_t s);
 void launch_partials_out(const Dev& d, const long long* packed, double* out, cudaStream_t s);
 void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
+// sum_i ||x_i||^2 of the shard (count = n d floats) in units of 2^x2_e, two parts into out[2] (zeroed)
+void launch_x2(const float* X, long long count, int x2_e, long long* out, cudaStream_t s);
 // f4 fused combine (comm.cu); comm is an ncclComm_t; setup returns an error message or nullptr
 const char* fused_setup(void** handle, void* comm, Dev& d, void* scratch, cudaStream_t s);
 void fused_free(void* handle, void* comm);
@@ -232,7 +238,8 @@ __host__ __device__ inline long long pk_n(const Dev& d) { return 2LL * d.K * d.d
 __host__ __device__ inline long long pk_ehi(const Dev& d) { return 2LL * d.K * d.d + d.K; }   // E_hi, E_lo
 __host__ __device__ inline long long pk_e(const Dev& d) { return pk_ehi(d) + 2; }             // E (fp64 bits)
 __host__ __device__ inline long long pk_ch(const Dev& d) { return pk_ehi(d) + 3; }            // changed
-__host__ __device__ inline long long pk_words(const Dev& d) { return pk_ehi(d) + 4; }
+__host__ __device__ inline long long pk_x2(const Dev& d) { return pk_ehi(d) + 4; }            // X2_hi, X2_lo
+__host__ __device__ inline long long pk_words(const Dev& d) { return pk_ehi(d) + 6; }
 // Energies e_i = ||x_i - c_rho_i||^2 go into the packed vector as a two-part fixed
 // point [E_hi (units 1/q) | E_lo (units 2^-30/q)]. q = 2^(21 - eb) with
 // 2^eb > B = 2 (max||x|| + max||c||)^2 >= every e_i, so any partial e of one row

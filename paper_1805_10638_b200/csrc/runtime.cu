@@ -167,7 +167,7 @@ struct Layout {
     size_t st, st_api, C, C32, Ca32, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, total,
+        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, total,
         scratch_bytes;
     std::vector<size_t> guards;   // AAKM_WS_CANARY=1: a 256-B canary after every region
 };
@@ -216,7 +216,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.cand_cnt = take((size_t)fc * 16 + 16);
     L.pair_rows = take((size_t)fc * 4 + 4);
     L.pair_j = take((size_t)fc * 8 + 8);
-    const size_t pk = (2 * KD + K + 4) * 8;     // [S_hi | S_lo | N | E_hi | E_lo | E | changed], int64 words (pk_words)
+    const size_t pk = (2 * KD + K + 6) * 8;     // [S_hi | S_lo | N | E_hi | E_lo | E | changed | X2_hi | X2_lo] (pk_words)
     L.scratch = o;                         // one block, zeroed every pass: no canaries inside
     o = al(o + 256);                       // flag counts
     o = al(o + pk);                        // packed[0]
@@ -248,6 +248,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.ub0 = take(nb * 4 + 4); L.lb0 = take(nb * 4 + 4); L.pj20 = take(nb * 4 + 4);
     L.C_ref0 = take(bounded ? KD * 8 : 8);
     L.xchk = take(16);
+    L.x2 = take(16);
     L.total = o;
     return L;
 }
@@ -369,6 +370,8 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         uevp = &h->uev[h->uev_used++];
         CK(h, cudaEventRecord(uevp->first, s));
     }
+    if (branch == 0 && h->feed_chunks > 0)                 // streamed X: the update reads every row and X2
+        CK(h, cudaStreamWaitEvent(s, h->feed_all, 0));
     if (d.fused) h->launches += launch_fused_zero(d, g, h->fused, s);      // f4: zero + "zeroed" barrier
     h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
     if (uevp) CK(h, cudaEventRecord(uevp->second, s));
@@ -380,6 +383,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         if (st != KMEANS_OK) return st;
     }
     if (h->comm) dbg("combine", s);
+    h->launches += launch_energy_x(d, g, s);        // sorted engine: E's parts from X2, N, S, C
     launch_control(d, branch, s);                   // E from the reduced parts + Algorithm 1 control
     dbg("control", s);
     h->launches += 1;
@@ -812,11 +816,23 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         int ex = 0;
         if (mf[0] > 0.f) frexpf(mf[0], &ex);                           // max |x| < 2^ex
         const bool srt = update_sorted(n_global, d, k);
+        // sorted engine energy (k_energy_x): sum_i ||x_i||^2 in units 2^x2_e, the finest
+        // grid any pass's energy_q can ask for (B >= 2 xn_gmax^2, the cm = 0 case)
+        const double xg = sqrt((double)mf[1]) * (1.0 + 1e-6);
+        const double B0 = 2.0 * (xg + 0.0) * (xg + 0.0);
+        int eb0 = 0;
+        frexp(B0 > 0.0 ? B0 : 1.0, &eb0);
         for (Dev* dv : {&h->d, &h->da}) {
             dv->fx_scale = ldexpf(1.0f, 22 - ex);
             dv->fx_inv = ldexp(1.0, ex - 22);
-            dv->xn_gmax = sqrt((double)mf[1]) * (1.0 + 1e-6);          // max_i ||x_i||, rounded up
+            dv->xn_gmax = xg;                                          // max_i ||x_i||, rounded up
             dv->upd_sorted = srt ? 1 : 0;
+            dv->x2_e = eb0 - 51;
+            dv->x2 = srt ? (long long*)(w + L.x2) : nullptr;
+        }
+        if (srt) {
+            CKC(cudaMemsetAsync(w + L.x2, 0, 16, h->stream));
+            launch_x2(X, n_local * d, eb0 - 51, (long long*)(w + L.x2), h->stream);
         }
         h->x_gamax = mf[0];
         if (cfg->fused_comm) {                                         // f4: packed vectors in a symmetric window
@@ -853,6 +869,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const double* C, const int32_t* la
     h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
     st = allreduce(h, d.packed[0], s);
     if (st != KMEANS_OK) return st;
+    h->launches += launch_energy_x(d, g, s);
     launch_energy(d, g, s);
     h->launches += 1;
     CK(h, cudaMemcpyAsync(h->scal_host, d.packed[0] + pk_e(d), 16, cudaMemcpyDeviceToHost, s));   // E, changed
@@ -979,6 +996,7 @@ kmeans_status kmeans_update_partials(kmeans_handle* h, const int32_t* labels, co
     g.prev_mode = labels_prev ? 2 : 1; g.lab_prev = labels_prev;
     combine(h, d, 2, C, s);                               // max ||c||^2 of C (the energy scale)
     h->launches += launch_update(d, g, s);
+    h->launches += launch_energy_x(d, g, s);                          // E_local from this rank's sums
     launch_partials_out(d, d.packed[0], packed_out, s);               // unreduced, as doubles
     h->launches += 1;
     SYNC(h, s);
@@ -1068,6 +1086,11 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
     launch_xstats_max(d.X, d.n, d.d, h->xchk, h->copy_stream);
     launch_xcheck(d, h->xchk, h->x_stat[0], h->x_stat[1], h->copy_stream);
     h->launches += 2;
+    if (d.x2) {                                                        // the new rows' sum ||x_i||^2 (k_energy_x)
+        CK(h, cudaMemsetAsync(d.x2, 0, 16, h->copy_stream));
+        launch_x2(d.X, d.n * d.d, d.x2_e, d.x2, h->copy_stream);
+        h->launches += 1;
+    }
     CK(h, cudaEventRecord(h->feed_all, h->copy_stream));
     if (d.ub) CK(h, cudaMemsetAsync(&d.st->bnd_ready, 0, sizeof(int), s));   // new rows: no valid bounds
     const bool streamed = nc > 0 && !d.ub && (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16);

@@ -11,8 +11,13 @@
 //          any number of ranks
 //   N_j  = #{i : rho_i = j}
 //   E    = sum_i ||x_i - c_{rho_i}||^2  (Eq. 1 with the given P):
-//          each row by direct differences in fp64 (fixed order), then the same
-//          kind of two-part fixed point (energy_q): exact zeros stay zero
+//          atomic engine (small n): each row by direct differences in fp64 (fixed
+//          order), then the same kind of two-part fixed point (energy_q);
+//          label-sorted engine: the same quantity through the identity
+//          E = sum_i ||x_i||^2 + sum_j (N_j ||c_j||^2 - 2 c_j . S_j)  (DESIGN R-A30),
+//          sum_i ||x_i||^2 once per X (k_xstats_max4, fixed point) and the cluster
+//          terms from the exact S_j, N_j after the combine (k_energy_x): no fp64
+//          work per coordinate in the pass over X
 //   changed = #{i : rho_i != rho_i^{prev}}
 // X is read once.
 #include "aakm_dev.cuh"
@@ -135,15 +140,17 @@ __global__ void __launch_bounds__(256) k_update(Dev d, GEval g) {
 // label, then a warp sums a chunk of <= SEG_ROWS rows of one cluster in int32
 // fixed-point registers (exact, see fx_add) and issues one int64 atomic per
 // coordinate and part per chunk instead of per row.  X is read exactly once;
-// the energy parts use the chunk's centroid.
-//   k_hist         N_j (block histograms in smem) + #changed + label check
+// E comes from the sums afterwards (k_energy_x).
+//   k_hist         N_j (block histograms in smem) + #changed + label check (+ this
+//                  rank's sum ||x_i||^2 into the packed vector, block 0)
 //   k_scan_a       per cluster: N_j -> packed, per-(block, cluster) offsets
 //   k_scan_b       exclusive scans over clusters (row offsets, chunk counts)
 //   k_scatter      chunk table {j, first row, rows} + perm[offset_j + rank] = row, written
 //                  from per-block counting-sorted sub-tiles (coalesced runs)
 //   k_segsum_bulk  d = 4 LPR: rows gathered by TMA tile::gather4 into per-warp
-//                  mbarrier rings; S_j += chunk rows, E += per-lane parts
+//                  mbarrier rings; S_j += chunk rows
 //   k_segsum       other d: lanes over coordinates, the same sums
+//   k_energy_x     (after the combine) E from X2, N, S and C
 
 constexpr int SEG_ROWS = 256;
 
@@ -227,6 +234,10 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
         atomicAdd(&hs[j], 1);
     }
     if (bad) d.st->label_error = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && d.x2) {               // this rank's sum ||x_i||^2 (k_energy_x)
+        pk_add(d, p, pk_x2(d), d.x2[0]);
+        pk_add(d, p, pk_x2(d) + 1, d.x2[1]);
+    }
     __syncthreads();
     int* bh = d.seg_bh + (long long)blockIdx.x * K;
     for (int j = threadIdx.x; j < K; j += blockDim.x) bh[j] = hs[j];
@@ -455,8 +466,6 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     const int lane = threadIdx.x & 31;
     const long long nchunks = d.seg_chunk[K];
     const float sc = d.fx_scale;
-    const double q = energy_q(d);
-    long long ehi = 0, elo = 0, ea = 0;
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nchunks;
          w += (long long)gridDim.x * (blockDim.x >> 5)) {
         const int4 ci = d.seg_cmap[w];
@@ -471,24 +480,17 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             rid[u] = qi < cnt ? d.perm[r0 + qi] : -1;
         }
         int hi[V], lo[V];                         // <= 256 rows per chunk: int32 cannot overflow
-        double cj[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            hi[v] = 0; lo[v] = 0;
-            const int k = lane + 32 * v;
-            cj[v] = k < D ? __ldg(p.C + (long long)j * D + k) : 0.0;
-        }
+        for (int v = 0; v < V; ++v) { hi[v] = 0; lo[v] = 0; }
 #pragma unroll
         for (int u = 0; u < SEG_ROWS / 32; ++u) {
             if (u * 32 < cnt) {                   // predicate, not break: keeps rid[] in registers
             float xv[8][V];
-            bool ok[8];
 #pragma unroll
             for (int b8 = 0; b8 < 32; b8 += 8) {
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int row = __shfl_sync(0xffffffffu, rid[u], b8 + t);
-                    ok[t] = row >= 0;
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
                         const int k = lane + 32 * v;
@@ -496,20 +498,12 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
                     }
                 }
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    double e = 0.0;
+                for (int t = 0; t < 8; ++t)
 #pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        fx_add(xv[t][v], sc, hi[v], lo[v]);   // zeros add nothing
-                        const int k = lane + 32 * v;
-                        if (k < D) { const double df = (double)xv[t][v] - cj[v]; e = fma(df, df, e); }
-                    }
-                    if (ok[t]) ea += energy_fx(e * q);   // this lane's part of e_row
-                }
+                    for (int v = 0; v < V; ++v) fx_add(xv[t][v], sc, hi[v], lo[v]);   // zeros add nothing
             }
             }
         }
-        energy_flush(ea, ehi, elo);              // <= 256 rows per chunk
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int k = lane + 32 * v;
@@ -519,11 +513,6 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
             }
         }
     }
-    for (int o = 16; o; o >>= 1) {
-        ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
-        elo += __shfl_xor_sync(0xffffffffu, elo, o);
-    }
-    if (lane == 0 && (ehi | elo)) { pk_add(d, p, pk_ehi(d), ehi); pk_add(d, p, pk_ehi(d) + 1, elo); }
 }
 
 // ------------------------------------------------------------------
@@ -531,15 +520,13 @@ __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
 // engine's production kernel for d = 4 LPR, LPR a power of two <= 32).
 // Each warp walks its chunks (<= SEG_ROWS rows of one cluster j) as items of
 // <= SR rows (32, or 16 for d = 128). Producer side: lanes 0..SR/4-1 each start one TMA tile::gather4
-// (4 rows by index from the X map) and lane 31 a cp.async.bulk of the centroid
-// row c_j into a slot of the warp's NS-deep shared-memory ring, all
-// completing on the slot's mbarrier; the item's {j, rows, last} go to the
-// slot's record. Row ids
+// (4 rows by index from the X map)
+// into a slot of the warp's NS-deep shared-memory ring, completing on the
+// slot's mbarrier; the item's {j, rows, last} go to the slot's record. Row ids
 // are loaded two items ahead and chunk records one chunk ahead, so no global
 // load sits on the consumer's path. Consumer side: LPR lanes per row (float4
 // each), RPW = 32 / LPR rows per shared-memory instruction. The sums are the
-// same exact fixed point as the other engines; the energy parts are this
-// lane's 4 coordinates by direct fp64 differences (energy_fx).
+// same exact fixed point as the other engines.
 #ifndef AAKM_SEG_WMAX
 #define AAKM_SEG_WMAX 16
 #endif
@@ -552,8 +539,7 @@ template <int LPR> struct SegBulk {
     static constexpr int RB = 16 * LPR;                               // row bytes
     static constexpr int SR = 16;                                      // rows per item
     static constexpr int GP = 4 * RB > 128 ? 4 * RB : 128;            // gather4 group pitch (TMA dst: 128 B aligned)
-    static constexpr int CO = SR / 4 * GP;                         // c_j row offset
-    static constexpr int SLOT = (CO + 2 * RB + 127) / 128 * 128;       // rows + c_j (fp64: 2 RB bytes)
+    static constexpr int SLOT = (SR / 4 * GP + 127) / 128 * 128;       // the item's rows
     static constexpr int WARP = (NS * SLOT + NS * 16 + NS * 8 + 127) / 128 * 128;
     static constexpr int WPB = SEG_SMEM / WARP > AAKM_SEG_WMAX ? AAKM_SEG_WMAX : SEG_SMEM / WARP;
     static constexpr int SMEM = WPB * WARP;
@@ -615,7 +601,6 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
     __syncwarp();
     const long long nchunks = d.seg_chunk[K];
     const long long TW = (long long)gridDim.x * SB::WPB;
-    const char* Cb = reinterpret_cast<const char*>(p.C);
     const int4 none = make_int4(0, 0, 0, 0);
 
     // item generator ("ahead" cursor): chunk aw, its record and the next one's
@@ -650,10 +635,9 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         uint64_t* b = bar + ps;
         unsigned char* slot = ring + ps * SB::SLOT;
         const int ng = (qa.nr + 3) >> 2;                               // gather4 instructions
-        if (lane == 0) { rec[ps] = make_int4(qa.j, qa.nr, qa.last, 0); sb_expect(b, (unsigned)((4 * ng + 2) * RB)); }
+        if (lane == 0) { rec[ps] = make_int4(qa.j, qa.nr, qa.last, 0); sb_expect(b, (unsigned)(4 * ng * RB)); }
         __syncwarp();
         if (lane < ng) sb_gather4(slot + lane * SB::GP, d.xg_map, qa.i0, qa.i1, qa.i2, qa.i3, b);
-        if (lane == 31) sb_copy(slot + SB::CO, Cb + (long long)qa.j * 2 * RB, 2 * RB, b);
         ps = ps + 1 == SEG_NS ? 0 : ps + 1;
         ++inflight;
         qa = qb;
@@ -663,10 +647,6 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
     for (int i = 0; i < SEG_NS; ++i) produce();
 
     const float sc = d.fx_scale;
-    const double q = energy_q(d);
-    long long ehi = 0, elo = 0, ea = 0;
-    long long eb = 0;                                                  // full items: biased energy bits
-    int ne = 0;                                                        //   ... and how many
     unsigned phase = 0;                                                // bit b: parity of slot b
     int cs = 0;                                                        // consumer slot
     int h0 = 0, h1 = 0, h2 = 0, h3 = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
@@ -675,20 +655,7 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         phase ^= 1u << cs;
         const int4 r = rec[cs];                                        // {j, rows, last}
         const unsigned char* slot = ring + cs * SB::SLOT;
-        const double2 c01 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i);
-        const double2 c23 = *reinterpret_cast<const double2*>(slot + SB::CO + 32 * c4i + 16);
-        const double cx = c01.x, cy = c01.y, cz = c23.x, cw = c23.y;
         if (d.dbg & 8) {                                               // AAKM_TC_DBG=8 probe: data movement only
-        } else if (d.dbg & 64) {                                       // AAKM_TC_DBG=64 probe: sums only, no energy
-#pragma unroll
-            for (int i = 0; i < IT; ++i) {
-                const int rr = i * RPW + h;
-                const unsigned char* a = SB::GP == 4 * RB ? slot + rr * RB + 16 * c4i
-                                                          : slot + (rr >> 2) * SB::GP + (rr & 3) * RB + 16 * c4i;
-                const float4 xv = *reinterpret_cast<const float4*>(a);
-                fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
-                fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
-            }
         } else if (RPW <= SR && r.y == SR) {                           // full item (warp-uniform): no masks
 #pragma unroll
             for (int i = 0; i < IT; ++i) {
@@ -698,13 +665,7 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
                 const float4 xv = *reinterpret_cast<const float4*>(a);
                 fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
                 fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
-                double df = (double)xv.x - cx, e = df * df;                // this lane's part of e_row
-                df = (double)xv.y - cy; e = fma(df, df, e);
-                df = (double)xv.z - cz; e = fma(df, df, e);
-                df = (double)xv.w - cw; e = fma(df, df, e);
-                eb += energy_bits(e, q);                                   // bias removed at the flush
             }
-            ne += IT;
         } else {
 #pragma unroll
             for (int i = 0; i < IT; ++i) {                             // branch-free: rows past r.y read as 0
@@ -713,16 +674,9 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
                 const unsigned char* a = SB::GP == 4 * RB ? slot + ra * RB + 16 * c4i
                                                           : slot + (ra >> 2) * SB::GP + (ra & 3) * RB + 16 * c4i;
                 float4 xv = *reinterpret_cast<const float4*>(a);
-                const bool ok = rr < r.y;
-                if (!ok) xv = make_float4(0.f, 0.f, 0.f, 0.f);          // adds nothing to the sums
+                if (rr >= r.y) xv = make_float4(0.f, 0.f, 0.f, 0.f);    // adds nothing to the sums
                 fx_add(xv.x, sc, h0, l0); fx_add(xv.y, sc, h1, l1);
                 fx_add(xv.z, sc, h2, l2); fx_add(xv.w, sc, h3, l3);
-                double df = (double)xv.x - cx, e = df * df;                // this lane's part of e_row
-                df = (double)xv.y - cy; e = fma(df, df, e);
-                df = (double)xv.z - cz; e = fma(df, df, e);
-                df = (double)xv.w - cw; e = fma(df, df, e);
-                const long long v = energy_fx(e * q);
-                ea += ok ? v : 0;
             }
         }
         __syncwarp();
@@ -732,9 +686,6 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         produce();
         if (!r.z) continue;
         // chunk done: combine the RPW row slots (lanes with equal c4i), exact int64 sums
-        ea += eb - (long long)ne * ENERGY_FX_BIAS;                     // (mod 2^64: exact)
-        eb = 0; ne = 0;
-        energy_flush(ea, ehi, elo);                                    // <= SEG_ROWS rows
         long long s8[8] = {h0, h1, h2, h3, l0, l1, l2, l3};
 #pragma unroll
         for (int o = LPR; o < 32; o <<= 1) {
@@ -748,11 +699,6 @@ __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, G
         }
         h0 = h1 = h2 = h3 = l0 = l1 = l2 = l3 = 0;
     }
-    for (int o = 16; o; o >>= 1) {
-        ehi += __shfl_xor_sync(0xffffffffu, ehi, o);
-        elo += __shfl_xor_sync(0xffffffffu, elo, o);
-    }
-    if (lane == 0 && (ehi | elo)) { pk_add(d, p, pk_ehi(d), ehi); pk_add(d, p, pk_ehi(d) + 1, elo); }
 }
 
 template <int LPR> static cudaError_t seg_attr() {
@@ -851,6 +797,73 @@ __global__ void k_energy(Dev d, GEval g) {
 
 void launch_energy(const Dev& d, const GEval& g, cudaStream_t s) { k_energy<<<1, 1, 0, s>>>(d, g); }
 
+// The label-sorted engine's energy (DESIGN R-A30): Eq. 1 through the identity
+//   E = sum_i ||x_i||^2 + sum_j sum_k (N_j c_jk^2 - 2 c_jk S_jk),
+// evaluated from this packed vector (the reduced one, or one rank's partials):
+// X2 (k_xstats_max4: each ||x_i||^2 in fp64, rounded to units of 2^x2_e), N_j, the
+// exact fixed-point S_jk and the fp64 C.  Each (j, k) term is split into exact fp64
+// pieces (two-product), each piece scaled by q (a power of 2) and rounded to the
+// E_hi / E_lo grid on its own (efx_add): a fixed function of (N_j, c_jk, S_jk), so
+// the integer sums -- and E -- do not depend on order, blocks or rank count.  The
+// pieces are computed to ~2^-106 of the term; every piece rounds by <= 2^-31/q.
+__device__ __forceinline__ void efx_add(double v, long long& hi, long long& lo) {   // v in units of 1/q
+    const double f = floor(v);
+    hi += (long long)f;
+    lo += __double2ll_rn((v - f) * 1073741824.0);                   // [0, 2^30], exact difference
+}
+__global__ void __launch_bounds__(256) k_energy_x(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    const Pick p = pick(d, g);
+    long long* pk = p.out;                                          // local replica (after the combine)
+    const int D = d.d;
+    const long long KD = (long long)d.K * D;
+    const double q = energy_q(d);
+    const double s22 = d.fx_inv, s44 = d.fx_inv * 2.384185791015625e-07;   // S = Sh 2^(e-22) + Sl 2^(e-44)
+    long long hi = 0, lo = 0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD; e += (long long)gridDim.x * blockDim.x) {
+        const long long nj = pk[pk_n(d) + e / D];
+        if (nj == 0) continue;
+        const double c = p.C[e] * q, cq = p.C[e];                   // c q exact (q a power of 2)
+        const double N = (double)nj;
+        // N c^2 q = N (c2 + c2e) q
+        const double c2 = cq * c, c2e = fma(cq, c, -c2);
+        const double a1 = N * c2, a1e = fma(N, c2, -a1);
+        const double a2 = N * c2e;
+        // -2 c S q = -2 c q (Sh s22 + Sl s44)
+        const double sh = (double)pk[e] * s22, sl = (double)pk[KD + e] * s44;     // exact
+        const double b1 = -2.0 * c * sh, b1e = fma(-2.0 * c, sh, -b1);
+        const double b2 = -2.0 * c * sl, b2e = fma(-2.0 * c, sl, -b2);
+        efx_add(a1, hi, lo); efx_add(a1e, hi, lo); efx_add(a2, hi, lo);
+        efx_add(b1, hi, lo); efx_add(b1e, hi, lo); efx_add(b2, hi, lo); efx_add(b2e, hi, lo);
+    }
+    for (int o = 16; o; o >>= 1) {
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (hi | lo)) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(pk + pk_ehi(d)), (unsigned long long)hi);
+        atomicAdd(reinterpret_cast<unsigned long long*>(pk + pk_ehi(d) + 1), (unsigned long long)lo);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // X2 (units 2^x2_e) -> units 2^-30/q = 2^(eb-51): a right shift by eb - 51 - x2_e >= 0, rounded
+        int eb = 0;
+        frexp(1.0 / q, &eb);                                        // q = 2^(21 - eb): 1/q = 2^(eb-21), frexp -> eb - 20
+        const int sh = (eb + 20) - 51 - d.x2_e;
+        __int128 v = ((__int128)pk[pk_x2(d)] << 30) + (__int128)pk[pk_x2(d) + 1];
+        if (sh > 0) v = (v + ((__int128)1 << (sh - 1))) >> sh;
+        atomicAdd(reinterpret_cast<unsigned long long*>(pk + pk_ehi(d)), (unsigned long long)(long long)(v >> 30));
+        atomicAdd(reinterpret_cast<unsigned long long*>(pk + pk_ehi(d) + 1), (unsigned long long)(long long)(v & 0x3fffffff));
+    }
+}
+
+int launch_energy_x(const Dev& d, const GEval& g, cudaStream_t s) {
+    if (!d.upd_sorted) return 0;
+    long long blocks = ((long long)d.K * d.d + 255) / 256;
+    if (blocks > 2 * d.num_sms) blocks = 2 * d.num_sms;
+    k_energy_x<<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(d, g);
+    return 1;
+}
+
 // kmeans_update_partials: this rank's unreduced [S | N | E_local | changed] as doubles.
 __global__ void k_partials_out(Dev d, const long long* pk, double* out) {
     const long long KD = (long long)d.K * d.d;
@@ -940,6 +953,43 @@ void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cu
         }
     }
     k_xstats_max<<<592, 256, 0, s>>>(X, n, d, out);
+}
+
+// sum_i ||x_i||^2 of the shard for the sorted engine's energy (k_energy_x): every
+// x_ik^2 (exact in fp64) rounded to units of 2^x2_e on its own, so the integer
+// sum is order-free and independent of how X is split into rows, ranks or kernels
+// (x2_e = eb0 - 51, 2^eb0 > 2 max||x||^2: each value < 2^50 units).  Two parts as
+// energy_flush (out[0] units 2^(x2_e+30), out[1] units 2^x2_e), out zeroed by the caller.
+__global__ void __launch_bounds__(256) k_x2(const float* X, long long count, int x2_e, long long* out) {
+    long long hi = 0, lo = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long n4 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) ? count / 4 : 0;
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const float4 v = __ldcs(X4 + i);
+        const long long a = __double2ll_rn(ldexp((double)v.x * v.x, -x2_e)) + __double2ll_rn(ldexp((double)v.y * v.y, -x2_e)) +
+                            __double2ll_rn(ldexp((double)v.z * v.z, -x2_e)) + __double2ll_rn(ldexp((double)v.w * v.w, -x2_e));
+        hi += a >> 30;
+        lo += a & 0x3fffffffLL;
+    }
+    for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const double v = X[i];
+        const long long a = __double2ll_rn(ldexp(v * v, -x2_e));
+        hi += a >> 30;
+        lo += a & 0x3fffffffLL;
+    }
+    for (int o = 16; o; o >>= 1) {
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (hi | lo)) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)hi);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)lo);
+    }
+}
+
+void launch_x2(const float* X, long long count, int x2_e, long long* out, cudaStream_t s) {
+    if (count > 0) k_x2<<<1184, 256, 0, s>>>(X, count, x2_e, out);
 }
 
 __global__ void k_xcheck(Dev d, const unsigned int* out, unsigned int amax, unsigned int nmax2) {

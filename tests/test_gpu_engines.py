@@ -350,3 +350,29 @@ def test_assign_and_update_timing_hooks():
     assert a_n == 4 and u_n == 4 and a_ms > 0 and u_ms > 0
     assert km.assign_timing() == (0.0, 0) and km.update_timing() == (0.0, 0)
     km.close()
+
+
+@pytest.mark.parametrize("offset,d", [(0.0, 64), (30.0, 128), (300.0, 32)])
+def test_sorted_energy_expansion_bound(offset, d):
+    """Sorted engine energy (DESIGN R-A30): E = sum ||x_i||^2 + sum_j (N_j ||c_j||^2
+    - 2 c_j . S_j) from the exact sums, against the oracle's direct differences,
+    within the stated bound: every x_ik^2 and every (j, k) piece rounds once to the
+    energy grid (<= half a unit of 2^-30/q each), plus 1e-13 E for the oracle's own
+    fp64 rounding.  offset > 0 puts the data far from the origin (||x||^2 >> e_i:
+    the expansion's cancellation case)."""
+    rng = np.random.default_rng(7 + d)
+    n, K = 70_000, 96
+    centers = offset + rng.normal(0, 2, (K, d))
+    lab = rng.integers(0, K, n).astype(np.int32)
+    X = (centers[lab] + rng.normal(0, 0.5, (n, d))).astype(np.float32)
+    C = (centers + rng.normal(0, 0.05, (K, d))).astype(np.float64)
+    km = aakm.KMeans(dev(X), K, aakm.config())
+    part = km.update_partials(dev(lab), dev(C)).cpu().numpy()
+    km.close()
+    E_ora = oracle.energy(X, C, lab)
+    xn = np.sqrt((X.astype(np.float64) ** 2).sum(1).max()) * (1 + 1e-6)
+    cm = np.sqrt(np.float32((C ** 2).sum(1).max()))
+    eb = np.frexp(2.0 * (xn + cm) ** 2)[1]
+    unit = 2.0 ** (eb - 51)                                    # 2^-30 / q
+    bound = (n * d + 7 * K * d) * unit / 2 + 1e-13 * E_ora
+    assert abs(part[-2] - E_ora) <= bound, (part[-2], E_ora, bound)
