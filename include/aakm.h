@@ -246,7 +246,9 @@ AAKM_API kmeans_status kmeans_state_import(kmeans_handle *h, const kmeans_state 
  * partials [S (K*d, S_j = sum of x_i over rho_i = j) | N (K) | E_local |
  * changed] as K*d + K + 2 doubles (device): S from the exact fixed-point sums,
  * E_local = sum over this rank's rows of ||x_i - c_{rho_i}||^2 (so the ranks'
- * values sum to the global E).  labels_prev nullable (changed = 0).
+ * values sum to the global E; label-sorted engine, n_global >= 65536: through
+ * sum ||x_i||^2 + sum_j (N_j ||c_j||^2 - 2 c_j . S_j) of this rank's sums,
+ * DESIGN.md R-A30).  labels_prev nullable (changed = 0).
  * Synchronises. */
 AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *labels,
                                      const int32_t *labels_prev, const double *C,
