@@ -204,6 +204,7 @@ int launch_refine(const Dev& d, const GEval& g, cudaStream_t s, long long first 
 int launch_refine_tc(const Dev& d, const GEval& g, const void* maps, cudaStream_t s);
 int launch_update(const Dev& d, const GEval& g, cudaStream_t s);
 bool update_sorted(long long n_global, int dd, int K);
+int seg_blocks_for(int K, int num_sms);
 void launch_control(const Dev& d, int stage, cudaStream_t s);
 void launch_finalize(const Dev& d, cudaStream_t s);
 void launch_gram(const Dev& d, cudaStream_t s);

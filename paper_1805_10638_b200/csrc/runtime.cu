@@ -729,7 +729,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     } while (0)
     CKC(cudaGetDevice(&D.dev));
     CKC(cudaDeviceGetAttribute(&D.num_sms, cudaDevAttrMultiProcessorCount, D.dev));
-    D.seg_blocks = std::min(AAKM_SEG_BLOCKS_MAX, D.num_sms);      // (2 per SM measured slower: c5 scatter 157 vs 129 us)
+    D.seg_blocks = seg_blocks_for(k, D.num_sms);
     h->da.dev = D.dev; h->da.num_sms = D.num_sms; h->da.seg_blocks = D.seg_blocks;
     CKC(setup_device(D.dev));
     CKC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));

@@ -331,17 +331,17 @@ __global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
 // Per sub-tile: [ranks: smem atomics] sync [bin scan] sync [stage] sync
 // [output + zero the counters + the next sub-tile's label loads] sync.  A row
 // travels as one packed word (label << 14 | rank or local row), T <= 2^14.
-constexpr int SCAT_BT = 1024;         // threads per block
-constexpr int SCAT_RPT = 16;          // rows per thread per sub-tile (T <= SCAT_RPT * SCAT_BT)
+constexpr int SCAT_RPT = 16;          // rows per thread per sub-tile (T <= SCAT_RPT * BT)
 constexpr int SCAT_LB = 14;           // local row / rank bits
-static_assert(SCAT_RPT * SCAT_BT <= (1 << SCAT_LB) && AAKM_SORTED_MAX_K <= (1 << (31 - SCAT_LB)), "packed rows");
+static_assert(SCAT_RPT * 1024 <= (1 << SCAT_LB) && AAKM_SORTED_MAX_K <= (1 << (31 - SCAT_LB)), "packed rows");
 
 // cnt[i] (counts) -> exclusive offsets over i < K; base[i] = gcur[i] - offset
 // (perm slot of sorted entry q of cluster i is base[i] + q); gcur[i] += count.
 // Thread t owns the contiguous bins [t per, (t + 1) per).  Returns the total.
+template <int SCAT_BT>
 __device__ __forceinline__ int scat_scan(int* cnt, int* gcur, int* base, int K) {
     __shared__ int ws[SCAT_BT / 32];
-    const int per = (K + SCAT_BT - 1) / SCAT_BT;            // <= 16
+    const int per = (K + SCAT_BT - 1) / SCAT_BT;            // <= 32
     const int a = threadIdx.x * per, b = min(K, a + per);
     int sum = 0;
     for (int i = a; i < b; ++i) sum += cnt[i];
@@ -355,13 +355,13 @@ __device__ __forceinline__ int scat_scan(int* cnt, int* gcur, int* base, int K) 
     if (lane == 31) ws[w] = inc;
     __syncthreads();
     if (w == 0) {
-        int x = ws[lane];
+        int x = lane < SCAT_BT / 32 ? ws[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += t;
         }
-        ws[lane] = x;
+        if (lane < SCAT_BT / 32) ws[lane] = x;
     }
     __syncthreads();
     int run = inc - sum + (w ? ws[w - 1] : 0);
@@ -376,7 +376,10 @@ __device__ __forceinline__ int scat_scan(int* cnt, int* gcur, int* base, int K) 
     return tot;
 }
 
-__global__ void __launch_bounds__(SCAT_BT, 1) k_scatter(Dev d, GEval g, int T) {
+// BT = 1024 (one block per SM) or 512 (two per SM, K <= 6144: phases of the two
+// blocks overlap)
+template <int SCAT_BT>
+__global__ void __launch_bounds__(SCAT_BT, SCAT_BT == 512 ? 2 : 1) k_scatter(Dev d, GEval g, int T) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     extern __shared__ __align__(16) int scat_sm[];
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(SCAT_BT, 1) k_scatter(Dev d, GEval g, int T) {
             pk[u] = (unsigned)j < (unsigned)K ? (j << SCAT_LB) | atomicAdd(&cnt[j], 1) : -1;
         }
         __syncthreads();
-        const int nv = scat_scan(cnt, gcur, base, K);
+        const int nv = scat_scan<SCAT_BT>(cnt, gcur, base, K);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < SCAT_RPT; ++u) {
@@ -451,10 +454,19 @@ __global__ void __launch_bounds__(SCAT_BT, 1) k_scatter(Dev d, GEval g, int T) {
 constexpr int SCAT_SMEM = 220 * 1024;   // dynamic shared memory of k_scatter (+ its static scan buffer)
 // sub-tile rows: a multiple of the block size, <= SCAT_RPT rows per thread, inside
 // the shared memory left after the three K-sized arrays
-static int scatter_tile(int K) {
-    int T = (SCAT_SMEM - 12 * K) / 4;
-    T = T / SCAT_BT * SCAT_BT;
-    return T > SCAT_RPT * SCAT_BT ? SCAT_RPT * SCAT_BT : T;
+static int scatter_tile(int K, int bt, int per_sm) {
+    int T = (SCAT_SMEM / per_sm - 12 * K) / 4;
+    T = T / bt * bt;
+    return T > SCAT_RPT * bt ? SCAT_RPT * bt : T;
+}
+// row blocks of the histogram / scatter partition: one per SM.  AAKM_SEG_PER_SM=2
+// (A/B runs) takes two 512-thread scatter blocks per SM where the K-sized arrays
+// leave room: measured slower (c5 update 0.905 vs 0.870 ms, c3 0.135 vs 0.119)
+int seg_blocks_for(int K, int num_sms) {
+    static const int env = getenv("AAKM_SEG_PER_SM") ? atoi(getenv("AAKM_SEG_PER_SM")) : 1;
+    const int per = env == 2 && scatter_tile(K, 512, 2) >= 4 * 512 ? 2 : 1;
+    const int b = per * num_sms;
+    return b < AAKM_SEG_BLOCKS_MAX ? b : AAKM_SEG_BLOCKS_MAX;
 }
 
 template <int V>   // floats per lane: d <= 32 * V
@@ -713,7 +725,9 @@ template <int LPR> static void seg_launch(const Dev& d, const GEval& g, cudaStre
 cudaError_t setup_update() {
     cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAT_SMEM);
+    e = cudaFuncSetAttribute(k_scatter<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAT_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_scatter<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAT_SMEM / 2);
     if (e != cudaSuccess) return e;
     for (cudaError_t f : {seg_attr<1>(), seg_attr<2>(), seg_attr<4>(), seg_attr<8>(), seg_attr<16>(), seg_attr<32>()})
         if (f != cudaSuccess) return f;
@@ -738,8 +752,13 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     k_scan_a<<<(d.K + 7) / 8, 256, 0, s>>>(d, g, d.seg_blocks);
     k_scan_b<<<1, 1024, 0, s>>>(d, g);
     {
-        const int T = scatter_tile(d.K);
-        k_scatter<<<d.seg_blocks, SCAT_BT, (size_t)(3 * d.K + T) * 4, s>>>(d, g, T);
+        if (d.seg_blocks > d.num_sms) {
+            const int T = scatter_tile(d.K, 512, 2);
+            k_scatter<512><<<d.seg_blocks, 512, (size_t)(3 * d.K + T) * 4, s>>>(d, g, T);
+        } else {
+            const int T = scatter_tile(d.K, 1024, 1);
+            k_scatter<1024><<<d.seg_blocks, 1024, (size_t)(3 * d.K + T) * 4, s>>>(d, g, T);
+        }
     }
     if (d.xg_map) {
         switch (d.d / 4) {
