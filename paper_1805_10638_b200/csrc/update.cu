@@ -975,10 +975,23 @@ void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cu
 }
 
 // sum_i ||x_i||^2 of the shard for the sorted engine's energy (k_energy_x): every
-// x_ik^2 (exact in fp64) rounded to units of 2^x2_e on its own, so the integer
-// sum is order-free and independent of how X is split into rows, ranks or kernels
-// (x2_e = eb0 - 51, 2^eb0 > 2 max||x||^2: each value < 2^50 units).  Two parts as
-// energy_flush (out[0] units 2^(x2_e+30), out[1] units 2^x2_e), out zeroed by the caller.
+// x_ik^2 rounded to units of 2^x2_e on its own (half up), so the integer sum is
+// order-free and independent of how X is split into rows, ranks or kernels
+// (x2_e = eb0 - 51, 2^eb0 > 2 max||x||^2: each value < 2^50 units).  Integer
+// arithmetic on the fp32 bits: x = m 2^(E'-150) (E' = max(E, 1), m with the
+// implicit bit), x^2 = m^2 2^(2E'-300), m^2 exact in 48 bits -- no fp64 or
+// conversion (XU) instructions.  Two parts as energy_flush (out[0] units
+// 2^(x2_e+30), out[1] units 2^x2_e), out zeroed by the caller.
+__device__ __forceinline__ long long x2_units(float x, int x2_e) {
+    const unsigned b = __float_as_uint(x);
+    const int E = (int)((b >> 23) & 0xFFu);
+    const unsigned long long m = (b & 0x7FFFFFu) | (E ? 0x800000u : 0u);
+    const unsigned long long m2 = m * m;
+    const int sh = 2 * (E ? E : 1) - 300 - x2_e;
+    if (sh >= 0) return (long long)(m2 << sh);                     // < 2^50 by the choice of x2_e
+    if (sh <= -49) return 0;                                       // m2 < 2^48: below half a unit
+    return (long long)((m2 + (1ull << (-sh - 1))) >> (-sh));
+}
 __global__ void __launch_bounds__(256) k_x2(const float* X, long long count, int x2_e, long long* out) {
     long long hi = 0, lo = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -986,14 +999,12 @@ __global__ void __launch_bounds__(256) k_x2(const float* X, long long count, int
     const float4* X4 = reinterpret_cast<const float4*>(X);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
         const float4 v = __ldcs(X4 + i);
-        const long long a = __double2ll_rn(ldexp((double)v.x * v.x, -x2_e)) + __double2ll_rn(ldexp((double)v.y * v.y, -x2_e)) +
-                            __double2ll_rn(ldexp((double)v.z * v.z, -x2_e)) + __double2ll_rn(ldexp((double)v.w * v.w, -x2_e));
+        const long long a = x2_units(v.x, x2_e) + x2_units(v.y, x2_e) + x2_units(v.z, x2_e) + x2_units(v.w, x2_e);
         hi += a >> 30;
         lo += a & 0x3fffffffLL;
     }
     for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-        const double v = X[i];
-        const long long a = __double2ll_rn(ldexp(v * v, -x2_e));
+        const long long a = x2_units(X[i], x2_e);
         hi += a >> 30;
         lo += a & 0x3fffffffLL;
     }

@@ -13,10 +13,11 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 for rep in sys.argv[1:]:
     raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
     print(f"== {rep.split('/')[-1]}")
-    print(f"{'Kernel Name':70s} {vals[hdr.index('Kernel Name')][:90]}")
-    for k in KEYS:
-        if k in hdr:
-            i = hdr.index(k)
-            print(f"{k:70s} {vals[i]:>18s} {units[i]}")
+    for vals in rows[2:]:                                  # every captured launch
+        print(f"{'Kernel Name':70s} {vals[hdr.index('Kernel Name')][:90]}")
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                print(f"{k:70s} {vals[i]:>18s} {units[i]}")
