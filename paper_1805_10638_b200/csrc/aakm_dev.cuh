@@ -217,7 +217,9 @@ void launch_energy(const Dev& d, const GEval& g, cudaStream_t s);       // E aft
 // sorted engine: E's parts from the (reduced or local) packed S, N, X2 and C (update.cu)
 int launch_energy_x(const Dev& d, const GEval& g, cudaStream_t s);
 void launch_partials_out(const Dev& d, const long long* packed, double* out, cudaStream_t s);
-void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s);
+// (x2: also sum_i ||x_i||^2 as launch_x2, in the same pass when d = 4 LPR); returns launches
+int launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s,
+                      long long* x2 = nullptr, int x2_e = 0);
 // sum_i ||x_i||^2 of the shard (count = n d floats) in units of 2^x2_e, two parts into out[2] (zeroed)
 void launch_x2(const float* X, long long count, int x2_e, long long* out, cudaStream_t s);
 // f4 fused combine (comm.cu); comm is an ncclComm_t; setup returns an error message or nullptr

@@ -1083,14 +1083,10 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
     // one stats pass on the copy stream, checked on the device (label_error bit 2,
     // reported by the next synchronising call)
     CK(h, cudaMemsetAsync(h->xchk, 0, 8, h->copy_stream));
-    launch_xstats_max(d.X, d.n, d.d, h->xchk, h->copy_stream);
+    if (d.x2) CK(h, cudaMemsetAsync(d.x2, 0, 16, h->copy_stream));   // + the new rows' sum ||x_i||^2 (k_energy_x)
+    h->launches += launch_xstats_max(d.X, d.n, d.d, h->xchk, h->copy_stream, d.x2, d.x2_e);
     launch_xcheck(d, h->xchk, h->x_stat[0], h->x_stat[1], h->copy_stream);
-    h->launches += 2;
-    if (d.x2) {                                                        // the new rows' sum ||x_i||^2 (k_energy_x)
-        CK(h, cudaMemsetAsync(d.x2, 0, 16, h->copy_stream));
-        launch_x2(d.X, d.n * d.d, d.x2_e, d.x2, h->copy_stream);
-        h->launches += 1;
-    }
+    h->launches += 1;
     CK(h, cudaEventRecord(h->feed_all, h->copy_stream));
     if (d.ub) CK(h, cudaMemsetAsync(&d.st->bnd_ready, 0, sizeof(int), s));   // new rows: no valid bounds
     const bool streamed = nc > 0 && !d.ub && (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16);

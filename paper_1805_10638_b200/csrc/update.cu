@@ -902,6 +902,17 @@ void launch_partials_out(const Dev& d, const long long* packed, double* out, cud
 }
 
 // ------------------------------------------------------------------ create-time statistics of X
+// sum_i ||x_i||^2 of the shard for the sorted engine's energy (k_energy_x): every
+// x_ik^2 rounded to units of 2^x2_e on its own (to nearest even, by adding
+// 1.5 2^52 in one fma: x^2 2^-x2_e < 2^50), so the integer sum is order-free and
+// independent of how X is split into rows, ranks or kernels (x2_e = eb0 - 51,
+// 2^eb0 > 2 max||x||^2).  Two parts as energy_flush (out[0] units 2^(x2_e+30),
+// out[1] units 2^x2_e), out zeroed by the caller.  At create k_x2 computes it;
+// a refresh of X gets it from the same pass as the range check (k_xstats_max4).
+__device__ __forceinline__ long long x2_units(float x, double s2) {     // s2 = 2^-x2_e
+    const double xd = (double)x;
+    return __double_as_longlong(fma(xd, xd * s2, 6755399441055744.0)) - 0x4338000000000000LL;
+}
 // out4[0] = max |x| (float bits), out4[1] = max ||x_i||^2 (float bits, rounded up)
 __global__ void k_xstats_max(const float* X, long long n, int D, unsigned int* out) {
     const int lane = threadIdx.x & 31;
@@ -925,10 +936,12 @@ __global__ void k_xstats_max(const float* X, long long n, int D, unsigned int* o
 // with one 16-B load each, four row groups in flight per warp (the generic kernel
 // above reads one float per lane and ran at ~1 TB/s on c5).
 template <int LPR>
-__global__ void __launch_bounds__(256) k_xstats_max4(const float4* X, long long n, unsigned int* out) {
+__global__ void __launch_bounds__(256) k_xstats_max4(const float4* X, long long n, unsigned int* out, long long* x2,
+                                                     double s2) {
     constexpr int RPW = 32 / LPR, U = 4;
     const int lane = threadIdx.x & 31, h = lane / LPR, c = lane % LPR;
     float am = 0.f, nm = 0.f;
+    long long xh = 0, xl = 0;                                       // sum ||x||^2 (x2_units), two parts
     const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long r0 = w0 * RPW * U; r0 < n; r0 += nw * RPW * U) {
@@ -941,6 +954,11 @@ __global__ void __launch_bounds__(256) k_xstats_max4(const float4* X, long long 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             am = fmaxf(am, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+            if (x2) {                                               // (rows past n read as zeros)
+                const long long a = x2_units(v[u].x, s2) + x2_units(v[u].y, s2) + x2_units(v[u].z, s2) + x2_units(v[u].w, s2);
+                xh += a >> 30;
+                xl += a & 0x3fffffffLL;
+            }
             double s = (double)v[u].x * v[u].x;
             s = fma((double)v[u].y, (double)v[u].y, s);
             s = fma((double)v[u].z, (double)v[u].z, s);
@@ -953,58 +971,50 @@ __global__ void __launch_bounds__(256) k_xstats_max4(const float4* X, long long 
     for (int o = 16; o; o >>= 1) {
         am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
         nm = fmaxf(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+        xh += __shfl_xor_sync(0xffffffffu, xh, o);
+        xl += __shfl_xor_sync(0xffffffffu, xl, o);
     }
     if (lane == 0) { atomicMax(out, __float_as_uint(am)); atomicMax(out + 1, __float_as_uint(nm)); }
+    if (lane == 0 && x2 && (xh | xl)) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(x2), (unsigned long long)xh);
+        atomicAdd(reinterpret_cast<unsigned long long*>(x2 + 1), (unsigned long long)xl);
+    }
 }
 
-void launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s) {
-    if (n <= 0) return;
+int launch_xstats_max(const float* X, long long n, int d, unsigned int* out, cudaStream_t s, long long* x2, int x2_e) {
+    if (n <= 0) return 0;
     const bool vec = d % 4 == 0 && d / 4 <= 32 && ((d / 4) & (d / 4 - 1)) == 0 && ((uintptr_t)X & 15) == 0;
     const float4* X4 = reinterpret_cast<const float4*>(X);
+    const double s2 = ldexp(1.0, -x2_e);
     if (vec) {
         switch (d / 4) {
-            case 1: k_xstats_max4<1><<<1184, 256, 0, s>>>(X4, n, out); return;
-            case 2: k_xstats_max4<2><<<1184, 256, 0, s>>>(X4, n, out); return;
-            case 4: k_xstats_max4<4><<<1184, 256, 0, s>>>(X4, n, out); return;
-            case 8: k_xstats_max4<8><<<1184, 256, 0, s>>>(X4, n, out); return;
-            case 16: k_xstats_max4<16><<<1184, 256, 0, s>>>(X4, n, out); return;
-            default: k_xstats_max4<32><<<1184, 256, 0, s>>>(X4, n, out); return;
+            case 1: k_xstats_max4<1><<<1184, 256, 0, s>>>(X4, n, out, x2, s2); return 1;
+            case 2: k_xstats_max4<2><<<1184, 256, 0, s>>>(X4, n, out, x2, s2); return 1;
+            case 4: k_xstats_max4<4><<<1184, 256, 0, s>>>(X4, n, out, x2, s2); return 1;
+            case 8: k_xstats_max4<8><<<1184, 256, 0, s>>>(X4, n, out, x2, s2); return 1;
+            case 16: k_xstats_max4<16><<<1184, 256, 0, s>>>(X4, n, out, x2, s2); return 1;
+            default: k_xstats_max4<32><<<1184, 256, 0, s>>>(X4, n, out, x2, s2); return 1;
         }
     }
     k_xstats_max<<<592, 256, 0, s>>>(X, n, d, out);
+    if (x2) { launch_x2(X, n * d, x2_e, x2, s); return 2; }
+    return 1;
 }
 
-// sum_i ||x_i||^2 of the shard for the sorted engine's energy (k_energy_x): every
-// x_ik^2 rounded to units of 2^x2_e on its own (half up), so the integer sum is
-// order-free and independent of how X is split into rows, ranks or kernels
-// (x2_e = eb0 - 51, 2^eb0 > 2 max||x||^2: each value < 2^50 units).  Integer
-// arithmetic on the fp32 bits: x = m 2^(E'-150) (E' = max(E, 1), m with the
-// implicit bit), x^2 = m^2 2^(2E'-300), m^2 exact in 48 bits -- no fp64 or
-// conversion (XU) instructions.  Two parts as energy_flush (out[0] units
-// 2^(x2_e+30), out[1] units 2^x2_e), out zeroed by the caller.
-__device__ __forceinline__ long long x2_units(float x, int x2_e) {
-    const unsigned b = __float_as_uint(x);
-    const int E = (int)((b >> 23) & 0xFFu);
-    const unsigned long long m = (b & 0x7FFFFFu) | (E ? 0x800000u : 0u);
-    const unsigned long long m2 = m * m;
-    const int sh = 2 * (E ? E : 1) - 300 - x2_e;
-    if (sh >= 0) return (long long)(m2 << sh);                     // < 2^50 by the choice of x2_e
-    if (sh <= -49) return 0;                                       // m2 < 2^48: below half a unit
-    return (long long)((m2 + (1ull << (-sh - 1))) >> (-sh));
-}
 __global__ void __launch_bounds__(256) k_x2(const float* X, long long count, int x2_e, long long* out) {
     long long hi = 0, lo = 0;
+    const double s2 = ldexp(1.0, -x2_e);
     const long long stride = (long long)gridDim.x * blockDim.x;
     const long long n4 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) ? count / 4 : 0;
     const float4* X4 = reinterpret_cast<const float4*>(X);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
         const float4 v = __ldcs(X4 + i);
-        const long long a = x2_units(v.x, x2_e) + x2_units(v.y, x2_e) + x2_units(v.z, x2_e) + x2_units(v.w, x2_e);
+        const long long a = x2_units(v.x, s2) + x2_units(v.y, s2) + x2_units(v.z, s2) + x2_units(v.w, s2);
         hi += a >> 30;
         lo += a & 0x3fffffffLL;
     }
     for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-        const long long a = x2_units(X[i], x2_e);
+        const long long a = x2_units(X[i], s2);
         hi += a >> 30;
         lo += a & 0x3fffffffLL;
     }
