@@ -334,6 +334,14 @@ AAKM_API kmeans_status kmeans_last_flagged(kmeans_handle *h, int64_t *flagged /*
 AAKM_API kmeans_status kmeans_bounded_stats(kmeans_handle *h, int64_t *rows_scored /*host*/,
                                             int64_t *rows_total /*host*/);
 
+/* Update work since the last Algorithm 1 line 1 (one rank, label-sorted engine;
+ * zeros otherwise): G-evaluations, how many took the incremental update
+ * S(P^t) = S(P^{t-1}) + the moved rows (exact: bitwise the full sums; chosen on
+ * the device when at most n_local / AAKM_DELTA_DIV (64) rows moved), and the
+ * rows those moved. */
+AAKM_API kmeans_status kmeans_update_stats(kmeans_handle *h, int64_t *n_evals /*host*/,
+                                           int64_t *n_incremental /*host*/, int64_t *rows_moved /*host*/);
+
 /* Exactness-margin probe (test hook): runs the handle's dense assignment
  * engine on C (K x d fp64) and writes, per local row, the engine's raw top-2
  * values and its near-tie threshold: rows_out (device, n_local x 4 float) =

@@ -90,6 +90,7 @@ def lib():
                 "kmeans_launch_count": ([P], I64),
                 "kmeans_last_flagged": ([P, ct.POINTER(I64)], I32),
                 "kmeans_bounded_stats": ([P, ct.POINTER(I64), ct.POINTER(I64)], I32),
+                "kmeans_update_stats": ([P, ct.POINTER(I64), ct.POINTER(I64), ct.POINTER(I64)], I32),
                 "kmeans_seed_pp": ([P, P, P, P], I32),
                 "kmeans_aa_step_host": ([P, P, I32, P, P], I32),
                 "kmeans_update_timing": ([P, ct.POINTER(D), ct.POINTER(I64)], I32),
@@ -375,6 +376,12 @@ class KMeans:
         a, b = ct.c_int64(), ct.c_int64()
         self._c(lib().kmeans_bounded_stats(self.h, ct.byref(a), ct.byref(b)))
         return a.value, b.value
+
+    def update_stats(self):
+        """(G-evaluations, of them incremental, their moved rows) since line 1."""
+        a, b, c = ct.c_int64(), ct.c_int64(), ct.c_int64()
+        self._c(lib().kmeans_update_stats(self.h, ct.byref(a), ct.byref(b), ct.byref(c)))
+        return a.value, b.value, c.value
 
     def seed_pp(self, u):
         """K-Means++ seeding (kmeans_seed_pp) with the caller's K uniforms in [0, 1):

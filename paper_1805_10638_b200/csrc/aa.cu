@@ -180,6 +180,15 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
         const double g = nj > 0 ? fx_value(pk[e], pk[KD + e], d.fx_inv) / (double)nj : c;   // G = S / N (Eq. 4)
         G[e] = g;
         F[e] = g - c;                                            // F^t = G^t - C^t (fp64)
+        if (d.sref) {                                            // S(P^t), N(P^t): the next pass's S_ref
+            d.sref[e] = pk[e];
+            d.sref[KD + e] = pk[KD + e];
+        }
+    }
+    if (d.sref) {
+        for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x)
+            d.sref[2 * KD + j] = pk[pk_n(d) + j];
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->sref_valid = 1;
     }
 }
 
@@ -451,6 +460,8 @@ __global__ void k_reset(Dev d) {
     st->hist_count = 0; st->accepted_now = 0; st->rejected_now = 0; st->label_error = 0;
     st->n_alpha = 1; st->fb_slot = 0; st->final_traced = 0;
     st->bnd_ready = 0; st->bnd_use = 0;                         // bounded engine: recompute every row first
+    st->sref_valid = 0; st->use_delta = 0;                      // incremental update: no S(P^{t-1}) yet
+    st->n_upd = 0; st->n_delta = 0; st->rows_moved = 0;
     st->rows_scored = 0; st->rows_total = 0;
 }
 

@@ -54,6 +54,9 @@ struct alignas(16) DevState {
     int seed_err, pad4;          // K-Means++: 2 = fewer distinct samples than K
     int bnd_ready0, pad5;        // bounded engine: bnd_ready at the snapshot
     unsigned int fc_ctr, pad6;   // f4 fused combine: blocks done zeroing (comm.cu)
+    int sref_valid, use_delta;   // incremental update: S_ref = S(P^{t-1}) valid / this evaluation uses it
+    unsigned int delta_ctr, pad7;
+    long long n_upd, n_delta, rows_moved;   //   evaluations / of them incremental / their moved rows
     double theta[AAKM_H_SLOTS];
     double alpha[AAKM_H_SLOTS];
     int alpha_slot[AAKM_H_SLOTS];
@@ -97,10 +100,14 @@ struct Dev {
     int* pair_rows;       // near-tie rows whose window holds exactly two centroids (capacity fcap)
     int2* pair_j;         //   their two centroids (best key, runner-up)
     long long* pair_count;//   [2] counts, branch A / B (zeroed per pass with the flags)
+    long long* delta_count;// [2] incremental update: moved rows of branch A / B (zeroed likewise)
     long long* packed[2]; // [S_hi (K*d) | S_lo (K*d) | N (K) | E_hi | E_lo | E (fp64 bits) | changed | X2_hi | X2_lo]
     float fx_scale;       // 2^(22-e), |x| <= 2^e over all ranks: S in exact fixed point (update.cu)
     double fx_inv;        // 2^(e-22)
     double xn_gmax;       // max_i ||x_i|| over all ranks (rounded up): bounds every ||x_i - c||
+    long long* sref;      // incremental update (1 rank, sorted engine): [S_hi | S_lo | N] of P^{t-1}
+                          //   (nullptr: off); k_finalize writes it, k_delta_* read it
+    long long delta_max;  //   at most this many moved rows take the incremental path
     long long* x2;        // sorted engine: this rank's sum_i ||x_i||^2 in units of 2^x2_e (two parts, as
     int x2_e;             //   energy_flush), refreshed with X; x2_e = frexp exponent of 2 xn_gmax^2 - 51
     double* upd_part;     // per-block (E, changed) partials

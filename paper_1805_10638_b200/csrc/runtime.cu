@@ -167,7 +167,7 @@ struct Layout {
     size_t st, st_api, C, C32, Ca32, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, total,
+        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, sref, total,
         scratch_bytes;
     std::vector<size_t> guards;   // AAKM_WS_CANARY=1: a 256-B canary after every region
 };
@@ -249,6 +249,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.C_ref0 = take(bounded ? KD * 8 : 8);
     L.xchk = take(16);
     L.x2 = take(16);
+    L.sref = take((2 * KD + K) * 8);                // incremental update: S_hi | S_lo | N of P^{t-1}
     L.total = o;
     return L;
 }
@@ -657,6 +658,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.flag_count = (long long*)(w + L.scratch);
     D.act_count = (long long*)(w + L.scratch + 32);                   // [2], zeroed per pass with the flags
     D.pair_count = (long long*)(w + L.scratch + 64);                  // [2], likewise
+    D.delta_count = (long long*)(w + L.scratch + 96);                 // [2], likewise
     D.pair_rows = (int*)(w + L.pair_rows); D.pair_j = (int2*)(w + L.pair_j);
     D.packed[0] = (long long*)(w + L.scratch + 256);
     D.packed[1] = (long long*)(w + L.packed1);
@@ -829,6 +831,16 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             dv->upd_sorted = srt ? 1 : 0;
             dv->x2_e = eb0 - 51;
             dv->x2 = srt ? (long long*)(w + L.x2) : nullptr;
+        }
+        // incremental update (update.cu k_delta_*): one rank (the rank's partial S is then the
+        // global S) and the plain combine; AAKM_DELTA_DIV: moved-row threshold n / DIV (0: off)
+        {
+            const char* dv = getenv("AAKM_DELTA_DIV");
+            const long long div = dv ? atoll(dv) : 64;
+            const bool on = srt && nranks == 1 && !cfg->fused_comm && div > 0;
+            h->d.sref = on ? (long long*)(w + L.sref) : nullptr;
+            h->d.delta_max = on ? n_local / div : 0;
+            h->da.sref = nullptr; h->da.delta_max = 0;                 // API calls: always the full update
         }
         if (srt) {
             CKC(cudaMemsetAsync(w + L.x2, 0, 16, h->stream));
@@ -1089,6 +1101,7 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
     h->launches += 1;
     CK(h, cudaEventRecord(h->feed_all, h->copy_stream));
     if (d.ub) CK(h, cudaMemsetAsync(&d.st->bnd_ready, 0, sizeof(int), s));   // new rows: no valid bounds
+    CK(h, cudaMemsetAsync(&d.st->sref_valid, 0, sizeof(int), s));            // ... and no valid S(P^{t-1})
     const bool streamed = nc > 0 && !d.ub && (h->path == KMEANS_PATH_TC || h->path == KMEANS_PATH_TC16);
     if (!streamed) {
         CK(h, cudaStreamWaitEvent(s, h->feed_all, 0));
@@ -1234,6 +1247,7 @@ kmeans_status kmeans_state_import(kmeans_handle* h, const kmeans_state* st) {
     S.hist_count = st->hist_count; S.n_accepted = st->n_accepted; S.n_rejected = st->n_rejected;
     S.n_assign = st->n_assign; S.trace_len = 0; S.final_traced = 0; S.label_error = 0;
     S.bnd_ready = 0; S.bnd_use = 0; S.rows_scored = 0; S.rows_total = 0;
+    S.sref_valid = 0; S.use_delta = 0;                                // no S(P^{t-1}) for the imported labels
     if (st->gram) {
         for (int a = 0; a < d.H; ++a)
             for (int b = 0; b < d.H; ++b) S.gram[a * d.H + b] = st->gram[a * d.H + b];
@@ -1395,6 +1409,17 @@ kmeans_status kmeans_bounded_stats(kmeans_handle* h, int64_t* rows_scored, int64
     SYNC(h, h->stream);
     *rows_scored = h->st_host->rows_scored;
     *rows_total = h->st_host->rows_total;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_update_stats(kmeans_handle* h, int64_t* n_evals, int64_t* n_incremental, int64_t* rows_moved) {
+    LIVE(h);
+    if (!n_evals || !n_incremental || !rows_moved) FAIL(h, KMEANS_ERR_INVALID, "NULL output");
+    CK(h, cudaMemcpyAsync(h->st_host, h->d.st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+    SYNC(h, h->stream);
+    *n_evals = h->d.sref ? h->st_host->n_upd : 0;
+    *n_incremental = h->d.sref ? h->st_host->n_delta : 0;
+    *rows_moved = h->d.sref ? h->st_host->rows_moved : 0;
     return KMEANS_OK;
 }
 

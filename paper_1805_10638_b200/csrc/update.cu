@@ -199,6 +199,7 @@ __device__ __forceinline__ void block_rows(const Dev& d, long long& r0, long lon
 
 __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
+    if (d.sref && d.st->use_delta) return;                        // the incremental path runs instead
     const Pick p = pick(d, g);
     extern __shared__ int hs[];
     const int K = d.K;
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(1024) k_hist(Dev d, GEval g) {
 // lane l owns a contiguous run of blocks, then a warp scan of the run sums).
 __global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
     if (!geval_active(d, g)) return;
+    if (d.sref && d.st->use_delta) return;                        // the incremental path runs instead
     const Pick p = pick(d, g);
     const int K = d.K;
     const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(256) k_scan_a(Dev d, GEval g, int nblk) {
 // chunk counts, chunk -> cluster map.  k_scatter adds seg_off[j] to the bases.
 __global__ void __launch_bounds__(1024) k_scan_b(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
+    if (d.sref && d.st->use_delta) return;                        // the incremental path runs instead
     const int K = d.K;
     __shared__ long long wsum[2][32];
     __shared__ long long carry[2];
@@ -381,6 +384,7 @@ __device__ __forceinline__ int scat_scan(int* cnt, int* gcur, int* base, int K) 
 template <int SCAT_BT>
 __global__ void __launch_bounds__(SCAT_BT, SCAT_BT == 512 ? 2 : 1) k_scatter(Dev d, GEval g, int T) {
     if (!geval_active(d, g)) return;
+    if (d.sref && d.st->use_delta) return;                        // the incremental path runs instead
     const Pick p = pick(d, g);
     extern __shared__ __align__(16) int scat_sm[];
     const int K = d.K;
@@ -472,6 +476,7 @@ int seg_blocks_for(int K, int num_sms) {
 template <int V>   // floats per lane: d <= 32 * V
 __global__ void __launch_bounds__(256) k_segsum(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
+    if (d.sref && d.st->use_delta) return;                        // the incremental path runs instead
     const Pick p = pick(d, g);
     const int D = d.d, K = d.K;
     const long long KD = (long long)K * D;
@@ -594,6 +599,7 @@ struct SegItem { int i0, i1, i2, i3, j, nr, last; };
 template <int LPR>
 __global__ void __launch_bounds__(32 * SegBulk<LPR>::WPB) k_segsum_bulk(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
+    if (d.sref && d.st->use_delta) return;                        // the incremental path runs instead
     using SB = SegBulk<LPR>;
     constexpr int RB = SB::RB, RPW = 32 / LPR;
     constexpr int SR = SB::SR;
@@ -740,10 +746,113 @@ bool update_sorted(long long n_global, int dd, int K) {
     return n_global >= AAKM_SORTED_MIN_ROWS && dd <= 128 && K <= AAKM_SORTED_MAX_K;
 }
 
+// ------------------------------------------------------------------
+// Incremental update (one rank, label-sorted engine, d.sref): S(P^t) =
+// S(P^{t-1}) + sum over the rows whose label moved of (x_i into the new cluster,
+// out of the old one), N likewise.  The fixed-point sums are exact integers, so
+// this is bitwise the full recomputation; E comes from the sums (k_energy_x), so
+// X is read only for the moved rows.  Late passes move few rows: a pass whose
+// moved rows exceed delta_max takes the full sort + segmented sums instead
+// (decided on the device per evaluation; the full-path kernels exit early
+// otherwise).  S_ref = S(P^{t-1}) is written by k_finalize from the final
+// evaluation of every pass and invalidated whenever P^{t-1} or X is replaced.
+//   k_delta_scan   moved rows -> list (perm), count; label check; the decision
+//   k_delta_copy   packed [S | N] <- S_ref, changed, X2
+//   k_delta_add    one warp per moved row: +x into S_new, -x out of S_old (int64)
+__global__ void __launch_bounds__(1024) k_delta_scan(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    DevState* st = d.st;
+    if (!st->sref_valid) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) { st->use_delta = 0; st->n_upd += 1; }
+        return;
+    }
+    const Pick p = pick(d, g);
+    const int K = d.K;
+    long long* cnt = d.delta_count + g.branch;
+    int bad = 0;
+    const int lane = threadIdx.x & 31;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < d.n; base += (long long)gridDim.x * blockDim.x) {
+        const long long i = base + threadIdx.x;
+        bool moved = false;
+        if (i < d.n) {
+            const int j = p.lab[i], jp = p.prev[i];
+            if (j < 0 || j >= K) bad = 1;
+            else moved = j != jp;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, moved);
+        if (!m) continue;
+        long long b0 = 0;
+        if (lane == 0) b0 = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)__popc(m));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        const long long idx = b0 + __popc(m & ((1u << lane) - 1u));
+        if (moved && idx < d.delta_max) d.perm[idx] = (int)i;
+    }
+    if (bad) st->label_error = 1;
+    __threadfence();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(&st->delta_ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    st->delta_ctr = 0;
+    const long long nm = *(volatile long long*)cnt;
+    st->use_delta = nm <= d.delta_max ? 1 : 0;
+    st->n_upd += 1;
+    if (st->use_delta) { st->n_delta += 1; st->rows_moved += nm; }
+}
+
+__global__ void __launch_bounds__(256) k_delta_copy(Dev d, GEval g) {
+    if (!geval_active(d, g) || !d.st->use_delta) return;
+    const Pick p = pick(d, g);
+    const long long W = 2LL * d.K * d.d + d.K;                     // [S_hi | S_lo | N], N at pk_n = 2 K d
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < W; e += (long long)gridDim.x * blockDim.x)
+        p.out[e] = d.sref[e];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.out[pk_ch(d)] = d.delta_count[g.branch];                 // changed = the moved rows
+        p.out[pk_x2(d)] = d.x2[0];
+        p.out[pk_x2(d) + 1] = d.x2[1];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_delta_add(Dev d, GEval g) {
+    if (!geval_active(d, g) || !d.st->use_delta) return;
+    const Pick p = pick(d, g);
+    const int D = d.d;
+    const long long KD = (long long)d.K * D;
+    const long long nm = d.delta_count[g.branch];
+    const int lane = threadIdx.x & 31;
+    const float sc = d.fx_scale;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nm;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const long long row = d.perm[w];
+        const long long jn = p.lab[row], jo = p.prev[row];
+        for (int k = lane; k < D; k += 32) {
+            int hi = 0, lo = 0;
+            fx_add(__ldg(d.X + row * D + k), sc, hi, lo);
+            red_add_s64(p.out + jn * D + k, hi);
+            red_add_s64(p.out + KD + jn * D + k, lo);
+            red_add_s64(p.out + jo * D + k, -(long long)hi);
+            red_add_s64(p.out + KD + jo * D + k, -(long long)lo);
+        }
+        if (lane == 0) {
+            red_add_s64(p.out + pk_n(d) + jn, 1);
+            red_add_s64(p.out + pk_n(d) + jo, -1);
+        }
+    }
+}
+
 int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     if (!d.upd_sorted) {
         k_update<<<d.upd_blocks, 256, 0, s>>>(d, g);
         return 1;
+    }
+    int nl = 0;
+    if (d.sref) {                                              // incremental path (one rank), decided on the device
+        k_delta_scan<<<d.num_sms, 1024, 0, s>>>(d, g);
+        k_delta_copy<<<2 * d.num_sms, 256, 0, s>>>(d, g);
+        k_delta_add<<<4 * d.num_sms, 256, 0, s>>>(d, g);
+        nl = 3;
     }
     const size_t hs = (size_t)d.K * 4;
     const int bt = 1024;
@@ -762,12 +871,12 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     }
     if (d.xg_map) {
         switch (d.d / 4) {
-            case 1: seg_launch<1>(d, g, s); return 5;
-            case 2: seg_launch<2>(d, g, s); return 5;
-            case 4: seg_launch<4>(d, g, s); return 5;
-            case 8: seg_launch<8>(d, g, s); return 5;
-            case 16: seg_launch<16>(d, g, s); return 5;
-            default: seg_launch<32>(d, g, s); return 5;
+            case 1: seg_launch<1>(d, g, s); return 5 + nl;
+            case 2: seg_launch<2>(d, g, s); return 5 + nl;
+            case 4: seg_launch<4>(d, g, s); return 5 + nl;
+            case 8: seg_launch<8>(d, g, s); return 5 + nl;
+            case 16: seg_launch<16>(d, g, s); return 5 + nl;
+            default: seg_launch<32>(d, g, s); return 5 + nl;
         }
     }
     const int V = (d.d + 31) / 32;
@@ -777,7 +886,7 @@ int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
         case 3: k_segsum<3><<<d.upd_blocks, 256, 0, s>>>(d, g); break;
         default: k_segsum<4><<<d.upd_blocks, 256, 0, s>>>(d, g); break;
     }
-    return 5;
+    return 5 + nl;
 }
 
 // kmeans_update API: G = S / N (empty -> C_prev row, R-A15), counts.

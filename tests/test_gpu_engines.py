@@ -376,3 +376,31 @@ def test_sorted_energy_expansion_bound(offset, d):
     unit = 2.0 ** (eb - 51)                                    # 2^-30 / q
     bound = (n * d + 7 * K * d) * unit / 2 + 1e-13 * E_ora
     assert abs(part[-2] - E_ora) <= bound, (part[-2], E_ora, bound)
+
+
+@pytest.mark.parametrize("cfg,N,K,bounded", [("c4", 120_000, 128, True), ("c5", 100_000, 256, False), ("c3", 90_000, 64, False)])
+def test_incremental_update_bitwise(cfg, N, K, bounded, monkeypatch):
+    """The incremental update (S(P^t) = S(P^{t-1}) + the moved rows, taken on the
+    device when few rows move) is the full sort + segmented sums in exact
+    integers: a whole Algorithm 1 run with it (every evaluation that qualifies)
+    and without it (AAKM_DELTA_DIV=0) gives bitwise the same centroids, labels,
+    energies and counts, and the trace shows it taken."""
+    X, C0, c = make(cfg, N=N, K=K)
+    out = {}
+    for div in ("1", "0"):                                       # 1: moved rows <= n take it (always)
+        monkeypatch.setenv("AAKM_DELTA_DIV", div)
+        path = "tc16" if c.d in (64, 128) else "auto"
+        km = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, bounded=bounded, assign_path=path, max_iters=60))
+        C, lab, rep = km.run(dev(C0))
+        out[div] = (C.cpu().numpy(), lab.cpu().numpy(), rep)
+        ne, ni, moved = km.update_stats()
+        if div == "1":
+            assert ni > 0 and ni >= ne - 1 and moved > 0, (ne, ni, moved, rep)   # all but line 1
+        else:
+            assert ni == 0, (ne, ni)
+        km.close()
+    (Ca, la, ra), (Cb, lb, rb) = out["1"], out["0"]
+    assert np.array_equal(Ca.view(np.int64), Cb.view(np.int64))
+    assert np.array_equal(la, lb)
+    for k in ("iters", "n_assign", "n_accepted", "n_rejected", "energy", "converged"):
+        assert ra[k] == rb[k], (k, ra[k], rb[k])
