@@ -334,11 +334,12 @@ AAKM_API kmeans_status kmeans_last_flagged(kmeans_handle *h, int64_t *flagged /*
 AAKM_API kmeans_status kmeans_bounded_stats(kmeans_handle *h, int64_t *rows_scored /*host*/,
                                             int64_t *rows_total /*host*/);
 
-/* Update work since the last Algorithm 1 line 1 (one rank, label-sorted engine;
- * zeros otherwise): G-evaluations, how many took the incremental update
- * S(P^t) = S(P^{t-1}) + the moved rows (exact: bitwise the full sums; chosen on
- * the device when at most n_local / AAKM_DELTA_DIV (64) rows moved), and the
- * rows those moved. */
+/* Update work of this rank since the last Algorithm 1 line 1 (label-sorted
+ * engine, plain combine; zeros otherwise): G-evaluations, how many took the
+ * incremental update S(P^t) = S(P^{t-1}) + the moved rows (exact: bitwise the
+ * full sums; chosen on the device, per rank, when at most n_local /
+ * AAKM_DELTA_DIV (64) of the rank's rows moved; S_ref is the rank's own partial,
+ * allreduced out of place), and the rows those moved. */
 AAKM_API kmeans_status kmeans_update_stats(kmeans_handle *h, int64_t *n_evals /*host*/,
                                            int64_t *n_incremental /*host*/, int64_t *rows_moved /*host*/);
 

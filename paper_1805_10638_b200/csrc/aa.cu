@@ -38,17 +38,21 @@ __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const double* 
     const int lane = threadIdx.x & 31;
     const long long w0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    int na = 1;
-    double al[AAKM_H_SLOTS];
-    const double* base[AAKM_H_SLOTS];
-    if (mode == 0) {
-        na = st->n_alpha;
-        for (int q = 0; q < na; ++q) { al[q] = st->alpha[q]; base[q] = d.Gring + (long long)st->alpha_slot[q] * KD; }
-    } else if (mode == 1) {
-        al[0] = 1.0; base[0] = d.Gring + (long long)st->fb_slot * KD;
-    } else {
-        al[0] = 1.0; base[0] = src;
+    // mixing weights and their ring rows in shared memory (a runtime-indexed local
+    // array would live in local memory)
+    __shared__ double al[AAKM_H_SLOTS];
+    __shared__ const double* base[AAKM_H_SLOTS];
+    const int na = mode == 0 ? st->n_alpha : 1;
+    if (threadIdx.x < (unsigned)na) {
+        if (mode == 0) {
+            al[threadIdx.x] = st->alpha[threadIdx.x];
+            base[threadIdx.x] = d.Gring + (long long)st->alpha_slot[threadIdx.x] * KD;
+        } else {
+            al[0] = 1.0;
+            base[0] = mode == 1 ? d.Gring + (long long)st->fb_slot * KD : src;
+        }
     }
+    __syncthreads();
     float bmax = 0.f;
     for (long long j = w0; j < d.K; j += nw) {
         double nrm = 0.0;
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
     const int D = d.d;
     const long long KD = (long long)d.K * D;
     const long long* pk = st->reject ? d.packed[1] : d.packed[0];
+    const long long* pl = st->reject ? d.partial[1] : d.partial[0];   // this rank's own sums (S_ref)
     const long long slot = st->t % d.H;
     double* G = d.Gring + slot * KD;
     double* F = d.Fring + slot * KD;
@@ -180,14 +185,14 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d) {
         const double g = nj > 0 ? fx_value(pk[e], pk[KD + e], d.fx_inv) / (double)nj : c;   // G = S / N (Eq. 4)
         G[e] = g;
         F[e] = g - c;                                            // F^t = G^t - C^t (fp64)
-        if (d.sref) {                                            // S(P^t), N(P^t): the next pass's S_ref
-            d.sref[e] = pk[e];
-            d.sref[KD + e] = pk[KD + e];
+        if (d.sref) {                                            // S(P^t), N(P^t) of this rank: the next S_ref
+            d.sref[e] = pl[e];
+            d.sref[KD + e] = pl[KD + e];
         }
     }
     if (d.sref) {
         for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x)
-            d.sref[2 * KD + j] = pk[pk_n(d) + j];
+            d.sref[2 * KD + j] = pl[pk_n(d) + j];
         if (blockIdx.x == 0 && threadIdx.x == 0) st->sref_valid = 1;
     }
 }
@@ -210,20 +215,25 @@ __global__ void __launch_bounds__(128) k_gram(Dev d) {
     const int H = d.H;
     const int W = (int)(t < H - 1 ? t : H - 1);
     const long long KD = (long long)d.K * d.d;
-    double acc_g[AAKM_H_SLOTS - 1], acc_b[AAKM_H_SLOTS - 1];
+    constexpr int Q = AAKM_H_SLOTS - 1;
+    // ring offsets of F^{t-q} in shared memory, the window loops fully unrolled with a
+    // (block-uniform) predicate: the accumulators stay in registers (a runtime-indexed
+    // array went to local memory) and the W + 1 ring loads of an element issue together
+    __shared__ long long soff[AAKM_H_SLOTS];
+    if (threadIdx.x <= W) soff[threadIdx.x] = ((t - threadIdx.x) % H) * KD;
+    __syncthreads();
+    double acc_g[Q], acc_b[Q];
 #pragma unroll
-    for (int q = 0; q < AAKM_H_SLOTS - 1; ++q) { acc_g[q] = 0.0; acc_b[q] = 0.0; }
-    const double* F[AAKM_H_SLOTS];
-    for (int q = 0; q <= W; ++q) F[q] = d.Fring + ((t - q) % H) * KD;   // F^{t-q}
+    for (int q = 0; q < Q; ++q) { acc_g[q] = 0.0; acc_b[q] = 0.0; }
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < KD;
          e += (long long)gridDim.x * blockDim.x) {
-        const double ft = F[0][e];
+        const double ft = d.Fring[soff[0] + e];
         double prev = ft;
         double dft = 0.0;
 #pragma unroll
-        for (int q = 0; q < AAKM_H_SLOTS - 1; ++q) {
+        for (int q = 0; q < Q; ++q) {
             if (q < W) {
-                const double older = F[q + 1][e];
+                const double older = d.Fring[soff[q + 1] + e];
                 const double df = prev - older;                  // dF(t-q)
                 if (q == 0) dft = df;
                 acc_g[q] = fma(dft, df, acc_g[q]);
@@ -232,15 +242,19 @@ __global__ void __launch_bounds__(128) k_gram(Dev d) {
             }
         }
     }
-    __shared__ __align__(16) double red[4][2 * (AAKM_H_SLOTS - 1)];
+    __shared__ __align__(16) double red[4][2 * Q];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int q = 0; q < W; ++q) {
-        double a = acc_g[q], b = acc_b[q];
-        for (int o = 16; o; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (q < W) {
+            double a = acc_g[q], b = acc_b[q];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+            }
+            if (lane == 0) { red[w][q] = a; red[w][W + q] = b; }
         }
-        if (lane == 0) { red[w][q] = a; red[w][W + q] = b; }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < 2 * W; q += blockDim.x) {
@@ -257,40 +271,76 @@ void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0,
 // plain statement): unit-diagonal scaling, ridge, Cholesky, drop-oldest.
 // Lane r owns row r of the matrix / Cholesky factor in shared memory.
 #define FULL 0xffffffffu
+// AAKM_SOLVE_PROBE builds: clock64 phase stamps of the last k_solve (perf only)
+#ifdef AAKM_SOLVE_PROBE
+#define SOLVE_STAMP(i) do { if (d.dbg_ts && threadIdx.x == 0) d.dbg_ts[2 * 8 * 256 + (i)] = clock64(); } while (0)
+#else
+#define SOLVE_STAMP(i) do { } while (0)
+#endif
 // Fixed-order reduction of this pass's Gram partials: one warp per entry, lanes
 // stride over the blocks, then a fixed xor tree (same bytes on every rank).
 __device__ __forceinline__ void gram_reduce(const Dev& d) {
     DevState* st = d.st;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
     const int H = d.H;
     const long long t = st->t;
     const int init = st->init_mode;
     const int W = init ? 0 : (int)(t < H - 1 ? t : H - 1);
     const int ts = (int)(t % H);
-    for (int q = warp; q < 2 * W; q += 32) {
-        double v = 0.0;
-        for (int b = lane; b < d.gram_blocks; b += 32) v += d.gram_part[(long long)b * 2 * H + q];
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) {
+    // entry q = warp + u * nw (u < EPW) of warp `warp`; every load of a lane in flight
+    // at once (blocks b = lane + 32 bb), then a fixed xor tree per entry
+    constexpr int EPW = 4, BPL = (AAKM_GRAM_BLOCKS + 31) / 32;
+    double v[EPW];
+#pragma unroll
+    for (int u = 0; u < EPW; ++u) v[u] = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < BPL; ++bb) {
+        const int b = lane + 32 * bb;
+#pragma unroll
+        for (int u = 0; u < EPW; ++u) {
+            const int q = warp + u * nw;
+            if (b < d.gram_blocks && q < 2 * W) v[u] += d.gram_part[(long long)b * 2 * H + q];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < EPW; ++u) {
+        const int q = warp + u * nw;
+        double x = v[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0 && q < 2 * W) {
             if (q < W) {
                 const int s2 = (int)((t - q) % H);
-                st->gram[ts * H + s2] = v;
-                st->gram[s2 * H + ts] = v;
+                st->gram[ts * H + s2] = x;
+                st->gram[s2 * H + ts] = x;
             } else {
-                st->bvec[q - W] = v;
+                st->bvec[q - W] = x;
             }
         }
     }
 }
 
-// one block: all 32 warps reduce the Gram partials (fixed order), then warp 0 solves
-__global__ void __launch_bounds__(1024) k_solve(Dev d) {
+// One block of 512 threads: its 16 warps reduce the Gram partials (fixed order);
+// warp 0 scales and compacts the columns; one thread per lower-triangle entry
+// factors the scaled, ridged normal matrix (right-looking Cholesky, the entry in
+// a register, two block barriers per column); warp 0 substitutes.  The
+// arithmetic is the oracle's (ora_ls_solve: sqrt, correctly rounded divisions,
+// no contraction; every factor entry and forward-substitution value subtracts
+// its terms in the same ascending order); only the back substitution subtracts
+// in descending order (right-looking: a serial ascending chain per row costs
+// more than the rest of the solve).  The Gram itself is a fixed-grid sum here,
+// a serial dot there, so theta agrees to rounding, not bitwise.
+constexpr int SOLVE_THREADS = 512;
+static_assert((AAKM_H_SLOTS - 1) * AAKM_H_SLOTS / 2 <= SOLVE_THREADS, "one thread per entry (m_t <= H - 1)");
+static_assert(2 * (AAKM_H_SLOTS - 1) <= 4 * (SOLVE_THREADS / 32), "gram_reduce: EPW entries per warp");
+__global__ void __launch_bounds__(SOLVE_THREADS) k_solve(Dev d) {
     DevState* st = d.st;
     if (st->done) return;
+    SOLVE_STAMP(0);
     gram_reduce(d);
     __syncthreads();                                 // st->gram / st->bvec written by the block
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
+    SOLVE_STAMP(1);
+    const int tid = threadIdx.x, lane = tid & 31;
     const int H = d.H;
     const long long t = st->t;
     const int init = st->init_mode;
@@ -298,81 +348,98 @@ __global__ void __launch_bounds__(1024) k_solve(Dev d) {
     const int ts = (int)(t % H);
     int m_t = init ? 0 : (st->m < t ? st->m : (int)t);
     if (m_t > W) m_t = W;
-    // column a <-> dF(t - a); lane a holds column a's scale and rhs
-    const int sa = (int)((((t - lane) % H) + H) % H);
-    double s_a = 0.0, b_a = 0.0;
-    bool act = false;
-    if (lane < m_t) {
-        s_a = sqrt(st->gram[sa * H + sa]);
-        act = s_a > 0.0 && isfinite(s_a);
-        b_a = act ? st->bvec[lane] / s_a : 0.0;
-    }
-    // compact the active columns (newest first): lane i <- column idx[i]
-    const unsigned am = __ballot_sync(FULL, act);
-    int na = __popc(am);
-    int col = -1;                                   // column held by this lane after compaction
-    {
-        // the i-th set bit of am
+    __shared__ double sL[AAKM_H_SLOTS][AAKM_H_SLOTS + 1];    // the factor (written once at the end)
+    __shared__ double s_s[AAKM_H_SLOTS], s_b[AAKM_H_SLOTS];
+    __shared__ double colv[AAKM_H_SLOTS], sdiag[AAKM_H_SLOTS];
+    __shared__ int s_slot[AAKM_H_SLOTS], s_col[AAKM_H_SLOTS];
+    __shared__ int s_na, s_ok;
+    if (tid < 32) {
+        // column a <-> dF(t - a); lane a holds column a's scale and rhs
+        const int sa = (int)((((t - lane) % H) + H) % H);
+        double s_a = 0.0, b_a = 0.0;
+        bool act = false;
+        if (lane < m_t) {
+            s_a = sqrt(st->gram[sa * H + sa]);
+            act = s_a > 0.0 && isfinite(s_a);
+            b_a = act ? st->bvec[lane] / s_a : 0.0;
+        }
+        // compact the active columns (newest first): lane i <- column idx[i]
+        const unsigned am = __ballot_sync(FULL, act);
+        const int na = __popc(am);
         unsigned m = am;
-        for (int i = 0; i < lane && m; ++i) m &= m - 1;
-        col = (lane < na) ? __ffs(m) - 1 : -1;
+        for (int i = 0; i < lane && m; ++i) m &= m - 1;          // the lane-th set bit of am
+        const int col = (lane < na) ? __ffs(m) - 1 : -1;
+        const double my_s = __shfl_sync(FULL, s_a, col >= 0 ? col : 0);
+        const double my_b = __shfl_sync(FULL, b_a, col >= 0 ? col : 0);
+        if (lane < na) {
+            s_slot[lane] = (int)((((t - col) % H) + H) % H);
+            s_s[lane] = my_s; s_b[lane] = my_b; s_col[lane] = col;
+        }
+        if (lane == 0) s_na = na;
     }
-    const int my_slot = col >= 0 ? (int)((((t - col) % H) + H) % H) : 0;
-    const double my_s = __shfl_sync(FULL, s_a, col >= 0 ? col : 0);
-    const double my_b = __shfl_sync(FULL, b_a, col >= 0 ? col : 0);
-    // The compacted, scaled, ridged normal matrix in shared memory (lane i = row i):
-    // all loads issued at once, then a right-looking Cholesky in which each lane
-    // updates its own row.  Every entry sees the same subtraction sequence as the
-    // dot-product form (q ascending), so theta is unchanged bit for bit.
-    __shared__ double sA[AAKM_H_SLOTS][AAKM_H_SLOTS + 1];    // scaled matrix (kept for restarts)
-    __shared__ double sL[AAKM_H_SLOTS][AAKM_H_SLOTS + 1];    // factor, built in place
-    __shared__ double s_s[AAKM_H_SLOTS];
-    __shared__ int s_slot[AAKM_H_SLOTS];
-    if (lane < na) { s_slot[lane] = my_slot; s_s[lane] = my_s; }
-    __syncwarp();
-    if (lane < na) {
-        for (int c = 0; c <= lane; ++c) sA[lane][c] = st->gram[my_slot * H + s_slot[c]];
-        for (int c = 0; c <= lane; ++c) sA[lane][c] = sA[lane][c] / (my_s * s_s[c]) + (c == lane ? d.ridge : 0.0);
-    }
-    __syncwarp();
+    __syncthreads();
+    int na = s_na;
+    // this thread's entry (ei, ej), ej <= ei: tid = ei (ei + 1) / 2 + ej
+    int ei = 0;
+    while ((ei + 1) * (ei + 2) / 2 <= tid) ++ei;
+    const int ej = tid - ei * (ei + 1) / 2;
+    double a0 = 0.0;                                 // the scaled, ridged entry (kept for restarts)
+    if (ei < na)
+        a0 = __dadd_rn(__ddiv_rn(st->gram[s_slot[ei] * H + s_slot[ej]], __dmul_rn(s_s[ei], s_s[ej])), ei == ej ? d.ridge : 0.0);
     double phi_mine = 0.0;
+    SOLVE_STAMP(2);
+    int tries = 0;
     while (na > 0) {
-        if (lane < na)
-            for (int c = 0; c <= lane; ++c) sL[lane][c] = sA[lane][c];
-        __syncwarp();
+        ++tries;
+        const bool act = ei < na;
+        double a = a0;
         bool ok = true;
         for (int c = 0; c < na; ++c) {
-            const double diag = sL[c][c];
-            if (!(diag > 0.0) || !isfinite(diag)) { ok = false; break; }
-            const double Lcc = sqrt(diag);
-            double Lic = 0.0;
-            if (lane > c && lane < na) { Lic = sL[lane][c] / Lcc; sL[lane][c] = Lic; }
-            __syncwarp();
-            if (lane == c) sL[c][c] = Lcc;
-            if (lane > c && lane < na)
-                for (int j = c + 1; j <= lane; ++j) sL[lane][j] -= Lic * sL[j][c];
-            __syncwarp();
+            if (act && ei == c && ej == c) {         // pivot (its trailing updates are done)
+                const bool okc = a > 0.0 && isfinite(a);
+                s_ok = okc;
+                a = okc ? sqrt(a) : 0.0;             // L_cc
+                sdiag[c] = a;
+            }
+            __syncthreads();
+            if (!s_ok) { ok = false; break; }
+            if (act && ej == c && ei > c) { a = __ddiv_rn(a, sdiag[c]); colv[ei] = a; }   // L_ic
+            __syncthreads();
+            if (act && ej > c) a = __dsub_rn(a, __dmul_rn(colv[ei], colv[ej]));       // trailing update
         }
-        if (!ok) { --na; __syncwarp(); continue; }   // drop the oldest active column
-        // forward: L y = bh (lane a ends up holding y_a)
-        double y_mine = 0.0;
-        double bres = my_b;                          // b_i - sum_{q < a} L_iq y_q, q ascending
-        for (int a = 0; a < na; ++a) {
-            const double ya = __shfl_sync(FULL, bres, a) / sL[a][a];
-            if (lane == a) y_mine = ya;
-            if (lane > a && lane < na) bres -= sL[lane][a] * ya;
-        }
-        // backward: L^T phi = y (fixed xor-tree sums)
-        phi_mine = 0.0;
-        for (int a = na - 1; a >= 0; --a) {
-            double contrib = (lane > a && lane < na) ? sL[lane][a] * phi_mine : 0.0;
-            for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(FULL, contrib, o);
-            const double ya = __shfl_sync(FULL, y_mine, a);
-            const double pa = (ya - contrib) / sL[a][a];
-            if (lane == a) phi_mine = pa;
+        SOLVE_STAMP(3);
+        if (!ok) { --na; __syncthreads(); continue; }   // drop the oldest active column
+        if (act) sL[ei][ej] = a;
+        __syncthreads();
+        if (tid < 32) {
+            // forward: L y = bh, y_a = (bh_a - sum_{q < a, ascending} L_aq y_q) / L_aa
+            double y_mine = 0.0;
+            double bres = lane < na ? s_b[lane] : 0.0;
+            for (int q = 0; q < na; ++q) {
+                const double yq = __ddiv_rn(__shfl_sync(FULL, bres, q), sdiag[q]);
+                if (lane == q) y_mine = yq;
+                if (lane > q && lane < na) bres = __dsub_rn(bres, __dmul_rn(sL[lane][q], yq));
+            }
+            // backward: L^T phi = y, right-looking: phi_a = (y_a - sum_{q > a} L_qa phi_q) / L_aa
+            // with the q terms subtracted as the phi_q appear (descending q; the oracle's
+            // dot-product form subtracts them ascending -- the one ordering difference)
+            double res = y_mine;
+            for (int q = na - 1; q >= 0; --q) {
+                const double pq = __ddiv_rn(__shfl_sync(FULL, res, q), sdiag[q]);
+                if (lane == q) phi_mine = pq;
+                if (lane < q) res = __dsub_rn(res, __dmul_rn(sL[q][lane], pq));
+            }
         }
         break;
     }
+    SOLVE_STAMP(4);
+#ifdef AAKM_SOLVE_PROBE
+    if (d.dbg_ts && tid == 0) { d.dbg_ts[2 * 8 * 256 + 5] = tries; d.dbg_ts[2 * 8 * 256 + 6] = na; d.dbg_ts[2 * 8 * 256 + 7] = m_t; }
+#endif
+    (void)tries;
+    if (tid >= 32) return;
+    const int col = lane < na ? s_col[lane] : -1;
+    const double my_s = lane < na ? s_s[lane] : 1.0;
     // theta per original column: theta_col = phi / s
     double th_lane = 0.0;                            // theta of column `lane`
     {
@@ -405,7 +472,7 @@ __global__ void __launch_bounds__(1024) k_solve(Dev d) {
 }
 #undef FULL
 
-void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, 1024, 0, s>>>(d); }
+void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, SOLVE_THREADS, 0, s>>>(d); }
 
 // ---------------------------------------------------------------- advance
 __global__ void k_advance(Dev d) {

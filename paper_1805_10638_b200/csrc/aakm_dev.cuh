@@ -105,7 +105,10 @@ struct Dev {
     float fx_scale;       // 2^(22-e), |x| <= 2^e over all ranks: S in exact fixed point (update.cu)
     double fx_inv;        // 2^(e-22)
     double xn_gmax;       // max_i ||x_i|| over all ranks (rounded up): bounds every ||x_i - c||
-    long long* sref;      // incremental update (1 rank, sorted engine): [S_hi | S_lo | N] of P^{t-1}
+    long long* sref;      // incremental update (sorted engine): this rank's [S_hi | S_lo | N] of P^{t-1}
+    long long* partial[2];// where the update kernels add this rank's contributions: packed[b]
+                          // itself, or (incremental update with a communicator) a local buffer
+                          // that the allreduce reads (out of place) -- S_ref is a LOCAL partial
                           //   (nullptr: off); k_finalize writes it, k_delta_* read it
     long long delta_max;  //   at most this many moved rows take the incremental path
     long long* x2;        // sorted engine: this rank's sum_i ||x_i||^2 in units of 2^x2_e (two parts, as

@@ -114,6 +114,7 @@ const char* fused_setup(void** handle, void* comm_v, Dev& d, void* scratch, cuda
     d.pk_off1 = (long long)(pkb / 8);
     d.packed[0] = reinterpret_cast<long long*>(f->buf);
     d.packed[1] = reinterpret_cast<long long*>(reinterpret_cast<char*>(f->buf) + pkb);
+    d.partial[0] = d.packed[0]; d.partial[1] = d.packed[1];   // the flushes add into the window itself
     return nullptr;
 }
 

@@ -167,7 +167,7 @@ struct Layout {
     size_t st, st_api, C, C32, Ca32, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, sref, total,
+        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, sref, part0, part1, total,
         scratch_bytes;
     std::vector<size_t> guards;   // AAKM_WS_CANARY=1: a 256-B canary after every region
 };
@@ -250,6 +250,8 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.xchk = take(16);
     L.x2 = take(16);
     L.sref = take((2 * KD + K) * 8);                // incremental update: S_hi | S_lo | N of P^{t-1}
+    L.part0 = take(pk);                             // ... with a communicator: this rank's partials
+    L.part1 = take(pk);                             //     (branch A / B; the allreduce's send buffers)
     L.total = o;
     return L;
 }
@@ -312,10 +314,11 @@ static void refine_engine(kmeans_handle* h, const Dev& d, const GEval& g, cudaSt
 // One integer allreduce of the packed partials: exact and order-free, so every
 // rank (and every rank count) sees the same bytes.  The E slot is still zero
 // here; k_energy fills it from the reduced sums afterwards.
-static kmeans_status allreduce(kmeans_handle* h, long long* buf, cudaStream_t s) {
+// Out of place when the incremental update keeps this rank's partial (d.partial).
+static kmeans_status allreduce(kmeans_handle* h, const Dev& d, int branch, cudaStream_t s) {
     if (!h->comm) return KMEANS_OK;                 // nranks == 1 (unless cfg.comm_always)
     const size_t cnt = (size_t)pk_words(h->d);     // the E slot is still 0 here (k_energy runs after)
-    NK(h, ncclAllReduce(buf, buf, cnt, ncclInt64, ncclSum, h->comm, s));
+    NK(h, ncclAllReduce(d.partial[branch], d.packed[branch], cnt, ncclInt64, ncclSum, h->comm, s));
     return KMEANS_OK;
 }
 
@@ -380,7 +383,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     if (d.fused) {
         h->launches += launch_fused_flushed(d, g, h->fused, s);           // f4: "flushed" barrier
     } else {
-        st = allreduce(h, d.packed[branch], s);
+        st = allreduce(h, d, branch, s);
         if (st != KMEANS_OK) return st;
     }
     if (h->comm) dbg("combine", s);
@@ -395,6 +398,11 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
 static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing) {
     const Dev& d = h->d;
     CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
+    if (d.partial[0] != d.packed[0]) {                    // this rank's local partials (both branches)
+        const size_t pkb = (size_t)pk_words(d) * 8;
+        CK(h, cudaMemsetAsync(d.partial[0], 0, pkb, s));
+        CK(h, cudaMemsetAsync(d.partial[1], 0, pkb, s));
+    }
     dbg("memset", s);
     kmeans_status st = geval(h, 0, s, timing);
     if (st != KMEANS_OK) return st;
@@ -662,6 +670,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.pair_rows = (int*)(w + L.pair_rows); D.pair_j = (int2*)(w + L.pair_j);
     D.packed[0] = (long long*)(w + L.scratch + 256);
     D.packed[1] = (long long*)(w + L.packed1);
+    D.partial[0] = D.packed[0]; D.partial[1] = D.packed[1];          // local buffers: below, if used
     D.upd_part = (double*)(w + L.upd_part);
     D.seg_bh = (int*)(w + L.seg_bh);
     D.seg_off = (int*)(w + L.seg_off);
@@ -697,8 +706,8 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     if (getenv("AAKM_TC_TRACE")) {                                     // perf probe only: a 32 KB stamp buffer
-        if (cudaMalloc(&D.dbg_ts, 2 * 8 * 256 * 8) != cudaSuccess) D.dbg_ts = nullptr;
-        else cudaMemset(D.dbg_ts, 0, 2 * 8 * 256 * 8);
+        if (cudaMalloc(&D.dbg_ts, (2 * 8 * 256 + 256) * 8) != cudaSuccess) D.dbg_ts = nullptr;
+        else cudaMemset(D.dbg_ts, 0, (2 * 8 * 256 + 256) * 8);
     }
     D.Chi16 = w + L.C16h; D.Clo16 = w + L.C16l;
     D.x_scale = 1.f; D.x_inv_scale = 1.f; D.x_absmax = 0.f;
@@ -832,15 +841,21 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             dv->x2_e = eb0 - 51;
             dv->x2 = srt ? (long long*)(w + L.x2) : nullptr;
         }
-        // incremental update (update.cu k_delta_*): one rank (the rank's partial S is then the
-        // global S) and the plain combine; AAKM_DELTA_DIV: moved-row threshold n / DIV (0: off)
+        // incremental update (update.cu k_delta_*): the sorted engine and the plain combine;
+        // S_ref is this rank's own partial (with a communicator the update adds into local
+        // buffers and the allreduce reads them out of place); AAKM_DELTA_DIV: moved-row
+        // threshold n_local / DIV (0: off)
         {
             const char* dv = getenv("AAKM_DELTA_DIV");
             const long long div = dv ? atoll(dv) : 64;
-            const bool on = srt && nranks == 1 && !cfg->fused_comm && div > 0;
+            const bool on = srt && !cfg->fused_comm && div > 0;
             h->d.sref = on ? (long long*)(w + L.sref) : nullptr;
             h->d.delta_max = on ? n_local / div : 0;
             h->da.sref = nullptr; h->da.delta_max = 0;                 // API calls: always the full update
+            if (on && h->comm) {                                       // S_ref must be this rank's own sums:
+                h->d.partial[0] = (long long*)(w + L.part0);          // the update adds into local buffers,
+                h->d.partial[1] = (long long*)(w + L.part1);          // the allreduce reads them out of place
+            }
         }
         if (srt) {
             CKC(cudaMemsetAsync(w + L.x2, 0, 16, h->stream));
@@ -879,7 +894,7 @@ kmeans_status kmeans_assign(kmeans_handle* h, const double* C, const int32_t* la
     if (st != KMEANS_OK) return st;
     refine_engine(h, d, g, s);
     h->launches += 1 + launch_update(d, g, s);       // + the assignment launch
-    st = allreduce(h, d.packed[0], s);
+    st = allreduce(h, d, 0, s);
     if (st != KMEANS_OK) return st;
     h->launches += launch_energy_x(d, g, s);
     launch_energy(d, g, s);
@@ -985,7 +1000,7 @@ kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const doubl
     g.branch = 0; g.force = 1; g.lab_out = const_cast<int*>(labels); g.prev_mode = 1;
     combine(h, d, 2, C_prev, s);                          // max ||c||^2 of C_prev (the energy scale)
     h->launches += launch_update(d, g, s);
-    kmeans_status st = allreduce(h, d.packed[0], s);
+    kmeans_status st = allreduce(h, d, 0, s);
     if (st != KMEANS_OK) return st;
     launch_update_G(d, d.packed[0], C_prev, G_out, (long long*)counts_out, s);
     h->launches += 1;
@@ -1462,6 +1477,14 @@ kmeans_status kmeans_destroy(kmeans_handle* h) {
                     fprintf(f, "\n");
                 }
             fclose(f);
+        }
+        if (const char* sp = getenv("AAKM_SOLVE_TRACE")) {            // k_solve phase clocks (probe builds)
+            std::vector<unsigned long long> sv(256);
+            cudaMemcpy(sv.data(), h->d.dbg_ts + 2 * 8 * 256, 256 * 8, cudaMemcpyDeviceToHost);
+            if (FILE* f = fopen(sp, "w")) {
+                for (int i = 0; i < 256; ++i) fprintf(f, "%llu\n", sv[i]);
+                fclose(f);
+            }
         }
         cudaFree(h->d.dbg_ts);
     }

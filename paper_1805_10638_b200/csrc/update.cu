@@ -28,7 +28,9 @@ struct Pick {
     const int* lab;
     const int* prev;
     const double* C;      // C^t (fp64)
-    long long* out;       // packed [S_hi | S_lo | N | E_hi | E_lo | E | changed] (local replica)
+    long long* out;       // packed [S_hi | S_lo | N | E_hi | E_lo | E | changed]: where this rank adds
+    long long* red;       // the combined vector (after the allreduce / fused flushes): the same
+                          // buffer as out unless the rank keeps a local partial (d.partial)
     int fz;               // f4 fused combine: 0 = local adds (+ ncclAllReduce), 1 = multimem, 2 = LSA peers
     long long wo;         // word offset of this branch's buffer in the symmetric window
 };
@@ -39,7 +41,8 @@ __device__ __forceinline__ Pick pick(const Dev& d, const GEval& g) {
     p.lab = g.lab_out ? g.lab_out : d.lab[cur];
     p.prev = g.prev_mode == 0 ? d.lab[cur ^ 1] : (g.prev_mode == 2 ? g.lab_prev : nullptr);
     p.C = d.C;
-    p.out = g.packed_out ? g.packed_out : d.packed[g.branch];
+    p.out = g.packed_out ? g.packed_out : d.partial[g.branch];   // this rank's partial (= packed[b] unless local)
+    p.red = g.packed_out ? g.packed_out : d.packed[g.branch];
     p.fz = g.packed_out ? 0 : d.fused;
     p.wo = g.branch ? d.pk_off1 : 0;
     return p;
@@ -770,22 +773,86 @@ __global__ void __launch_bounds__(1024) k_delta_scan(Dev d, GEval g) {
     const int K = d.K;
     long long* cnt = d.delta_count + g.branch;
     int bad = 0;
-    const int lane = threadIdx.x & 31;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < d.n; base += (long long)gridDim.x * blockDim.x) {
-        const long long i = base + threadIdx.x;
-        bool moved = false;
-        if (i < d.n) {
-            const int j = p.lab[i], jp = p.prev[i];
-            if (j < 0 || j >= K) bad = 1;
-            else moved = j != jp;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+    // Each block owns a contiguous, 4-aligned row range, read as int4 (4 rows per
+    // thread per step: enough loads in flight to stream the two label arrays).
+    // Pass 1 counts the moved rows (and checks the labels) without atomics; one
+    // counter atomic per block reserves its list slots; pass 2 (only if the whole
+    // list can still fit under delta_max) re-reads the labels (L2) and writes the
+    // moved rows in row order.
+    const long long per = ((d.n + gridDim.x - 1) / gridDim.x + 3) & ~3LL;
+    const long long r0 = min(d.n, (long long)blockIdx.x * per), r1 = min(d.n, r0 + per);
+    // moved-row mask of rows i0 .. i0 + 3 (bit k: row i0 + k), label check into bad
+    auto moved4 = [&](long long i0, int& badv) -> unsigned {
+        int j[4], jp[4];
+        if (i0 + 3 < r1) {
+            const int4 a = *reinterpret_cast<const int4*>(p.lab + i0);
+            const int4 b = *reinterpret_cast<const int4*>(p.prev + i0);
+            j[0] = a.x; j[1] = a.y; j[2] = a.z; j[3] = a.w;
+            jp[0] = b.x; jp[1] = b.y; jp[2] = b.z; jp[3] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool in = i0 + k < r1;
+                j[k] = in ? p.lab[i0 + k] : 0;
+                jp[k] = in ? p.prev[i0 + k] : 0;
+            }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, moved);
-        if (!m) continue;
-        long long b0 = 0;
-        if (lane == 0) b0 = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)__popc(m));
-        b0 = __shfl_sync(0xffffffffu, b0, 0);
-        const long long idx = b0 + __popc(m & ((1u << lane) - 1u));
-        if (moved && idx < d.delta_max) d.perm[idx] = (int)i;
+        unsigned mk = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i0 + k >= r1) continue;
+            if (j[k] < 0 || j[k] >= K) badv = 1;
+            else if (j[k] != jp[k]) mk |= 1u << k;
+        }
+        return mk;
+    };
+    int mine = 0;
+    for (long long i0 = r0 + 4LL * threadIdx.x; i0 < r1; i0 += 4LL * blockDim.x) mine += __popc(moved4(i0, bad));
+    __shared__ int wsum[32];
+    __shared__ int itot;
+    __shared__ long long bbase;
+    __shared__ bool listed;
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) wsum[warp] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long tot = 0;
+        for (int w = 0; w < nw; ++w) tot += wsum[w];
+        bbase = tot ? (long long)atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)tot) : 0;
+        listed = tot > 0 && bbase + tot <= d.delta_max;           // else the list is not used
+    }
+    __syncthreads();
+    if (listed) {
+        long long run = bbase;                                     // next free slot of this block
+        int bad2 = 0;
+        for (long long b0 = r0; b0 < r1; b0 += 4LL * blockDim.x) {
+            const long long i0 = b0 + 4LL * threadIdx.x;
+            const unsigned mk = i0 < r1 ? moved4(i0, bad2) : 0u;
+            if (!__syncthreads_or(mk != 0)) continue;
+            const int c = __popc(mk);
+            int x = c;                                             // inclusive scan over the warp
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            if (warp == 0) {                                       // exclusive scan of the warp totals
+                const int cw = lane < nw ? wsum[lane] : 0;
+                int z = cw;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, z, o);
+                    if (lane >= o) z += y;
+                }
+                if (lane < nw) wsum[lane] = z - cw;
+                if (lane == 31) itot = z;
+            }
+            __syncthreads();
+            long long slot = run + wsum[warp] + (x - c);
+            for (unsigned m = mk; m; m &= m - 1) d.perm[slot++] = (int)(i0 + __ffs(m) - 1);
+            run += itot;
+        }
     }
     if (bad) st->label_error = 1;
     __threadfence();
@@ -919,8 +986,8 @@ __global__ void k_energy(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     const double q = energy_q(d);
-    const long long* e = p.out + pk_ehi(d);
-    p.out[pk_e(d)] = __double_as_longlong(((double)e[0] + (double)e[1] * 9.313225746154785e-10) / q);
+    const long long* e = p.red + pk_ehi(d);
+    p.red[pk_e(d)] = __double_as_longlong(((double)e[0] + (double)e[1] * 9.313225746154785e-10) / q);
 }
 
 void launch_energy(const Dev& d, const GEval& g, cudaStream_t s) { k_energy<<<1, 1, 0, s>>>(d, g); }
@@ -942,7 +1009,7 @@ __device__ __forceinline__ void efx_add(double v, long long& hi, long long& lo) 
 __global__ void __launch_bounds__(256) k_energy_x(Dev d, GEval g) {
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
-    long long* pk = p.out;                                          // local replica (after the combine)
+    long long* pk = p.red;                                          // the combined vector (local replica)
     const int D = d.d;
     const long long KD = (long long)d.K * D;
     const double q = energy_q(d);

@@ -378,19 +378,23 @@ def test_sorted_energy_expansion_bound(offset, d):
     assert abs(part[-2] - E_ora) <= bound, (part[-2], E_ora, bound)
 
 
-@pytest.mark.parametrize("cfg,N,K,bounded", [("c4", 120_000, 128, True), ("c5", 100_000, 256, False), ("c3", 90_000, 64, False)])
-def test_incremental_update_bitwise(cfg, N, K, bounded, monkeypatch):
+@pytest.mark.parametrize("cfg,N,K,bounded,comm", [("c4", 120_000, 128, True, False), ("c5", 100_000, 256, False, False),
+                                                  ("c3", 90_000, 64, False, False), ("c5", 100_000, 256, False, True)])
+def test_incremental_update_bitwise(cfg, N, K, bounded, comm, monkeypatch):
     """The incremental update (S(P^t) = S(P^{t-1}) + the moved rows, taken on the
     device when few rows move) is the full sort + segmented sums in exact
     integers: a whole Algorithm 1 run with it (every evaluation that qualifies)
     and without it (AAKM_DELTA_DIV=0) gives bitwise the same centroids, labels,
-    energies and counts, and the trace shows it taken."""
+    energies and counts, and the trace shows it taken.  comm: through a real
+    1-rank NCCL communicator, where S_ref is the rank's local partial and the
+    allreduce reads it out of place (the multi-rank form)."""
     X, C0, c = make(cfg, N=N, K=K)
     out = {}
     for div in ("1", "0"):                                       # 1: moved rows <= n take it (always)
         monkeypatch.setenv("AAKM_DELTA_DIV", div)
         path = "tc16" if c.d in (64, 128) else "auto"
-        km = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, bounded=bounded, assign_path=path, max_iters=60))
+        km = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, bounded=bounded, assign_path=path, max_iters=60,
+                                                  comm_always=comm))
         C, lab, rep = km.run(dev(C0))
         out[div] = (C.cpu().numpy(), lab.cpu().numpy(), rep)
         ne, ni, moved = km.update_stats()
