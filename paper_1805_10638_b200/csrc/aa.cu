@@ -30,6 +30,8 @@ namespace aakm {
 // C^t is fp64 (the whole Anderson state is, R-A17); fl32(C) for SIMT and ||c||^2
 // are derived from it here, the tensor engines' operands by k_csplit16 / k_csplit32.
 __global__ void __launch_bounds__(256) k_combine(Dev d, int mode, const double* src) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     DevState* st = d.st;
     if (mode == 0 && st->done) return;
     if (mode == 1 && (st->done || !st->reject)) return;
@@ -99,7 +101,7 @@ void launch_combine(const Dev& d, int mode, const double* src, cudaStream_t s) {
     int blocks = (int)((warps + 7) / 8);
     if (blocks > 1184) blocks = 1184;
     if (blocks < 1) blocks = 1;
-    k_combine<<<blocks, 256, 0, s>>>(d, mode, src);
+    launch_pdl(k_combine, blocks, 256, 0, s, d, mode, src);
 }
 
 // ---------------------------------------------------------------- control
@@ -114,6 +116,8 @@ __device__ int adjust_m(int m, int m_max, double Et, double E1, double E2, doubl
 }
 
 __global__ void k_control(Dev d, int stage) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     DevState* st = d.st;
     if (st->done) return;
     if (stage == 1 && !st->reject) return;
@@ -165,10 +169,12 @@ __global__ void k_control(Dev d, int stage) {
     }
 }
 
-void launch_control(const Dev& d, int stage, cudaStream_t s) { k_control<<<1, 1, 0, s>>>(d, stage); }
+void launch_control(const Dev& d, int stage, cudaStream_t s) { launch_pdl(k_control, 1, 1, 0, s, d, stage); }
 
 // ---------------------------------------------------------------- finalize
 __global__ void __launch_bounds__(256) k_finalize(Dev d) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     DevState* st = d.st;
     if (st->done) return;
     const int D = d.d;
@@ -201,7 +207,7 @@ void launch_finalize(const Dev& d, cudaStream_t s) {
     long long KD = (long long)d.K * d.d;
     int blocks = (int)((KD + 255) / 256);
     if (blocks > 1184) blocks = 1184;
-    k_finalize<<<blocks, 256, 0, s>>>(d);
+    launch_pdl(k_finalize, blocks, 256, 0, s, d);
 }
 
 // ---------------------------------------------------------------- gram
@@ -209,6 +215,8 @@ void launch_finalize(const Dev& d, cudaStream_t s) {
 //   q < W : <dF(t), dF(t-q)>,   q >= W : <dF(t-(q-W)), F^t>,
 // dF(tau) = F^tau - F^{tau-1} formed in fp64 from the fp64 ring.
 __global__ void __launch_bounds__(128) k_gram(Dev d) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     DevState* st = d.st;
     if (st->done || st->init_mode) return;
     const long long t = st->t;
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(128) k_gram(Dev d) {
     }
 }
 
-void launch_gram(const Dev& d, cudaStream_t s) { k_gram<<<d.gram_blocks, 128, 0, s>>>(d); }
+void launch_gram(const Dev& d, cudaStream_t s) { launch_pdl(k_gram, d.gram_blocks, 128, 0, s, d); }
 
 // ---------------------------------------------------------------- solve
 // One warp.  Eq. (7) under reading R-A14 (see oracle ora_ls_solve for the
@@ -334,6 +342,8 @@ constexpr int SOLVE_THREADS = 512;
 static_assert((AAKM_H_SLOTS - 1) * AAKM_H_SLOTS / 2 <= SOLVE_THREADS, "one thread per entry (m_t <= H - 1)");
 static_assert(2 * (AAKM_H_SLOTS - 1) <= 4 * (SOLVE_THREADS / 32), "gram_reduce: EPW entries per warp");
 __global__ void __launch_bounds__(SOLVE_THREADS) k_solve(Dev d) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     DevState* st = d.st;
     if (st->done) return;
     SOLVE_STAMP(0);
@@ -472,10 +482,12 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_solve(Dev d) {
 }
 #undef FULL
 
-void launch_solve(const Dev& d, cudaStream_t s) { k_solve<<<1, SOLVE_THREADS, 0, s>>>(d); }
+void launch_solve(const Dev& d, cudaStream_t s) { launch_pdl(k_solve, 1, SOLVE_THREADS, 0, s, d); }
 
 // ---------------------------------------------------------------- advance
 __global__ void k_advance(Dev d) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     DevState* st = d.st;
     if (st->done) {
         if (!st->final_traced) {
@@ -515,7 +527,7 @@ __global__ void k_advance(Dev d) {
     st->cur ^= 1;
 }
 
-void launch_advance(const Dev& d, cudaStream_t s) { k_advance<<<1, 1, 0, s>>>(d); }
+void launch_advance(const Dev& d, cudaStream_t s) { launch_pdl(k_advance, 1, 1, 0, s, d); }
 
 __global__ void k_reset(Dev d) {
     DevState* st = d.st;

@@ -10,6 +10,8 @@
 #define AAKM_TRACE_CAP 8192
 #define AAKM_MAXC 32               // candidates kept per flagged row
 #define AAKM_SORTED_MIN_ROWS 65536  // label-sorted update engine from this many rows
+#define AAKM_PRIV_MAX_KD 4096       // ... whose S/N fit one block's shared memory (2 K d + K int32)
+#define AAKM_PRIV_MAX_ROWS (1 << 18) // and shards small enough that one kernel beats sort + segmented sums
 #define AAKM_SORTED_MAX_K 16384     // ... and up to this many clusters (smem histograms)
 #define AAKM_SEG_BLOCKS_MAX 512     // row blocks of the histogram / scatter (Dev::seg_blocks)
 #define AAKM_MAX_RANKS 1024         // NCCL ranks per communicator this build sizes for
@@ -145,6 +147,7 @@ struct Dev {
     int nranks;
     int upd_blocks;
     int upd_sorted;       // label-sorted update engine (chosen from n_global, d, K: the same on every rank)
+    int upd_priv;         // small K*d shards of the sorted engine: one kernel, S/N in shared memory
     int seg_blocks;       // its row blocks (histogram / scatter partition; 2 per SM for K <= 4096)
     int gram_blocks;
     float tau_gamma;      // near-tie threshold factor of the active assignment engine
@@ -279,6 +282,27 @@ __device__ inline void energy_flush(long long& acc, long long& hi, long long& lo
     hi += acc >> 30;
     lo += acc & 0x3fffffffLL;
     acc = 0;
+}
+
+// ---- programmatic dependent launch (PDL) for the latency-bound kernels of a pass.
+// A kernel launched through launch_pdl may be scheduled while its predecessor in the
+// stream is still running; its FIRST statement is pdl_wait() (griddepcontrol.wait:
+// blocks until the predecessor grid completed and its writes are visible; a no-op
+// when the launch had no programmatic dependency), so nothing it reads can be stale.
+// pdl_trigger() lets the successor's launch begin early.  g_pdl (AAKM_PDL, default
+// on) switches the attribute off for A/B runs.
+extern int g_pdl;
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 // one-time kernel attribute setup (max dynamic smem); never during stream capture

@@ -79,6 +79,9 @@ __global__ void __launch_bounds__(256) k_assign_simt(Dev d, GEval g, int KT) {
             cs[e] = -2.0f * d.C32[(long long)kt * D + e];
         for (int e = threadIdx.x; e < kc; e += blockDim.x) cns[e] = d.cn[kt + e];
         __syncthreads();
+        // unrolled: the independent FFMA chains of four centroids interleave (one chain
+        // of d dependent FFMAs per score would leave the pipe idle at 1 row per thread)
+#pragma unroll 4
         for (int j = 0; j < kc; ++j) {
             float c[D];
             if constexpr (D % 4 == 0) {

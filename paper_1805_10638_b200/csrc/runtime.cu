@@ -576,6 +576,8 @@ static void x_range_error(kmeans_handle* h) {
 
 // One-time kernel attribute setup (max dynamic shared memory) PER DEVICE: the
 // attributes are device state, so a handle on a second GPU repeats it.
+namespace aakm { int g_pdl = [] { const char* v = getenv("AAKM_PDL"); return v ? atoi(v) : 1; }(); }
+
 static cudaError_t setup_device(int dev) {
     static std::mutex mu;
     static bool done[AAKM_MAX_DEVICES] = {};
@@ -838,6 +840,9 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
             dv->fx_inv = ldexp(1.0, ex - 22);
             dv->xn_gmax = xg;                                          // max_i ||x_i||, rounded up
             dv->upd_sorted = srt ? 1 : 0;
+            // one-kernel update for small K*d shards (AAKM_UPD_PRIV=0 forces the sort path)
+            dv->upd_priv = srt && (long long)k * d <= AAKM_PRIV_MAX_KD && d <= 64 && n_local <= AAKM_PRIV_MAX_ROWS &&
+                           !(getenv("AAKM_UPD_PRIV") && atoi(getenv("AAKM_UPD_PRIV")) == 0);
             dv->x2_e = eb0 - 51;
             dv->x2 = srt ? (long long*)(w + L.x2) : nullptr;
         }
@@ -848,7 +853,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         {
             const char* dv = getenv("AAKM_DELTA_DIV");
             const long long div = dv ? atoll(dv) : 64;
-            const bool on = srt && !cfg->fused_comm && div > 0;
+            const bool on = srt && !h->d.upd_priv && !cfg->fused_comm && div > 0;
             h->d.sref = on ? (long long*)(w + L.sref) : nullptr;
             h->d.delta_max = on ? n_local / div : 0;
             h->da.sref = nullptr; h->da.delta_max = 0;                 // API calls: always the full update

@@ -731,6 +731,8 @@ template <int LPR> static void seg_launch(const Dev& d, const GEval& g, cudaStre
     k_segsum_bulk<LPR><<<d.num_sms * per_sm, 32 * SB::WPB, SB::SMEM, s>>>(d, g);
 }
 
+template <int CPL> __global__ void k_update_priv(Dev d, GEval g);
+
 cudaError_t setup_update() {
     cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * AAKM_SORTED_MAX_K);
     if (e != cudaSuccess) return e;
@@ -738,6 +740,10 @@ cudaError_t setup_update() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_scatter<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAT_SMEM / 2);
     if (e != cudaSuccess) return e;
+    for (const void* f : {(const void*)k_update_priv<1>, (const void*)k_update_priv<2>}) {
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (2 * AAKM_PRIV_MAX_KD + 4096) * 4);
+        if (e != cudaSuccess) return e;
+    }
     for (cudaError_t f : {seg_attr<1>(), seg_attr<2>(), seg_attr<4>(), seg_attr<8>(), seg_attr<16>(), seg_attr<32>()})
         if (f != cudaSuccess) return f;
     return cudaSuccess;
@@ -909,13 +915,104 @@ __global__ void __launch_bounds__(256) k_delta_add(Dev d, GEval g) {
     }
 }
 
+// Small K*d shards of the sorted engine (c2: 100 000 x 16, K = 64): one kernel
+// instead of sort + segmented sums (5 launches) or the incremental path (3).
+// Each block owns <= PRIV_ROWS contiguous rows and accumulates the SAME two-part
+// fixed-point integers (fx_add: |hi| <= 2^22, |lo| <= 2^21 per row) into
+// shared-memory int32 sums (native shared atomics; 511 rows cannot overflow),
+// order-free, so bitwise the sorted engine's S; N_j likewise; then flushes its
+// nonzero entries with one int64 red each.  E still comes from the sums
+// (k_energy_x).  Lanes are grouped per row (GS = next pow2 >= d): one coalesced
+// read per row.
+constexpr int PRIV_ROWS = 511;
+template <int CPL>                                                  // coordinates per lane: ceil(d / GS)
+__global__ void __launch_bounds__(512) k_update_priv(Dev d, GEval g) {
+    if (!geval_active(d, g)) return;
+    const Pick p = pick(d, g);
+    const int D = d.d, K = d.K;
+    const int KD = K * D;
+    extern __shared__ int sp[];
+    int* sh = sp;                                                   // S_hi [K*d]
+    int* sl = sp + KD;                                              // S_lo [K*d]
+    int* sn = sp + 2 * KD;                                          // N    [K]
+    for (int e = threadIdx.x; e < 2 * KD + K; e += blockDim.x) sp[e] = 0;
+    __syncthreads();
+    int GS = 1;
+    while (GS < D && GS < 32) GS <<= 1;
+    const int gl = threadIdx.x % GS, gpb = blockDim.x / GS;       // row groups per block
+    const long long r0 = min(d.n, (long long)blockIdx.x * PRIV_ROWS), r1 = min(d.n, r0 + PRIV_ROWS);
+    const float sc = d.fx_scale;
+    long long ch = 0;
+    int bad = 0;
+    // RB rows per row group and step, every load issued before the first atomic (the
+    // loop is latency-bound: one row per step left one global round trip per row)
+    constexpr int RB = 8;
+    for (long long rb = r0 + threadIdx.x / GS; rb < r1; rb += (long long)RB * gpb) {
+        int jr[RB], jp[RB];
+        float xv[RB][CPL];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const long long row = rb + (long long)u * gpb;
+            const bool in = row < r1;
+            jr[u] = in ? p.lab[row] : -1;
+            jp[u] = in && p.prev ? p.prev[row] : -1;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int k = gl + q * GS;
+                xv[u][q] = in && k < D ? __ldcs(d.X + row * D + k) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const long long row = rb + (long long)u * gpb;
+            if (row >= r1) break;
+            const int j = jr[u];
+            if (j < 0 || j >= K) { bad = 1; continue; }          // uniform within the row group
+            if (gl == 0) {
+                if (p.prev) ch += (jp[u] != j);
+                atomicAdd(&sn[j], 1);
+            }
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int k = gl + q * GS;
+                if (k < D) {
+                    int hi = 0, lo = 0;
+                    fx_add(xv[u][q], sc, hi, lo);
+                    atomicAdd(&sh[j * D + k], hi);
+                    atomicAdd(&sl[j * D + k], lo);
+                }
+            }
+        }
+    }
+    if (bad) d.st->label_error = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && d.x2) {            // this rank's sum ||x_i||^2 (k_energy_x)
+        pk_add(d, p, pk_x2(d), d.x2[0]);
+        pk_add(d, p, pk_x2(d) + 1, d.x2[1]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < KD; e += blockDim.x) {
+        if (sh[e]) pk_add(d, p, e, sh[e]);
+        if (sl[e]) pk_add(d, p, (long long)KD + e, sl[e]);
+    }
+    for (int j = threadIdx.x; j < K; j += blockDim.x)
+        if (sn[j]) pk_add(d, p, pk_n(d) + j, sn[j]);
+    finish_changed(d, p, ch);
+}
+
 int launch_update(const Dev& d, const GEval& g, cudaStream_t s) {
     if (!d.upd_sorted) {
         k_update<<<d.upd_blocks, 256, 0, s>>>(d, g);
         return 1;
     }
+    if (d.upd_priv) {
+        const size_t sm = (size_t)(2 * d.K * d.d + d.K) * 4;
+        const unsigned nb = (unsigned)((d.n + PRIV_ROWS - 1) / PRIV_ROWS);
+        if (d.d <= 32) k_update_priv<1><<<nb, 512, sm, s>>>(d, g);
+        else k_update_priv<2><<<nb, 512, sm, s>>>(d, g);
+        return 1;
+    }
     int nl = 0;
-    if (d.sref) {                                              // incremental path (one rank), decided on the device
+    if (d.sref) {                                              // incremental path, decided on the device
         k_delta_scan<<<d.num_sms, 1024, 0, s>>>(d, g);
         k_delta_copy<<<2 * d.num_sms, 256, 0, s>>>(d, g);
         k_delta_add<<<4 * d.num_sms, 256, 0, s>>>(d, g);
@@ -1007,6 +1104,8 @@ __device__ __forceinline__ void efx_add(double v, long long& hi, long long& lo) 
     lo += __double2ll_rn((v - f) * 1073741824.0);                   // [0, 2^30], exact difference
 }
 __global__ void __launch_bounds__(256) k_energy_x(Dev d, GEval g) {
+    pdl_wait();                                     // PDL: the predecessor's writes are visible
+    pdl_trigger();
     if (!geval_active(d, g)) return;
     const Pick p = pick(d, g);
     long long* pk = p.red;                                          // the combined vector (local replica)
@@ -1055,7 +1154,7 @@ int launch_energy_x(const Dev& d, const GEval& g, cudaStream_t s) {
     if (!d.upd_sorted) return 0;
     long long blocks = ((long long)d.K * d.d + 255) / 256;
     if (blocks > 2 * d.num_sms) blocks = 2 * d.num_sms;
-    k_energy_x<<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(d, g);
+    launch_pdl(k_energy_x, (int)(blocks > 0 ? blocks : 1), 256, 0, s, d, g);
     return 1;
 }
 

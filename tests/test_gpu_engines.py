@@ -390,6 +390,7 @@ def test_incremental_update_bitwise(cfg, N, K, bounded, comm, monkeypatch):
     allreduce reads it out of place (the multi-rank form)."""
     X, C0, c = make(cfg, N=N, K=K)
     out = {}
+    monkeypatch.setenv("AAKM_UPD_PRIV", "0")                     # small K*d: the sort path (priv has no S_ref)
     for div in ("1", "0"):                                       # 1: moved rows <= n take it (always)
         monkeypatch.setenv("AAKM_DELTA_DIV", div)
         path = "tc16" if c.d in (64, 128) else "auto"
@@ -408,3 +409,36 @@ def test_incremental_update_bitwise(cfg, N, K, bounded, comm, monkeypatch):
     assert np.array_equal(la, lb)
     for k in ("iters", "n_assign", "n_accepted", "n_rejected", "energy", "converged"):
         assert ra[k] == rb[k], (k, ra[k], rb[k])
+
+
+@pytest.mark.parametrize("cfg,N,K,comm", [("c2", None, None, False), ("c2", 70_001, 100, False),
+                                          ("c1", 80_000, 37, False), ("c2", None, None, True)])
+def test_private_update_bitwise(cfg, N, K, comm, monkeypatch):
+    """The one-kernel update of small K*d shards (shared-memory int32 sums of the
+    same two-part fixed-point integers, <= 511 rows per block) against the
+    label-sorted engine (sort + segmented sums, AAKM_UPD_PRIV=0): whole Algorithm 1
+    runs bitwise equal (centroids, labels, energies, counts), ragged row counts,
+    odd K, d = 2 and 16, and through a 1-rank NCCL communicator; and the partials
+    of one G-evaluation equal the oracle's exact sums."""
+    X, C0, c = make(cfg, N=N, K=K)
+    out = {}
+    for priv in ("1", "0"):
+        monkeypatch.setenv("AAKM_UPD_PRIV", priv)
+        km = aakm.KMeans(dev(X), c.K, aakm.config(m0=5, max_iters=200, comm_always=comm))
+        C, lab, rep = km.run(dev(C0))
+        out[priv] = (C.cpu().numpy(), lab.cpu().numpy(), rep)
+        km.close()
+    (Ca, la, ra), (Cb, lb, rb) = out["1"], out["0"]
+    assert np.array_equal(Ca.view(np.int64), Cb.view(np.int64))
+    assert np.array_equal(la, lb)
+    for k in ("iters", "n_assign", "n_accepted", "n_rejected", "energy", "converged"):
+        assert ra[k] == rb[k], (k, ra[k], rb[k])
+    # one G-evaluation's sums against the oracle (Eq. 4: G = S / N, empty -> C row)
+    monkeypatch.setenv("AAKM_UPD_PRIV", "1")
+    km = aakm.KMeans(dev(X), c.K, aakm.config())
+    lab0, _, _ = km.assign(dev(C0))
+    G, n = km.update(lab0, dev(C0))
+    G_ora, n_ora = oracle.update(X, lab0.cpu().numpy(), C0.astype(np.float64))
+    assert np.array_equal(n.cpu().numpy(), n_ora)
+    np.testing.assert_allclose(G.cpu().numpy(), G_ora, rtol=1e-12, atol=1e-12)
+    km.close()
