@@ -36,9 +36,12 @@
 //   warps 0-15 epilogue, four per SMSP (TMEM lane quarter = warp % 4): each
 //              column quarter scores 64 of the 256 columns of every tile (two
 //              tcgen05.ld.x32 in flight, accumulator released right after) with
-//              4 independent top-2 trackers per thread; quarters merge per row
-//              through shared memory (KIND 1 also keeps the runner-up's index
-//              and a lower bound on every other key: the two-centroid test)
+//              2 independent top-2 trackers per thread (4 measured 8 % slower on
+//              c3, 1 % on c5: the tracker merge is per row tile); quarters merge
+//              per row through shared memory, handed over on mbarriers so no
+//              quarter waits for a merge, the merging quarter rotating per row
+//              tile when NT == 1 (KIND 1 also keeps the runner-up's index and a
+//              lower bound on every other key: the two-centroid test)
 // X is read from HBM once per pass; C tiles stream from L2.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -50,7 +53,13 @@ namespace aakm {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BN = 128;
-constexpr int NTRK = 4;                            // independent top-2 trackers per thread (ILP)
+// independent top-2 trackers per epilogue thread, per kind (ILP against the merge cost)
+#ifndef AAKM_NTRK0
+#define AAKM_NTRK0 2
+#endif
+#ifndef AAKM_NTRK1
+#define AAKM_NTRK1 2
+#endif
 constexpr int NQ = 4;                              // epilogue column quarters (warps per SMSP)
 // 16 epilogue warps + producer + MMA issuer + NSW X-splitter warps (2, or 4: one per SMSP)
 constexpr int tc_threads(int nsw) { return 32 * (NQ * 4 + 2 + nsw); }
@@ -62,6 +71,8 @@ constexpr int ATOM_BYTES_X = TC_BM * 128;          // one 32-element K-atom of t
 constexpr int STAGE_MAIN = 2 * TC_BN * 128;        // C_hi atom + C_lo atom
 constexpr int STAGE_BYTES = STAGE_MAIN + AAKM_CNIMG_BYTES;   // + the folded block (last atom only)
 constexpr int SMEM_LIMIT = 232448;                 // 227 KB opt-in
+// quarter-merge handoff slots: a ring of 4 when every row tile is one accumulator tile
+__host__ __device__ constexpr int nmrg_of(int NT) { return NT == 1 ? 2 : 1; }
 
 // Error bound of the 3xTF32 scores: per-product split
 // error <= 3 * 2^-20 |x_k c_k|; tensor-core fp32 accumulation over the
@@ -419,9 +430,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint8_t* opb = (inplace || DX) ? smem : xst + nst * A * ATOM_BYTES_X;   // operand buffers [hi | lo (| A block)]
     uint8_t* stg = opb + nxb * OPB;                                // S stages of C operand atoms (this CTA's half)
     float* xnorm = reinterpret_cast<float*>(stg + (size_t)S * STAGE_BYTES);   // [XRr][128] ||x||^2 ring (slot = iteration % XRr)
-    // [NMRG][NQ-1][128] partial results of quarters 1..3: double-buffered when every row
-    // tile is one accumulator tile (NT == 1), where the merge is a large share of a tile
-    const int nmrg = NT == 1 ? 2 : 1;
+    // [NMRG][NQ-1][128] partial results of the three non-merging quarters: double-buffered
+    // when every row tile is one accumulator tile (NT == 1), where the merge is a large
+    // share of a tile
+    const int nmrg = nmrg_of(NT);
     float4* mrg = reinterpret_cast<float4*>(xnorm + XRr * TC_BM);
     uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + nmrg * (NQ - 1) * TC_BM);
     uint64_t* full = bars;                                         // [S]  stage landed (leader: both halves)
@@ -432,7 +444,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
     uint64_t* opready = stfull + 8;                                // [4] operand buffer split (leader: both CTAs)
     uint64_t* opempty = opready + 4;                               // [4] operand buffer consumed by the MMAs
     uint64_t* xready = opempty + 4;                                // [XRr] ||x||^2 slot written (epilogue side)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + XRr);
+    // quarter handoff per TMEM lane quarter q and slot: mfull (the three non-merging
+    // quarters wrote their partials: 96 arrivals, only the merging quarter waits on it) and
+    // mfree (the merging quarter read them: 32 arrivals), so no quarter waits for a merge
+    uint64_t* mfull = xready + XRr;                                // [4][nmrg]
+    uint64_t* mfree = mfull + 4 * nmrg;                            // [4][nmrg]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mfree + 4 * nmrg);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = d.K;
@@ -450,6 +467,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
         for (int b = 0; b < 4; ++b) { mbar_init(opready + b, NSW * CG); mbar_init(opempty + b, 1); }
         for (int b = 0; b < 8; ++b) mbar_init(stfull + b, 1);
         for (int b = 0; b < XRr; ++b) mbar_init(xready + b, NSW);
+        for (int b = 0; b < 4 * nmrg; ++b) { mbar_init(mfull + b, (NQ - 1) * 32); mbar_init(mfree + b, 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_SPLIT) {
@@ -794,11 +812,16 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
             // accumulators); the ring has one slot more (xr_of), so it neither
             // aliases a phase nor overwrites an unread slot.
             mbar_wait(xready + (it & (XRr - 1)), (uint32_t)(it / XRr) & 1u);
-            const float xn = cq == 0 ? xnorm[(it & (XRr - 1)) * TC_BM + r] : 0.f;
+            // the quarter that merges this row tile: rotating when every row tile is one
+            // accumulator tile (NT == 1: the merge would otherwise lengthen one warp's
+            // chain every tile), else quarter 0
+            const int mg = NT == 1 ? (int)(it & (NQ - 1)) : 0;
+            const float xn = cq == mg ? xnorm[(it & (XRr - 1)) * TC_BM + r] : 0.f;
             // NTRK independent top-2 trackers.  MODE 0 keys pack the column's position
             // inside its 32-column batch into the 5 low mantissa bits of the score (a
             // <= 2^-18 |s| perturbation, added to tau), so one FMNMX carries value and
             // index; BB remembers the batch base where each tracker's best moved.
+            constexpr int NTRK = KIND == 0 ? AAKM_NTRK0 : AAKM_NTRK1;
             float B1[NTRK], B2[NTRK];
             int BB[NTRK];
 #pragma unroll
@@ -880,18 +903,31 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     const int iu = BB[u] + (int)(__float_as_uint(B1[u]) & 31u);
                     top2l_merge(t, B1[u], iu, B2[u], -1, B2[u]);
                 }
-                if (cq > 0) {
+                if (d.dbg & 512) {                                  // probe: no quarter merge (labels wrong)
+                    if (cq == 0 && frow < n_rows) lab_out[frow] = t.i1;
+                    continue;
+                }
+                const int ms = (int)(it & (nmrg - 1));                     // handoff slot
+                const uint32_t mk = (uint32_t)(nmrg == 1 ? it : (it >> 1));    // its use count (nmrg 1 or 2)
+                if (cq != mg) {
                     const unsigned hi = (t.i2 >= 0 && (t.i2 >> 5) < 0xFFF) ? (unsigned)(t.i2 >> 5) : 0xFFFu;
                     const float Lp = __uint_as_float((__float_as_uint(t.L) & ~0xFFFu) | hi);
-                    mrg[((nmrg == 2 ? (int)(it & 1) : 0) * (NQ - 1) + cq - 1) * TC_BM + r] = make_float4(t.b1, t.b2, __int_as_float(t.i1), Lp);
+                    if (mk > 0) mbar_wait(mfree + q * nmrg + ms, (mk - 1) & 1u);   // quarter 0 read the slot
+                    const int o = (cq - mg + NQ - 1) & (NQ - 1);                  // 0 .. NQ - 2
+                    mrg[(ms * (NQ - 1) + o) * TC_BM + r] = make_float4(t.b1, t.b2, __int_as_float(t.i1), Lp);
+                    mbar_arrive(mfull + q * nmrg + ms);                          // release: the partials
                 }
-                asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");
-                if (cq == 0) {
+                if (cq == mg) {
+                    mbar_wait(mfull + q * nmrg + ms, mk & 1u);                   // acquire: the other quarters
+                    float4 mq[NQ - 1];
+#pragma unroll
+                    for (int o = 0; o < NQ - 1; ++o) mq[o] = mrg[(ms * (NQ - 1) + o) * TC_BM + r];
+                    mbar_arrive(mfree + q * nmrg + ms);
                     float b1, b2;
                     int i1;
 #pragma unroll
                     for (int o = 0; o < NQ - 1; ++o) {
-                        const float4 m = mrg[((nmrg == 2 ? (int)(it & 1) : 0) * (NQ - 1) + o) * TC_BM + r];
+                        const float4 m = mq[o];
                         const int oi1 = __float_as_int(m.z);
                         const unsigned hi = __float_as_uint(m.w) & 0xFFFu;
                         const int oi2 = hi == 0xFFFu ? -1 : (int)(hi << 5) + (int)(__float_as_uint(m.y) & 31u);
@@ -942,11 +978,6 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                     push_flag_tc(d, g.branch, flag && !pair, row, b1, tau);
                     push_pair_tc(d, g.branch, pair, row, i1, t.i2, b1, tau);
                 }
-                // double-buffered (NT == 1): no second barrier.  Quarters 1..3 write this
-                // slot again (tile it + 2) only after the next tile's barrier, which quarter 0
-                // reaches once it has read it here, so they start the next tile while
-                // quarter 0 merges this one
-                if (nmrg == 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(NQ * 32) : "memory");   // mrg reusable
                 if (warp == 0 && lane == 0) tc_stamp(d, 5, it);    // epilogue done with the tile
             } else if (frow < n_rows) {
                 d.cand_cnt[frow * NQ + cq] = cnt;
@@ -981,14 +1012,15 @@ static int env_cap(const char* name, int dflt) {
 }
 
 static size_t smem_need(int kind, int A, int S, int NT, int NXB, int cg = 2, int nst = 2) {
+    const int nm = nmrg_of(NT);
     const int natom = kind ? A / 2 : A;
     const int staging = (NXB == 0 || kind == 1) ? 0 : nst * A;   // in place / direct X: none; KIND 0: nst tiles
     const int nb = NXB == 0 ? 1 : NXB;
     const size_t opb = (size_t)2 * natom * ATOM_BYTES_X + AAKM_CNIMG_BYTES;
     const int xr = xr_of(NT, NXB, cg);
     return 1024 + (size_t)staging * ATOM_BYTES_X + (size_t)nb * opb + (size_t)S * STAGE_BYTES +
-           (size_t)xr * TC_BM * 4 + (NT == 1 ? 2 : 1) * (NQ - 1) * TC_BM * 16 +
-           (size_t)(2 * S + 24 + xr) * 8 + 16;
+           (size_t)xr * TC_BM * 4 + (size_t)nm * (NQ - 1) * TC_BM * 16 +
+           (size_t)(2 * S + 24 + xr + 8 * nm) * 8 + 16;
 }
 
 // NT == 1 (K <= 256 with CTA pairs), KIND 0: the C operand tile never changes, so it
