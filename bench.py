@@ -381,6 +381,10 @@ def main():
         line["update_roofline"] = {"bound": "hbm", "achieved": ubytes / (u_avg / 1e3) / 1e9,
                                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                    "frac": ubytes / (u_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                   # the peak is a copy (read + write); the update is a read stream
+                                   # (X once + the labels), which can run slightly above it (a torch
+                                   # fp32 sum over the same X measured 6.35 TB/s on this pool)
+                                   "peak_kind": "copy (read+write), MEASURED_PEAKS.json",
                                    "kernel": "update (label sort + segmented sums; E from the sums by k_energy_x)",
                                    "avg_ms": u_avg, "launches": u_n}
     km.close()
