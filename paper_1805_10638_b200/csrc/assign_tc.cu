@@ -31,8 +31,10 @@
 //   warps 18-19 TMEM allocator (warp 18), then the X splitter: KIND 0 TMAs two
 //              fp32 staging tiles (two row tiles ahead), KIND 1 reads its rows
 //              straight from global (L2-prefetched one tile ahead; gather4 for
-//              row lists); both write the double-buffered hi/lo operand tiles
-//              (+ KIND 1's per-row folded A block) + ||x||^2
+//              row lists), eight lanes per row and 16 float4 loads in flight per
+//              lane (one thread per row serialised its L2 round trips: c4 2.62 ->
+//              2.40 ms per 4 M rows); both write the double-buffered hi/lo operand
+//              tiles (+ the per-row folded A block) + ||x||^2
 //   warps 0-15 epilogue, four per SMSP (TMEM lane quarter = warp % 4): each
 //              column quarter scores 64 of the 256 columns of every tile (two
 //              tcgen05.ld.x32 in flight, accumulator released right after) with
@@ -53,6 +55,10 @@ namespace aakm {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BN = 128;
+// float4s in flight per lane in the KIND 1 splitter
+#ifndef AAKM_SPLIT_F4
+#define AAKM_SPLIT_F4 16
+#endif
 // independent top-2 trackers per epilogue thread, per kind (ILP against the merge cost)
 #ifndef AAKM_NTRK0
 #define AAKM_NTRK0 2
@@ -696,67 +702,96 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
 #pragma unroll
                 for (int rr = 0; rr < RPT; ++rr) xsave[rr] = xnk[rr] = (q[rr][0] + q[rr][1]) + (q[rr][2] + q[rr][3]);
             }
-#pragma unroll (KIND == 0 ? RPT : 1)
-            for (int rr = 0; rr < RPT; ++rr) {
+#pragma unroll
+            for (int rr = 0; rr < (KIND == 0 ? RPT : 0); ++rr) {      // KIND 0: per-row norms + folded block
                 const int r = t + SPT * rr;
-                float xn = 0.f;
-                if (KIND == 0) {
-                    xn = xnk[rr];
-                } else {
-                    // the row's source, resolved ONCE (through the row list for MODE 1/2): the
-                    // compiler cannot hoist a load of rows_of past the shared-memory stores below
-                    const long long grow = tile_of(it) * TC_BM + r;
-                    const bool live_row = grow < n_rows;
-                    const long long xrow = !live_row ? 0
-                                         : (MODE == 1 || use_list) ? (long long)__ldg(rows_of + grow) : grow;
-                    const float4* srow = reinterpret_cast<const float4*>(Xsrc + xrow * A * 32);
+                const float xn = xnk[rr];
+                xnorm[(it & (XRr - 1)) * TC_BM + r] = xn;
+                uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;      // A side of the folded block, row r (tf32)
+                const float v = fmaf(xn, hxs, 6.0f);
+                const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                const float m = __uint_as_float(__float_as_uint(v - h) & 0xFFFFE000u);
+                const float l = (v - h) - m;                       // exact: v = h + m + l
+                *reinterpret_cast<float4*>(fa + cnimg_off(r, 0)) = make_float4(1.f, 1.f, 1.f, h);
+                *reinterpret_cast<float4*>(fa + cnimg_off(r, 16)) = make_float4(m, l, 0.f, 0.f);
+            }
+            if (KIND == 1 && !((d.dbg & 256) && it >= nxb)) {
+                // KIND 1: eight lanes per row, four rows per warp instruction; lane sub holds
+                // the float4s sub, sub + 8, ... of its row (every load instruction reads 128
+                // contiguous bytes of four rows) and 8 float4s per lane are in flight;
+                // ||x||^2 by a per-lane chain over its 4A values and an xor tree over the
+                // row's 8 lanes (any summation order is inside the fp32 bound that the
+                // near-tie threshold and the Hamerly decode assume); each lane writes one
+                // of the row's 8 folded-block words.  Probe 256 skips it (timing only: the
+                // operand buffer keeps the tile of nxb row tiles ago).
+                constexpr int RPW = 4;                             // rows per warp instruction
+                constexpr int NG = TC_BM / (NSW * RPW);            // row groups per warp per tile
+                constexpr int RB = AAKM_SPLIT_F4 / A;              // row groups per batch (float4s in flight per lane)
+                const int wi = warp - W_SPLIT;
+                const int sub = lane & 7, rsub = lane >> 3;
+                uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
+                for (int g0 = 0; g0 < NG; g0 += RB) {
+                    float4 v[RB][A];
 #pragma unroll
-                    for (int a16 = 0; a16 < NATOM; ++a16) {
+                    for (int b = 0; b < RB; ++b) {
+                        const int r = ((g0 + b) * NSW + wi) * RPW + rsub;
+                        const long long grow = tile_of(it) * TC_BM + r;
+                        const bool live_row = grow < n_rows;
+                        const long long xrow = !live_row ? 0
+                                             : (MODE == 1 || use_list) ? (long long)__ldg(rows_of + grow) : grow;
+                        const float4* src = reinterpret_cast<const float4*>(Xsrc + xrow * (A * 32)) + sub;
 #pragma unroll
-                        for (int c16 = 0; c16 < 8; ++c16) {
-                            // columns 64 a16 + 8 c16 .. + 8 of row r (zeros past the last row)
-                            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-                            if (live_row) {
-                                const float4* src = srow + a16 * 16 + c16 * 2;
-                                v0 = __ldg(src); v1 = __ldg(src + 1);
-                            }
-                            const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                            uint32_t hp[4], lp[4];
+                        for (int i = 0; i < A; ++i)
+                            v[b][i] = live_row ? __ldg(src + 8 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    float q[RB];
 #pragma unroll
-                            for (int e = 0; e < 8; e += 2) {
-                                xn = fmaf(vv[e], vv[e], xn); xn = fmaf(vv[e + 1], vv[e + 1], xn);
-                                const float s0 = vv[e] * inv_sx, s1 = vv[e + 1] * inv_sx;       // exact (power of 2)
-                                const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
-                                const __half l0 = __float2half_rn(s0 - __half2float(h0));
-                                const __half l1 = __float2half_rn(s1 - __half2float(h1));
-                                hp[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-                                lp[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-                            }
-                            const int off = a16 * ATOM_BYTES_X + r * 128 + ((c16 ^ (r & 7)) << 4);
-                            *reinterpret_cast<uint4*>(xhi + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-                            *reinterpret_cast<uint4*>(xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+                    for (int b = 0; b < RB; ++b) {
+                        q[b] = 0.f;
+#pragma unroll
+                        for (int i = 0; i < A; ++i) {
+                            q[b] = fmaf(v[b][i].x, v[b][i].x, q[b]); q[b] = fmaf(v[b][i].y, v[b][i].y, q[b]);
+                            q[b] = fmaf(v[b][i].z, v[b][i].z, q[b]); q[b] = fmaf(v[b][i].w, v[b][i].w, q[b]);
                         }
                     }
-                }
-                xnorm[(it & (XRr - 1)) * TC_BM + r] = xn;
-                if (KIND == 0) {                                   // A side of the folded block, row r (tf32)
-                    uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
-                    const float v = fmaf(xn, hxs, 6.0f);
-                    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-                    const float m = __uint_as_float(__float_as_uint(v - h) & 0xFFFFE000u);
-                    const float l = (v - h) - m;                   // exact: v = h + m + l
-                    *reinterpret_cast<float4*>(fa + cnimg_off(r, 0)) = make_float4(1.f, 1.f, 1.f, h);
-                    *reinterpret_cast<float4*>(fa + cnimg_off(r, 16)) = make_float4(m, l, 0.f, 0.f);
-                } else {                                           // A side of the folded block, row r (fp16)
-                    uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
-                    const float v = fmaf(xn, hxs, 6.0f);
-                    const __half h = __float2half_rn(v);
-                    const __half l = __float2half_rn(v - __half2float(h));
-                    *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, 0)) = 0x3C003C00u;            // (1, 1)
-                    *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, 4)) =
-                        (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(l) << 16);
 #pragma unroll
-                    for (int b = 8; b < 32; b += 4) *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, b)) = 0u;
+                    for (int o = 4; o; o >>= 1)
+#pragma unroll
+                        for (int b = 0; b < RB; ++b) q[b] += __shfl_xor_sync(0xffffffffu, q[b], o);
+#pragma unroll
+                    for (int b = 0; b < RB; ++b) {
+                        const int r = ((g0 + b) * NSW + wi) * RPW + rsub;
+#pragma unroll
+                        for (int i = 0; i < A; ++i) {
+                            const float4 w = v[b][i];
+                            const float s0 = w.x * inv_sx, s1 = w.y * inv_sx;          // exact (power of 2)
+                            const float s2 = w.z * inv_sx, s3 = w.w * inv_sx;
+                            const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
+                            const __half h2 = __float2half_rn(s2), h3 = __float2half_rn(s3);
+                            const __half l0 = __float2half_rn(s0 - __half2float(h0));
+                            const __half l1 = __float2half_rn(s1 - __half2float(h1));
+                            const __half l2 = __float2half_rn(s2 - __half2float(h2));
+                            const __half l3 = __float2half_rn(s3 - __half2float(h3));
+                            const int c = 4 * (sub + 8 * i);               // first column of this float4
+                            const int off = (c >> 6) * ATOM_BYTES_X + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) +
+                                            ((c & 4) << 1);
+                            *reinterpret_cast<uint2*>(xhi + off) =
+                                make_uint2((uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16),
+                                           (uint32_t)__half_as_ushort(h2) | ((uint32_t)__half_as_ushort(h3) << 16));
+                            *reinterpret_cast<uint2*>(xlo + off) =
+                                make_uint2((uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16),
+                                           (uint32_t)__half_as_ushort(l2) | ((uint32_t)__half_as_ushort(l3) << 16));
+                        }
+                        if (sub == 0) xnorm[(it & (XRr - 1)) * TC_BM + r] = q[b];
+                        // A side of the folded block, row r (fp16): word sub of (1, 1 | h, l | 0 ...)
+                        const float vf = fmaf(q[b], hxs, 6.0f);
+                        const __half fh = __float2half_rn(vf);
+                        const __half fl = __float2half_rn(vf - __half2float(fh));
+                        const uint32_t fw = sub == 0 ? 0x3C003C00u
+                                          : sub == 1 ? ((uint32_t)__half_as_ushort(fh) | ((uint32_t)__half_as_ushort(fl) << 16))
+                                                     : 0u;
+                        *reinterpret_cast<uint32_t*>(fa + cnimg_off(r, 4 * sub)) = fw;
+                    }
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
