@@ -9,6 +9,7 @@
 // (and captured in the graph).
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -69,6 +70,23 @@ struct kmeans_handle {
     std::vector<size_t> guards;                              // AAKM_WS_CANARY: canary offsets in the workspace
     char* ws_base = nullptr;
     void* fused = nullptr;                                   // f4 fused combine resources (comm.cu)
+};
+
+// NVTX ranges (SURVEY §5 tracing): one per API call and per Algorithm 1 step as it
+// is enqueued -- the eager launches of aa_step / assign / update / seed_pp sit
+// inside them (ncu --nvtx --nvtx-include "aakm:assign/" selects one step's
+// kernels); under graph capture they mark the capture.  No-ops without a tool.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
+// consecutive steps inside one scope: to() closes the open range and opens the next
+struct NvtxStep {
+    bool on = false;
+    void to(const char* name) { if (on) nvtxRangePop(); nvtxRangePushA(name); on = true; }
+    ~NvtxStep() { if (on) nvtxRangePop(); }
 };
 
 static thread_local std::string g_create_err;
@@ -342,11 +360,14 @@ static kmeans_status timed_assign(kmeans_handle* h, const Dev& d, const GEval& g
 
 // One G-evaluation (assign -> refine -> update partials -> allreduce -> control).
 static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool timing) {
+    Nvtx r0(branch == 0 ? "aakm:G-evaluation" : "aakm:G-evaluation (fallback)");
     const Dev& d = h->d;
     GEval g{};
     g.branch = branch; g.force = 0; g.prev_mode = 0;
     if (branch == 1) { combine(h, d, 1, nullptr, s); dbg("combine_fb", s); }
     kmeans_status st = KMEANS_OK;
+    NvtxStep step;
+    step.to("aakm:assign");                                 // Eq. 3: contraction + argmin + refine
     if (branch == 0 && h->feed_chunks > 0) {                // streamed X: each row chunk once it landed
         const long long T = (d.n + 127) / 128;
         for (int c = 0; c < h->feed_chunks; ++c) {
@@ -364,6 +385,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
     dbg("assign", s);
     refine_engine(h, d, g, s);
     dbg("refine", s);
+    step.to("aakm:update");                                 // Eq. 4: partial sums S, N (+ combine)
     std::pair<cudaEvent_t, cudaEvent_t>* uevp = nullptr;
     if (timing && branch == 0) {
         if (h->uev_used == h->uev.size()) {
@@ -387,6 +409,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
         if (st != KMEANS_OK) return st;
     }
     if (h->comm) dbg("combine", s);
+    step.to("aakm:energy+control");                         // Eq. 1 and Algorithm 1's rules
     h->launches += launch_energy_x(d, g, s);        // sorted engine: E's parts from X2, N, S, C
     launch_control(d, branch, s);                   // E from the reduced parts + Algorithm 1 control
     dbg("control", s);
@@ -396,6 +419,7 @@ static kmeans_status geval(kmeans_handle* h, int branch, cudaStream_t s, bool ti
 
 // One loop pass of Algorithm 1 (also used for line 1 when init_mode is set).
 static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing) {
+    Nvtx r0("aakm:pass");
     const Dev& d = h->d;
     CK(h, cudaMemsetAsync(h->scratch, 0, h->scratch_bytes, s));
     if (d.partial[0] != d.packed[0]) {                    // this rank's local partials (both branches)
@@ -438,6 +462,7 @@ static kmeans_status enqueue_pass(kmeans_handle* h, cudaStream_t s, bool timing)
         st = geval(h, 1, s, false);
         if (st != KMEANS_OK) return st;
     }
+    Nvtx r2("aakm:anderson");                               // Eq. 6-8: G, F, Gram, solve, mix
     launch_finalize(d, s);
     dbg("finalize", s);
     launch_gram(d, s);
@@ -627,6 +652,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
                             int32_t d, int32_t k, const kmeans_config* cfg, void* workspace,
                             size_t workspace_bytes, int32_t rank, int32_t nranks, const void* uid128,
                             kmeans_stream_t stream) {
+    Nvtx nvtx_("kmeans_create");
     std::string why;
     if (!out) { g_create_err = "out is NULL"; return KMEANS_ERR_INVALID; }
     *out = nullptr;
@@ -886,6 +912,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
 
 kmeans_status kmeans_assign(kmeans_handle* h, const double* C, const int32_t* labels_prev, int32_t* labels_out,
                             double* energy_out, int64_t* changed_out) {
+    Nvtx nvtx_("kmeans_assign");
     LIVE(h);
     if (!C || (!labels_out && h->d.n > 0)) FAIL(h, KMEANS_ERR_INVALID, "C or labels_out is NULL");
     cudaStream_t s = h->stream;
@@ -995,6 +1022,7 @@ kmeans_status kmeans_bounds_repeat(kmeans_handle* h, float* ub1_out, float* lb1_
 
 kmeans_status kmeans_update(kmeans_handle* h, const int32_t* labels, const double* C_prev, double* G_out,
                             int64_t* counts_out) {
+    Nvtx nvtx_("kmeans_update");
     LIVE(h);
     if ((!labels && h->d.n > 0) || !C_prev || !G_out) FAIL(h, KMEANS_ERR_INVALID, "NULL labels/C_prev/G_out");
     cudaStream_t s = h->stream;
@@ -1071,6 +1099,7 @@ static kmeans_status step_info(kmeans_handle* h, kmeans_step_info* info, double*
 }
 
 kmeans_status kmeans_aa_step(kmeans_handle* h, const double* C0, kmeans_step_info* info, double* theta_out) {
+    Nvtx nvtx_("kmeans_aa_step");
     LIVE(h);
     kmeans_status st;
     if (C0) st = start(h, C0);
@@ -1084,6 +1113,7 @@ kmeans_status kmeans_aa_step(kmeans_handle* h, const double* C0, kmeans_step_inf
 // each chunk as it lands, so the transfer overlaps the contraction.
 kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t chunks, kmeans_step_info* info,
                                   double* theta_out) {
+    Nvtx nvtx_("kmeans_aa_step_host");
     LIVE(h);
     const Dev& d = h->d;
     if (!h->cfg.x_refresh) FAIL(h, KMEANS_ERR_INVALID, "kmeans_aa_step_host needs cfg.x_refresh = 1 at create");
@@ -1139,6 +1169,7 @@ kmeans_status kmeans_aa_step_host(kmeans_handle* h, const float* X_host, int32_t
 }
 
 kmeans_status kmeans_run(kmeans_handle* h, const double* C0, double* C_out, int32_t* labels_out, kmeans_report* rep) {
+    Nvtx nvtx_("kmeans_run");
     LIVE(h);
     if (!C0 || !rep) FAIL(h, KMEANS_ERR_INVALID, "C0 or rep is NULL");
     cudaStream_t s = h->stream;
@@ -1368,6 +1399,7 @@ int64_t kmeans_launch_count(const kmeans_handle* h) { return h ? h->launches : 0
 // plus three small kernels; with nranks > 1 three tiny allreduces per round
 // (max D2, the ranks' weight totals, the chosen row).
 kmeans_status kmeans_seed_pp(kmeans_handle* h, const double* u, float* C_out, int64_t* idx_out) {
+    Nvtx nvtx_("kmeans_seed_pp");
     LIVE(h);
     const Dev& d = h->d;
     const int K = d.K;
@@ -1468,6 +1500,7 @@ const char* kmeans_assign_path_name(const kmeans_handle* h) {
 }
 
 kmeans_status kmeans_destroy(kmeans_handle* h) {
+    Nvtx nvtx_("kmeans_destroy");
     if (!h) return KMEANS_ERR_INVALID;
     if (g_prof) prof_dump();
     if (h->d.dbg_ts) {                                                 // AAKM_TC_TRACE: dump the stamps
