@@ -1110,7 +1110,8 @@ float tau_gamma_tc16(int d) { return AAKM_TAU_MARGIN * (3.0f * 2.3841858e-7f + (
     X(1, 0, 0, CG, 2) X(2, 0, 0, CG, 2) X(3, 0, 0, CG, 2) X(4, 0, 0, CG, 2) X(1, 0, 0, CG, 4)             \
     X(2, 0, 0, CG, 4) X(3, 0, 0, CG, 4) X(4, 0, 0, CG, 4) X(1, 1, 0, CG, 2) X(2, 1, 0, CG, 2)             \
     X(3, 1, 0, CG, 2) X(4, 1, 0, CG, 2) X(2, 0, 1, CG, 2) X(4, 0, 1, CG, 2) X(2, 1, 1, CG, 2)             \
-    X(4, 1, 1, CG, 2) X(2, 2, 1, CG, 2) X(4, 2, 1, CG, 2)
+    X(4, 1, 1, CG, 2) X(2, 2, 1, CG, 2) X(4, 2, 1, CG, 2) X(2, 0, 1, CG, 4) X(4, 0, 1, CG, 4)                 \
+    X(2, 2, 1, CG, 4) X(4, 2, 1, CG, 4)
 
 cudaError_t setup_tc() {
     cudaError_t e = cudaSuccess;
@@ -1247,6 +1248,17 @@ static int tc_nsw() {
     static const int v = getenv("AAKM_TC_NSW") ? atoi(getenv("AAKM_TC_NSW")) : 2;
     return v == 4 ? 4 : 2;
 }
+// 2xFP16 splitter warps: four (one per SMSP) when a row tile carries few accumulator
+// tiles (NT <= 8), where the split of each row tile is a large share of the MMA time
+// (c4, NT = 4: 2.46 -> 2.19 ms per 4 M rows), else two (c5, NT = 16: four cost 6 %:
+// 704 threads leave 80 registers and the epilogue spills a little).  AAKM_TC_NSW1=2|4
+// overrides (experiments).
+static int nsw_kind1(int NT) {
+    static const int v = getenv("AAKM_TC_NSW1") ? atoi(getenv("AAKM_TC_NSW1")) : 0;
+    if (v == 2 || v == 4) return v;
+    return NT <= 8 ? 4 : 2;
+}
+
 template <int A, int MODE, int CG>
 static void launch_k0(const TcMaps* m, const CUtensorMap& xm, const Dev& d, const GEval& g, int S, int NT, int NXB,
                       int XRr, long long n_tiles, size_t smem, cudaStream_t s, int NST, int RES) {
@@ -1280,6 +1292,13 @@ static void launch_tc_cg(const Dev& d, const GEval& g, const TcMaps* m, cudaStre
             default: launch_k0<4, MODE, CG>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES); break;
         }
     } else {
+        if constexpr (MODE != 1) {
+            if (nsw_kind1(NT) == 4) {
+                if (A == 2) launch_one<2, MODE, 1, CG, 4>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
+                else launch_one<4, MODE, 1, CG, 4>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
+                return;
+            }
+        }
         if (A == 2) launch_one<2, MODE, 1, CG, 2>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
         else launch_one<4, MODE, 1, CG, 2>(m, xm, d, g, S, NT, NXB, xr, n_tiles, smem, s, NST, RES);
     }
