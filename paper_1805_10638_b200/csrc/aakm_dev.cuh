@@ -120,6 +120,8 @@ struct Dev {
     int* seg_off;         // row offsets of cluster j in perm (K+1)
     int* seg_chunk;       // chunk offsets (K+1)
     long long* seed_d2;   // K-Means++: D2_i (n, fixed point, seed.cu)
+    int* seed_near;       // K-Means++: index of a chosen center at D2_i from row i (n)
+    double* seed_cc;      // K-Means++: lower bounds of ||c_q - c_j||, j < q, for the newest center q (K)
     long long* seed_part; // K-Means++: per-block weight sums (AAKM_SEED_BLOCKS)
     long long* seed_T;    // K-Means++: every rank's weight total (nranks)
     int* seed_x;          // K-Means++: exchange row (d fp32 bits + global index)
@@ -199,7 +201,7 @@ bool encode_gather_rows(void* map128, const float* X, long long n, int d);
 cudaError_t setup_seed();
 int seed_blocks(const Dev& d);
 void launch_seed_first(const Dev& d, long long row_local, long long gi, cudaStream_t s);
-void launch_seed_dist(const Dev& d, const float* c, int first, double scale, cudaStream_t s);
+int launch_seed_dist(const Dev& d, const float* C, int q, double scale, cudaStream_t s);   // launches
 void launch_seed_weights(const Dev& d, int log2n, int rank, int nranks, cudaStream_t s);
 void launch_seed_select(const Dev& d, int r, int log2n, int rank, int nranks, long long row_offset, cudaStream_t s);
 void launch_seed_commit(const Dev& d, float* C_out, int r, cudaStream_t s);

@@ -184,7 +184,7 @@ namespace {
 struct Layout {
     size_t st, st_api, C, C32, Ca32, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
-        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
+        upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_near, seed_cc, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
         ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, sref, part0, part1, total,
         scratch_bytes;
     std::vector<size_t> guards;   // AAKM_WS_CANARY=1: a 256-B canary after every region
@@ -250,6 +250,8 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.perm = take((size_t)n * 4 + 4);
     L.xg_map = take(128);
     L.seed_d2 = take((size_t)n * 8 + 16);           // + the 16-B tail of a bulk-copied odd run
+    L.seed_near = take((size_t)n * 4);
+    L.seed_cc = take((size_t)K * 8);
     L.seed_part = take((size_t)AAKM_SEED_BLOCKS * 8);
     L.seed_T = take((size_t)AAKM_MAX_RANKS * 8);
     L.seed_x = take((size_t)(d + 2) * 4);
@@ -705,6 +707,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     D.seg_chunk = (int*)(w + L.seg_chunk);
     D.seg_cmap = (int4*)(w + L.seg_cmap);
     D.seed_d2 = (long long*)(w + L.seed_d2); D.seed_part = (long long*)(w + L.seed_part);
+    D.seed_near = (int*)(w + L.seed_near); D.seed_cc = (double*)(w + L.seed_cc);
     D.seed_T = (long long*)(w + L.seed_T); D.seed_x = (int*)(w + L.seed_x);
     D.seed_idx = (long long*)(w + L.seed_idx); D.seed_u = (double*)(w + L.seed_u);
     D.perm = (int*)(w + L.perm);
@@ -1434,7 +1437,7 @@ kmeans_status kmeans_seed_pp(kmeans_handle* h, const double* u, float* C_out, in
     launch_seed_commit(d, C_out, 0, s);
     h->launches += 2;
     for (int r = 1; r < K; ++r) {
-        launch_seed_dist(d, C_out + (long long)(r - 1) * d.d, r == 1, scale, s);
+        h->launches += launch_seed_dist(d, C_out, r - 1, scale, s) - 1;   // D2 against the newest center r - 1
         if (h->comm)
             NK(h, ncclAllReduce(&d.st->seed_max, &d.st->seed_max, 1, ncclInt64, ncclMax, h->comm, s));
         launch_seed_weights(d, log2n, h->rank, h->nranks, s);

@@ -11,7 +11,8 @@
 //   D2_i      = min over chosen centers;  M = max_i D2_i;
 //   w_i       = D2_i >> sh, sh = max(0, bitlen(M) + ceil(log2 N) - 62);
 //   center r  = smallest i with w_0 + ... + w_i > floor(u_r T) (T = sum w).
-// Per round: k_seed_dist (one pass over X: D2 update + max), [allreduce max],
+// Per round: k_seed_dist (one pass over X: D2 update + max; by default the pruned
+// k_seed_dist_pr, which reads X only for the rows whose minimum can change), [allreduce max],
 // k_seed_weights (block sums of w over contiguous row blocks), k_seed_total
 // (this rank's T into its slot), [allreduce of the slots], k_seed_select (owner
 // rank, block, row; the row's bits to the exchange buffer), [allreduce of the
@@ -159,6 +160,101 @@ __global__ void __launch_bounds__(256) k_seed_dist_any(Dev d, const float* c, in
             d.seed_d2[row] = v;
             mx = max(mx, v);
         }
+    }
+    mx = warp_max_ll(mx);
+    if (lane == 0 && mx > 0) atomicMax(reinterpret_cast<unsigned long long*>(&d.st->seed_max), (unsigned long long)mx);
+}
+
+// ---------------------------------------------------------------- pruned D2 update
+// The same D2_i = min(D2_i, dist_i(c_q)) for the newest center q, skipping every row
+// whose minimum provably cannot change (triangle inequality over the chosen centers,
+// as in accelerated K-Means++; the result is the same integers, so the draw is
+// unchanged).  Row i keeps j = near_i with D2_i = dist_i(c_j).  In real arithmetic
+//   a^2 = ||x - c_j||^2 <= (D2_i + d) 2^-t (1 + 4u)   (each term of dist is
+//   rint(fl(fl(x - c)^2) 2^t): >= that square (1 - 2u)^... 2^t - 1/2),
+// and if ||c_q - c_j|| >= 2 a_up (1 + 1e-9) then b = ||x - c_q|| >= a_up (1 + 2e-9), so
+//   dist_i(c_q) >= b^2 2^t (1 - 4u) - d/2 >= (D2_i + d)(1 + 4e-9)(1 - 4u) - d/2 > D2_i:
+// the minimum stays D2_i.  cc_j below is a lower bound of ||c_q - c_j|| (fp64, rounded
+// down by a relative 1e-9, far above the few-ulp error of the d-term sum).
+__global__ void __launch_bounds__(256) k_seed_cc(Dev d, const float* C, int q) {
+    const int D = d.d;
+    const float* cq = C + (long long)q * D;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < q; j += gridDim.x * blockDim.x) {
+        const float* cj = C + (long long)j * D;
+        double s = 0.0;
+        for (int k = 0; k < D; ++k) {
+            const double df = (double)cq[k] - (double)cj[k];
+            s = fma(df, df, s);
+        }
+        d.seed_cc[j] = sqrt(s) * (1.0 - 1e-9);
+    }
+}
+
+// Warps over 32-row batches: lane = row for the test (D2, near, cc[near]: 12 B per
+// row), then the rows that need it LPR lanes per row, RPW rows per load instruction,
+// U instructions in flight; the newest center is in registers (one float4 per lane).
+template <int LPR>
+__global__ void __launch_bounds__(256) k_seed_dist_pr(Dev d, const float* C, int q, double scale) {
+    if (d.st->seed_err) return;
+    constexpr int RPW = 32 / LPR, U = 4;
+    __shared__ int lst[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int h = lane / LPR, c4i = lane % LPR;
+    const long long wg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
+    const float4 cf = reinterpret_cast<const float4*>(C + (long long)q * d.d)[c4i];
+    const double c0 = cf.x, c1 = cf.y, c2 = cf.z, c3 = cf.w;
+    const double two_mt = 1.0 / scale, dd = (double)d.d;            // 2^-t exact
+    const float4* X4 = reinterpret_cast<const float4*>(d.X);
+    long long mx = 0;
+    for (long long base = wg * 32; base < d.n; base += nwg * 32) {
+        const long long i = base + lane;
+        const bool ok = i < d.n;
+        long long D2 = 0;
+        bool need = false;
+        if (ok) {
+            if (q == 0) {
+                need = true;                                         // first center: every row
+            } else {
+                D2 = d.seed_d2[i];
+                const int nr = d.seed_near[i];
+                const double aup = sqrt(((double)D2 + dd) * two_mt * (1.0 + 1e-12)) * (1.0 + 1e-12);
+                need = !(d.seed_cc[nr] >= 2.0 * aup * (1.0 + 1e-9));
+                if (!need) mx = max(mx, D2);
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        const int cnt = __popc(m);
+        if (need) lst[wib][__popc(m & ((1u << lane) - 1))] = lane;
+        __syncwarp();
+        for (int k0 = 0; k0 < cnt; k0 += U * RPW) {
+            float4 xv[U];
+            int src[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + u * RPW + h;
+                src[u] = k < cnt ? lst[wib][k] : -1;
+                xv[u] = src[u] >= 0 ? __ldg(X4 + (base + src[u]) * (long long)LPR + c4i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                long long s = seed_term(xv[u].x, c0, scale) + seed_term(xv[u].y, c1, scale) +
+                              seed_term(xv[u].z, c2, scale) + seed_term(xv[u].w, c3, scale);
+#pragma unroll
+                for (int o = 1; o < LPR; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                const long long old = __shfl_sync(0xffffffffu, D2, src[u] >= 0 ? src[u] : 0);
+                if (src[u] >= 0 && c4i == 0) {
+                    const long long row = base + src[u];
+                    const long long v = q == 0 ? s : min(s, old);
+                    if (q == 0 || s < old) {
+                        d.seed_d2[row] = v;
+                        d.seed_near[row] = q;
+                    }
+                    mx = max(mx, v);
+                }
+            }
+        }
+        __syncwarp();
     }
     mx = warp_max_ll(mx);
     if (lane == 0 && mx > 0) atomicMax(reinterpret_cast<unsigned long long*>(&d.st->seed_max), (unsigned long long)mx);
@@ -350,20 +446,43 @@ void launch_seed_first(const Dev& d, long long row_local, long long gi, cudaStre
     k_seed_first<<<1, 128, 0, s>>>(d, row_local, gi);
 }
 
-void launch_seed_dist(const Dev& d, const float* c, int first, double scale, cudaStream_t s) {
+// AAKM_SEED_PRUNE=0: every round streams all of X (k_seed_dist); default: the pruned
+// update (k_seed_dist_pr, same integers) for d % 4 == 0 with d / 4 a power of two <= 32
+static bool seed_prune() {
+    static const bool v = !(getenv("AAKM_SEED_PRUNE") && atoi(getenv("AAKM_SEED_PRUNE")) == 0);
+    return v;
+}
+
+int launch_seed_dist(const Dev& d, const float* C, int q, double scale, cudaStream_t s) {
     const int nb = seed_blocks(d);
     const int lpr = d.d / 4;
+    const float* c = C + (long long)q * d.d;
+    const int first = q == 0;
+    if (d.d % 4 == 0 && lpr <= 32 && (lpr & (lpr - 1)) == 0 && seed_prune() && ((uintptr_t)d.X & 15) == 0) {
+        if (q > 0) k_seed_cc<<<(q + 255) / 256, 256, 0, s>>>(d, C, q);
+        const int nl = q > 0 ? 2 : 1;
+        const int pb = 8 * d.num_sms;
+        switch (lpr) {
+            case 1: k_seed_dist_pr<1><<<pb, 256, 0, s>>>(d, C, q, scale); return nl;
+            case 2: k_seed_dist_pr<2><<<pb, 256, 0, s>>>(d, C, q, scale); return nl;
+            case 4: k_seed_dist_pr<4><<<pb, 256, 0, s>>>(d, C, q, scale); return nl;
+            case 8: k_seed_dist_pr<8><<<pb, 256, 0, s>>>(d, C, q, scale); return nl;
+            case 16: k_seed_dist_pr<16><<<pb, 256, 0, s>>>(d, C, q, scale); return nl;
+            default: k_seed_dist_pr<32><<<pb, 256, 0, s>>>(d, C, q, scale); return nl;
+        }
+    }
     if (d.d % 4 == 0 && lpr <= 32 && (lpr & (lpr - 1)) == 0) {
         switch (lpr) {
-            case 1: k_seed_dist<1><<<nb, 256, SeedRing<1>::SMEM, s>>>(d, c, first, scale, nb); return;
-            case 2: k_seed_dist<2><<<nb, 256, SeedRing<2>::SMEM, s>>>(d, c, first, scale, nb); return;
-            case 4: k_seed_dist<4><<<nb, 256, SeedRing<4>::SMEM, s>>>(d, c, first, scale, nb); return;
-            case 8: k_seed_dist<8><<<nb, 256, SeedRing<8>::SMEM, s>>>(d, c, first, scale, nb); return;
-            case 16: k_seed_dist<16><<<nb, 256, SeedRing<16>::SMEM, s>>>(d, c, first, scale, nb); return;
-            default: k_seed_dist<32><<<nb, 256, SeedRing<32>::SMEM, s>>>(d, c, first, scale, nb); return;
+            case 1: k_seed_dist<1><<<nb, 256, SeedRing<1>::SMEM, s>>>(d, c, first, scale, nb); return 1;
+            case 2: k_seed_dist<2><<<nb, 256, SeedRing<2>::SMEM, s>>>(d, c, first, scale, nb); return 1;
+            case 4: k_seed_dist<4><<<nb, 256, SeedRing<4>::SMEM, s>>>(d, c, first, scale, nb); return 1;
+            case 8: k_seed_dist<8><<<nb, 256, SeedRing<8>::SMEM, s>>>(d, c, first, scale, nb); return 1;
+            case 16: k_seed_dist<16><<<nb, 256, SeedRing<16>::SMEM, s>>>(d, c, first, scale, nb); return 1;
+            default: k_seed_dist<32><<<nb, 256, SeedRing<32>::SMEM, s>>>(d, c, first, scale, nb); return 1;
         }
     }
     k_seed_dist_any<<<nb, 256, 0, s>>>(d, c, first, scale, nb);
+    return 1;
 }
 
 void launch_seed_weights(const Dev& d, int log2n, int rank, int nranks, cudaStream_t s) {
