@@ -727,7 +727,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CU
                 constexpr int RPW = 4;                             // rows per warp instruction
                 constexpr int NG = TC_BM / (NSW * RPW);            // row groups per warp per tile
                 constexpr int RB = AAKM_SPLIT_F4 / A;              // row groups per batch (float4s in flight per lane)
-                static_assert(RB >= 1 && NG % RB == 0, "splitter batches must tile the warp's row groups");
+                static_assert(KIND != 1 || (RB >= 1 && NG % RB == 0), "splitter batches must tile the warp's row groups");
                 const int wi = warp - W_SPLIT;
                 const int sub = lane & 7, rsub = lane >> 3;
                 uint8_t* fa = xhi + 2 * NATOM * ATOM_BYTES_X;
