@@ -1406,10 +1406,17 @@ __global__ void __launch_bounds__(256) k_csplit32(Dev d, int mode) {
         d.Chi[e] = hi;
         d.Clo[e] = (float)(v - (double)hi);
     }
-    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d.K; j += (long long)gridDim.x * blockDim.x) {
+    // ||c_j||^2 in fp64: a warp per centroid, lanes over the coordinates, a fixed xor
+    // tree (one thread per centroid walked d dependent L2 loads: 7 us per launch on c3)
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwp = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long j = w0; j < d.K; j += nwp) {
         const double* c = d.C + j * d.d;
         double nrm = 0.0;
-        for (int k = 0; k < d.d; ++k) nrm = fma(c[k], c[k], nrm);
+        for (int k = lane; k < d.d; k += 32) nrm = fma(c[k], c[k], nrm);
+        for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+        if (lane != 0) continue;
         const double v = nrm * U;
         const float h = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
         const float m = __uint_as_float(__float_as_uint((float)(v - (double)h)) & 0xFFFFE000u);
