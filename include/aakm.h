@@ -265,7 +265,9 @@ AAKM_API kmeans_status kmeans_update_partials(kmeans_handle *h, const int32_t *l
  *   C_out   device, K x d fp32 row-major, caller-owned: the chosen samples.
  *   idx_out host, K int64 (nullable): their global row indices.
  * Collective when nranks > 1 (three small allreduces per center). Uses the
- * handle's X and workspace; does not touch the Algorithm 1 state.
+ * handle's X and workspace; does not touch the Algorithm 1 state.  Rows whose
+ * D^2 provably cannot drop (triangle inequality over the chosen centers) are
+ * not re-read; the weights are the same integers (AAKM_SEED_PRUNE=0: every row).
  * Synchronises. Errors: INVALID for NULL u / C_out, a u outside [0, 1), or
  * fewer than K distinct samples (every remaining D^2 = 0). */
 AAKM_API kmeans_status kmeans_seed_pp(kmeans_handle *h, const double *u /*host*/, float *C_out,
