@@ -23,7 +23,9 @@ def _gpu():
 
 
 @pytest.mark.parametrize("path,cfg", [("tc", "c3"), ("tc", "c5"), ("tc16", "c5"), ("tc16", "c4")])
-@pytest.mark.parametrize("K", [1, 100, 129, 257, 300, 1000])
+# K = 2048 / 2049: the 2xFP16 engine's last four-splitter-warp tiling (8 accumulator
+# tiles per row tile) and the first two-splitter one (9)
+@pytest.mark.parametrize("K", [1, 100, 129, 257, 300, 1000, 2048, 2049])
 def test_ragged_k(path, cfg, K):
     X, C0, c = make(cfg, N=3001, K=K)
     km = aakm.KMeans(dev(X), c.K, aakm.config(assign_path=path))
