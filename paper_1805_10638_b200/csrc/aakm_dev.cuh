@@ -134,6 +134,8 @@ struct Dev {
     float* lb;            //   ... and lower bound on min_{j != rho_i} ||x_i - c_j||, w.r.t. C_ref
     int* pj2;             //   two-centroid rows: the other candidate (-1: none); then ub bounds
                           //   both candidates' distances and lb every other centroid's
+    float* pgap;          //   two-centroid rows: lower bound on d(x, c_other) - d(x, c_label)
+                          //   from the last exact decision, moved by the shifts (w.r.t. C_ref)
     int* act_rows;        //   rows the bounds could not prove unchanged (capacity n)
     long long* act_count; //   [2] their counts, branch A / B (zeroed per pass with packed)
     double* C_ref;        //   centroids the bounds refer to (the last assigned set)
@@ -141,6 +143,7 @@ struct Dev {
     float* ub0;           //   snapshot of (ub, lb, pj2, C_ref) taken before branch A, restored
     float* lb0;           //   for the fallback B on a rejection (bounds w.r.t. the previous
     int* pj20;            //   pass's set instead of the rejected jump)
+    float* pgap0;
     double* C_ref0;
     double* Gring;        // H x K*d (fp64)
     double* Fring;        // H x K*d (fp64)

@@ -1559,6 +1559,14 @@ __global__ void __launch_bounds__(256) k_refine_pair(Dev d, GEval g) {
                 const bool w1 = a1 < a0 || (a1 == a0 && jj[u].y < jj[u].x);
                 lab_out[row[u]] = w1 ? jj[u].y : jj[u].x;
                 if (d.pj2) d.pj2[row[u]] = w1 ? jj[u].x : jj[u].y;  // bounded: the other candidate
+                if (d.pgap) {
+                    // real-distance gap between the candidates, less the fp64 error of the
+                    // two computed squared distances (relative <= (d + 2) 2^-53, far below
+                    // 1e-12), rounded down; k_bounds moves it by the shifts
+                    const double dw = sqrt(w1 ? a1 : a0), dl = sqrt(w1 ? a0 : a1);
+                    const double gap = (dl - dw) - 1e-12 * (dl + dw) - 1e-300;
+                    d.pgap[row[u]] = gap > 0.0 ? __double2float_rd(gap) : 0.f;
+                }
             }
         }
     }

@@ -121,7 +121,18 @@ __global__ void __launch_bounds__(256) k_bounds(Dev d, GEval g) {
                     d.ub[i] = u;
                     d.lb[i] = l;
                     lab_out[i] = a;
-                    if (p2 >= 0) { pm |= 1u << k; pa[k] = a; pb2[k] = p2; }
+                    if (p2 >= 0) {
+                        // two-centroid row: if the last exact decision's distance gap, less
+                        // both candidates' shifts (rounded down), still exceeds the fp64
+                        // rounding of the distances (1e-9 of u, with room to spare), the
+                        // exact argmin is still a -- no pair refine
+                        const float gp = d.pgap ? __fsub_rd(__fsub_rd(d.pgap[i], d.shift[a]), d.shift[p2]) : 0.f;
+                        if (gp > 1e-9f * u) {
+                            d.pgap[i] = gp;
+                        } else {
+                            pm |= 1u << k; pa[k] = a; pb2[k] = p2;
+                        }
+                    }
                 } else {
                     um |= 1u << k;
                 }
@@ -164,15 +175,19 @@ __global__ void __launch_bounds__(256) k_bnd_save(Dev d, GEval g, int restore) {
     const float* lbs = restore ? d.lb0 : d.lb;
     const int* p2s = restore ? d.pj20 : d.pj2;
     const double* crs = restore ? d.C_ref0 : d.C_ref;
+    float* pg = restore ? d.pgap : d.pgap0;
+    const float* pgs = restore ? d.pgap0 : d.pgap;
     // 16-B copies (the arrays are 256-B aligned carve regions), scalar tail
     const long long n4 = n >> 2;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += st) {
         reinterpret_cast<float4*>(ub)[i] = reinterpret_cast<const float4*>(ubs)[i];
         reinterpret_cast<float4*>(lb)[i] = reinterpret_cast<const float4*>(lbs)[i];
         reinterpret_cast<int4*>(p2)[i] = reinterpret_cast<const int4*>(p2s)[i];
+        if (pg) reinterpret_cast<float4*>(pg)[i] = reinterpret_cast<const float4*>(pgs)[i];
     }
     for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
         ub[i] = ubs[i]; lb[i] = lbs[i]; p2[i] = p2s[i];
+        if (pg) pg[i] = pgs[i];
     }
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < KD; i += st) cr[i] = crs[i];
     if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -185,7 +185,7 @@ struct Layout {
     size_t st, st_api, C, C32, Ca32, Chi, Clo, cn, cnimg, Ca, Cahi, Calo, cna, cnimga, C16h, C16l, Ca16h, Ca16l, lab0, lab1, flags, fb1, ftau, Xf, cand, cand_cnt, pair_rows, pair_j,
         scratch, packed1,
         upd_part, seg_bh, seg_off, seg_chunk, seg_cmap, xg_map, seed_d2, seed_near, seed_cc, seed_part, seed_T, seed_x, seed_idx, seed_u, perm, Gring, Fring, gram_part, trace,
-        ub, lb, act_rows, pj2, C_ref, shift, ub0, lb0, pj20, C_ref0, xchk, x2, sref, part0, part1, total,
+        ub, lb, act_rows, pj2, pgap, C_ref, shift, ub0, lb0, pj20, pgap0, C_ref0, xchk, x2, sref, part0, part1, total,
         scratch_bytes;
     std::vector<size_t> guards;   // AAKM_WS_CANARY=1: a 256-B canary after every region
 };
@@ -266,6 +266,7 @@ Layout layout(long long n, int d, int K, int m_max, bool bounded) {
     L.ub = take(nb * 4 + 4); L.lb = take(nb * 4 + 4); L.act_rows = take(nb * 4 + 4); L.pj2 = take(nb * 4 + 4);
     L.C_ref = take(bounded ? KD * 8 : 8); L.shift = take(bounded ? (size_t)K * 4 : 4);
     L.ub0 = take(nb * 4 + 4); L.lb0 = take(nb * 4 + 4); L.pj20 = take(nb * 4 + 4);
+    L.pgap = take(nb * 4 + 4); L.pgap0 = take(nb * 4 + 4);
     L.C_ref0 = take(bounded ? KD * 8 : 8);
     L.xchk = take(16);
     L.x2 = take(16);
@@ -734,6 +735,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
         D.C_ref = (double*)(w + L.C_ref); D.shift = (float*)(w + L.shift);
         D.ub0 = (float*)(w + L.ub0); D.lb0 = (float*)(w + L.lb0); D.pj20 = (int*)(w + L.pj20);
         D.C_ref0 = (double*)(w + L.C_ref0);
+        if (!getenv("AAKM_NO_PGAP")) { D.pgap = (float*)(w + L.pgap); D.pgap0 = (float*)(w + L.pgap0); }
     }
     D.dbg = getenv("AAKM_TC_DBG") ? atoi(getenv("AAKM_TC_DBG")) : 0;
     if (getenv("AAKM_TC_TRACE")) {                                     // perf probe only: a 32 KB stamp buffer
@@ -749,6 +751,7 @@ kmeans_status kmeans_create(kmeans_handle** out, const float* X, int64_t n_local
     h->da.pj2 = nullptr;
     h->da.C_ref = nullptr; h->da.shift = nullptr;
     h->da.ub0 = nullptr; h->da.lb0 = nullptr; h->da.pj20 = nullptr; h->da.C_ref0 = nullptr;
+    h->da.pgap = nullptr; h->da.pgap0 = nullptr;
     h->da.st = (DevState*)(w + L.st_api);
     h->da.C = (double*)(w + L.Ca); h->da.C32 = (float*)(w + L.Ca32); h->da.Chi = (float*)(w + L.Cahi); h->da.Clo = (float*)(w + L.Calo);
     h->da.cn = (float*)(w + L.cna);
